@@ -1,0 +1,133 @@
+/*
+ * cn_b200.h — C ABI of the B200-native recursive corrective-motion solver.
+ *
+ * Drop-in boundary for the hot path of the reference package `contactnewton`
+ * (arXiv 2306.06946, fast scheme = paper Alg. 3).  The reference boundary is an
+ * in-process Python API; every entry point below replaces one
+ * reference function and is bound from Python with ctypes
+ * (paper_2306_06946_b200/_lib.py).  INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - every pointer argument named d_* (and every double* / int* data array
+ *     unless stated "host") is DEVICE memory owned by the caller; the library
+ *     never frees caller memory;
+ *   - `stream` is a cudaStream_t passed as void* (torch's current stream);
+ *   - all floating point is IEEE fp64, matrices are row-major with a leading
+ *     dimension `ld*` in elements;
+ *   - every function returns a status code (CNB_OK on success); the message of
+ *     the last failure on the calling thread is available from
+ *     cnb_last_error();
+ *   - kernels that detect data errors (non-positive pivots, singular contact
+ *     blocks) record them in a device status word `d_status`
+ *     (cnb_status_t, zero-initialised by the caller) that the host reads when
+ *     it synchronises; status codes match the reference exceptions.
+ */
+#ifndef CN_B200_H
+#define CN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (reference: contactnewton/errors.py:4-45) ------------- */
+#define CNB_OK 0
+#define CNB_E_DIMENSION 1          /* DimensionMismatchError  errors.py:8   */
+#define CNB_E_NOT_SPD 2            /* NotSPDError             errors.py:12  */
+#define CNB_E_SINGULAR_BLOCK 3     /* SingularBlockError      errors.py:36  */
+#define CNB_E_DEGENERATE_FRAME 4   /* DegenerateFrameError    errors.py:32  */
+#define CNB_E_NONFINITE 5          /* NonFiniteForceError     errors.py:24  */
+#define CNB_E_VALIDATION 6         /* ValidationError         errors.py:44  */
+#define CNB_E_INVALID_ATTACHMENT 7 /* InvalidAttachmentError  errors.py:28  */
+#define CNB_E_DEGENERATE_TET 8     /* DegenerateTetError      errors.py:20  */
+#define CNB_E_CUDA 100             /* CUDA runtime failure                  */
+#define CNB_E_INTERNAL 200
+
+typedef struct cnb_status {
+  int32_t code;
+  int32_t index;
+  double value;
+} cnb_status_t;
+
+int cnb_abi_version(void);
+const char* cnb_last_error(void);
+
+/* ---- constraint-space operators (contactnewton/constraints.py) ---------- */
+
+/* W = D Wg D^T, D block-diagonal (groups x 3 x 3, rows n,t1,t2).
+ * Replaces rebuild_W_fast  constraints.py:182-191 (+ gemm linalg.py:121-147);
+ * bit-identical to the reference's naive-order double gemm. */
+int cnb_rebuild_w(int64_t groups, const double* D, const double* Wg, int64_t ldwg,
+                  double* W, int64_t ldw, void* stream);
+
+/* delta = D (p_a - p_b).  Replaces compute_violation constraints.py:208-214. */
+int cnb_violation(int64_t groups, const double* D, const double* p_a, const double* p_b,
+                  double* delta, void* stream);
+
+/* t = D^T lam; if accumulated != NULL also accumulated += t.
+ * Replaces DirectionMatrix.apply_transposed constraints.py:62-64 and the
+ * impulse accumulation of newton_fast solver.py:346. */
+int cnb_apply_dt(int64_t groups, const double* D, const double* lam, double* t,
+                 double* accumulated, void* stream);
+
+/* Fast proximity update for ONE dynamic object o:
+ *   y = h^2 U_o t[idx],  p_a[idx[k]] += y_k (side +1)  or  p_b[idx[k]] -= y_k (side -1).
+ * U_o is the compact (3*mo x 3*mo) restriction of the object's S A^-1 S^T to
+ * the mo pairs it takes part in; idx (int64, mo) lists those pairs and
+ * side (int8, mo) the side the object owns.  Replaces the per-object loop of
+ * fast_update_proximity constraints.py:217-244. */
+int cnb_prox_update(int64_t mo, const double* U, int64_t ldu, const int64_t* idx,
+                    const int8_t* side, const double* t, double h, double* p_a, double* p_b,
+                    void* stream);
+
+/* ---- frames (contactnewton/collision.py) --------------------------------- */
+
+/* Detection frames from p_a - p_b with the element normal as orientation
+ * reference / fallback.  Replaces build_frames collision.py:359-375.
+ * Degenerate pairs set d_status to CNB_E_DEGENERATE_FRAME. */
+int cnb_build_frames(int64_t pairs, const double* p_a, const double* p_b,
+                     const double* ref_normal, double* frames, cnb_status_t* d_status,
+                     void* stream);
+
+/* Re-linearised frames and the largest normal rotation (radians, written to
+ * rotation[0]).  Replaces relinearize collision.py:381-405 and
+ * max_frame_rotation collision.py:408-414. */
+int cnb_relinearize(int64_t pairs, const double* p_a, const double* p_b,
+                    const double* prev, double* frames, double* rotation, void* stream);
+
+/* ---- projected Gauss-Seidel (contactnewton/solver.py) -------------------- */
+
+/* Workspace bytes needed by cnb_pgs for c = 3*groups rows. */
+int64_t cnb_pgs_work_bytes(int64_t groups);
+
+/* PGS with Signorini + isotropic Coulomb disk in the reference's canonical
+ * group order.  Replaces pgs solver.py:168-202, local_solve 124-165 and
+ * regularize 99-121.
+ *   lam (c), delta_end (c): outputs; eps_hist (max_iter): per-sweep epsilon;
+ *   iters_conv (2 int32): sweeps performed, converged flag.
+ * Singular blocks set d_status to CNB_E_SINGULAR_BLOCK (index = group). */
+int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_base,
+            double h, double mu, double tol, int32_t max_iter, double* lam,
+            double* delta_end, double* eps_hist, int32_t* iters_conv, void* work,
+            cnb_status_t* d_status, void* stream);
+
+/* One group's local solve (solver.py:124-165) as a device call, for API
+ * parity with local_solve; out (3). */
+int cnb_local_solve(int64_t alpha, int64_t groups, const double* W, int64_t ldw,
+                    const double* delta_cur, const double* lam, double mu, double h2,
+                    double* out, cnb_status_t* d_status, void* stream);
+
+/* ---- dense products (contactnewton/linalg.py) ---------------------------- */
+
+/* C (m x n) = op(A) op(B), accumulated over k in ascending order with
+ * separately rounded products and sums: bit-identical to gemm
+ * linalg.py:121-147. */
+int cnb_gemm_naive(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                   int32_t trans_a, const double* B, int64_t ldb, int32_t trans_b,
+                   double* C, int64_t ldc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CN_B200_H */

@@ -1,0 +1,84 @@
+// Shared helpers for the B200 (sm_100a) contact-solver kernels.
+//
+// Status codes mirror the reference's exception classes
+// (/root/reference/pkg/src/contactnewton/errors.py); the Python layer maps
+// them back onto the same class names.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/cn_b200.h"
+
+namespace cnb {
+
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+
+#define CNB_CUDA(call)                                                         \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) return ::cnb::cuda_status(_e, #call);               \
+  } while (0)
+
+#define CNB_LAUNCH_CHECK(where)                                                \
+  do {                                                                         \
+    cudaError_t _e = cudaGetLastError();                                       \
+    if (_e != cudaSuccess) return ::cnb::cuda_status(_e, where);               \
+  } while (0)
+
+// IEEE round-to-nearest arithmetic without FMA contraction.  The reference
+// evaluates products and sums through numpy temporaries (a*b rounded, then
+// the add rounded), so kernels whose output is compared bit-for-bit use
+// these instead of the contracting operators.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+// Device-side status word: kernels record the first failure here and the
+// host reads it back when it synchronises for scalar outputs.
+struct DevStatus {
+  int code;     // CNB_OK or one of the CNB_E_* values
+  int index;    // offending group / pivot / pair
+  double value; // offending value (pivot, W_nn, determinant)
+};
+
+__device__ __forceinline__ void raise_status(DevStatus* st, int code, int index, double value) {
+  if (st && atomicCAS(&st->code, 0, code) == 0) {
+    st->index = index;
+    st->value = value;
+  }
+}
+
+inline int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > (1 << 30)) g = 1 << 30;
+  return (int)g;
+}
+
+// fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).  Lowers to
+// SASS DMMA.8x8x4 on sm_100a (tcgen05 has no f64 kind).
+// Fragment layout (lane = 4*g + t): a = A[g][t], b = B[t][g],
+// c0,c1 = C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace cnb

@@ -1,0 +1,461 @@
+// Projected Gauss-Seidel with Signorini + isotropic Coulomb friction, in the
+// reference's exact canonical group order.
+//
+// Reference: pgs solver.py:168-202, local_solve solver.py:124-165,
+// regularize solver.py:99-121 (paths under /root/reference/pkg/src/contactnewton).
+//
+// Gauss-Seidel over a dense W is sequential in the group index: group g's
+// local solve needs  delta_g = delta_base_g + h^2 W[g,:] lam  with every
+// earlier group of the sweep already updated.  The reference keeps delta for
+// all rows current by a rank-3 update after every group (8 c^2 bytes of W per
+// sweep).  Here the sweep is blocked, 32 groups per block:
+//
+//   * one SOLVER warp owns the block being solved, lane l <-> group l; the
+//     block's diagonal W tile sits in shared memory and the in-block rank-3
+//     updates are warp-synchronous (shuffles, no barriers);
+//   * while it solves block b, the HELPER warps evaluate, for the rows of the
+//     next block b', the lazy row products  P = W[b', not b] lam  — every
+//     lambda they read is final for this point of the sweep;
+//   * after the barrier all warps add the cross term W[b', b] lam_b and stage
+//     block b''s diagonal tile, and the solver continues.
+//
+// The iterate is mathematically the reference's; only the association of
+// the floating-point sums of delta differs (the per-group arithmetic of
+// local_solve is reproduced operation by operation).
+#include "common.cuh"
+
+namespace cnb {
+
+constexpr int kBG = 32;         // groups per block (one per solver lane)
+constexpr int kBR = 3 * kBG;    // rows per block
+constexpr int kPgsThreads = 256;
+
+struct PgsScene {
+  int64_t groups;
+  const double* W;
+  int64_t ldw;
+  const double* delta_base;
+  double h2, mu, tol;
+  int max_iter;
+  double* lam;
+  double* delta_end;
+  double* eps_hist;
+  int* iters_conv;
+  DevStatus* status;
+};
+
+// eigenvalues of a symmetric 3x3 by cyclic Jacobi (converges to rounding)
+__device__ void sym3_eigs(double a[3][3], double out[3]) {
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+    if (off == 0.0) break;
+    for (int p = 0; p < 2; ++p) {
+      for (int q = p + 1; q < 3; ++q) {
+        double apq = a[p][q];
+        if (apq == 0.0) continue;
+        double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 3; ++k) {  // columns p, q
+          double akp = a[k][p], akq = a[k][q];
+          a[k][p] = c * akp - s * akq;
+          a[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {  // rows p, q
+          double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = c * apk - s * aqk;
+          a[q][k] = s * apk + c * aqk;
+        }
+        a[p][q] = a[q][p] = 0.0;
+      }
+    }
+  }
+  out[0] = a[0][0];
+  out[1] = a[1][1];
+  out[2] = a[2][2];
+}
+
+// local_solve solver.py:124-165 on one group; Wd = regularised diagonal
+// block (row-major).  Returns 0, or CNB_E_SINGULAR_BLOCK.
+__device__ __forceinline__ int local_solve_dev(const double d[3], const double l[3], const double Wd[9],
+                                               double mu, double h2, double out[3]) {
+  const double Wnn = Wd[0];
+  if (!(Wnn > 0.0)) return CNB_E_SINGULAR_BLOCK;
+  const double ln_old = l[0];
+  const double x = sub(ln_old, __ddiv_rn(d[0], mul(h2, Wnn)));
+  const double ln = x > 0.0 ? x : 0.0;  // Python max(0.0, x)
+  if (ln == 0.0) {
+    out[0] = out[1] = out[2] = 0.0;
+    return 0;
+  }
+  if (mu == 0.0) {
+    out[0] = ln;
+    out[1] = out[2] = 0.0;
+    return 0;
+  }
+  const double dln = sub(ln, ln_old);
+  const double dt0 = add(d[1], mul(mul(h2, Wd[3]), dln));
+  const double dt1 = add(d[2], mul(mul(h2, Wd[6]), dln));
+  const double T00 = mul(h2, Wd[4]), T01 = mul(h2, Wd[5]);
+  const double T10 = mul(h2, Wd[7]), T11 = mul(h2, Wd[8]);
+  const double det = sub(mul(T00, T11), mul(T01, T10));
+  if (!(det > 0.0)) return CNB_E_SINGULAR_BLOCK;
+  const double r0 = -dt0, r1 = -dt1;
+  const double dl0 = __ddiv_rn(sub(mul(T11, r0), mul(T01, r1)), det);
+  const double dl1 = __ddiv_rn(sub(mul(T00, r1), mul(T10, r0)), det);
+  double lt0 = add(l[1], dl0), lt1 = add(l[2], dl1);
+  const double radius = mul(mu, ln);
+  const double nt = hypot(lt0, lt1);
+  if (nt > radius) {
+    const double s = __ddiv_rn(radius, nt);
+    lt0 = mul(lt0, s);
+    lt1 = mul(lt1, s);
+  }
+  out[0] = ln;
+  out[1] = lt0;
+  out[2] = lt1;
+  return 0;
+}
+
+// Shared-memory layout of one scene's PGS.
+struct PgsSmem {
+  double* lam;     // c
+  double* dshift;  // groups (regularisation shift per group, 0 if none)
+  double* Wbb;     // kBR x kBR diagonal tile of the block being solved
+  double* P;       // kBR lazy row products for the next block (helpers)
+  double* dnext;   // kBR delta of the next block (read by the solver)
+  double* red;     // 32 reduction slots
+  int* flags;      // [0] abort code, [1] converged
+};
+
+__device__ __forceinline__ double w_reg(const PgsScene& s, const PgsSmem& sm, int64_t r, int64_t c) {
+  double w = s.W[r * s.ldw + c];
+  if (r == c) w = add(w, sm.dshift[r / 3]);
+  return w;
+}
+
+__device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t G = s.groups, c = 3 * G;
+  const int nb = (int)((G + kBG - 1) / kBG);
+
+  // ---- regularize (solver.py:99-121) ----
+  double tr = 0.0;
+  for (int64_t i = tid; i < c; i += blockDim.x) tr += s.W[i * s.ldw + i];
+  tr = warp_sum(tr);
+  if (lane == 0) sm.red[warp] = tr;
+  if (tid == 0) sm.flags[0] = sm.flags[1] = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < nwarps; ++w) t += sm.red[w];
+    sm.red[31] = t;
+  }
+  __syncthreads();
+  double shift = 1e-10 * sm.red[31] / (double)c;
+  if (shift <= 0.0) shift = 1e-30;
+  for (int64_t g = tid; g < G; g += blockDim.x) {
+    double a[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        a[i][j] = 0.5 * (s.W[(3 * g + i) * s.ldw + 3 * g + j] + s.W[(3 * g + j) * s.ldw + 3 * g + i]);
+    double e[3];
+    sym3_eigs(a, e);
+    double mn = fmin(e[0], fmin(e[1], e[2]));
+    double scale = fmax(fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))), 1e-300);
+    sm.dshift[g] = (mn <= 1e-12 * scale) ? shift : 0.0;
+  }
+  for (int64_t i = tid; i < c; i += blockDim.x) sm.lam[i] = 0.0;
+  __syncthreads();
+
+  // stage block 0: delta = delta_base (lambda = 0), diagonal tile
+  auto stage_tile = [&](int b) {
+    const int64_t r0 = (int64_t)b * kBR;
+    const int rows = (int)min((int64_t)kBR, c - r0);
+    for (int e = tid; e < rows * rows; e += blockDim.x) {
+      int i = e / rows, j = e - i * rows;
+      sm.Wbb[i * kBR + j] = w_reg(s, sm, r0 + i, r0 + j);
+    }
+  };
+  stage_tile(0);
+  for (int i = tid; i < (int)min((int64_t)kBR, c); i += blockDim.x) sm.dnext[i] = s.delta_base[i];
+  // solver lane state
+  double dl_[3] = {0, 0, 0}, lm[3] = {0, 0, 0};
+  __syncthreads();
+
+  const double h2 = s.h2;
+  int iterations = 0;
+  bool converged = false;
+  for (int sweep = 0; sweep < s.max_iter; ++sweep) {
+    iterations = sweep + 1;
+    double dsq = 0.0;  // solver lanes: sum of squared lambda changes
+    for (int b = 0; b < nb; ++b) {
+      const int64_t g0 = (int64_t)b * kBG;
+      const int ng = (int)min((int64_t)kBG, G - g0);
+      const int bn = (b + 1 == nb) ? 0 : b + 1;  // next block (wraps to the next sweep)
+      const int64_t gn0 = (int64_t)bn * kBG;
+      const int ngn = (int)min((int64_t)kBG, G - gn0);
+      if (warp == 0) {
+        // ---- sequential block solve ----
+        const bool mine = lane < ng;
+        if (mine)
+          for (int a = 0; a < 3; ++a) {
+            lm[a] = sm.lam[3 * (g0 + lane) + a];
+            dl_[a] = sm.dnext[3 * lane + a];
+          }
+        int err = 0;
+        for (int g = 0; g < ng; ++g) {
+          double d0 = 0, d1 = 0, d2 = 0;
+          int any = 0;
+          if (lane == g) {
+            double Wd[9];
+            for (int i = 0; i < 3; ++i)
+              for (int j = 0; j < 3; ++j) Wd[3 * i + j] = sm.Wbb[(3 * g + i) * kBR + 3 * g + j];
+            double nw[3];
+            err = local_solve_dev(dl_, lm, Wd, s.mu, h2, nw);
+            if (!err) {
+              d0 = sub(nw[0], lm[0]);
+              d1 = sub(nw[1], lm[1]);
+              d2 = sub(nw[2], lm[2]);
+              any = (d0 != 0.0) || (d1 != 0.0) || (d2 != 0.0);
+              dsq += d0 * d0 + d1 * d1 + d2 * d2;
+              if (any) {
+                lm[0] = nw[0];
+                lm[1] = nw[1];
+                lm[2] = nw[2];
+              }
+            } else {
+              raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), Wd[0]);
+            }
+          }
+          if (__shfl_sync(0xffffffffu, err, g)) {
+            err = 1;
+            break;
+          }
+          any = __shfl_sync(0xffffffffu, any, g);
+          if (!any) continue;
+          d0 = __shfl_sync(0xffffffffu, d0, g);
+          d1 = __shfl_sync(0xffffffffu, d1, g);
+          d2 = __shfl_sync(0xffffffffu, d2, g);
+          if (mine) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const double* wr = sm.Wbb + (3 * lane + a) * kBR + 3 * g;
+              double tmp = add(add(mul(wr[0], d0), mul(wr[1], d1)), mul(wr[2], d2));
+              dl_[a] = add(dl_[a], mul(h2, tmp));
+            }
+          }
+        }
+        if (err) {
+          if (lane == 0) sm.flags[0] = CNB_E_SINGULAR_BLOCK;
+        } else if (mine) {
+          for (int a = 0; a < 3; ++a) sm.lam[3 * (g0 + lane) + a] = lm[a];
+        }
+      } else if (nb > 1) {
+        // ---- helpers: P[r] = W[r, not block b] lam for rows of block bn ----
+        const int64_t rn0 = gn0 * 3;
+        const int rows = 3 * ngn;
+        const int64_t cb0 = g0 * 3, cb1 = cb0 + 3 * ng;
+        for (int i = warp - 1; i < rows; i += nwarps - 1) {
+          const int64_t r = rn0 + i;
+          const double* wr = s.W + r * s.ldw;
+          double acc = 0.0;
+          for (int64_t cc = lane; cc < c; cc += 32) {
+            if (cc >= cb0 && cc < cb1) continue;
+            acc = fma(wr[cc], sm.lam[cc], acc);
+          }
+          acc = warp_sum(acc);
+          if (lane == 0) {
+            // regularised diagonal of row r (inside block bn, never block b
+            // unless nb == 1, which has no helpers)
+            sm.P[i] = fma(sm.dshift[r / 3], sm.lam[r], acc);
+          }
+        }
+      }
+      __syncthreads();
+      if (sm.flags[0]) break;
+      if (b + 1 == nb) {
+        // ---- end of sweep: epsilon (solver.py:194-199) ----
+        if (warp == 0) {
+          double v = warp_sum(dsq);
+          if (lane == 0) sm.red[0] = v;
+        }
+        double nl = 0.0;
+        for (int64_t i = tid; i < c; i += blockDim.x) nl += sm.lam[i] * sm.lam[i];
+        nl = warp_sum(nl);
+        if (lane == 0) sm.red[1 + warp] = nl;
+        __syncthreads();
+        if (tid == 0) {
+          double den2 = 0.0;
+          for (int w = 0; w < nwarps; ++w) den2 += sm.red[1 + w];
+          const double num = sqrt(sm.red[0]), den = sqrt(den2);
+          const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
+          s.eps_hist[sweep] = eps;
+          sm.flags[1] = (eps <= s.tol) ? 1 : 0;
+        }
+        __syncthreads();
+        if (sm.flags[1]) {
+          converged = true;
+          break;
+        }
+      }
+      // ---- delta for the next block, its diagonal tile ----
+      {
+        const int64_t rn0 = gn0 * 3;
+        const int rows = 3 * ngn;
+        const int64_t cb0 = g0 * 3;
+        const int cols = 3 * ng;
+        for (int i = warp; i < rows; i += nwarps) {
+          const int64_t r = rn0 + i;
+          double acc = 0.0;
+          if (nb > 1) {
+            for (int j = lane; j < cols; j += 32) acc = fma(s.W[r * s.ldw + cb0 + j], sm.lam[cb0 + j], acc);
+          } else {
+            for (int j = lane; j < cols; j += 32) acc = fma(w_reg(s, sm, r, cb0 + j), sm.lam[cb0 + j], acc);
+          }
+          acc = warp_sum(acc);
+          if (lane == 0) sm.dnext[i] = add(s.delta_base[r], mul(h2, (nb > 1 ? sm.P[i] : 0.0) + acc));
+        }
+        if (nb > 1) stage_tile(bn);
+      }
+      __syncthreads();
+    }
+    if (sm.flags[0] || converged) break;
+  }
+  __syncthreads();
+  // ---- delta_end = delta_base + h^2 W_reg lam (solver.py:201) ----
+  for (int64_t r = warp; r < c; r += nwarps) {
+    const double* wr = s.W + r * s.ldw;
+    double acc = 0.0;
+    for (int64_t cc = lane; cc < c; cc += 32) acc = fma(wr[cc], sm.lam[cc], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      acc = fma(sm.dshift[r / 3], sm.lam[r], acc);
+      s.delta_end[r] = add(s.delta_base[r], mul(h2, acc));
+    }
+  }
+  for (int64_t i = tid; i < c; i += blockDim.x) s.lam[i] = sm.lam[i];
+  if (tid == 0) {
+    s.iters_conv[0] = iterations;
+    s.iters_conv[1] = converged ? 1 : 0;
+  }
+}
+
+__host__ __device__ inline size_t pgs_smem_bytes(int64_t groups) {
+  return sizeof(double) * (size_t)(3 * groups + groups + kBR * kBR + 2 * kBR + 32) + 2 * sizeof(int) + 16;
+}
+
+__device__ __forceinline__ PgsSmem carve(char* base, int64_t groups) {
+  PgsSmem sm;
+  double* p = (double*)base;
+  sm.lam = p;
+  p += 3 * groups;
+  sm.dshift = p;
+  p += groups;
+  sm.Wbb = p;
+  p += kBR * kBR;
+  sm.P = p;
+  p += kBR;
+  sm.dnext = p;
+  p += kBR;
+  sm.red = p;
+  p += 32;
+  sm.flags = (int*)p;
+  return sm;
+}
+
+__global__ void __launch_bounds__(kPgsThreads) pgs_single_kernel(PgsScene s) {
+  extern __shared__ __align__(16) char smem[];
+  pgs_cta(s, carve(smem, s.groups));
+}
+
+__global__ void __launch_bounds__(kPgsThreads) pgs_batched_kernel(const PgsScene* scenes) {
+  extern __shared__ __align__(16) char smem[];
+  PgsScene s = scenes[blockIdx.x];
+  pgs_cta(s, carve(smem, s.groups));
+}
+
+__global__ void local_solve_kernel(int64_t alpha, const double* W, int64_t ldw, const double* dc,
+                                   const double* lam, double mu, double h2, double* out,
+                                   DevStatus* st) {
+  const int64_t i = 3 * alpha;
+  double Wd[9], d[3], l[3], o[3];
+  for (int a = 0; a < 3; ++a) {
+    d[a] = dc[i + a];
+    l[a] = lam[i + a];
+    for (int b = 0; b < 3; ++b) Wd[3 * a + b] = W[(i + a) * ldw + i + b];
+  }
+  if (local_solve_dev(d, l, Wd, mu, h2, o)) {
+    raise_status(st, CNB_E_SINGULAR_BLOCK, (int)alpha, Wd[0]);
+    o[0] = o[1] = o[2] = 0.0;
+  }
+  for (int a = 0; a < 3; ++a) out[a] = o[a];
+}
+
+size_t pgs_max_smem() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return (size_t)v;
+}
+
+}  // namespace cnb
+
+using namespace cnb;
+
+extern "C" {
+
+int64_t cnb_pgs_work_bytes(int64_t groups) { (void)groups; return 0; }
+
+int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_base, double h, double mu,
+            double tol, int32_t max_iter, double* lam, double* delta_end, double* eps_hist,
+            int32_t* iters_conv, void* work, cnb_status_t* d_status, void* stream) {
+  (void)work;
+  if (groups < 0 || max_iter < 1) {
+    set_error("pgs: invalid arguments (groups=%lld, max_iter=%d)", (long long)groups, max_iter);
+    return CNB_E_VALIDATION;
+  }
+  if (groups == 0) return CNB_OK;
+  PgsScene s;
+  s.groups = groups;
+  s.W = W;
+  s.ldw = ldw;
+  s.delta_base = delta_base;
+  s.h2 = h * h;
+  s.mu = mu;
+  s.tol = tol;
+  s.max_iter = max_iter;
+  s.lam = lam;
+  s.delta_end = delta_end;
+  s.eps_hist = eps_hist;
+  s.iters_conv = iters_conv;
+  s.status = (DevStatus*)d_status;
+  const size_t smem = pgs_smem_bytes(groups);
+  if (smem > pgs_max_smem()) {
+    set_error("pgs: %lld groups exceed the single-CTA shared-memory budget", (long long)groups);
+    return CNB_E_DIMENSION;
+  }
+  CNB_CUDA(cudaFuncSetAttribute(pgs_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  pgs_single_kernel<<<1, kPgsThreads, smem, (cudaStream_t)stream>>>(s);
+  CNB_LAUNCH_CHECK("pgs_single_kernel");
+  return CNB_OK;
+}
+
+int cnb_local_solve(int64_t alpha, int64_t groups, const double* W, int64_t ldw, const double* delta_cur,
+                    const double* lam, double mu, double h2, double* out, cnb_status_t* d_status,
+                    void* stream) {
+  if (alpha < 0 || alpha >= groups) {
+    set_error("local_solve: group %lld out of range", (long long)alpha);
+    return CNB_E_DIMENSION;
+  }
+  local_solve_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(alpha, W, ldw, delta_cur, lam, mu, h2, out,
+                                                         (DevStatus*)d_status);
+  CNB_LAUNCH_CHECK("local_solve_kernel");
+  return CNB_OK;
+}
+
+}  // extern "C"

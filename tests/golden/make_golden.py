@@ -1,0 +1,230 @@
+"""Generate golden fixtures from the REFERENCE implementation itself.
+
+Run in the build container, where the reference is importable:
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  The fixtures pin the oracle (oracle/cn_oracle.py)
+and the CUDA path to the reference's own outputs; /root/reference is never
+read at test time.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import contactnewton as cn  # noqa: E402  (the reference)
+from contactnewton import collision as rcol  # noqa: E402
+from contactnewton import constraints as rcon  # noqa: E402
+from contactnewton import scene as rsc  # noqa: E402
+from contactnewton import solver as rsol  # noqa: E402
+
+from paper_2306_06946_b200.mesh import five_tet_grid  # noqa: E402  (shared input generator)
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+def random_frame(rng):
+    n = rng.standard_normal(3)
+    n /= np.linalg.norm(n)
+    t1 = np.cross(n, rng.standard_normal(3))
+    t1 /= np.linalg.norm(t1)
+    return rcol.ContactFrame(n=n, t1=t1, t2=np.cross(n, t1))
+
+
+def kat_rebuild():
+    rng = np.random.default_rng(100)
+    out = {}
+    for k, groups in enumerate((1, 7, 40)):
+        c = 3 * groups
+        B = rng.standard_normal((c, c))
+        wg = B @ B.T / c + np.eye(c)
+        frames = [random_frame(rng) for _ in range(groups)]
+        D = rcon.assemble_direction(frames)
+        W = rcon.rebuild_W_fast(D, rcon.MappingDelassus(wg, {0: wg})).W
+        out[f"wg{k}"], out[f"D{k}"], out[f"W{k}"] = wg, D.blocks, W
+        p_a, p_b = rng.standard_normal((groups, 3)), rng.standard_normal((groups, 3))
+        out[f"pa{k}"], out[f"pb{k}"] = p_a, p_b
+        out[f"delta{k}"] = rcon.compute_violation(D, p_a, p_b).delta
+        lam = rng.standard_normal(c)
+        out[f"lam{k}"], out[f"dt{k}"] = lam, D.apply_transposed(lam)
+    A = rng.standard_normal((5, 4))
+    Bm = rng.standard_normal((6, 4))
+    out["gA"], out["gB"] = A, Bm
+    out["gC"] = cn.gemm(A, Bm, transpose_b=True)
+    save("kat_rebuild.npz", **out)
+
+
+def kat_pgs():
+    rng = np.random.default_rng(200)
+    cases = []
+    # (groups, mu, tol, max_iter, cond-ish)
+    specs = [(1, 0.0, 1e-6, 30), (3, 0.4, 1e-6, 200), (5, 0.5, 1e-10, 1000), (33, 0.5, 1e-10, 500),
+             (70, 0.3, 1e-8, 300), (70, 0.0, 1e-12, 2000), (100, 0.8, 1e-6, 30)]
+    out = {}
+    for k, (G, mu, tol, it) in enumerate(specs):
+        c = 3 * G
+        B = rng.standard_normal((c, c + 4))
+        W = B @ B.T / c + 0.05 * np.eye(c)
+        delta = rng.uniform(-0.02, 0.01, c)
+        res = rsol.pgs(W, delta, 0.01, rsol.PgsConfig(max_iterations=it, tolerance=tol, friction=mu))
+        out.update({f"W{k}": W, f"delta{k}": delta, f"lam{k}": res.lam, f"dend{k}": res.delta_end,
+                    f"eps{k}": np.array(res.eps_history), f"it{k}": res.iterations,
+                    f"conv{k}": res.converged, f"cfg{k}": np.array([mu, tol, it])})
+    # duplicated contact -> regularisation path (test_solver.py:215-226 shape)
+    W1 = np.eye(3)
+    W = np.block([[W1, W1], [W1, W1]])
+    delta = np.array([-0.01, 0, 0, -0.01, 0, 0.0])
+    res = rsol.pgs(W, delta, 0.01, rsol.PgsConfig(max_iterations=300, tolerance=1e-10))
+    k = len(specs)
+    out.update({f"W{k}": W, f"delta{k}": delta, f"lam{k}": res.lam, f"dend{k}": res.delta_end,
+                f"eps{k}": np.array(res.eps_history), f"it{k}": res.iterations,
+                f"conv{k}": res.converged, f"cfg{k}": np.array([0.5, 1e-10, 300])})
+    out["n"] = len(specs) + 1
+    save("kat_pgs.npz", **out)
+
+
+def kat_frames():
+    rng = np.random.default_rng(300)
+    m = 64
+    p_b = rng.standard_normal((m, 3))
+    d = rng.standard_normal((m, 3)) * 1e-3
+    d[3] = 0.0  # coincident -> element normal fallback
+    d[5] = np.array([0.0, 0.0, 1e-3])  # normal along z (tangent fallback axis)
+    d[7] = np.array([1e-3, 0.0, 0.0])  # normal along x -> e_z fallback for t1
+    ref = rng.standard_normal((m, 3))
+    ref /= np.linalg.norm(ref, axis=1, keepdims=True)
+    ref[7] = np.array([1.0, 0.0, 0.0])
+    p_a = p_b + d
+    pairs = [rcol.ProximityPair(0, 1, None, None, p_a[i], p_b[i], ref[i], 0.0, i, -1) for i in range(m)]
+    frames = rcol.build_frames(pairs)
+    F = np.stack([f.as_matrix() for f in frames])
+    # relinearise: small motions, one collapse, one > 60 degree tilt
+    p_a2 = p_a + rng.standard_normal((m, 3)) * 2e-4
+    p_a2[10] = p_b[10]
+    p_a2[11] = p_b[11] + 1e-3 * np.cross(F[11, 0], F[11, 1])  # 90 degrees away
+    new = rcol.relinearize(pairs, p_a2, p_b, frames)
+    rot = rcol.max_frame_rotation(frames, new)
+    save("kat_frames.npz", p_a=p_a, p_b=p_b, ref=ref, frames=F, p_a2=p_a2,
+         frames2=np.stack([f.as_matrix() for f in new]), rotation=rot)
+
+
+def _run_scene(config, steps, capture_steps, jitter_seed=None, tag=""):
+    sim = rsc.Simulation(config)
+    if jitter_seed is not None:
+        rng = np.random.default_rng(jitter_seed)
+        for obj in sim.dynamic_objects:
+            obj.state.q = obj.state.q + rng.uniform(-1e-4, 1e-4, obj.state.q.shape)
+    out = {}
+    for s in range(steps):
+        if s in capture_steps:
+            ctx, free, states, pen_before, timings, t_next = sim.prepare_step(build_wg=True)
+            res = rsol.newton_fast(ctx, config.newton, config.pgs)
+            keys = np.array([(p.object_a, p.object_b, p.vertex_id, p.element_id) for p in ctx.pairs],
+                            dtype=np.int64).reshape(-1, 4)
+            out[f"s{s}_keys"] = keys
+            out[f"s{s}_frames"] = np.stack([f.as_matrix() for f in ctx.detection_frames]) if ctx.pairs \
+                else np.zeros((0, 3, 3))
+            out[f"s{s}_pa0"], out[f"s{s}_pb0"] = ctx.p_a0, ctx.p_b0
+            if ctx.pairs:
+                out[f"s{s}_wg"] = ctx.wg.wg
+                for oid, U in ctx.wg.per_object.items():
+                    out[f"s{s}_U{oid}"] = U
+                out[f"s{s}_lamhist"] = np.stack(res.lam_history) if res.lam_history else np.zeros((0, 0))
+                out[f"s{s}_acc"] = res.state.accumulated
+                out[f"s{s}_final_frames"] = np.stack([f.as_matrix() for f in res.final_frames])
+                for oid, dv in res.dv_by_object.items():
+                    out[f"s{s}_dv{oid}"] = dv
+                out[f"s{s}_sweeps"] = np.array([it.pgs_iterations for it in res.iterations])
+                out[f"s{s}_rot"] = np.array([it.rotation for it in res.iterations])
+            for obj in sim.dynamic_objects:
+                out[f"s{s}_qfree{obj.oid}"] = free[obj.oid].q_free
+            out[f"s{s}_pen_before"] = pen_before
+        rep = sim.step()
+        out[f"s{s}_npairs"] = rep.c_groups
+        out[f"s{s}_newton"] = rep.newton_iterations
+        out[f"s{s}_pen_after"] = rep.pen_after
+        for obj in sim.dynamic_objects:
+            out[f"s{s}_q{obj.oid}"] = obj.state.q.copy()
+            out[f"s{s}_v{obj.oid}"] = obj.state.v.copy()
+        print(tag, "step", s, "pairs", rep.c_groups, "newton", rep.newton_iterations,
+              "pgs", rep.pgs_iterations_total, "pen_after", rep.pen_after)
+    return out
+
+
+def beam_cfg0(steps=10, drop=0.02):
+    """BASELINE cfg0: 20x4x4-node 5-tet beam over a 10-degree plane."""
+    ang = np.deg2rad(10.0)
+    normal = np.array([np.sin(ang), np.cos(ang), 0.0])
+    y0 = drop / normal[1]
+    mesh = five_tet_grid((20, 4, 4), 0.01, (0.0, y0, 0.0))
+    soft = rsc.SoftSpec(name="beam", mesh=cn.TetMesh(mesh.nodes, mesh.tets), young=5e3, poisson=0.45,
+                        density=1000.0, rayleigh_mass=0.1, rayleigh_stiffness=0.1)
+    plane = rsc.PlaneSpec(name="ground", normal=tuple(normal), offset=0.0)
+    cfg = rsc.SceneConfig(objects=[soft, plane], h=0.01, threshold=0.005,
+                          pgs=rsol.PgsConfig(max_iterations=1000, tolerance=1e-10, friction=0.5),
+                          newton=rsol.NewtonConfig(scheme="fast", max_iterations=5, penetration_tol=-1,
+                                                   rotation_tol=-1),
+                          output=rsc.OutputConfig(snapshots=False, metrics=False))
+    return cfg, mesh
+
+
+def scenes():
+    # cfg0 beam, started 2 mm above the plane so contacts appear in step 1
+    cfg, mesh = beam_cfg0(drop=0.002)
+    out = _run_scene(cfg, 6, {2, 4}, jitter_seed=0, tag="beam")
+    out.update(nodes=mesh.nodes, tets=mesh.tets, normal=np.array(cfg.objects[1].normal))
+    save("beam_cfg0.npz", **out)
+    # reference fixtures, forced fast scheme
+    ref_scenes = "/root/reference/pkg/scenes"
+    for name, steps, cap in (("block_on_plane", 3, {0, 2}), ("two_body_press", 2, {0, 1})):
+        cfg = rsc.load_scene(os.path.join(ref_scenes, name + ".scn"))
+        from dataclasses import replace
+
+        cfg = replace(cfg, newton=replace(cfg.newton, scheme="fast", max_iterations=4,
+                                          penetration_tol=-1.0, rotation_tol=-1.0),
+                      pgs=replace(cfg.pgs, max_iterations=300, tolerance=1e-10),
+                      output=rsc.OutputConfig(snapshots=False, metrics=False))
+        out = _run_scene(cfg, steps, cap, tag=name)
+        for obj in rsc.Simulation(cfg).dynamic_objects:
+            out[f"mesh{obj.oid}_nodes"] = obj.spec.mesh.nodes
+            out[f"mesh{obj.oid}_tets"] = obj.spec.mesh.tets
+            out[f"mat{obj.oid}"] = np.array([obj.spec.young, obj.spec.poisson, obj.spec.density,
+                                             obj.spec.rayleigh_mass, obj.spec.rayleigh_stiffness])
+            out[f"vel{obj.oid}"] = np.array(obj.spec.velocity)
+        save(f"{name}.npz", **out)
+
+
+def kat_linalg():
+    rng = np.random.default_rng(400)
+    mesh = cn.box_mesh((0.1, 0.1, 0.1), (2, 2, 2), (0.0, 0.05, 0.0))
+    body = cn.SoftBody(mesh, young=5e4, poisson=0.3, fixed_nodes=np.array([0, 1, 2]))
+    st = body.initial_state((0.1, -0.2, 0.0))
+    A, b = body.assemble(st, 0.01, (0.0, -9.81, 0.0))
+    F = cn.factorize(A)
+    x = F.solve(b)
+    B = rng.standard_normal((A.dim, 5))
+    X = F.solve_multi(B)
+    csr = A.csr
+    K = body.stiffness()
+    save("kat_linalg.npz", nodes=mesh.nodes, tets=mesh.tets, indptr=csr.indptr, indices=csr.indices,
+         data=csr.data, b=b, x=x, B=B, X=X, q=st.q, v=st.v, K_indptr=K.indptr, K_indices=K.indices,
+         K_data=K.data, masses=body.masses())
+
+
+if __name__ == "__main__":
+    kat_rebuild()
+    kat_pgs()
+    kat_frames()
+    kat_linalg()
+    scenes()
