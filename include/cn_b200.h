@@ -96,6 +96,24 @@ int cnb_build_frames(int64_t pairs, const double* p_a, const double* p_b,
 int cnb_relinearize(int64_t pairs, const double* p_a, const double* p_b,
                     const double* prev, double* frames, double* rotation, void* stream);
 
+/* Proximity positions of both sides of every pair, p = g(q).  Replaces
+ * refresh_proximity / attachment_point collision.py:497-520.
+ * Pair table: kind, obj (m x 2), node (m x 2 x 3, int64), w, local, world
+ * (m x 2 x 3); views: device array of per-object node-coordinate pointers
+ * (deformable objects); poses: per-object R (9, row-major) + t (3). */
+int cnb_refresh_proximity(int64_t m, const int8_t* kind, const int32_t* obj, const int64_t* node,
+                          const double* w, const double* local, const double* world,
+                          const double* const* views, const double* poses, double* p_a, double* p_b,
+                          void* stream);
+
+/* Signed gaps along the current supporting-element normal and
+ * pen = max(0, -min gap) (pen[0]).  Replaces signed_gaps collision.py:523-548
+ * and the pen_before/pen_after reductions scene.py:658-662,713-718. */
+int cnb_signed_gaps(int64_t m, const int8_t* kind, const int32_t* obj, const int64_t* node, const double* w,
+                    const double* local, const double* world, const double* lnormal, const int8_t* has_ln,
+                    const double* ref_normal, const double* const* views, const double* poses, double* gaps,
+                    double* pen, void* stream);
+
 /* ---- projected Gauss-Seidel (contactnewton/solver.py) -------------------- */
 
 /* Workspace bytes needed by cnb_pgs for c = 3*groups rows. */
@@ -117,6 +135,53 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
 int cnb_local_solve(int64_t alpha, int64_t groups, const double* W, int64_t ldw,
                     const double* delta_cur, const double* lam, double mu, double h2,
                     double* out, cnb_status_t* d_status, void* stream);
+
+/* ---- sparse Cholesky (contactnewton/linalg.py:58-118) -------------------- */
+
+typedef struct cnb_chol_opaque* cnb_chol_t;
+
+/* Host-only symbolic analysis of a symmetric CSR pattern (host arrays, both
+ * triangles): nested-dissection ordering (geometric when coords != NULL,
+ * n/bs x 3 node coordinates), elimination tree, supernodes, fronts.
+ * Replaces the ordering/symbolic part of Factorization.__init__
+ * linalg.py:68-76 (SuperLU MMD_AT_PLUS_A). */
+int cnb_chol_analyze(int64_t n, const int64_t* rowptr, const int64_t* col, int32_t bs,
+                     const double* coords, int32_t leaf_nodes, cnb_chol_t* out);
+int cnb_chol_destroy(cnb_chol_t h);
+/* info[7] = {n, supernodes, nnz(L), front doubles, levels, csr nnz, bs};
+ * flops[2] = {factorisation flops, solve flops per right-hand side}. */
+int cnb_chol_info(cnb_chol_t h, int64_t* info, double* flops);
+/* Copy a named host array of the symbolic structure (tests / tooling). */
+int64_t cnb_chol_export_bytes(cnb_chol_t h, const char* name);
+int cnb_chol_export(cnb_chol_t h, const char* name, void* dst);
+
+/* Numeric factorisation on the device from CSR values (device, same pattern
+ * as analysed).  A non-positive pivot sets d_status to CNB_E_NOT_SPD, as the
+ * reference's pivot check (linalg.py:77-84). */
+int cnb_chol_factor(cnb_chol_t h, const double* vals, cnb_status_t* d_status, void* stream);
+
+/* X = A^{-1} B for k right-hand sides stored as k contiguous length-n
+ * vectors (leading dimensions ldb/ldx); X may alias B.  Replaces
+ * Factorization.solve / solve_multi linalg.py:89-106. */
+int cnb_chol_solve(cnb_chol_t h, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t k,
+                   void* stream);
+
+/* Mapping compliance of one object, U = S A^{-1} S^T (ncols x ncols, row-major
+ * device output) for the ncols right-hand-side columns of S^T given in host
+ * CSC form (colptr, rowidx = DoF ids, vals).  Y = L^{-1} P S^T is formed only
+ * on the elimination paths of the columns and U = Y^T Y by fp64 MMA tiles.
+ * Replaces solve_multi(S^T) + S @ X of assemble_Wg constraints.py:175-178.
+ * flops_out (host, may be NULL) = {forward-solve flops, Gram flops}. */
+int cnb_chol_compliance(cnb_chol_t h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
+                        const double* vals, double* U, int64_t ldu, double* flops_out, void* stream);
+
+/* ---- sparse products ----------------------------------------------------- */
+
+/* y = alpha A x, A in CSR (device), one row per thread in column order.
+ * Used for S^T t of _mechanical_correction solver.py:250-257 and the
+ * stiffness products of SoftBody.assemble dynamics.py:202-208. */
+int cnb_csr_spmv(int64_t rows, const int64_t* rowptr, const int64_t* col, const double* val,
+                 const double* x, double* y, double alpha, void* stream);
 
 /* ---- dense products (contactnewton/linalg.py) ---------------------------- */
 

@@ -1,0 +1,43 @@
+"""Device-array helpers shared by the API modules."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def device() -> torch.device:
+    return _lib.require_cuda()
+
+
+def f64(x, dev=None) -> torch.Tensor:
+    """Contiguous fp64 CUDA tensor view/copy of an array-like."""
+    dev = dev or device()
+    if isinstance(x, torch.Tensor):
+        if x.device != dev or x.dtype != torch.float64:
+            x = x.to(device=dev, dtype=torch.float64)
+        return x.contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=dev)
+
+
+def i64(x, dev=None) -> torch.Tensor:
+    dev = dev or device()
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=torch.int64).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int64), device=dev)
+
+
+def host(x) -> np.ndarray:
+    if isinstance(x, torch.Tensor):
+        return x.detach().cpu().numpy()
+    return np.asarray(x)
+
+
+def empty(shape, dev=None, dtype=torch.float64) -> torch.Tensor:
+    return torch.empty(shape, dtype=dtype, device=dev or device())
+
+
+def zeros(shape, dev=None, dtype=torch.float64) -> torch.Tensor:
+    return torch.zeros(shape, dtype=dtype, device=dev or device())

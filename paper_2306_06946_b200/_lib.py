@@ -33,14 +33,26 @@ _SIGNATURES: dict[str, list] = {
     "cnb_prox_update": [I64, P, I64, P, P, P, F64, P, P, P],
     "cnb_build_frames": [I64, P, P, P, P, P, P],
     "cnb_relinearize": [I64, P, P, P, P, P, P],
+    "cnb_refresh_proximity": [I64, P, P, P, P, P, P, P, P, P, P, P],
+    "cnb_signed_gaps": [I64, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "cnb_pgs_work_bytes": [I64],
     "cnb_pgs": [I64, P, I64, P, F64, F64, F64, I32, P, P, P, P, P, P, P],
     "cnb_local_solve": [I64, I64, P, I64, P, P, F64, F64, P, P, P],
     "cnb_gemm_naive": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, P],
+    "cnb_csr_spmv": [I64, P, P, P, P, P, F64, P],
+    "cnb_chol_analyze": [I64, P, P, I32, P, I32, P],
+    "cnb_chol_destroy": [P],
+    "cnb_chol_info": [P, P, P],
+    "cnb_chol_export_bytes": [P, ctypes.c_char_p],
+    "cnb_chol_export": [P, ctypes.c_char_p, P],
+    "cnb_chol_factor": [P, P, P, P],
+    "cnb_chol_solve": [P, P, I64, P, I64, I64, P],
+    "cnb_chol_compliance": [P, I64, P, P, P, P, I64, P, P],
 }
 _RESTYPES = {
     "cnb_last_error": ctypes.c_char_p,
     "cnb_pgs_work_bytes": I64,
+    "cnb_chol_export_bytes": I64,
 }
 
 STATUS_ERRORS = {

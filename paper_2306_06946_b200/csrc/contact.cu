@@ -297,6 +297,19 @@ __global__ void gemm_naive_kernel(int64_t m, int64_t n, int64_t k, const double*
   C[i * ldc + j] = s;
 }
 
+// y = alpha * A x for a CSR matrix, one thread per row, entries summed in
+// column order (deterministic).  Used for S^T t of the mechanical correction
+// (solver.py:250-257) and the stiffness products of the RHS assembly.
+__global__ void csr_spmv_kernel(int64_t rows, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
+                                const double* __restrict__ va, const double* __restrict__ x,
+                                double* __restrict__ y, double alpha) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double s = 0.0;
+  for (int64_t e = rp[r]; e < rp[r + 1]; ++e) s = fma(va[e], x[ci[e]], s);
+  y[r] = alpha == 1.0 ? s : alpha * s;
+}
+
 static void split_rows(int64_t rows, dim3& grid, int64_t cols_blocks) {
   // rows across y (<= 65535) and z
   int64_t gy = rows < 65535 ? rows : 65535;
@@ -371,6 +384,14 @@ int cnb_relinearize(int64_t pairs, const double* p_a, const double* p_b, const d
   relinearize_kernel<<<grid_for(pairs, 128), 128, 0, (cudaStream_t)stream>>>(
       pairs, p_a, p_b, prev, frames, (unsigned long long*)rotation);
   CNB_LAUNCH_CHECK("relinearize_kernel");
+  return CNB_OK;
+}
+
+int cnb_csr_spmv(int64_t rows, const int64_t* rowptr, const int64_t* col, const double* val, const double* x,
+                 double* y, double alpha, void* stream) {
+  if (rows <= 0) return CNB_OK;
+  csr_spmv_kernel<<<grid_for(rows, 128), 128, 0, (cudaStream_t)stream>>>(rows, rowptr, col, val, x, y, alpha);
+  CNB_LAUNCH_CHECK("csr_spmv_kernel");
   return CNB_OK;
 }
 
