@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(256) rebuild_w_kernel(int64_t groups, const do
   }
 }
 
-// delta_g = D_g (p_a[g] - p_b[g])   (einsum "gij,gj->gi", constraints.py:58-60)
+// delta_g = D_g (p_a[g] - p_b[g])   (einsum "gij,gj->gi", constraints.py:58-60).
+// numpy's einsum contracts a contiguous length-3 index as (x0 y0 + x2 y2) + x1 y1
+// (checked bit-for-bit against the reference's outputs, tests/golden).
 __global__ void violation_kernel(int64_t groups, const double* __restrict__ D,
                                  const double* __restrict__ pa, const double* __restrict__ pb,
                                  double* __restrict__ delta) {
@@ -98,9 +100,8 @@ __global__ void violation_kernel(int64_t groups, const double* __restrict__ D,
   const double* d = D + 9 * g;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    double s = mul(d[3 * i + 0], r0);
+    double s = add(mul(d[3 * i + 0], r0), mul(d[3 * i + 2], r2));
     s = add(s, mul(d[3 * i + 1], r1));
-    s = add(s, mul(d[3 * i + 2], r2));
     delta[3 * g + i] = s;
   }
 }
