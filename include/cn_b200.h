@@ -148,7 +148,7 @@ typedef struct cnb_chol_opaque* cnb_chol_t;
 int cnb_chol_analyze(int64_t n, const int64_t* rowptr, const int64_t* col, int32_t bs,
                      const double* coords, int32_t leaf_nodes, cnb_chol_t* out);
 int cnb_chol_destroy(cnb_chol_t h);
-/* info[7] = {n, supernodes, nnz(L), front doubles, levels, csr nnz, bs};
+/* info[9] = {n, supernodes, nnz(L), front doubles, levels, csr nnz, bs, launches per factorisation, launches per solve};
  * flops[2] = {factorisation flops, solve flops per right-hand side}. */
 int cnb_chol_info(cnb_chol_t h, int64_t* info, double* flops);
 /* Copy a named host array of the symbolic structure (tests / tooling). */
@@ -175,6 +175,29 @@ int cnb_chol_solve(cnb_chol_t h, const double* B, int64_t ldb, double* X, int64_
 int cnb_chol_compliance(cnb_chol_t h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
                         const double* vals, double* U, int64_t ldu, double* flops_out, void* stream);
 
+/* ---- FE assembly (contactnewton/dynamics.py) ------------------------------ */
+
+/* One thread per tet: the 16 (rotated) 3x3 stiffness blocks Kb (tets x 16 x 9)
+ * and the 4 element elastic forces fe (tets x 4 x 3) at positions x.
+ * corot = 0: linear material, K_e from rest gradients, fe = K_e (x - x0)
+ * (dynamics.py:81-99,172-177); corot = 1: R_e = polar(F), R K_e R^T and
+ * R K_e (R^T x - x0).  R (tets x 9, may be NULL) receives the rotations. */
+int cnb_fe_element(int64_t ntets, const int64_t* tets, const double* grads, const double* vol, const double* x,
+                   const double* x0, double lam, double mu, int32_t corot, double* Kb, double* fe, double* R,
+                   void* stream);
+/* Deterministic gathers: global 3x3 blocks into DoF-CSR values (dst = CSR
+ * index of each block row's first entry) and nodal elastic forces. */
+int cnb_fe_gather(int64_t nblocks, const int64_t* cptr, const int64_t* contrib, const double* Kb, const int64_t* dst,
+                  double* vals, int64_t nnodes, const int64_t* fptr, const int64_t* fidx, const double* fe,
+                  double* f, void* stream);
+/* A = (1 + h alpha) M + (h beta + h^2) K with fixed rows/cols -> identity and
+ * b = h (f_ext - f_el - alpha M v - beta K v) - h^2 K v, b[fixed] = 0
+ * (SoftBody.assemble dynamics.py:183-211); non-finite b -> CNB_E_NONFINITE. */
+int cnb_fe_system(int64_t n, const int64_t* rowptr, const int64_t* col, const double* Kvals, const double* m3,
+                  const int8_t* fixed, double h, double alpha, double beta, const double* fel, const double* Kv,
+                  const double* v, const double* fext, double* Avals, double* b, cnb_status_t* d_status,
+                  void* stream);
+
 /* ---- sparse products ----------------------------------------------------- */
 
 /* y = alpha A x, A in CSR (device), one row per thread in column order.
@@ -182,6 +205,14 @@ int cnb_chol_compliance(cnb_chol_t h, int64_t ncols, const int64_t* colptr, cons
  * stiffness products of SoftBody.assemble dynamics.py:202-208. */
 int cnb_csr_spmv(int64_t rows, const int64_t* rowptr, const int64_t* col, const double* val,
                  const double* x, double* y, double alpha, void* stream);
+
+/* ---- tooling --------------------------------------------------------------- */
+
+/* Number of kernels this library has launched in the process so far. */
+long long cnb_launch_count(void);
+
+/* fp64 MMA (DMMA) throughput of the whole GPU in TFLOP/s (out: host). */
+int cnb_bench_dmma(int32_t iters, double* out, void* stream);
 
 /* ---- dense products (contactnewton/linalg.py) ---------------------------- */
 

@@ -61,4 +61,30 @@ from .solver import (
     regularize,
 )
 
+from .dynamics import (
+    FreeMotion,
+    MechanicalState,
+    SoftBody,
+    compute_free_motion,
+    integrate_correction,
+    lame_parameters,
+    lumped_masses,
+)
+from .scene import (
+    KinematicMeshSpec,
+    MotionSpec,
+    OutputConfig,
+    PlaneSpec,
+    SceneConfig,
+    Simulation,
+    Snapshot,
+    SoftSpec,
+    StepReport,
+    load_scene,
+    load_snapshot,
+    run,
+    save_snapshot,
+    take_snapshot,
+)
+
 __version__ = "0.1.0"

@@ -40,6 +40,9 @@ _SIGNATURES: dict[str, list] = {
     "cnb_local_solve": [I64, I64, P, I64, P, P, F64, F64, P, P, P],
     "cnb_gemm_naive": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, P],
     "cnb_csr_spmv": [I64, P, P, P, P, P, F64, P],
+    "cnb_fe_element": [I64, P, P, P, P, P, F64, F64, I32, P, P, P, P],
+    "cnb_fe_gather": [I64, P, P, P, P, P, I64, P, P, P, P, P],
+    "cnb_fe_system": [I64, P, P, P, P, P, F64, F64, F64, P, P, P, P, P, P, P, P],
     "cnb_chol_analyze": [I64, P, P, I32, P, I32, P],
     "cnb_chol_destroy": [P],
     "cnb_chol_info": [P, P, P],
@@ -48,8 +51,11 @@ _SIGNATURES: dict[str, list] = {
     "cnb_chol_factor": [P, P, P, P],
     "cnb_chol_solve": [P, P, I64, P, I64, I64, P],
     "cnb_chol_compliance": [P, I64, P, P, P, P, I64, P, P],
+    "cnb_bench_dmma": [I32, P, P],
+    "cnb_launch_count": [],
 }
 _RESTYPES = {
+    "cnb_launch_count": ctypes.c_longlong,
     "cnb_last_error": ctypes.c_char_p,
     "cnb_pgs_work_bytes": I64,
     "cnb_chol_export_bytes": I64,

@@ -819,6 +819,15 @@ int cnb_chol_info(cnb_chol_t hh, int64_t* info, double* fl) {
   info[4] = S.n_levels;
   info[5] = S.csr_nnz;
   info[6] = S.bs;
+  // kernel launches of one numeric factorisation and of one solve (k <= 64)
+  int64_t fl_launch = 1 + (S.map_src.empty() ? 0 : 1);
+  for (const LevelTasks& T : S.tasks) {
+    fl_launch += T.ea.empty() ? 0 : 1;
+    for (size_t p = 0; p < T.potrf.size(); ++p)
+      fl_launch += (T.potrf[p].empty() ? 0 : 1) + (T.trsm[p].empty() ? 0 : 1) + (T.syrk[p].empty() ? 0 : 1);
+  }
+  info[7] = fl_launch;
+  info[8] = 2 + 2 * (int64_t)S.n_levels;
   fl[0] = S.flops;
   fl[1] = S.solve_flops_per_rhs;
   return CNB_OK;

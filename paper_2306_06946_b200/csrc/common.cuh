@@ -22,8 +22,12 @@ int cuda_status(cudaError_t e, const char* where);
     if (_e != cudaSuccess) return ::cnb::cuda_status(_e, #call);               \
   } while (0)
 
+// Every kernel launch is followed by this check; it also counts launches
+// (cnb_launch_count) so benchmarks report how many of our kernels ran.
+void count_launch();
 #define CNB_LAUNCH_CHECK(where)                                                \
   do {                                                                         \
+    ::cnb::count_launch();                                                     \
     cudaError_t _e = cudaGetLastError();                                       \
     if (_e != cudaSuccess) return ::cnb::cuda_status(_e, where);               \
   } while (0)

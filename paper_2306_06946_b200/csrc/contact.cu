@@ -8,6 +8,7 @@
 //   fast_update_proximity constraints.py:217-244
 //   build_frames / _frame_from_direction / _tangents  collision.py:351-375
 //   relinearize / max_frame_rotation                 collision.py:381-414
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 
@@ -16,6 +17,9 @@
 namespace cnb {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -325,6 +329,8 @@ using namespace cnb;
 extern "C" {
 
 int cnb_abi_version(void) { return 1; }
+
+long long cnb_launch_count(void) { return g_launches.load(); }
 
 const char* cnb_last_error(void) { return g_last_error.c_str(); }
 

@@ -118,7 +118,7 @@ class Factorization:
             coords.ctypes.data if coords is not None else None, int(leaf_nodes), ctypes.byref(handle)),
             "chol_analyze")
         self._h = handle
-        info = (ctypes.c_int64 * 7)()
+        info = (ctypes.c_int64 * 9)()
         fl = (ctypes.c_double * 2)()
         _lib.call("cnb_chol_info", self._h, info, fl)
         self.n_supernodes = int(info[1])

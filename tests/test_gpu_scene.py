@@ -1,0 +1,115 @@
+"""Scene-level GPU parity: whole fast-scheme steps through Simulation.step against
+trajectories produced by the reference (tests/golden), plus the corotational
+material's own checks (reduction to linear, rigid-rotation invariance)."""
+
+import numpy as np
+import pytest
+import torch
+
+import cn_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cn():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2306_06946_b200 as m
+
+    return m
+
+
+def _h(x):
+    return x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
+def _config(cn, g, n_obj, threshold, newton_iter, pgs_iter, pgs_tol, normal=(0.0, 1.0, 0.0), material="linear"):
+    objs = []
+    for o in range(n_obj):
+        E, nu, rho, a, b = g[f"mat{o}"]
+        objs.append(cn.SoftSpec(name=f"b{o}", mesh=cn.TetMesh(g[f"mesh{o}_nodes"], g[f"mesh{o}_tets"]), young=E,
+                                poisson=nu, density=rho, rayleigh_mass=a, rayleigh_stiffness=b,
+                                velocity=tuple(g[f"vel{o}"]), material=material))
+    objs.append(cn.PlaneSpec(name="ground", normal=normal, offset=0.0))
+    return cn.SceneConfig(objects=objs, threshold=threshold,
+                          pgs=cn.PgsConfig(max_iterations=pgs_iter, tolerance=pgs_tol, friction=0.5),
+                          newton=cn.NewtonConfig(scheme="fast", max_iterations=newton_iter, penetration_tol=-1.0,
+                                                 rotation_tol=-1.0),
+                          output=cn.OutputConfig(snapshots=False, metrics=False))
+
+
+def _run_and_compare(sim, g, steps, n_obj, tol_q=1e-6):
+    for s in range(steps):
+        rep = sim.step()
+        assert rep.c_groups == int(g[f"s{s}_npairs"])
+        if f"s{s}_keys" in g and rep.c_groups:
+            keys = np.array([(p.object_a, p.object_b, p.vertex_id, p.element_id) for p in sim.last_pairs])
+            assert np.array_equal(keys, g[f"s{s}_keys"])  # bit-exact integers
+            lh = torch.stack(sim.last_result.lam_history)
+            ref = g[f"s{s}_lamhist"]
+            assert np.abs(_h(lh) - ref).max() <= 1e-6 * max(np.abs(ref).max(), 1e-300)
+        assert rep.newton_iterations == int(g[f"s{s}_newton"])
+        for o in range(n_obj):
+            q = g[f"s{s}_q{o}"]
+            qo = _h(sim.objects[o].state.q)
+            assert np.abs(qo - q).max() <= tol_q * np.abs(q).max(), (s, o, np.abs(qo - q).max())
+
+
+def test_block_on_plane_steps(cn, golden):
+    g = golden("block_on_plane.npz")
+    sim = cn.Simulation(_config(cn, g, 1, 0.01, 4, 300, 1e-10))
+    _run_and_compare(sim, g, 3, 1)
+
+
+def test_two_body_press_steps(cn, golden):
+    g = golden("two_body_press.npz")
+    sim = cn.Simulation(_config(cn, g, 2, 0.01, 4, 300, 1e-10))
+    _run_and_compare(sim, g, 2, 2)
+
+
+def test_beam_cfg0_steps(cn, golden):
+    g = golden("beam_cfg0.npz")
+    mesh = cn.TetMesh(g["nodes"], g["tets"])
+    cfg = cn.SceneConfig(
+        objects=[cn.SoftSpec(name="beam", mesh=mesh, young=5e3, poisson=0.45, density=1000.0),
+                 cn.PlaneSpec(name="ground", normal=tuple(g["normal"]), offset=0.0)],
+        threshold=0.005, pgs=cn.PgsConfig(1000, 1e-10, 0.5),
+        newton=cn.NewtonConfig(scheme="fast", max_iterations=5, penetration_tol=-1.0, rotation_tol=-1.0),
+        output=cn.OutputConfig(snapshots=False, metrics=False))
+    sim = cn.Simulation(cfg)
+    rng = np.random.default_rng(0)
+    st = sim.objects[0].state
+    sim.objects[0].state = cn.MechanicalState(_h(st.q) + rng.uniform(-1e-4, 1e-4, st.q.shape[0]), st.v)
+    _run_and_compare(sim, g, 6, 1)
+
+
+def test_corotational_reduces_to_linear_at_rest(cn):
+    mesh = cn.five_tet_grid((4, 3, 3), 0.01)
+    lin = cn.SoftBody(mesh, young=5e3, poisson=0.45, material="linear")
+    cor = cn.SoftBody(mesh, young=5e3, poisson=0.45, material="corotational")
+    st = lin.initial_state((0.1, -0.2, 0.05))
+    A1, b1 = lin.assemble(st, 0.01, (0, -9.81, 0))
+    A2, b2 = cor.assemble(st, 0.01, (0, -9.81, 0))
+    assert np.abs(_h(A1.values) - _h(A2.values)).max() <= 1e-12 * np.abs(_h(A1.values)).max()
+    assert np.abs(_h(b1) - _h(b2)).max() <= 1e-12 * np.abs(_h(b1)).max()
+    # linear material against the CPU oracle (reference formulas)
+    body = orc.Body(mesh.nodes, mesh.tets, young=5e3, poisson=0.45)
+    Ao, bo = body.system(_h(st.q), _h(st.v), 0.01, (0, -9.81, 0))
+    assert np.abs(_h(b1) - bo).max() <= 1e-12 * np.abs(bo).max()
+    A1h = A1.csr.toarray()
+    assert np.abs(A1h - Ao.toarray()).max() <= 1e-12 * np.abs(Ao.data).max()
+
+
+def test_corotational_rigid_rotation_has_no_elastic_force(cn):
+    mesh = cn.five_tet_grid((4, 3, 3), 0.01)
+    cor = cn.SoftBody(mesh, young=5e3, poisson=0.45, rayleigh_mass=0.0, rayleigh_stiffness=0.0,
+                      material="corotational")
+    ang = 0.7
+    R = np.array([[np.cos(ang), -np.sin(ang), 0], [np.sin(ang), np.cos(ang), 0], [0, 0, 1.0]])
+    q = (mesh.nodes @ R.T + np.array([0.1, 0.2, 0.3])).ravel()
+    f = _h(cor.internal_force(q, np.zeros_like(q)))
+    assert np.abs(f).max() <= 1e-9
+    # K(q) = R K0 R^T blockwise -> symmetric
+    K = cor.stiffness().toarray()
+    assert np.abs(K - K.T).max() <= 1e-9 * np.abs(K).max()

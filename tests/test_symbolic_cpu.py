@@ -28,7 +28,7 @@ def analyze(A, bs=1, coords=None, leaf=8):
     c = None if coords is None else np.ascontiguousarray(coords, dtype=np.float64)
     _lib.check(_lib.lib().cnb_chol_analyze(A.shape[0], indptr.ctypes.data, indices.ctypes.data, bs,
                                            c.ctypes.data if c is not None else None, leaf, ctypes.byref(h)))
-    info = (ctypes.c_int64 * 7)()
+    info = (ctypes.c_int64 * 9)()
     fl = (ctypes.c_double * 2)()
     _lib.call("cnb_chol_info", h, info, fl)
     out = {"info": list(info), "flops": fl[0]}
