@@ -1,0 +1,106 @@
+// Device-side structures of the supernodal Cholesky shared by the factor
+// (chol.cu) and solve / compliance (solve.cu) translation units.
+#pragma once
+
+#include <algorithm>
+#include <vector>
+
+#include "chol.h"
+#include "common.cuh"
+
+namespace cnb {
+
+struct DevSym {
+  const int64_t* first;
+  const int64_t* rows_ptr;
+  const int64_t* rows;
+  const int64_t* front_off;
+  const int64_t* child_ptr;
+  const int64_t* child;
+  const int64_t* rel_ptr;
+  const int32_t* rel;
+  const int64_t* linv_off;  // offsets of the inverted diagonal blocks L11^{-1}
+};
+
+__device__ __forceinline__ int64_t d_nc(const DevSym& S, int64_t s) { return S.first[s + 1] - S.first[s]; }
+__device__ __forceinline__ int64_t d_nr(const DevSym& S, int64_t s) { return S.rows_ptr[s + 1] - S.rows_ptr[s]; }
+
+struct DevTasks {
+  int32_t* ptr = nullptr;
+  int64_t count = 0;
+};
+
+struct GrowBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return CNB_OK;
+    release();
+    CNB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    cap = std::max<size_t>(bytes, 256);
+    return CNB_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+template <typename T>
+inline int upload_vec(T** dptr, const std::vector<T>& v) {
+  size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+  CNB_CUDA(cudaMalloc((void**)dptr, bytes));
+  if (!v.empty()) CNB_CUDA(cudaMemcpy(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return CNB_OK;
+}
+
+// Dense-solve plan for right-hand-side chunks of a fixed width.
+struct SolvePlan {
+  int64_t width = -1;
+  int32_t* d_tasks = nullptr;
+  std::vector<DevTasks> asm_t, panel_t, bwd_t;  // per level
+  int64_t *d_roff = nullptr, *d_lo = nullptr, *d_w = nullptr;
+  double* d_rhs = nullptr;
+  void release() {
+    for (void* p : {(void*)d_tasks, (void*)d_roff, (void*)d_lo, (void*)d_w, (void*)d_rhs})
+      if (p) cudaFree(p);
+    d_tasks = nullptr;
+    d_roff = d_lo = d_w = nullptr;
+    d_rhs = nullptr;
+    width = -1;
+  }
+};
+
+struct CholHandle {
+  Symbolic S;
+  bool uploaded = false;
+  bool factored = false;
+  int64_t *d_first = nullptr, *d_rows_ptr = nullptr, *d_rows = nullptr, *d_front_off = nullptr;
+  int64_t *d_child_ptr = nullptr, *d_child = nullptr, *d_rel_ptr = nullptr, *d_perm = nullptr;
+  int64_t* d_linv_off = nullptr;
+  int32_t* d_rel = nullptr;
+  int64_t *d_map_src = nullptr, *d_map_dst = nullptr;
+  double* d_front = nullptr;
+  double* d_linv = nullptr;
+  std::vector<int64_t> linv_off;
+  int32_t* d_tasks = nullptr;
+  std::vector<DevTasks> ea, trinv;                       // per level
+  std::vector<std::vector<DevTasks>> potrf, trsm, syrk;  // per level, per panel
+  SolvePlan plan1, plan8;                                // single-RHS / multi-RHS dense solves
+  GrowBuf bp, tbuf;                                      // permuted RHS, backward temp
+  GrowBuf c_int, c_rhs, c_val, c_y;                      // compliance workspace
+  double last_gram_flops = 0.0, last_fwd_flops = 0.0;
+
+  DevSym sym() const {
+    return DevSym{d_first, d_rows_ptr, d_rows, d_front_off, d_child_ptr, d_child, d_rel_ptr, d_rel, d_linv_off};
+  }
+};
+
+// solve.cu
+int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t k, cudaStream_t st);
+int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx, const double* vals,
+               double* U, int64_t ldu, double* flops_out, cudaStream_t st);
+int trinv_level(CholHandle* h, int level, cudaStream_t st);
+
+}  // namespace cnb

@@ -1,0 +1,718 @@
+// Triangular solves and the mapping compliance on the supernodal factor.
+//
+// Reference being replaced: Factorization.solve / solve_multi
+// (linalg.py:89-106) and the multi-RHS solve + product of assemble_Wg
+// (constraints.py:175-178).
+//
+// At factorisation time every diagonal block L11 of a supernode is inverted
+// (trinv_kernel).  A forward solve step of supernode s is then one
+// matrix product over its front panel M_s = [L11^{-1}; L21] (f_s x nc_s):
+//     [y_s ; u_s] = M_s r_s,   y_s -> solution rows,  R_parent -= u_s (extend-add)
+// and a backward step is two GEMVs,  x_s = L11^{-T} (y_s - L21^T x_rows).
+// No serial triangle chains remain on the solve path: single right-hand
+// sides are coalesced GEMVs (bandwidth-bound), the compliance's many
+// right-hand sides are fp64 tensor-core GEMMs (mma.sync m8n8k4 f64 = DMMA).
+#include <cstring>
+#include <numeric>
+
+#include "chol_dev.cuh"
+
+namespace cnb {
+
+constexpr int kSolveThreads = 128;
+constexpr int kAsmRows = 128;   // rows per assemble task
+constexpr int kAsmCols = 64;    // columns per assemble task (sparse mode)
+constexpr int kGemvRows = 128;  // rows per dense panel task
+constexpr int kGemvJ = 256;     // staged pivot rows of the RHS per pass
+constexpr int kBwdRows = 4;     // pivot rows per backward task (warp per row)
+constexpr int kMT = 64;         // DMMA panel tile (rows, cols)
+constexpr int kMK = 32;         // DMMA k-chunk
+constexpr int kMS = kMK + 4;    // smem stride (== 4 mod 16)
+
+// RHS block of supernode s: R_s = rhs + roff[s], f_s x w_s column-major;
+// global columns [lo_s, lo_s + w_s).
+struct RhsView {
+  double* rhs;
+  const int64_t* roff;
+  const int64_t* lo;
+  const int64_t* w;
+};
+
+__device__ __forceinline__ double panel_entry(const double* __restrict__ F, const double* __restrict__ Li,
+                                              int64_t nc, int64_t f, int64_t i, int64_t j) {
+  // M_s[i][j]: rows < nc from L11^{-1} (lower), rows >= nc from L21
+  if (i < nc) return j <= i ? Li[j * nc + i] : 0.0;
+  return F[j * f + i];
+}
+
+// ---- L11^{-1}, 16 columns per task ----------------------------------------------
+constexpr int kInvCols = 16;
+__global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __restrict__ tasks,
+                                                    const double* __restrict__ front, double* __restrict__ linv) {
+  __shared__ double sL[32][33];
+  __shared__ double y[32][kInvCols];
+  const int64_t s = tasks[2 * blockIdx.x], j0 = tasks[2 * blockIdx.x + 1];
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const double* F = front + S.front_off[s];
+  double* X = linv + S.linv_off[s];
+  const int ncols = (int)min((int64_t)kInvCols, nc - j0);
+  for (int64_t e = threadIdx.x; e < nc * ncols; e += blockDim.x) {
+    const int64_t i = e % nc, c = e / nc;
+    X[(j0 + c) * nc + i] = (i == j0 + c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t kb = (j0 / 32) * 32; kb < nc; kb += 32) {
+    const int bw = (int)min((int64_t)32, nc - kb);
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+      const int i = e & 31, j = e >> 5;
+      sL[i][j] = (i < bw && j < bw && i >= j) ? F[(kb + j) * f + kb + i] : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double v[kInvCols];
+#pragma unroll
+      for (int c = 0; c < kInvCols; ++c) v[c] = (lane < bw && c < ncols) ? X[(j0 + c) * nc + kb + lane] : 0.0;
+      for (int j = 0; j < bw; ++j) {
+        const double ljj = sL[j][j], lij = sL[lane][j];
+#pragma unroll
+        for (int c = 0; c < kInvCols; ++c) {
+          if (lane == j) v[c] = v[c] / ljj;
+          const double yj = __shfl_sync(0xffffffffu, v[c], j);
+          if (lane > j) v[c] = fma(-lij, yj, v[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kInvCols; ++c) {
+        y[lane][c] = lane < bw ? v[c] : 0.0;
+        if (lane < bw && c < ncols) X[(j0 + c) * nc + kb + lane] = v[c];
+      }
+    }
+    __syncthreads();
+    for (int64_t i = kb + bw + threadIdx.x; i < nc; i += blockDim.x) {
+      double acc[kInvCols];
+#pragma unroll
+      for (int c = 0; c < kInvCols; ++c) acc[c] = 0.0;
+      for (int j = 0; j < bw; ++j) {
+        const double l = F[(kb + j) * f + i];
+#pragma unroll
+        for (int c = 0; c < kInvCols; ++c) acc[c] = fma(l, y[j][c], acc[c]);
+      }
+      for (int c = 0; c < ncols; ++c) X[(j0 + c) * nc + i] -= acc[c];
+    }
+    __syncthreads();
+  }
+}
+
+// ---- assemble front RHS blocks: init (dense) + extend-add children -----------
+// task = (s, row chunk r0, column chunk c0)
+__global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
+                                                            int dense, const double* __restrict__ Bp, int64_t n) {
+  const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t r1 = min(f, r0 + kAsmRows);
+  const int64_t ws = R.w[s], los = R.lo[s];
+  const int64_t c1 = min(ws, c0 + kAsmCols);
+  double* Rs = R.rhs + R.roff[s];
+  const int64_t first = S.first[s];
+  if (dense) {
+    for (int64_t c = c0; c < c1; ++c)
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+        Rs[c * f + i] = i < nc ? Bp[(los + c) * n + first + i] : 0.0;
+    __syncthreads();
+  }
+  for (int64_t ci = S.child_ptr[s]; ci < S.child_ptr[s + 1]; ++ci) {
+    const int64_t ch = S.child[ci];
+    const int64_t wc = R.w[ch];
+    if (wc == 0) continue;
+    const int64_t ncc = d_nc(S, ch), nrc = d_nr(S, ch), fc = ncc + nrc;
+    const int32_t* rel = S.rel + S.rel_ptr[ch];
+    int64_t a = 0, b = nrc;
+    while (a < b) {
+      int64_t m = (a + b) >> 1;
+      if (rel[m] < r0) a = m + 1; else b = m;
+    }
+    const int64_t k0 = a;
+    b = nrc;
+    while (a < b) {
+      int64_t m = (a + b) >> 1;
+      if (rel[m] < r1) a = m + 1; else b = m;
+    }
+    const int64_t k1 = a;
+    const int64_t off = R.lo[ch] - los;
+    const double* Rc = R.rhs + R.roff[ch];
+    const int64_t cc0 = max(c0, off), cc1 = min(c1, off + wc);
+    for (int64_t c = cc0; c < cc1; ++c) {
+      const double* src = Rc + (c - off) * fc + ncc;
+      double* dst = Rs + c * f;
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) dst[rel[k]] += src[k];
+    }
+    __syncthreads();
+  }
+}
+
+// ---- dense forward panel product (GEMV-like, NC <= 8 columns) -----------------
+// task = (s, row chunk r0, 0): rows i of M_s r_s; y -> Bp pivot rows, u -> R_s.
+template <int NC>
+__global__ void __launch_bounds__(kGemvRows) panel_gemv_kernel(DevSym S, const int32_t* __restrict__ tasks,
+                                                               RhsView R, const double* __restrict__ front,
+                                                               const double* __restrict__ linv, double* Bp, int64_t n) {
+  __shared__ double rt[kGemvJ][NC];
+  const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1];
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t ws = R.w[s], los = R.lo[s];
+  const int ncols = (int)min((int64_t)NC, ws);
+  const double* Rs = R.rhs + R.roff[s];
+  double* Rw = R.rhs + R.roff[s];
+  const double* F = front + S.front_off[s];
+  const double* Li = linv + S.linv_off[s];
+  const int64_t i = r0 + threadIdx.x;
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  for (int64_t jb = 0; jb < nc; jb += kGemvJ) {
+    const int jn = (int)min((int64_t)kGemvJ, nc - jb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < jn * NC; e += blockDim.x) {
+      const int j = e % jn, c = e / jn;
+      rt[j][c] = c < ncols ? Rs[c * f + jb + j] : 0.0;
+    }
+    __syncthreads();
+    if (i < f) {
+      if (i < nc) {
+        const int jend = (int)min((int64_t)jn, i - jb + 1);
+        for (int j = 0; j < jend; ++j) {
+          const double m = Li[(jb + j) * nc + i];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) acc[c] = fma(m, rt[j][c], acc[c]);
+        }
+      } else {
+        for (int j = 0; j < jn; ++j) {
+          const double m = F[(jb + j) * f + i];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) acc[c] = fma(m, rt[j][c], acc[c]);
+        }
+      }
+    }
+  }
+  if (i < f) {
+    const int64_t first = S.first[s];
+    for (int c = 0; c < ncols; ++c) {
+      if (i < nc)
+        Bp[(los + c) * n + first + i] = acc[c];
+      else
+        Rw[c * f + i] -= acc[c];
+    }
+  }
+}
+
+// ---- sparse-mode forward panel product on DMMA tiles --------------------------
+// task = (s, r0, c0): 64 x 64 tile of M_s (f x nc) x R_s[0:nc, c0:c0+64];
+// rows < nc -> Y_s (nc x w, ld nc), rows >= nc: R_s -= .
+__global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
+                                                        const double* __restrict__ front,
+                                                        const double* __restrict__ linv, double* __restrict__ Y,
+                                                        const int64_t* __restrict__ yoff) {
+  __shared__ double As[kMT * kMS];
+  __shared__ double Bs[kMT * kMS];
+  const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t ws = R.w[s];
+  double* Rs = R.rhs + R.roff[s];
+  const double* F = front + S.front_off[s];
+  const double* Li = linv + S.linv_off[s];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wy = (warp >> 1) * 32, wx = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // rows of this tile that lie in L11^{-1} only need k <= row
+  const int64_t kend = (r0 + kMT <= nc) ? min(nc, r0 + kMT) : nc;
+  for (int64_t k0 = 0; k0 < kend; k0 += kMK) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
+      const int rr = e % kMT, kk = e / kMT;
+      const int64_t i = r0 + rr, j = k0 + kk;
+      As[rr * kMS + kk] = (i < f && j < nc) ? panel_entry(F, Li, nc, f, i, j) : 0.0;
+    }
+    for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
+      const int kk = e % kMK, cc = e / kMK;
+      const int64_t j = k0 + kk, c = c0 + cc;
+      Bs[cc * kMS + kk] = (j < nc && c < ws) ? Rs[c * f + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kMK; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) fa[a] = As[(wy + 8 * a + g) * kMS + kk + t];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) fb[b] = Bs[(wx + 8 * b + g) * kMS + kk + t];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+    }
+  }
+  double* Ys = Y + yoff[s];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int64_t i = r0 + wy + 8 * a + g;
+        const int64_t c = c0 + wx + 8 * b + 2 * t + hh;
+        if (i >= f || c >= ws) continue;
+        if (i < nc)
+          Ys[c * nc + i] = acc[a][b][hh];
+        else
+          Rs[c * f + i] -= acc[a][b][hh];
+      }
+}
+
+// ---- dense backward: t = y - L21^T x_rows ; x = L11^{-T} t (warp per row) ------
+template <int NC>
+__global__ void __launch_bounds__(32 * kBwdRows) bwd_t_kernel(DevSym S, const int32_t* __restrict__ tasks,
+                                                              const double* __restrict__ front,
+                                                              const double* __restrict__ Bp, double* __restrict__ T,
+                                                              int64_t n, int64_t k) {
+  const int64_t s = tasks[3 * blockIdx.x];
+  const int64_t i = tasks[3 * blockIdx.x + 1] + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
+  if (i >= nc) return;
+  const int ncols = (int)min((int64_t)NC, k);
+  const double* lcol = front + S.front_off[s] + i * f + nc;
+  const int64_t* rows = S.rows + S.rows_ptr[s];
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  for (int64_t q = lane; q < nr; q += 32) {
+    const double l = lcol[q];
+    const int64_t rq = rows[q];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < ncols) acc[c] = fma(l, Bp[c * n + rq], acc[c]);
+  }
+  const int64_t first = S.first[s];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const double v = warp_sum(acc[c]);
+    if (lane == 0 && c < ncols) T[c * n + first + i] = Bp[c * n + first + i] - v;
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(32 * kBwdRows) bwd_x_kernel(DevSym S, const int32_t* __restrict__ tasks,
+                                                              const double* __restrict__ linv,
+                                                              const double* __restrict__ T, double* __restrict__ Bp,
+                                                              int64_t n, int64_t k) {
+  const int64_t s = tasks[3 * blockIdx.x];
+  const int64_t i = tasks[3 * blockIdx.x + 1] + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t nc = d_nc(S, s);
+  if (i >= nc) return;
+  const int ncols = (int)min((int64_t)NC, k);
+  const double* lcol = linv + S.linv_off[s] + i * nc;  // column i of L11^{-1} = row i of L11^{-T}
+  const int64_t first = S.first[s];
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  for (int64_t j = i + lane; j < nc; j += 32) {
+    const double l = lcol[j];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < ncols) acc[c] = fma(l, T[c * n + first + j], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const double v = warp_sum(acc[c]);
+    if (lane == 0 && c < ncols) Bp[c * n + first + i] = v;
+  }
+}
+
+__global__ void permute_kernel(int64_t n, int64_t k, const int64_t* __restrict__ perm, const double* __restrict__ src,
+                               int64_t lds, double* __restrict__ dst, int64_t ldd, int inverse) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (p >= n || c >= k) return;
+  if (!inverse)
+    dst[c * ldd + p] = src[c * lds + perm[p]];
+  else
+    dst[c * ldd + perm[p]] = src[c * lds + p];
+}
+
+// ----------------------------------------------------------------------------
+// host orchestration
+// ----------------------------------------------------------------------------
+int trinv_level(CholHandle* h, int level, cudaStream_t st) {
+  const DevTasks& T = h->trinv[level];
+  if (!T.count) return CNB_OK;
+  trinv_kernel<<<(unsigned)T.count, 256, 0, st>>>(h->sym(), T.ptr, h->d_front, h->d_linv);
+  CNB_LAUNCH_CHECK("trinv_kernel");
+  return CNB_OK;
+}
+
+static int build_plan(CholHandle* h, SolvePlan& P, int64_t width) {
+  if (P.width == width) return CNB_OK;
+  P.release();
+  const Symbolic& S = h->S;
+  std::vector<int32_t> all;
+  std::vector<std::pair<int64_t, int64_t>> ra, rp, rb;
+  for (int l = 0; l < S.n_levels; ++l) {
+    int64_t off = (int64_t)all.size();
+    for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
+      const int64_t s = S.level_sn[q];
+      for (int64_t r = 0; r < S.f(s); r += kAsmRows) all.insert(all.end(), {(int32_t)s, (int32_t)r, 0});
+    }
+    ra.push_back({off, ((int64_t)all.size() - off) / 3});
+    off = (int64_t)all.size();
+    for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
+      const int64_t s = S.level_sn[q];
+      for (int64_t r = 0; r < S.f(s); r += kGemvRows) all.insert(all.end(), {(int32_t)s, (int32_t)r, 0});
+    }
+    rp.push_back({off, ((int64_t)all.size() - off) / 3});
+    off = (int64_t)all.size();
+    for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
+      const int64_t s = S.level_sn[q];
+      for (int64_t r = 0; r < S.nc(s); r += kBwdRows) all.insert(all.end(), {(int32_t)s, (int32_t)r, 0});
+    }
+    rb.push_back({off, ((int64_t)all.size() - off) / 3});
+  }
+  int rc;
+  if ((rc = upload_vec(&P.d_tasks, all))) return rc;
+  P.asm_t.clear();
+  P.panel_t.clear();
+  P.bwd_t.clear();
+  for (int l = 0; l < S.n_levels; ++l) {
+    P.asm_t.push_back({P.d_tasks + ra[l].first, ra[l].second});
+    P.panel_t.push_back({P.d_tasks + rp[l].first, rp[l].second});
+    P.bwd_t.push_back({P.d_tasks + rb[l].first, rb[l].second});
+  }
+  std::vector<int64_t> roff(S.ns + 1, 0), lo(S.ns, 0), w(S.ns, width);
+  for (int64_t s = 0; s < S.ns; ++s) roff[s + 1] = roff[s] + S.f(s) * width;
+  if ((rc = upload_vec(&P.d_roff, roff))) return rc;
+  if ((rc = upload_vec(&P.d_lo, lo))) return rc;
+  if ((rc = upload_vec(&P.d_w, w))) return rc;
+  CNB_CUDA(cudaMalloc((void**)&P.d_rhs, std::max<int64_t>(1, roff[S.ns]) * sizeof(double)));
+  P.width = width;
+  return CNB_OK;
+}
+
+template <int NC>
+static int solve_chunk(CholHandle* h, SolvePlan& P, int64_t kk, cudaStream_t st) {
+  const Symbolic& S = h->S;
+  const int64_t n = S.n;
+  DevSym sym = h->sym();
+  RhsView R{P.d_rhs, P.d_roff, P.d_lo, P.d_w};
+  double* Bp = (double*)h->bp.p;
+  double* T = (double*)h->tbuf.p;
+  for (int l = 0; l < S.n_levels; ++l) {
+    asm_kernel<<<(unsigned)P.asm_t[l].count, kSolveThreads, 0, st>>>(sym, P.asm_t[l].ptr, R, 1, Bp, n);
+    CNB_LAUNCH_CHECK("asm_kernel");
+    panel_gemv_kernel<NC><<<(unsigned)P.panel_t[l].count, kGemvRows, 0, st>>>(sym, P.panel_t[l].ptr, R, h->d_front,
+                                                                               h->d_linv, Bp, n);
+    CNB_LAUNCH_CHECK("panel_gemv_kernel");
+  }
+  for (int l = S.n_levels - 1; l >= 0; --l) {
+    bwd_t_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_front, Bp, T, n,
+                                                                          kk);
+    CNB_LAUNCH_CHECK("bwd_t_kernel");
+    bwd_x_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_linv, T, Bp, n,
+                                                                          kk);
+    CNB_LAUNCH_CHECK("bwd_x_kernel");
+  }
+  return CNB_OK;
+}
+
+int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t k, cudaStream_t st) {
+  if (k <= 0) return CNB_OK;
+  const int64_t n = h->S.n;
+  const int64_t width = k == 1 ? 1 : 8;
+  SolvePlan& P = width == 1 ? h->plan1 : h->plan8;
+  int rc;
+  if ((rc = build_plan(h, P, width))) return rc;
+  if ((rc = h->bp.ensure(n * width * sizeof(double)))) return rc;
+  if ((rc = h->tbuf.ensure(n * width * sizeof(double)))) return rc;
+  double* Bp = (double*)h->bp.p;
+  for (int64_t c0 = 0; c0 < k; c0 += width) {
+    const int64_t kk = std::min(width, k - c0);
+    if (kk < width) CNB_CUDA(cudaMemsetAsync(Bp, 0, n * width * sizeof(double), st));
+    dim3 g(grid_for(n, 256), (unsigned)kk);
+    permute_kernel<<<g, 256, 0, st>>>(n, kk, h->d_perm, B + c0 * ldb, ldb, Bp, n, 0);
+    CNB_LAUNCH_CHECK("permute_kernel");
+    rc = width == 1 ? solve_chunk<1>(h, P, kk, st) : solve_chunk<8>(h, P, kk, st);
+    if (rc) return rc;
+    permute_kernel<<<g, 256, 0, st>>>(n, kk, h->d_perm, Bp, n, X + c0 * ldx, ldx, 1);
+    CNB_LAUNCH_CHECK("permute_kernel");
+  }
+  return CNB_OK;
+}
+
+// ----------------------------------------------------------------------------
+// Mapping compliance U = S A^{-1} S^T (constraints.py:155-179)
+// ----------------------------------------------------------------------------
+// U = Y^T Y with Y = L^{-1} P S^T.  Column j of Y is non-zero only on the
+// elimination paths of its S entries: RHS columns are sorted by their first
+// touched supernode and every supernode keeps a window [lo_s, hi_s) of sorted
+// columns (nested along the tree).  The forward solve runs on those windows
+// (asm_kernel + panel_mma_kernel); the Gram product accumulates, for each
+// 64x64 output tile, Y_s^T Y_s of exactly the supernodes whose window covers
+// it, in a fixed order (deterministic), on DMMA.
+constexpr int kGT = 64;
+constexpr int kGK = 32;
+constexpr int kGS = kGT + 4;
+
+__global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const double* __restrict__ Y,
+                                                   const int64_t* __restrict__ yoff, const int32_t* __restrict__ tile_ptr,
+                                                   const int32_t* __restrict__ tile_sn, int64_t ncols,
+                                                   const int64_t* __restrict__ sorted_cols, double* __restrict__ U,
+                                                   int64_t ldu) {
+  __shared__ double Ya[kGK * kGS];
+  __shared__ double Yb[kGK * kGS];
+  const int64_t t = blockIdx.x;
+  int64_t A = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((A + 1) * (A + 2) / 2 <= t) ++A;
+  while (A * (A + 1) / 2 > t) --A;
+  const int64_t B = t - A * (A + 1) / 2;
+  const int64_t ra0 = A * kGT, rb0 = B * kGT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wy = (warp >> 1) * 32, wx = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int32_t e = tile_ptr[t]; e < tile_ptr[t + 1]; ++e) {
+    const int64_t s = tile_sn[e];
+    const int64_t nc = d_nc(S, s);
+    const int64_t lo = R.lo[s], w = R.w[s];
+    const double* Ys = Y + yoff[s];
+    for (int64_t k0 = 0; k0 < nc; k0 += kGK) {
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < kGK * kGT; idx += blockDim.x) {
+        const int kk = idx % kGK, cc = idx / kGK;
+        const int64_t k = k0 + kk;
+        const int64_t la = ra0 + cc - lo, lb = rb0 + cc - lo;
+        Ya[cc * kGS + kk] = (k < nc && la >= 0 && la < w) ? Ys[la * nc + k] : 0.0;
+        Yb[cc * kGS + kk] = (k < nc && lb >= 0 && lb < w) ? Ys[lb * nc + k] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kGK; kk += 4) {
+        double fa[4], fb[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) fa[a] = Ya[(wy + 8 * a + g) * kGS + kk + tq];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) fb[b] = Yb[(wx + 8 * b + g) * kGS + kk + tq];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int64_t ra = ra0 + wy + 8 * a + g;
+        const int64_t rb = rb0 + wx + 8 * b + 2 * tq + hh;
+        if (ra >= ncols || rb >= ncols) continue;
+        if (A == B && rb > ra) continue;
+        const int64_t ja = sorted_cols[ra], jb = sorted_cols[rb];
+        U[ja * ldu + jb] = acc[a][b][hh];
+        U[jb * ldu + ja] = acc[a][b][hh];
+      }
+}
+
+__global__ void scatter_rhs_kernel(int64_t nnz, const int64_t* __restrict__ dst, const double* __restrict__ val,
+                                   double* __restrict__ rhs) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nnz) rhs[dst[k]] = val[k];
+}
+
+struct CompliancePlan {
+  std::vector<int64_t> sorted_cols, lo, w, roff, yoff, sc_dst;
+  std::vector<double> sc_val;
+  std::vector<std::vector<int32_t>> asm_t, panel_t;  // per level, (s, r0, c0)
+  std::vector<int32_t> tile_ptr, tile_sn;
+  double gram_flops = 0.0, fwd_flops = 0.0;
+};
+
+static int build_compliance_plan(const Symbolic& S, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
+                                 const double* vals, CompliancePlan& P) {
+  const int64_t ns = S.ns;
+  std::vector<int64_t> dof_sn(S.n);
+  for (int64_t s = 0; s < ns; ++s)
+    for (int64_t d = S.first[s]; d < S.first[s + 1]; ++d) dof_sn[d] = s;
+  std::vector<int64_t> key(ncols, ns);
+  for (int64_t j = 0; j < ncols; ++j)
+    for (int64_t e = colptr[j]; e < colptr[j + 1]; ++e) {
+      const int64_t d = rowidx[e];
+      if (d < 0 || d >= S.n) {
+        set_error("compliance: row index %lld out of range", (long long)d);
+        return CNB_E_INVALID_ATTACHMENT;
+      }
+      key[j] = std::min(key[j], dof_sn[S.iperm[d]]);
+    }
+  P.sorted_cols.resize(ncols);
+  std::iota(P.sorted_cols.begin(), P.sorted_cols.end(), 0);
+  std::stable_sort(P.sorted_cols.begin(), P.sorted_cols.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+  std::vector<int64_t> rank(ncols);
+  for (int64_t r = 0; r < ncols; ++r) rank[P.sorted_cols[r]] = r;
+  std::vector<int64_t> lo(ns, INT64_MAX), hi(ns, -1);
+  for (int64_t j = 0; j < ncols; ++j)
+    for (int64_t e = colptr[j]; e < colptr[j + 1]; ++e) {
+      const int64_t s = dof_sn[S.iperm[rowidx[e]]];
+      lo[s] = std::min(lo[s], rank[j]);
+      hi[s] = std::max(hi[s], rank[j] + 1);
+    }
+  for (int64_t s = 0; s < ns; ++s) {
+    const int64_t p = S.parent[s];
+    if (p >= 0 && hi[s] > 0) {
+      lo[p] = std::min(lo[p], lo[s]);
+      hi[p] = std::max(hi[p], hi[s]);
+    }
+  }
+  P.lo.assign(ns, 0);
+  P.w.assign(ns, 0);
+  P.roff.assign(ns + 1, 0);
+  P.yoff.assign(ns + 1, 0);
+  for (int64_t s = 0; s < ns; ++s) {
+    if (hi[s] > 0) {
+      P.lo[s] = lo[s];
+      P.w[s] = hi[s] - lo[s];
+    }
+    P.roff[s + 1] = P.roff[s] + S.f(s) * P.w[s];
+    P.yoff[s + 1] = P.yoff[s] + S.nc(s) * P.w[s];
+    const double nc = (double)S.nc(s), nr = (double)S.nr(s), w = (double)P.w[s];
+    P.fwd_flops += w * (nc * nc + 2.0 * nc * nr);
+  }
+  for (int64_t j = 0; j < ncols; ++j)
+    for (int64_t e = colptr[j]; e < colptr[j + 1]; ++e) {
+      const int64_t p = S.iperm[rowidx[e]];
+      const int64_t s = dof_sn[p];
+      P.sc_dst.push_back(P.roff[s] + (rank[j] - P.lo[s]) * S.f(s) + (p - S.first[s]));
+      P.sc_val.push_back(vals[e]);
+    }
+  P.asm_t.assign(S.n_levels, {});
+  P.panel_t.assign(S.n_levels, {});
+  for (int l = 0; l < S.n_levels; ++l)
+    for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
+      const int64_t s = S.level_sn[q];
+      if (P.w[s] == 0) continue;
+      if (S.child_ptr[s + 1] > S.child_ptr[s])
+        for (int64_t r = 0; r < S.f(s); r += kAsmRows)
+          for (int64_t c = 0; c < P.w[s]; c += kAsmCols)
+            P.asm_t[l].insert(P.asm_t[l].end(), {(int32_t)s, (int32_t)r, (int32_t)c});
+      for (int64_t r = 0; r < S.f(s); r += kMT)
+        for (int64_t c = 0; c < P.w[s]; c += kMT) P.panel_t[l].insert(P.panel_t[l].end(), {(int32_t)s, (int32_t)r, (int32_t)c});
+    }
+  const int64_t nt = (ncols + kGT - 1) / kGT;
+  const int64_t npairs = nt * (nt + 1) / 2;
+  std::vector<int32_t> count(npairs + 1, 0);
+  for (int64_t s = 0; s < ns; ++s) {
+    if (P.w[s] == 0) continue;
+    const int64_t t0 = P.lo[s] / kGT, t1 = (P.lo[s] + P.w[s] - 1) / kGT;
+    for (int64_t a = t0; a <= t1; ++a)
+      for (int64_t b = t0; b <= a; ++b) count[a * (a + 1) / 2 + b + 1]++;
+    P.gram_flops += (double)S.nc(s) * (double)P.w[s] * (double)(P.w[s] + 1);
+  }
+  for (int64_t t = 0; t < npairs; ++t) count[t + 1] += count[t];
+  P.tile_ptr = count;
+  P.tile_sn.assign(count[npairs], 0);
+  std::vector<int32_t> fill(count.begin(), count.end() - 1);
+  for (int64_t s = 0; s < ns; ++s) {
+    if (P.w[s] == 0) continue;
+    const int64_t t0 = P.lo[s] / kGT, t1 = (P.lo[s] + P.w[s] - 1) / kGT;
+    for (int64_t a = t0; a <= t1; ++a)
+      for (int64_t b = t0; b <= a; ++b) P.tile_sn[fill[a * (a + 1) / 2 + b]++] = (int32_t)s;
+  }
+  return CNB_OK;
+}
+
+int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx, const double* vals,
+               double* U, int64_t ldu, double* flops_out, cudaStream_t st) {
+  if (ncols <= 0) return CNB_OK;
+  const Symbolic& S = h->S;
+  CompliancePlan P;
+  int rc = build_compliance_plan(S, ncols, colptr, rowidx, vals, P);
+  if (rc) return rc;
+  if (flops_out) {
+    flops_out[0] = P.fwd_flops;
+    flops_out[1] = P.gram_flops;
+  }
+  std::vector<int64_t> ints;
+  auto put = [&](const std::vector<int64_t>& v) {
+    size_t o = ints.size();
+    ints.insert(ints.end(), v.begin(), v.end());
+    return o;
+  };
+  const size_t o_lo = put(P.lo), o_w = put(P.w), o_roff = put(P.roff), o_yoff = put(P.yoff),
+               o_sorted = put(P.sorted_cols), o_dst = put(P.sc_dst);
+  std::vector<int32_t> i32;
+  std::vector<std::pair<size_t, size_t>> arec, prec;
+  for (int l = 0; l < S.n_levels; ++l) {
+    arec.push_back({i32.size(), P.asm_t[l].size() / 3});
+    i32.insert(i32.end(), P.asm_t[l].begin(), P.asm_t[l].end());
+    prec.push_back({i32.size(), P.panel_t[l].size() / 3});
+    i32.insert(i32.end(), P.panel_t[l].begin(), P.panel_t[l].end());
+  }
+  const size_t o_tptr = i32.size();
+  i32.insert(i32.end(), P.tile_ptr.begin(), P.tile_ptr.end());
+  const size_t o_tsn = i32.size();
+  i32.insert(i32.end(), P.tile_sn.begin(), P.tile_sn.end());
+  const size_t bytes64 = ints.size() * sizeof(int64_t);
+  const size_t bytes32 = i32.size() * sizeof(int32_t);
+  if ((rc = h->c_int.ensure(bytes64 + bytes32 + 16))) return rc;
+  if ((rc = h->c_rhs.ensure(std::max<int64_t>(1, P.roff[S.ns]) * sizeof(double)))) return rc;
+  if ((rc = h->c_y.ensure(std::max<int64_t>(1, P.yoff[S.ns]) * sizeof(double)))) return rc;
+  if ((rc = h->c_val.ensure(std::max<size_t>(1, P.sc_val.size()) * sizeof(double)))) return rc;
+  char* base = (char*)h->c_int.p;
+  int64_t* d64 = (int64_t*)base;
+  int32_t* d32 = (int32_t*)(base + ((bytes64 + 15) & ~(size_t)15));
+  CNB_CUDA(cudaMemcpyAsync(d64, ints.data(), bytes64, cudaMemcpyHostToDevice, st));
+  if (bytes32) CNB_CUDA(cudaMemcpyAsync(d32, i32.data(), bytes32, cudaMemcpyHostToDevice, st));
+  if (!P.sc_val.empty())
+    CNB_CUDA(cudaMemcpyAsync(h->c_val.p, P.sc_val.data(), P.sc_val.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             st));
+  double* rhs = (double*)h->c_rhs.p;
+  double* Y = (double*)h->c_y.p;
+  CNB_CUDA(cudaMemsetAsync(rhs, 0, std::max<int64_t>(1, P.roff[S.ns]) * sizeof(double), st));
+  const int64_t nnz = (int64_t)P.sc_val.size();
+  if (nnz) {
+    scatter_rhs_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, d64 + o_dst, (const double*)h->c_val.p, rhs);
+    CNB_LAUNCH_CHECK("scatter_rhs_kernel");
+  }
+  DevSym sym = h->sym();
+  RhsView R{rhs, d64 + o_roff, d64 + o_lo, d64 + o_w};
+  for (int l = 0; l < S.n_levels; ++l) {
+    if (arec[l].second) {
+      asm_kernel<<<(unsigned)arec[l].second, kSolveThreads, 0, st>>>(sym, d32 + arec[l].first, R, 0, nullptr, S.n);
+      CNB_LAUNCH_CHECK("asm_kernel(sparse)");
+    }
+    if (prec[l].second) {
+      panel_mma_kernel<<<(unsigned)prec[l].second, 128, 0, st>>>(sym, d32 + prec[l].first, R, h->d_front, h->d_linv,
+                                                                 Y, d64 + o_yoff);
+      CNB_LAUNCH_CHECK("panel_mma_kernel");
+    }
+  }
+  const int64_t nt = (ncols + kGT - 1) / kGT;
+  const int64_t npairs = nt * (nt + 1) / 2;
+  gram_kernel<<<(unsigned)npairs, 128, 0, st>>>(sym, R, Y, d64 + o_yoff, d32 + o_tptr, d32 + o_tsn, ncols,
+                                                d64 + o_sorted, U, ldu);
+  CNB_LAUNCH_CHECK("gram_kernel");
+  h->last_fwd_flops = P.fwd_flops;
+  h->last_gram_flops = P.gram_flops;
+  return CNB_OK;
+}
+
+}  // namespace cnb
