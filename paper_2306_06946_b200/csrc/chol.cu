@@ -220,7 +220,7 @@ static int chol_upload(CholHandle* h) {
   struct Rec {
     int64_t off, count;
   };
-  std::vector<Rec> ea_rec, ti_rec;
+  std::vector<Rec> ea_rec, ti_rec, p2_rec;
   std::vector<std::vector<Rec>> po_rec, tr_rec, sy_rec;
   for (int l = 0; l < S.n_levels; ++l) {
     const LevelTasks& T = S.tasks[l];
@@ -247,17 +247,29 @@ static int chol_upload(CholHandle* h) {
       }
     }
     ti_rec.push_back({off, ((int64_t)all.size() - off) / 2});
+    // P21 = L21 L11^{-1} tasks: (s, 64-row block of L21)
+    const int64_t off2 = (int64_t)all.size();
+    for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
+      const int64_t s = S.level_sn[q];
+      for (int64_t q0 = 0; q0 < S.nr(s); q0 += 64) {
+        all.push_back((int32_t)s);
+        all.push_back((int32_t)q0);
+      }
+    }
+    p2_rec.push_back({off2, ((int64_t)all.size() - off2) / 2});
   }
   if ((rc = upload_vec(&h->d_tasks, all)) != CNB_OK) return rc;
   auto mk = [&](const Rec& r) { return DevTasks{h->d_tasks + r.off, r.count}; };
   h->ea.clear();
   h->trinv.clear();
+  h->p21.clear();
   h->potrf.assign(S.n_levels, {});
   h->trsm.assign(S.n_levels, {});
   h->syrk.assign(S.n_levels, {});
   for (int l = 0; l < S.n_levels; ++l) {
     h->ea.push_back(mk(ea_rec[l]));
     h->trinv.push_back(mk(ti_rec[l]));
+    h->p21.push_back(mk(p2_rec[l]));
     for (auto& r : po_rec[l]) h->potrf[l].push_back(mk(r));
     for (auto& r : tr_rec[l]) h->trsm[l].push_back(mk(r));
     for (auto& r : sy_rec[l]) h->syrk[l].push_back(mk(r));

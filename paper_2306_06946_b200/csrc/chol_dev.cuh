@@ -85,7 +85,7 @@ struct CholHandle {
   double* d_linv = nullptr;
   std::vector<int64_t> linv_off;
   int32_t* d_tasks = nullptr;
-  std::vector<DevTasks> ea, trinv;                       // per level
+  std::vector<DevTasks> ea, trinv, p21;                  // per level
   std::vector<std::vector<DevTasks>> potrf, trsm, syrk;  // per level, per panel
   SolvePlan plan1, plan8;                                // single-RHS / multi-RHS dense solves
   GrowBuf bp, tbuf;                                      // permuted RHS, backward temp

@@ -274,50 +274,24 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
       }
 }
 
-// ---- dense backward: t = y - L21^T x_rows ; x = L11^{-T} t (warp per row) ------
+// ---- dense backward: x_s = L11^{-T} y_s - P21^T x_rows (warp per pivot row) -----
+// P21 = L21 L11^{-1} overwrote L21 at factorisation time.  y comes from Bp
+// (forward result), ancestors' x from X; the supernode's x is written to X.
 template <int NC>
-__global__ void __launch_bounds__(32 * kBwdRows) bwd_t_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                              const double* __restrict__ front,
-                                                              const double* __restrict__ Bp, double* __restrict__ T,
-                                                              int64_t n, int64_t k) {
+__global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int32_t* __restrict__ tasks,
+                                                            const double* __restrict__ front,
+                                                            const double* __restrict__ linv,
+                                                            const double* __restrict__ Bp, double* __restrict__ X,
+                                                            int64_t n, int64_t k) {
   const int64_t s = tasks[3 * blockIdx.x];
   const int64_t i = tasks[3 * blockIdx.x + 1] + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
   if (i >= nc) return;
   const int ncols = (int)min((int64_t)NC, k);
-  const double* lcol = front + S.front_off[s] + i * f + nc;
+  const double* pcol = front + S.front_off[s] + i * f + nc;  // P21[:, i]
+  const double* lcol = linv + S.linv_off[s] + i * nc;       // L11^{-1}[:, i] = row i of L11^{-T}
   const int64_t* rows = S.rows + S.rows_ptr[s];
-  double acc[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-  for (int64_t q = lane; q < nr; q += 32) {
-    const double l = lcol[q];
-    const int64_t rq = rows[q];
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < ncols) acc[c] = fma(l, Bp[c * n + rq], acc[c]);
-  }
-  const int64_t first = S.first[s];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const double v = warp_sum(acc[c]);
-    if (lane == 0 && c < ncols) T[c * n + first + i] = Bp[c * n + first + i] - v;
-  }
-}
-
-template <int NC>
-__global__ void __launch_bounds__(32 * kBwdRows) bwd_x_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                              const double* __restrict__ linv,
-                                                              const double* __restrict__ T, double* __restrict__ Bp,
-                                                              int64_t n, int64_t k) {
-  const int64_t s = tasks[3 * blockIdx.x];
-  const int64_t i = tasks[3 * blockIdx.x + 1] + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  const int64_t nc = d_nc(S, s);
-  if (i >= nc) return;
-  const int ncols = (int)min((int64_t)NC, k);
-  const double* lcol = linv + S.linv_off[s] + i * nc;  // column i of L11^{-1} = row i of L11^{-T}
   const int64_t first = S.first[s];
   double acc[NC];
 #pragma unroll
@@ -326,12 +300,80 @@ __global__ void __launch_bounds__(32 * kBwdRows) bwd_x_kernel(DevSym S, const in
     const double l = lcol[j];
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      if (c < ncols) acc[c] = fma(l, T[c * n + first + j], acc[c]);
+      if (c < ncols) acc[c] = fma(l, Bp[c * n + first + j], acc[c]);
+  }
+  for (int64_t q = lane; q < nr; q += 32) {
+    const double pq = pcol[q];
+    const int64_t rq = rows[q];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < ncols) acc[c] = fma(-pq, X[c * n + rq], acc[c]);
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const double v = warp_sum(acc[c]);
-    if (lane == 0 && c < ncols) Bp[c * n + first + i] = v;
+    if (lane == 0 && c < ncols) X[c * n + first + i] = v;
+  }
+}
+
+// ---- factor epilogue: P21 = L21 L11^{-1} in place (DMMA) -------------------------
+// task = (s, 64-row block of L21).  Column chunks are produced in ascending
+// order: chunk [c0, c0+64) only reads L21 columns k >= c0 (L11^{-1} is lower
+// triangular), so overwriting it after its k-loop never clobbers live input.
+__global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __restrict__ tasks, double* __restrict__ front,
+                                                  const double* __restrict__ linv) {
+  __shared__ double As[kMT * kMS];
+  __shared__ double Bs[kMT * kMS];
+  const int64_t s = tasks[2 * blockIdx.x], q0 = tasks[2 * blockIdx.x + 1];
+  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
+  double* F = front + S.front_off[s];
+  const double* Li = linv + S.linv_off[s];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wy = (warp >> 1) * 32, wx = (warp & 1) * 32;
+  for (int64_t c0 = 0; c0 < nc; c0 += kMT) {
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int64_t k0 = c0; k0 < nc; k0 += kMK) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
+        const int rr = e % kMT, kk = e / kMT;
+        const int64_t q = q0 + rr, k = k0 + kk;
+        As[rr * kMS + kk] = (q < nr && k < nc) ? F[k * f + nc + q] : 0.0;
+      }
+      for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
+        const int kk = e % kMK, cc = e / kMK;
+        const int64_t k = k0 + kk, c = c0 + cc;
+        Bs[cc * kMS + kk] = (k < nc && c < nc && k >= c) ? Li[c * nc + k] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kMK; kk += 4) {
+        double fa[4], fb[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) fa[a] = As[(wy + 8 * a + g) * kMS + kk + t];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) fb[b] = Bs[(wx + 8 * b + g) * kMS + kk + t];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int64_t q = q0 + wy + 8 * a + g;
+          const int64_t c = c0 + wx + 8 * b + 2 * t + hh;
+          if (q < nr && c < nc) F[c * f + nc + q] = acc[a][b][hh];
+        }
   }
 }
 
@@ -354,6 +396,11 @@ int trinv_level(CholHandle* h, int level, cudaStream_t st) {
   if (!T.count) return CNB_OK;
   trinv_kernel<<<(unsigned)T.count, 256, 0, st>>>(h->sym(), T.ptr, h->d_front, h->d_linv);
   CNB_LAUNCH_CHECK("trinv_kernel");
+  const DevTasks& P = h->p21[level];
+  if (P.count) {
+    p21_kernel<<<(unsigned)P.count, 128, 0, st>>>(h->sym(), P.ptr, h->d_front, h->d_linv);
+    CNB_LAUNCH_CHECK("p21_kernel");
+  }
   return CNB_OK;
 }
 
@@ -419,12 +466,9 @@ static int solve_chunk(CholHandle* h, SolvePlan& P, int64_t kk, cudaStream_t st)
     CNB_LAUNCH_CHECK("panel_gemv_kernel");
   }
   for (int l = S.n_levels - 1; l >= 0; --l) {
-    bwd_t_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_front, Bp, T, n,
-                                                                          kk);
-    CNB_LAUNCH_CHECK("bwd_t_kernel");
-    bwd_x_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_linv, T, Bp, n,
-                                                                          kk);
-    CNB_LAUNCH_CHECK("bwd_x_kernel");
+    bwd_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_front, h->d_linv,
+                                                                        Bp, T, n, kk);
+    CNB_LAUNCH_CHECK("bwd_kernel");
   }
   return CNB_OK;
 }
@@ -447,7 +491,7 @@ int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t 
     CNB_LAUNCH_CHECK("permute_kernel");
     rc = width == 1 ? solve_chunk<1>(h, P, kk, st) : solve_chunk<8>(h, P, kk, st);
     if (rc) return rc;
-    permute_kernel<<<g, 256, 0, st>>>(n, kk, h->d_perm, Bp, n, X + c0 * ldx, ldx, 1);
+    permute_kernel<<<g, 256, 0, st>>>(n, kk, h->d_perm, (double*)h->tbuf.p, n, X + c0 * ldx, ldx, 1);
     CNB_LAUNCH_CHECK("permute_kernel");
   }
   return CNB_OK;
@@ -465,15 +509,15 @@ int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t 
 // it, in a fixed order (deterministic), on DMMA.
 constexpr int kGT = 64;
 constexpr int kGK = 32;
-constexpr int kGS = kGT + 4;
+constexpr int kGS = kGK + 4;  // [column][k] staging stride (== 4 mod 16: conflict-free fragments)
 
 __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const double* __restrict__ Y,
                                                    const int64_t* __restrict__ yoff, const int32_t* __restrict__ tile_ptr,
                                                    const int32_t* __restrict__ tile_sn, int64_t ncols,
                                                    const int64_t* __restrict__ sorted_cols, double* __restrict__ U,
                                                    int64_t ldu) {
-  __shared__ double Ya[kGK * kGS];
-  __shared__ double Yb[kGK * kGS];
+  __shared__ double Ya[kGT * kGS];
+  __shared__ double Yb[kGT * kGS];
   const int64_t t = blockIdx.x;
   int64_t A = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
   while ((A + 1) * (A + 2) / 2 <= t) ++A;
