@@ -77,28 +77,34 @@ __global__ void __launch_bounds__(256) potrf_kernel(DevSym S, const int32_t* __r
     a[i][j] = (i >= j) ? F[(int64_t)(k0 + j) * f + k0 + i] : 0.0;
   }
   __syncthreads();
-  // warp 0 factors the block: lane i owns row i (right-looking, shuffles)
+  // warp 0 factors the block with rows in registers: lane i owns row i, the
+  // column entries it needs from other rows arrive by shuffle (right-looking)
   if (threadIdx.x < 32) {
     const int i = threadIdx.x;
-    for (int j = 0; j < kw; ++j) {
-      double d = a[j][j];
-      if (i == j) {
+    double r[kPanel];
+#pragma unroll
+    for (int l = 0; l < kPanel; ++l) r[l] = (i < kw && l < kw) ? a[i][l] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kPanel; ++j) {
+      if (j < kw) {
+        double d = __shfl_sync(0xffffffffu, r[j], j);
         if (!(d > 0.0)) {
-          raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
+          if (i == 0) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
           d = nan("");
         }
-        a[j][j] = sqrt(d);
+        const double piv = sqrt(d), rp = 1.0 / piv;
+        if (i == j) r[j] = piv;
+        else if (i > j) r[j] *= rp;
+#pragma unroll
+        for (int l = j + 1; l < kPanel; ++l) {
+          const double llj = __shfl_sync(0xffffffffu, r[j], l);
+          if (i >= l) r[l] = fma(-r[j], llj, r[l]);
+        }
       }
-      __syncwarp();
-      const double piv = a[j][j];
-      if (i > j && i < kw) a[i][j] /= piv;
-      __syncwarp();
-      if (i > j && i < kw) {
-        const double lij = a[i][j];
-        for (int l = j + 1; l <= i; ++l) a[i][l] -= lij * a[l][j];
-      }
-      __syncwarp();
     }
+#pragma unroll
+    for (int l = 0; l < kPanel; ++l)
+      if (i < kw && l <= i) a[i][l] = r[l];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kw * kw; e += blockDim.x) {
@@ -216,6 +222,9 @@ static int chol_upload(CholHandle* h) {
   h->linv_off.assign(S.ns + 1, 0);
   for (int64_t s = 0; s < S.ns; ++s) h->linv_off[s + 1] = h->linv_off[s] + S.nc(s) * S.nc(s);
   if ((rc = upload_vec(&h->d_linv_off, h->linv_off)) != CNB_OK) return rc;
+  h->p21_off.assign(S.ns + 1, 0);
+  for (int64_t s = 0; s < S.ns; ++s) h->p21_off[s + 1] = h->p21_off[s] + S.nr(s) * S.nc(s);
+  if ((rc = upload_vec(&h->d_p21_off, h->p21_off)) != CNB_OK) return rc;
   std::vector<int32_t> all;
   struct Rec {
     int64_t off, count;
@@ -241,7 +250,7 @@ static int chol_upload(CholHandle* h) {
     const int64_t off = (int64_t)all.size();
     for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
       const int64_t s = S.level_sn[q];
-      for (int64_t j0 = 0; j0 < S.nc(s); j0 += 16) {
+      for (int64_t j0 = 0; j0 < S.nc(s); j0 += kInvCols) {
         all.push_back((int32_t)s);
         all.push_back((int32_t)j0);
       }
@@ -251,12 +260,14 @@ static int chol_upload(CholHandle* h) {
     const int64_t off2 = (int64_t)all.size();
     for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
       const int64_t s = S.level_sn[q];
-      for (int64_t q0 = 0; q0 < S.nr(s); q0 += 64) {
-        all.push_back((int32_t)s);
-        all.push_back((int32_t)q0);
-      }
+      for (int64_t q0 = 0; q0 < S.nr(s); q0 += 64)
+        for (int64_t c0 = 0; c0 < S.nc(s); c0 += 64) {
+          all.push_back((int32_t)s);
+          all.push_back((int32_t)q0);
+          all.push_back((int32_t)c0);
+        }
     }
-    p2_rec.push_back({off2, ((int64_t)all.size() - off2) / 2});
+    p2_rec.push_back({off2, ((int64_t)all.size() - off2) / 3});
   }
   if ((rc = upload_vec(&h->d_tasks, all)) != CNB_OK) return rc;
   auto mk = [&](const Rec& r) { return DevTasks{h->d_tasks + r.off, r.count}; };
@@ -276,6 +287,7 @@ static int chol_upload(CholHandle* h) {
   }
   CNB_CUDA(cudaMalloc((void**)&h->d_front, std::max<int64_t>(1, S.front_off[S.ns]) * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_linv, std::max<int64_t>(1, h->linv_off[S.ns]) * sizeof(double)));
+  CNB_CUDA(cudaMalloc((void**)&h->d_p21, std::max<int64_t>(1, h->p21_off[S.ns]) * sizeof(double)));
   h->uploaded = true;
   return CNB_OK;
 }
@@ -283,7 +295,7 @@ static int chol_upload(CholHandle* h) {
 static void chol_free(CholHandle* h) {
   void* ptrs[] = {h->d_first, h->d_rows_ptr, h->d_rows, h->d_front_off, h->d_child_ptr, h->d_child,
                   h->d_rel_ptr, h->d_rel, h->d_map_src, h->d_map_dst, h->d_perm, h->d_front, h->d_tasks,
-                  h->d_linv, h->d_linv_off};
+                  h->d_linv, h->d_linv_off, h->d_p21, h->d_p21_off};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->plan1.release();

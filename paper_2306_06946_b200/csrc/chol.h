@@ -20,6 +20,7 @@ namespace cnb {
 constexpr int kPanel = 32;   // pivot panel width of the dense front factorisation
 constexpr int kTile = 64;    // SYRK / GEMM output tile
 constexpr int kEaCols = 32;  // parent columns per extend-add task
+constexpr int kInvCols = 8;  // columns of L11^{-1} per inversion task
 
 struct LevelTasks {
   // extend-add: (parent supernode, parent col lo, parent col hi)

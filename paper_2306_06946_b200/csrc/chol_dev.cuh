@@ -20,6 +20,7 @@ struct DevSym {
   const int64_t* rel_ptr;
   const int32_t* rel;
   const int64_t* linv_off;  // offsets of the inverted diagonal blocks L11^{-1}
+  const int64_t* p21_off;   // offsets of P21 = L21 L11^{-1} (nr x nc, column-major)
 };
 
 __device__ __forceinline__ int64_t d_nc(const DevSym& S, int64_t s) { return S.first[s + 1] - S.first[s]; }
@@ -79,11 +80,13 @@ struct CholHandle {
   int64_t *d_first = nullptr, *d_rows_ptr = nullptr, *d_rows = nullptr, *d_front_off = nullptr;
   int64_t *d_child_ptr = nullptr, *d_child = nullptr, *d_rel_ptr = nullptr, *d_perm = nullptr;
   int64_t* d_linv_off = nullptr;
+  int64_t* d_p21_off = nullptr;
   int32_t* d_rel = nullptr;
   int64_t *d_map_src = nullptr, *d_map_dst = nullptr;
   double* d_front = nullptr;
   double* d_linv = nullptr;
-  std::vector<int64_t> linv_off;
+  double* d_p21 = nullptr;
+  std::vector<int64_t> linv_off, p21_off;
   int32_t* d_tasks = nullptr;
   std::vector<DevTasks> ea, trinv, p21;                  // per level
   std::vector<std::vector<DevTasks>> potrf, trsm, syrk;  // per level, per panel
@@ -93,7 +96,8 @@ struct CholHandle {
   double last_gram_flops = 0.0, last_fwd_flops = 0.0;
 
   DevSym sym() const {
-    return DevSym{d_first, d_rows_ptr, d_rows, d_front_off, d_child_ptr, d_child, d_rel_ptr, d_rel, d_linv_off};
+    return DevSym{d_first,   d_rows_ptr, d_rows, d_front_off, d_child_ptr,
+                  d_child,   d_rel_ptr,  d_rel,  d_linv_off,  d_p21_off};
   }
 };
 

@@ -22,7 +22,7 @@ namespace cnb {
 constexpr int kSolveThreads = 128;
 constexpr int kAsmRows = 128;   // rows per assemble task
 constexpr int kAsmCols = 64;    // columns per assemble task (sparse mode)
-constexpr int kGemvRows = 128;  // rows per dense panel task
+constexpr int kGemvRows = 32;   // rows per dense panel task
 constexpr int kGemvJ = 256;     // staged pivot rows of the RHS per pass
 constexpr int kBwdRows = 4;     // pivot rows per backward task (warp per row)
 constexpr int kMT = 64;         // DMMA panel tile (rows, cols)
@@ -38,15 +38,14 @@ struct RhsView {
   const int64_t* w;
 };
 
-__device__ __forceinline__ double panel_entry(const double* __restrict__ F, const double* __restrict__ Li,
-                                              int64_t nc, int64_t f, int64_t i, int64_t j) {
-  // M_s[i][j]: rows < nc from L11^{-1} (lower), rows >= nc from L21
+__device__ __forceinline__ double panel_entry(const double* __restrict__ P, const double* __restrict__ Li,
+                                              int64_t nc, int64_t nr, int64_t i, int64_t j) {
+  // M_s[i][j]: rows < nc from L11^{-1} (lower), rows >= nc from P21 = L21 L11^{-1}
   if (i < nc) return j <= i ? Li[j * nc + i] : 0.0;
-  return F[j * f + i];
+  return P[j * nr + (i - nc)];
 }
 
-// ---- L11^{-1}, 16 columns per task ----------------------------------------------
-constexpr int kInvCols = 16;
+// ---- L11^{-1}, kInvCols columns per task -----------------------------------------
 __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                     const double* __restrict__ front, double* __restrict__ linv) {
   __shared__ double sL[32][33];
@@ -74,10 +73,10 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
 #pragma unroll
       for (int c = 0; c < kInvCols; ++c) v[c] = (lane < bw && c < ncols) ? X[(j0 + c) * nc + kb + lane] : 0.0;
       for (int j = 0; j < bw; ++j) {
-        const double ljj = sL[j][j], lij = sL[lane][j];
+        const double rjj = 1.0 / sL[j][j], lij = sL[lane][j];
 #pragma unroll
         for (int c = 0; c < kInvCols; ++c) {
-          if (lane == j) v[c] = v[c] / ljj;
+          if (lane == j) v[c] *= rjj;
           const double yj = __shfl_sync(0xffffffffu, v[c], j);
           if (lane > j) v[c] = fma(-lij, yj, v[c]);
         }
@@ -151,22 +150,25 @@ __global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int3
   }
 }
 
-// ---- dense forward panel product (GEMV-like, NC <= 8 columns) -----------------
-// task = (s, row chunk r0, 0): rows i of M_s r_s; y -> Bp pivot rows, u -> R_s.
+// ---- dense forward panel product (GEMV, NC <= 8 columns) ----------------------
+// task = (s, row tile r0 of 32 rows): 8 warps split the pivot index j, lanes
+// take consecutive rows (coalesced column reads of M_s), partial sums reduced
+// through shared memory.  y -> Bp pivot rows, u subtracted from R_s.
 template <int NC>
-__global__ void __launch_bounds__(kGemvRows) panel_gemv_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                               RhsView R, const double* __restrict__ front,
-                                                               const double* __restrict__ linv, double* Bp, int64_t n) {
+__global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
+                                                         const double* __restrict__ p21,
+                                                         const double* __restrict__ linv, double* Bp, int64_t n) {
   __shared__ double rt[kGemvJ][NC];
+  __shared__ double red[8][32][NC];
   const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1];
-  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
   const int64_t ws = R.w[s], los = R.lo[s];
   const int ncols = (int)min((int64_t)NC, ws);
-  const double* Rs = R.rhs + R.roff[s];
-  double* Rw = R.rhs + R.roff[s];
-  const double* F = front + S.front_off[s];
+  double* Rs = R.rhs + R.roff[s];
   const double* Li = linv + S.linv_off[s];
-  const int64_t i = r0 + threadIdx.x;
+  const double* P = p21 + S.p21_off[s];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t i = r0 + lane;
   double acc[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = 0.0;
@@ -181,27 +183,37 @@ __global__ void __launch_bounds__(kGemvRows) panel_gemv_kernel(DevSym S, const i
     if (i < f) {
       if (i < nc) {
         const int jend = (int)min((int64_t)jn, i - jb + 1);
-        for (int j = 0; j < jend; ++j) {
+        for (int j = grp; j < jend; j += 8) {
           const double m = Li[(jb + j) * nc + i];
 #pragma unroll
           for (int c = 0; c < NC; ++c) acc[c] = fma(m, rt[j][c], acc[c]);
         }
       } else {
-        for (int j = 0; j < jn; ++j) {
-          const double m = F[(jb + j) * f + i];
+        const double* pc = P + jb * nr + (i - nc);
+#pragma unroll 4
+        for (int j = grp; j < jn; j += 8) {
+          const double m = pc[(int64_t)j * nr];
 #pragma unroll
           for (int c = 0; c < NC; ++c) acc[c] = fma(m, rt[j][c], acc[c]);
         }
       }
     }
   }
-  if (i < f) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) red[grp][lane][c] = acc[c];
+  __syncthreads();
+  if (grp == 0 && i < f) {
     const int64_t first = S.first[s];
-    for (int c = 0; c < ncols; ++c) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (c >= ncols) break;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v += red[q][lane][c];
       if (i < nc)
-        Bp[(los + c) * n + first + i] = acc[c];
+        Bp[(los + c) * n + first + i] = v;
       else
-        Rw[c * f + i] -= acc[c];
+        Rs[c * f + i] -= v;
     }
   }
 }
@@ -210,16 +222,16 @@ __global__ void __launch_bounds__(kGemvRows) panel_gemv_kernel(DevSym S, const i
 // task = (s, r0, c0): 64 x 64 tile of M_s (f x nc) x R_s[0:nc, c0:c0+64];
 // rows < nc -> Y_s (nc x w, ld nc), rows >= nc: R_s -= .
 __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
-                                                        const double* __restrict__ front,
+                                                        const double* __restrict__ p21,
                                                         const double* __restrict__ linv, double* __restrict__ Y,
                                                         const int64_t* __restrict__ yoff) {
   __shared__ double As[kMT * kMS];
   __shared__ double Bs[kMT * kMS];
   const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
-  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
   const int64_t ws = R.w[s];
   double* Rs = R.rhs + R.roff[s];
-  const double* F = front + S.front_off[s];
+  const double* P = p21 + S.p21_off[s];
   const double* Li = linv + S.linv_off[s];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -236,7 +248,7 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int rr = e % kMT, kk = e / kMT;
       const int64_t i = r0 + rr, j = k0 + kk;
-      As[rr * kMS + kk] = (i < f && j < nc) ? panel_entry(F, Li, nc, f, i, j) : 0.0;
+      As[rr * kMS + kk] = (i < f && j < nc) ? panel_entry(P, Li, nc, nr, i, j) : 0.0;
     }
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int kk = e % kMK, cc = e / kMK;
@@ -279,17 +291,17 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
 // (forward result), ancestors' x from X; the supernode's x is written to X.
 template <int NC>
 __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                            const double* __restrict__ front,
+                                                            const double* __restrict__ p21,
                                                             const double* __restrict__ linv,
                                                             const double* __restrict__ Bp, double* __restrict__ X,
                                                             int64_t n, int64_t k) {
   const int64_t s = tasks[3 * blockIdx.x];
   const int64_t i = tasks[3 * blockIdx.x + 1] + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
+  const int64_t nc = d_nc(S, s), nr = d_nr(S, s);
   if (i >= nc) return;
   const int ncols = (int)min((int64_t)NC, k);
-  const double* pcol = front + S.front_off[s] + i * f + nc;  // P21[:, i]
+  const double* pcol = p21 + S.p21_off[s] + i * nr;  // P21[:, i]
   const double* lcol = linv + S.linv_off[s] + i * nc;       // L11^{-1}[:, i] = row i of L11^{-T}
   const int64_t* rows = S.rows + S.rows_ptr[s];
   const int64_t first = S.first[s];
@@ -316,65 +328,63 @@ __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int3
   }
 }
 
-// ---- factor epilogue: P21 = L21 L11^{-1} in place (DMMA) -------------------------
-// task = (s, 64-row block of L21).  Column chunks are produced in ascending
-// order: chunk [c0, c0+64) only reads L21 columns k >= c0 (L11^{-1} is lower
-// triangular), so overwriting it after its k-loop never clobbers live input.
-__global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __restrict__ tasks, double* __restrict__ front,
-                                                  const double* __restrict__ linv) {
+// ---- factor epilogue: P21 = L21 L11^{-1} (DMMA, nr x nc, column-major ld nr) -----
+// task = (s, 64-row block q0 of L21, 64-column block c0); L11^{-1} is lower
+// triangular, so only k >= c0 contributes.
+__global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __restrict__ tasks,
+                                                  const double* __restrict__ front, const double* __restrict__ linv,
+                                                  double* __restrict__ p21) {
   __shared__ double As[kMT * kMS];
   __shared__ double Bs[kMT * kMS];
-  const int64_t s = tasks[2 * blockIdx.x], q0 = tasks[2 * blockIdx.x + 1];
+  const int64_t s = tasks[3 * blockIdx.x], q0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
-  double* F = front + S.front_off[s];
+  const double* F = front + S.front_off[s];
   const double* Li = linv + S.linv_off[s];
+  double* P = p21 + S.p21_off[s];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wy = (warp >> 1) * 32, wx = (warp & 1) * 32;
-  for (int64_t c0 = 0; c0 < nc; c0 += kMT) {
-    double acc[4][4][2];
+  double acc[4][4][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    for (int64_t k0 = c0; k0 < nc; k0 += kMK) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
-        const int rr = e % kMT, kk = e / kMT;
-        const int64_t q = q0 + rr, k = k0 + kk;
-        As[rr * kMS + kk] = (q < nr && k < nc) ? F[k * f + nc + q] : 0.0;
-      }
-      for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
-        const int kk = e % kMK, cc = e / kMK;
-        const int64_t k = k0 + kk, c = c0 + cc;
-        Bs[cc * kMS + kk] = (k < nc && c < nc && k >= c) ? Li[c * nc + k] : 0.0;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < kMK; kk += 4) {
-        double fa[4], fb[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) fa[a] = As[(wy + 8 * a + g) * kMS + kk + t];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) fb[b] = Bs[(wx + 8 * b + g) * kMS + kk + t];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
-      }
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int64_t k0 = c0; k0 < nc; k0 += kMK) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
+      const int rr = e % kMT, kk = e / kMT;
+      const int64_t q = q0 + rr, k = k0 + kk;
+      As[rr * kMS + kk] = (q < nr && k < nc) ? F[k * f + nc + q] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
+      const int kk = e % kMK, cc = e / kMK;
+      const int64_t k = k0 + kk, c = c0 + cc;
+      Bs[cc * kMS + kk] = (k < nc && c < nc && k >= c) ? Li[c * nc + k] : 0.0;
     }
     __syncthreads();
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int kk = 0; kk < kMK; kk += 4) {
+      double fa[4], fb[4];
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int a = 0; a < 4; ++a) fa[a] = As[(wy + 8 * a + g) * kMS + kk + t];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int64_t q = q0 + wy + 8 * a + g;
-          const int64_t c = c0 + wx + 8 * b + 2 * t + hh;
-          if (q < nr && c < nc) F[c * f + nc + q] = acc[a][b][hh];
-        }
+      for (int b = 0; b < 4; ++b) fb[b] = Bs[(wx + 8 * b + g) * kMS + kk + t];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+    }
   }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int64_t q = q0 + wy + 8 * a + g;
+        const int64_t c = c0 + wx + 8 * b + 2 * t + hh;
+        if (q < nr && c < nc) P[c * nr + q] = acc[a][b][hh];
+      }
 }
 
 __global__ void permute_kernel(int64_t n, int64_t k, const int64_t* __restrict__ perm, const double* __restrict__ src,
@@ -398,7 +408,7 @@ int trinv_level(CholHandle* h, int level, cudaStream_t st) {
   CNB_LAUNCH_CHECK("trinv_kernel");
   const DevTasks& P = h->p21[level];
   if (P.count) {
-    p21_kernel<<<(unsigned)P.count, 128, 0, st>>>(h->sym(), P.ptr, h->d_front, h->d_linv);
+    p21_kernel<<<(unsigned)P.count, 128, 0, st>>>(h->sym(), P.ptr, h->d_front, h->d_linv, h->d_p21);
     CNB_LAUNCH_CHECK("p21_kernel");
   }
   return CNB_OK;
@@ -461,12 +471,12 @@ static int solve_chunk(CholHandle* h, SolvePlan& P, int64_t kk, cudaStream_t st)
   for (int l = 0; l < S.n_levels; ++l) {
     asm_kernel<<<(unsigned)P.asm_t[l].count, kSolveThreads, 0, st>>>(sym, P.asm_t[l].ptr, R, 1, Bp, n);
     CNB_LAUNCH_CHECK("asm_kernel");
-    panel_gemv_kernel<NC><<<(unsigned)P.panel_t[l].count, kGemvRows, 0, st>>>(sym, P.panel_t[l].ptr, R, h->d_front,
-                                                                               h->d_linv, Bp, n);
+    panel_gemv_kernel<NC><<<(unsigned)P.panel_t[l].count, 256, 0, st>>>(sym, P.panel_t[l].ptr, R, h->d_p21,
+                                                                         h->d_linv, Bp, n);
     CNB_LAUNCH_CHECK("panel_gemv_kernel");
   }
   for (int l = S.n_levels - 1; l >= 0; --l) {
-    bwd_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_front, h->d_linv,
+    bwd_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_p21, h->d_linv,
                                                                         Bp, T, n, kk);
     CNB_LAUNCH_CHECK("bwd_kernel");
   }
@@ -744,7 +754,7 @@ int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_
       CNB_LAUNCH_CHECK("asm_kernel(sparse)");
     }
     if (prec[l].second) {
-      panel_mma_kernel<<<(unsigned)prec[l].second, 128, 0, st>>>(sym, d32 + prec[l].first, R, h->d_front, h->d_linv,
+      panel_mma_kernel<<<(unsigned)prec[l].second, 128, 0, st>>>(sym, d32 + prec[l].first, R, h->d_p21, h->d_linv,
                                                                  Y, d64 + o_yoff);
       CNB_LAUNCH_CHECK("panel_mma_kernel");
     }
