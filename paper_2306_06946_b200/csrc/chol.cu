@@ -64,86 +64,100 @@ __global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t
   }
 }
 
-// POTRF of the kw x kw diagonal block of panel k0 (one CTA per front).
-__global__ void __launch_bounds__(256) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
-                                                    double* __restrict__ front, DevStatus* st) {
+// POTRF of the kw x kw diagonal block of panel k0 and the inverse of the
+// resulting L_kk (kept in kkinv[s], 32 x 32 row-major, for the TRSM, which
+// then is a plain DMMA product).  One CTA per front, one thread per block
+// entry (32 x 32 = 1024 threads): every elimination step is a single
+// parallel update between barriers, and the code stays a compact loop
+// (a fully unrolled register version thrashes the instruction cache).
+// Rows / columns >= kw are padded with the identity.
+__global__ void __launch_bounds__(1024) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
+                                                     double* __restrict__ front, double* __restrict__ kkinv,
+                                                     DevStatus* st) {
   __shared__ double a[kPanel][kPanel + 1];
+  __shared__ double y[kPanel][kPanel + 1];
   const int64_t s = tasks[blockIdx.x];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
   const int kw = (int)min((int64_t)kPanel, nc - k0);
   double* F = front + S.front_off[s];
-  for (int e = threadIdx.x; e < kw * kw; e += blockDim.x) {
-    int i = e % kw, j = e / kw;
-    a[i][j] = (i >= j) ? F[(int64_t)(k0 + j) * f + k0 + i] : 0.0;
-  }
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // column, row
+  a[ty][tx] = (ty < kw && tx <= ty) ? F[(int64_t)(k0 + tx) * f + k0 + ty] : (tx == ty ? 1.0 : 0.0);
   __syncthreads();
-  // warp 0 factors the block with rows in registers: lane i owns row i, the
-  // column entries it needs from other rows arrive by shuffle (right-looking)
-  if (threadIdx.x < 32) {
-    const int i = threadIdx.x;
-    double r[kPanel];
-#pragma unroll
-    for (int l = 0; l < kPanel; ++l) r[l] = (i < kw && l < kw) ? a[i][l] : 0.0;
-#pragma unroll
-    for (int j = 0; j < kPanel; ++j) {
-      if (j < kw) {
-        double d = __shfl_sync(0xffffffffu, r[j], j);
-        if (!(d > 0.0)) {
-          if (i == 0) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
-          d = nan("");
-        }
-        const double piv = sqrt(d), rp = 1.0 / piv;
-        if (i == j) r[j] = piv;
-        else if (i > j) r[j] *= rp;
-#pragma unroll
-        for (int l = j + 1; l < kPanel; ++l) {
-          const double llj = __shfl_sync(0xffffffffu, r[j], l);
-          if (i >= l) r[l] = fma(-r[j], llj, r[l]);
-        }
-      }
+  for (int j = 0; j < kw; ++j) {
+    if (tx == j && ty == j) {
+      const double d = a[j][j];
+      if (!(d > 0.0)) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
+      a[j][j] = d > 0.0 ? sqrt(d) : __longlong_as_double(0x7ff8000000000000LL);
     }
-#pragma unroll
-    for (int l = 0; l < kPanel; ++l)
-      if (i < kw && l <= i) a[i][l] = r[l];
+    __syncthreads();
+    if (tx == j && ty > j) a[ty][j] /= a[j][j];
+    __syncthreads();
+    if (tx > j && ty >= tx) a[ty][tx] = fma(-a[ty][j], a[tx][j], a[ty][tx]);
+    __syncthreads();
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < kw * kw; e += blockDim.x) {
-    int i = e % kw, j = e / kw;
-    if (i >= j) F[(int64_t)(k0 + j) * f + k0 + i] = a[i][j];
+  if (ty < kw && tx <= ty) F[(int64_t)(k0 + tx) * f + k0 + ty] = a[ty][tx];
+  // Y = L^{-1} row by row: Y[k][c] = (delta_kc - sum_{m<k} L[k][m] Y[m][c]) / L[k][k]
+  double acc = 0.0;
+  for (int k = 0; k < kPanel; ++k) {
+    if (ty == k) y[k][tx] = tx <= k ? ((tx == k ? 1.0 : 0.0) - acc) / a[k][k] : 0.0;
+    __syncthreads();
+    if (ty > k && tx <= k) acc = fma(a[ty][k], y[k][tx], acc);
   }
+  kkinv[s * (kPanel * kPanel) + ty * kPanel + tx] = y[ty][tx];
 }
 
-// TRSM: rows below the diagonal block, X L_kk^T = B (task = front, chunk).
-__global__ void __launch_bounds__(kTile) trsm_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
-                                                     double* __restrict__ front) {
-  __shared__ double L[kPanel][kPanel + 1];
+// TRSM of the rows below the diagonal block: X = B L_kk^{-T} as a DMMA product
+// with the inverse from potrf.  task = (front, 64-row chunk); 4 warps x 16 rows.
+__global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
+                                                   double* __restrict__ front, const double* __restrict__ kkinv) {
+  constexpr int LD = kPanel + 4;
+  __shared__ double As[64 * LD];
+  __shared__ double Is[kPanel * LD];
   const int64_t s = tasks[2 * blockIdx.x];
   const int64_t chunk = tasks[2 * blockIdx.x + 1];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
   const int kw = (int)min((int64_t)kPanel, nc - k0);
   double* F = front + S.front_off[s];
-  for (int e = threadIdx.x; e < kw * kw; e += blockDim.x) {
-    int i = e % kw, j = e / kw;
-    L[i][j] = (i >= j) ? F[(int64_t)(k0 + j) * f + k0 + i] : 0.0;
+  const int64_t r0 = k0 + kw + chunk * 64;
+  for (int e = threadIdx.x; e < 64 * kPanel; e += blockDim.x) {
+    const int rr = e % 64, k = e / 64;
+    const int64_t r = r0 + rr;
+    cp_async8(&As[rr * LD + k], F + (int64_t)(k0 + k) * f + r, r < f && k < kw);
   }
+  const double* Y = kkinv + s * (kPanel * kPanel);
+  for (int e = threadIdx.x; e < kPanel * kPanel; e += blockDim.x)
+    cp_async8(&Is[(e / kPanel) * LD + (e % kPanel)], Y + e, true);
+  cp_async_wait_all();
   __syncthreads();
-  const int64_t r = k0 + kw + chunk * kTile + threadIdx.x;
-  if (r >= f) return;
-  double x[kPanel];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[2][4][2];
 #pragma unroll
-  for (int j = 0; j < kPanel; ++j) x[j] = j < kw ? F[(int64_t)(k0 + j) * f + r] : 0.0;
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
-  for (int j = 0; j < kPanel; ++j) {
-    if (j < kw) {
-      double v = x[j];
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll
-      for (int l = 0; l < j; ++l) v = fma(-x[l], L[j][l], v);
-      x[j] = v / L[j][j];
-    }
+  for (int kk = 0; kk < kPanel; kk += 4) {
+    double fa[2], fb[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) fa[a] = As[(16 * warp + 8 * a + g) * LD + kk + t];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) fb[b] = Is[(8 * b + g) * LD + kk + t];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
   }
 #pragma unroll
-  for (int j = 0; j < kPanel; ++j)
-    if (j < kw) F[(int64_t)(k0 + j) * f + r] = x[j];
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int64_t r = r0 + 16 * warp + 8 * a + g;
+        const int j = 8 * b + 2 * t + hh;
+        if (r < f && j < kw) F[(int64_t)(k0 + j) * f + r] = acc[a][b][hh];
+      }
 }
 
 // SYRK trailing update on a 64x64 tile with DMMA:
@@ -165,9 +179,10 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
     const int rr = e % kTile, kk = e / kTile;
     const bool kin = kk < kw;
     const int64_t ri = r0 + rr, rj = c0 + rr;
-    Pi[rr * kSP + kk] = (kin && ri < f) ? F[(int64_t)(k0 + kk) * f + ri] : 0.0;
-    Pj[rr * kSP + kk] = (kin && rj < f) ? F[(int64_t)(k0 + kk) * f + rj] : 0.0;
+    cp_async8(&Pi[rr * kSP + kk], F + (int64_t)(k0 + kk) * f + ri, kin && ri < f);
+    cp_async8(&Pj[rr * kSP + kk], F + (int64_t)(k0 + kk) * f + rj, kin && rj < f);
   }
+  cp_async_wait_all();
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -189,6 +204,9 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
 #pragma unroll
       for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
   }
+  // epilogue: issue every C load before the first store (F aliases itself, so
+  // the compiler would otherwise serialise load -> subtract -> store)
+  double cv[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -197,7 +215,17 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
       for (int h = 0; h < 2; ++h) {
         const int64_t r = r0 + wy + 8 * a + g;
         const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-        if (r < f && c < f && r >= c) F[c * f + r] -= acc[a][b][h];
+        cv[a][b][h] = (r < f && c < f && r >= c) ? F[c * f + r] : 0.0;
+      }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = r0 + wy + 8 * a + g;
+        const int64_t c = c0 + wx + 8 * b + 2 * t + h;
+        if (r < f && c < f && r >= c) F[c * f + r] = cv[a][b][h] - acc[a][b][h];
       }
 }
 
@@ -288,6 +316,8 @@ static int chol_upload(CholHandle* h) {
   CNB_CUDA(cudaMalloc((void**)&h->d_front, std::max<int64_t>(1, S.front_off[S.ns]) * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_linv, std::max<int64_t>(1, h->linv_off[S.ns]) * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_p21, std::max<int64_t>(1, h->p21_off[S.ns]) * sizeof(double)));
+  CNB_CUDA(cudaMalloc((void**)&h->d_kkinv, std::max<int64_t>(1, S.ns) * kPanel * kPanel * sizeof(double)));
+  CNB_CUDA(cudaMalloc((void**)&h->d_vals, std::max<int64_t>(1, S.csr_nnz) * sizeof(double)));
   h->uploaded = true;
   return CNB_OK;
 }
@@ -295,7 +325,11 @@ static int chol_upload(CholHandle* h) {
 static void chol_free(CholHandle* h) {
   void* ptrs[] = {h->d_first, h->d_rows_ptr, h->d_rows, h->d_front_off, h->d_child_ptr, h->d_child,
                   h->d_rel_ptr, h->d_rel, h->d_map_src, h->d_map_dst, h->d_perm, h->d_front, h->d_tasks,
-                  h->d_linv, h->d_linv_off, h->d_p21, h->d_p21_off};
+                  h->d_linv, h->d_linv_off, h->d_p21, h->d_p21_off, h->d_kkinv, h->d_vals};
+  if (h->factor_exec) cudaGraphExecDestroy(h->factor_exec);
+  h->factor_exec = nullptr;
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  h->cap_stream = nullptr;
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->plan1.release();
@@ -324,6 +358,43 @@ static std::map<std::string, std::pair<const void*, size_t>> export_table(const 
   add("level_ptr", S.level_ptr);
   add("level_sn", S.level_sn);
   return t;
+}
+
+static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
+  const Symbolic& S = h->S;
+  DevSym sym = h->sym();
+  int rc;
+  CNB_CUDA(cudaMemsetAsync(h->d_front, 0, std::max<int64_t>(1, S.front_off[S.ns]) * sizeof(double), st));
+  const int64_t nmap = (int64_t)S.map_src.size();
+  if (nmap) {
+    scatter_kernel<<<grid_for(nmap, 256), 256, 0, st>>>(nmap, h->d_map_src, h->d_map_dst, h->d_vals, h->d_front);
+    CNB_LAUNCH_CHECK("scatter_kernel");
+  }
+  for (int l = 0; l < S.n_levels; ++l) {
+    if (h->ea[l].count) {
+      extend_add_kernel<<<(unsigned)h->ea[l].count, 256, 0, st>>>(sym, h->ea[l].ptr, h->d_front);
+      CNB_LAUNCH_CHECK("extend_add_kernel");
+    }
+    for (size_t p = 0; p < h->potrf[l].size(); ++p) {
+      const int k0 = (int)(p * kPanel);
+      if (h->potrf[l][p].count) {
+        potrf_kernel<<<(unsigned)h->potrf[l][p].count, 1024, 0, st>>>(sym, h->potrf[l][p].ptr, k0, h->d_front,
+                                                                       h->d_kkinv, d_status);
+        CNB_LAUNCH_CHECK("potrf_kernel");
+      }
+      if (h->trsm[l][p].count) {
+        trsm_kernel<<<(unsigned)h->trsm[l][p].count, 128, 0, st>>>(sym, h->trsm[l][p].ptr, k0, h->d_front,
+                                                                   h->d_kkinv);
+        CNB_LAUNCH_CHECK("trsm_kernel");
+      }
+      if (h->syrk[l][p].count) {
+        syrk_kernel<<<(unsigned)h->syrk[l][p].count, 128, 0, st>>>(sym, h->syrk[l][p].ptr, k0, h->d_front);
+        CNB_LAUNCH_CHECK("syrk_kernel");
+      }
+    }
+    if ((rc = trinv_level(h, l, st))) return rc;
+  }
+  return CNB_OK;
 }
 
 }  // namespace cnb
@@ -401,35 +472,38 @@ int cnb_chol_factor(cnb_chol_t hh, const double* vals, cnb_status_t* d_status, v
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const Symbolic& S = h->S;
-  DevSym sym = h->sym();
-  CNB_CUDA(cudaMemsetAsync(h->d_front, 0, std::max<int64_t>(1, S.front_off[S.ns]) * sizeof(double), st));
-  const int64_t nmap = (int64_t)S.map_src.size();
-  if (nmap) {
-    scatter_kernel<<<grid_for(nmap, 256), 256, 0, st>>>(nmap, h->d_map_src, h->d_map_dst, vals, h->d_front);
-    CNB_LAUNCH_CHECK("scatter_kernel");
-  }
-  for (int l = 0; l < S.n_levels; ++l) {
-    if (h->ea[l].count) {
-      extend_add_kernel<<<(unsigned)h->ea[l].count, 256, 0, st>>>(sym, h->ea[l].ptr, h->d_front);
-      CNB_LAUNCH_CHECK("extend_add_kernel");
+  // values into the handle's own buffer: the captured graph reads fixed addresses
+  CNB_CUDA(cudaMemcpyAsync(h->d_vals, vals, std::max<int64_t>(1, S.csr_nnz) * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st));
+  if (use_graphs()) {
+    if (h->factor_exec && h->factor_status != (void*)d_status) {
+      cudaGraphExecDestroy(h->factor_exec);
+      h->factor_exec = nullptr;
     }
-    for (size_t p = 0; p < h->potrf[l].size(); ++p) {
-      const int k0 = (int)(p * kPanel);
-      if (h->potrf[l][p].count) {
-        potrf_kernel<<<(unsigned)h->potrf[l][p].count, 256, 0, st>>>(sym, h->potrf[l][p].ptr, k0, h->d_front,
-                                                                      (DevStatus*)d_status);
-        CNB_LAUNCH_CHECK("potrf_kernel");
+    if (!h->factor_exec) {
+      // capture on a private stream (the legacy default stream cannot capture)
+      if (!h->cap_stream) CNB_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+      const long long before = launch_count();
+      CNB_CUDA(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue_factor(h, (DevStatus*)d_status, h->cap_stream);
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(h->cap_stream, &graph);
+      if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
       }
-      if (h->trsm[l][p].count) {
-        trsm_kernel<<<(unsigned)h->trsm[l][p].count, kTile, 0, st>>>(sym, h->trsm[l][p].ptr, k0, h->d_front);
-        CNB_LAUNCH_CHECK("trsm_kernel");
-      }
-      if (h->syrk[l][p].count) {
-        syrk_kernel<<<(unsigned)h->syrk[l][p].count, 128, 0, st>>>(sym, h->syrk[l][p].ptr, k0, h->d_front);
-        CNB_LAUNCH_CHECK("syrk_kernel");
-      }
+      if (e != cudaSuccess) return cuda_status(e, "cudaStreamEndCapture(factor)");
+      e = cudaGraphInstantiate(&h->factor_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return cuda_status(e, "cudaGraphInstantiate(factor)");
+      h->factor_nodes = launch_count() - before;
+      add_launches(-h->factor_nodes);  // captured, not launched
+      h->factor_status = (void*)d_status;
     }
-    if ((rc = trinv_level(h, l, st))) return rc;
+    CNB_CUDA(cudaGraphLaunch(h->factor_exec, st));
+    add_launches(h->factor_nodes);
+  } else {
+    if ((rc = enqueue_factor(h, (DevStatus*)d_status, st))) return rc;
   }
   h->factored = true;
   return CNB_OK;

@@ -86,6 +86,12 @@ struct CholHandle {
   double* d_front = nullptr;
   double* d_linv = nullptr;
   double* d_p21 = nullptr;
+  double* d_kkinv = nullptr;  // per supernode: inverse of the current 32x32 panel diagonal block
+  double* d_vals = nullptr;   // CSR values being factorised (fixed address for the graph)
+  cudaGraphExec_t factor_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  void* factor_status = nullptr;
+  long long factor_nodes = 0;
   std::vector<int64_t> linv_off, p21_off;
   int32_t* d_tasks = nullptr;
   std::vector<DevTasks> ea, trinv, p21;                  // per level

@@ -25,6 +25,9 @@ int cuda_status(cudaError_t e, const char* where);
 // Every kernel launch is followed by this check; it also counts launches
 // (cnb_launch_count) so benchmarks report how many of our kernels ran.
 void count_launch();
+void add_launches(long long n);
+long long launch_count();
+bool use_graphs();
 #define CNB_LAUNCH_CHECK(where)                                                \
   do {                                                                         \
     ::cnb::count_launch();                                                     \
@@ -72,6 +75,17 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
+
+// Asynchronous global -> shared copy of one fp64 (LDGSTS): the warp keeps
+// issuing instead of waiting for each load before its shared store.
+// pred == false zero-fills the destination without touching src.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

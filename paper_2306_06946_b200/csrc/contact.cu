@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -20,6 +21,17 @@ static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
+// CUDA graphs replay static launch sequences (factorisation); CNB_NO_GRAPHS=1 disables
+bool use_graphs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CNB_NO_GRAPHS");
+    v = (e && e[0] && e[0] != '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 void set_error(const char* fmt, ...) {
   char buf[1024];

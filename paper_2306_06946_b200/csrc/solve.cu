@@ -65,8 +65,9 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
     const int bw = (int)min((int64_t)32, nc - kb);
     for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
       const int i = e & 31, j = e >> 5;
-      sL[i][j] = (i < bw && j < bw && i >= j) ? F[(kb + j) * f + kb + i] : 0.0;
+      cp_async8(&sL[i][j], F + (kb + j) * f + kb + i, i < bw && j < bw && i >= j);
     }
+    cp_async_wait_all();
     __syncthreads();
     if (warp == 0) {
       double v[kInvCols];
@@ -177,8 +178,9 @@ __global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t
     __syncthreads();
     for (int e = threadIdx.x; e < jn * NC; e += blockDim.x) {
       const int j = e % jn, c = e / jn;
-      rt[j][c] = c < ncols ? Rs[c * f + jb + j] : 0.0;
+      cp_async8(&rt[j][c], Rs + c * f + jb + j, c < ncols);
     }
+    cp_async_wait_all();
     __syncthreads();
     if (i < f) {
       if (i < nc) {
@@ -248,13 +250,15 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int rr = e % kMT, kk = e / kMT;
       const int64_t i = r0 + rr, j = k0 + kk;
-      As[rr * kMS + kk] = (i < f && j < nc) ? panel_entry(P, Li, nc, nr, i, j) : 0.0;
+      const bool in = i < f && j < nc && (i >= nc || j <= i);
+      cp_async8(&As[rr * kMS + kk], i < nc ? Li + j * nc + i : P + j * nr + (i - nc), in);
     }
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int kk = e % kMK, cc = e / kMK;
       const int64_t j = k0 + kk, c = c0 + cc;
-      Bs[cc * kMS + kk] = (j < nc && c < ws) ? Rs[c * f + j] : 0.0;
+      cp_async8(&Bs[cc * kMS + kk], Rs + c * f + j, j < nc && c < ws);
     }
+    cp_async_wait_all();
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < kMK; kk += 4) {
@@ -354,13 +358,14 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int rr = e % kMT, kk = e / kMT;
       const int64_t q = q0 + rr, k = k0 + kk;
-      As[rr * kMS + kk] = (q < nr && k < nc) ? F[k * f + nc + q] : 0.0;
+      cp_async8(&As[rr * kMS + kk], F + k * f + nc + q, q < nr && k < nc);
     }
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int kk = e % kMK, cc = e / kMK;
       const int64_t k = k0 + kk, c = c0 + cc;
-      Bs[cc * kMS + kk] = (k < nc && c < nc && k >= c) ? Li[c * nc + k] : 0.0;
+      cp_async8(&Bs[cc * kMS + kk], Li + c * nc + k, k < nc && c < nc && k >= c);
     }
+    cp_async_wait_all();
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < kMK; kk += 4) {
@@ -553,9 +558,10 @@ __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const do
         const int kk = idx % kGK, cc = idx / kGK;
         const int64_t k = k0 + kk;
         const int64_t la = ra0 + cc - lo, lb = rb0 + cc - lo;
-        Ya[cc * kGS + kk] = (k < nc && la >= 0 && la < w) ? Ys[la * nc + k] : 0.0;
-        Yb[cc * kGS + kk] = (k < nc && lb >= 0 && lb < w) ? Ys[lb * nc + k] : 0.0;
+        cp_async8(&Ya[cc * kGS + kk], Ys + la * nc + k, k < nc && la >= 0 && la < w);
+        cp_async8(&Yb[cc * kGS + kk], Ys + lb * nc + k, k < nc && lb >= 0 && lb < w);
       }
+      cp_async_wait_all();
       __syncthreads();
 #pragma unroll
       for (int kk = 0; kk < kGK; kk += 4) {
