@@ -171,9 +171,14 @@ int cnb_chol_solve(cnb_chol_t h, const double* B, int64_t ldb, double* X, int64_
  * CSC form (colptr, rowidx = DoF ids, vals).  Y = L^{-1} P S^T is formed only
  * on the elimination paths of the columns and U = Y^T Y by fp64 MMA tiles.
  * Replaces solve_multi(S^T) + S @ X of assemble_Wg constraints.py:175-178.
- * flops_out (host, may be NULL) = {forward-solve flops, Gram flops}. */
+ * flops_out (host, may be NULL) = {forward-solve flops, Gram flops}.
+ * Multi-GPU: with world > 1 the 64x64 Gram tiles are split
+ * round-robin over ranks; this rank writes its tiles and zeros elsewhere, and
+ * the caller sums U over ranks (NCCL all-reduce) — exact, since every entry is
+ * produced by exactly one rank.  world = 1: the whole U. */
 int cnb_chol_compliance(cnb_chol_t h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
-                        const double* vals, double* U, int64_t ldu, double* flops_out, void* stream);
+                        const double* vals, double* U, int64_t ldu, double* flops_out, int32_t rank,
+                        int32_t world, void* stream);
 
 /* ---- FE assembly (contactnewton/dynamics.py) ------------------------------ */
 

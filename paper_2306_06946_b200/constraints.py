@@ -207,7 +207,7 @@ def assemble_W_standard(H_by_object: dict, F_by_object: dict) -> Delassus:
     return Delassus(W)
 
 
-def assemble_Wg(S_by_object: dict, F_by_object: dict) -> MappingDelassus:
+def assemble_Wg(S_by_object: dict, F_by_object: dict, group=None) -> MappingDelassus:
     """W_g = sum_o S_o A_o^-1 S_o^T and the per-object parts (constraints.py:155-179).
 
     Per object: Y = L^-1 P S^T by a sparse-RHS forward solve over the supernodal
@@ -228,7 +228,7 @@ def assemble_Wg(S_by_object: dict, F_by_object: dict) -> MappingDelassus:
         F = F_by_object[oid]
         if S.shape[1] != F.dim:
             raise DimensionMismatchError(f"object {oid}: S has {S.shape[1]} columns, factorization dim {F.dim}")
-        comp = object_compliance(S, F, dim)
+        comp = object_compliance(S, F, dim, group=group)
         per[oid] = comp
         if wg is None:
             wg = comp.dense(dim).clone() if len(ids) > 1 else comp.dense(dim)

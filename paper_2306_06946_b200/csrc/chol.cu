@@ -519,13 +519,14 @@ int cnb_chol_solve(cnb_chol_t hh, const double* B, int64_t ldb, double* X, int64
 }
 
 int cnb_chol_compliance(cnb_chol_t hh, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
-                        const double* vals, double* U, int64_t ldu, double* flops_out, void* stream) {
+                        const double* vals, double* U, int64_t ldu, double* flops_out, int32_t rank, int32_t world,
+                        void* stream) {
   CholHandle* h = H(hh);
   if (!h->factored) {
     set_error("chol_compliance: not factorised");
     return CNB_E_VALIDATION;
   }
-  return compliance(h, ncols, colptr, rowidx, vals, U, ldu, flops_out, (cudaStream_t)stream);
+  return compliance(h, ncols, colptr, rowidx, vals, U, ldu, flops_out, rank, world, (cudaStream_t)stream);
 }
 
 }  // extern "C"

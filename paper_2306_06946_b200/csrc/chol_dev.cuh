@@ -110,7 +110,7 @@ struct CholHandle {
 // solve.cu
 int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t k, cudaStream_t st);
 int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx, const double* vals,
-               double* U, int64_t ldu, double* flops_out, cudaStream_t st);
+               double* U, int64_t ldu, double* flops_out, int rank, int world, cudaStream_t st);
 int trinv_level(CholHandle* h, int level, cudaStream_t st);
 
 }  // namespace cnb

@@ -530,10 +530,11 @@ __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const do
                                                    const int64_t* __restrict__ yoff, const int32_t* __restrict__ tile_ptr,
                                                    const int32_t* __restrict__ tile_sn, int64_t ncols,
                                                    const int64_t* __restrict__ sorted_cols, double* __restrict__ U,
-                                                   int64_t ldu) {
+                                                   int64_t ldu, int rank, int world) {
   __shared__ double Ya[kGT * kGS];
   __shared__ double Yb[kGT * kGS];
-  const int64_t t = blockIdx.x;
+  // multi-GPU: this rank owns tiles t = rank, rank + world, ... (round robin)
+  const int64_t t = (int64_t)blockIdx.x * world + rank;
   int64_t A = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
   while ((A + 1) * (A + 2) / 2 <= t) ++A;
   while (A * (A + 1) / 2 > t) --A;
@@ -700,8 +701,12 @@ static int build_compliance_plan(const Symbolic& S, int64_t ncols, const int64_t
 }
 
 int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx, const double* vals,
-               double* U, int64_t ldu, double* flops_out, cudaStream_t st) {
+               double* U, int64_t ldu, double* flops_out, int rank, int world, cudaStream_t st) {
   if (ncols <= 0) return CNB_OK;
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("compliance: invalid rank %d / world %d", rank, world);
+    return CNB_E_VALIDATION;
+  }
   const Symbolic& S = h->S;
   CompliancePlan P;
   int rc = build_compliance_plan(S, ncols, colptr, rowidx, vals, P);
@@ -767,9 +772,16 @@ int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_
   }
   const int64_t nt = (ncols + kGT - 1) / kGT;
   const int64_t npairs = nt * (nt + 1) / 2;
-  gram_kernel<<<(unsigned)npairs, 128, 0, st>>>(sym, R, Y, d64 + o_yoff, d32 + o_tptr, d32 + o_tsn, ncols,
-                                                d64 + o_sorted, U, ldu);
-  CNB_LAUNCH_CHECK("gram_kernel");
+  if (world > 1) {
+    // only this rank's tiles are written; the caller sums U over ranks
+    for (int64_t r = 0; r < ncols; ++r) CNB_CUDA(cudaMemsetAsync(U + r * ldu, 0, ncols * sizeof(double), st));
+  }
+  const int64_t owned = (npairs - rank + world - 1) / world;
+  if (owned > 0) {
+    gram_kernel<<<(unsigned)owned, 128, 0, st>>>(sym, R, Y, d64 + o_yoff, d32 + o_tptr, d32 + o_tsn, ncols,
+                                                 d64 + o_sorted, U, ldu, rank, world);
+    CNB_LAUNCH_CHECK("gram_kernel");
+  }
   h->last_fwd_flops = P.fwd_flops;
   h->last_gram_flops = P.gram_flops;
   return CNB_OK;

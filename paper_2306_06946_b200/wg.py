@@ -19,8 +19,13 @@ from . import _device as dv
 from . import _lib
 
 
-def object_compliance(S, F, dim: int, stats: dict | None = None):
+def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, shard: bool = True):
+    """U_o for one object.  Under torch.distributed (world > 1) the Gram tiles are
+    split across ranks and summed with one all-reduce (parallel.py)."""
     from .constraints import ObjectCompliance
+    from .parallel import reduce_shards, world_info
+
+    rank, world = world_info(group) if shard else (0, 1)
 
     idx, side = S.idx, S.side
     mo = len(idx)
@@ -40,7 +45,9 @@ def object_compliance(S, F, dim: int, stats: dict | None = None):
         vals = np.ascontiguousarray(csr.data[sel], dtype=np.float64)
         fl = (ctypes.c_double * 2)()
         _lib.call("cnb_chol_compliance", F._h, 3 * mo, colptr.ctypes.data, rowidx.ctypes.data, vals.ctypes.data,
-                  U.data_ptr(), 3 * mo, fl, _lib.stream())
+                  U.data_ptr(), 3 * mo, fl, rank, world, _lib.stream())
+        if world > 1:
+            reduce_shards(U, group)
         if stats is not None:
             stats["fwd_flops"] = stats.get("fwd_flops", 0.0) + fl[0]
             stats["gram_flops"] = stats.get("gram_flops", 0.0) + fl[1]
