@@ -71,39 +71,54 @@ __global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t
 // parallel update between barriers, and the code stays a compact loop
 // (a fully unrolled register version thrashes the instruction cache).
 // Rows / columns >= kw are padded with the identity.
-__global__ void __launch_bounds__(1024) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
-                                                     double* __restrict__ front, double* __restrict__ kkinv,
-                                                     DevStatus* st) {
+__global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
+                                                   double* __restrict__ front, double* __restrict__ kkinv,
+                                                   DevStatus* st) {
+  // One warp per front.  Left-looking by columns: at step j lane i (row i)
+  // forms l_ij = (a_ij - sum_{k<j} l_ik l_jk) / l_jj with a rolled dot-product
+  // loop over shared memory (own row + broadcast row j); no block barriers.
   __shared__ double a[kPanel][kPanel + 1];
   __shared__ double y[kPanel][kPanel + 1];
+  __shared__ double rdiag[kPanel];
   const int64_t s = tasks[blockIdx.x];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
   const int kw = (int)min((int64_t)kPanel, nc - k0);
   double* F = front + S.front_off[s];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // column, row
-  a[ty][tx] = (ty < kw && tx <= ty) ? F[(int64_t)(k0 + tx) * f + k0 + ty] : (tx == ty ? 1.0 : 0.0);
-  __syncthreads();
+  const int i = threadIdx.x;
+  for (int l = 0; l < kPanel; ++l)  // lane i loads column l: coalesced over rows
+    a[i][l] = (i < kw && l < kw && l <= i) ? F[(int64_t)(k0 + l) * f + k0 + i] : (l == i ? 1.0 : 0.0);
+  __syncwarp();
   for (int j = 0; j < kw; ++j) {
-    if (tx == j && ty == j) {
-      const double d = a[j][j];
-      if (!(d > 0.0)) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
-      a[j][j] = d > 0.0 ? sqrt(d) : __longlong_as_double(0x7ff8000000000000LL);
+    double v = a[i][j];
+    for (int k = 0; k < j; ++k) v = fma(-a[i][k], a[j][k], v);
+    const double d = __shfl_sync(0xffffffffu, v, j);
+    if (!(d > 0.0) && i == 0) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
+    const double ljj = d > 0.0 ? sqrt(d) : __longlong_as_double(0x7ff8000000000000LL);
+    const double r = 1.0 / ljj;
+    if (i == j) {
+      a[j][j] = ljj;
+      rdiag[j] = r;
+    } else if (i > j) {
+      a[i][j] = v * r;
     }
-    __syncthreads();
-    if (tx == j && ty > j) a[ty][j] /= a[j][j];
-    __syncthreads();
-    if (tx > j && ty >= tx) a[ty][tx] = fma(-a[ty][j], a[tx][j], a[ty][tx]);
-    __syncthreads();
+    __syncwarp();
   }
-  if (ty < kw && tx <= ty) F[(int64_t)(k0 + tx) * f + k0 + ty] = a[ty][tx];
-  // Y = L^{-1} row by row: Y[k][c] = (delta_kc - sum_{m<k} L[k][m] Y[m][c]) / L[k][k]
-  double acc = 0.0;
-  for (int k = 0; k < kPanel; ++k) {
-    if (ty == k) y[k][tx] = tx <= k ? ((tx == k ? 1.0 : 0.0) - acc) / a[k][k] : 0.0;
-    __syncthreads();
-    if (ty > k && tx <= k) acc = fma(a[ty][k], y[k][tx], acc);
+  for (int l = kw; l < kPanel; ++l)
+    if (i == l) rdiag[l] = 1.0;
+  __syncwarp();
+  for (int l = 0; l < kw; ++l)
+    if (i < kw && l <= i) F[(int64_t)(k0 + l) * f + k0 + i] = a[i][l];
+  // Y = L^{-1}: row by row, lane c owns column c:
+  // Y[r][c] = (delta_rc - sum_{k=c}^{r-1} L[r][k] Y[k][c]) / L[r][r]
+  const int c = threadIdx.x;
+  for (int r = 0; r < kPanel; ++r) {
+    double v = (r == c) ? 1.0 : 0.0;
+    for (int k = c; k < r; ++k) v = fma(-a[r][k], y[k][c], v);
+    y[r][c] = c <= r ? v * rdiag[r] : 0.0;
+    __syncwarp();
   }
-  kkinv[s * (kPanel * kPanel) + ty * kPanel + tx] = y[ty][tx];
+  double* Y = kkinv + s * (kPanel * kPanel);
+  for (int r = 0; r < kPanel; ++r) Y[r * kPanel + c] = y[r][c];
 }
 
 // TRSM of the rows below the diagonal block: X = B L_kk^{-T} as a DMMA product
@@ -378,7 +393,7 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
     for (size_t p = 0; p < h->potrf[l].size(); ++p) {
       const int k0 = (int)(p * kPanel);
       if (h->potrf[l][p].count) {
-        potrf_kernel<<<(unsigned)h->potrf[l][p].count, 1024, 0, st>>>(sym, h->potrf[l][p].ptr, k0, h->d_front,
+        potrf_kernel<<<(unsigned)h->potrf[l][p].count, 32, 0, st>>>(sym, h->potrf[l][p].ptr, k0, h->d_front,
                                                                        h->d_kkinv, d_status);
         CNB_LAUNCH_CHECK("potrf_kernel");
       }
