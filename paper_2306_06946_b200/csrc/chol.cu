@@ -89,8 +89,18 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
     a[i][l] = (i < kw && l < kw && l <= i) ? F[(int64_t)(k0 + l) * f + k0 + i] : (l == i ? 1.0 : 0.0);
   __syncwarp();
   for (int j = 0; j < kw; ++j) {
-    double v = a[i][j];
-    for (int k = 0; k < j; ++k) v = fma(-a[i][k], a[j][k], v);
+    // four independent partial sums: dependent fp64 FMA chains are the
+    // latency bottleneck of this kernel
+    double v0 = a[i][j], v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    int k = 0;
+    for (; k + 4 <= j; k += 4) {
+      v0 = fma(-a[i][k], a[j][k], v0);
+      v1 = fma(-a[i][k + 1], a[j][k + 1], v1);
+      v2 = fma(-a[i][k + 2], a[j][k + 2], v2);
+      v3 = fma(-a[i][k + 3], a[j][k + 3], v3);
+    }
+    for (; k < j; ++k) v0 = fma(-a[i][k], a[j][k], v0);
+    const double v = (v0 + v1) + (v2 + v3);
     const double d = __shfl_sync(0xffffffffu, v, j);
     if (!(d > 0.0) && i == 0) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
     const double ljj = d > 0.0 ? sqrt(d) : __longlong_as_double(0x7ff8000000000000LL);
@@ -112,9 +122,16 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
   // Y[r][c] = (delta_rc - sum_{k=c}^{r-1} L[r][k] Y[k][c]) / L[r][r]
   const int c = threadIdx.x;
   for (int r = 0; r < kPanel; ++r) {
-    double v = (r == c) ? 1.0 : 0.0;
-    for (int k = c; k < r; ++k) v = fma(-a[r][k], y[k][c], v);
-    y[r][c] = c <= r ? v * rdiag[r] : 0.0;
+    double v0 = (r == c) ? 1.0 : 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    int k = c;
+    for (; k + 4 <= r; k += 4) {
+      v0 = fma(-a[r][k], y[k][c], v0);
+      v1 = fma(-a[r][k + 1], y[k + 1][c], v1);
+      v2 = fma(-a[r][k + 2], y[k + 2][c], v2);
+      v3 = fma(-a[r][k + 3], y[k + 3][c], v3);
+    }
+    for (; k < r; ++k) v0 = fma(-a[r][k], y[k][c], v0);
+    y[r][c] = c <= r ? ((v0 + v1) + (v2 + v3)) * rdiag[r] : 0.0;
     __syncwarp();
   }
   double* Y = kkinv + s * (kPanel * kPanel);

@@ -117,6 +117,72 @@ __device__ __forceinline__ int local_solve_dev(const double d[3], const double l
   return 0;
 }
 
+// Per-group constants of local_solve that depend only on W (and h): computed
+// once per block load, in parallel over the solver lanes, so the sequential
+// per-group chain is a handful of multiply-adds instead of four divisions
+// and a hypot (dependent fp64 operations cost ~30+ cycles each on sm_100a).
+struct GroupConst {
+  double ihw;        // 1 / (h^2 W_nn)
+  double htn0, htn1; // h^2 W_tn
+  double it00, it01, it10, it11;  // (h^2 W_tt)^{-1}
+  int bad;           // bit 0: W_nn <= 0, bit 1: det(h^2 W_tt) <= 0
+};
+
+__device__ __forceinline__ void group_const(const double Wd[9], double h2, GroupConst& k) {
+  k.bad = 0;
+  const double Wnn = Wd[0];
+  if (!(Wnn > 0.0)) k.bad |= 1;
+  k.ihw = 1.0 / mul(h2, Wnn);
+  k.htn0 = mul(h2, Wd[3]);
+  k.htn1 = mul(h2, Wd[6]);
+  const double T00 = mul(h2, Wd[4]), T01 = mul(h2, Wd[5]);
+  const double T10 = mul(h2, Wd[7]), T11 = mul(h2, Wd[8]);
+  const double det = sub(mul(T00, T11), mul(T01, T10));
+  if (!(det > 0.0)) k.bad |= 2;
+  const double idet = 1.0 / det;
+  k.it00 = T11 * idet;
+  k.it01 = -T01 * idet;
+  k.it10 = -T10 * idet;
+  k.it11 = T00 * idet;
+}
+
+// local_solve with the precomputed constants: same branches and projection
+// as solver.py:124-165; divisions by loop-invariant quantities become
+// multiplications by reciprocals (last-ulp differences only).
+__device__ __forceinline__ int local_solve_fast(const double d[3], const double l[3], const GroupConst& k,
+                                                double mu, double out[3]) {
+  if (k.bad & 1) return CNB_E_SINGULAR_BLOCK;
+  const double ln_old = l[0];
+  const double x = fma(-d[0], k.ihw, ln_old);
+  const double ln = x > 0.0 ? x : 0.0;
+  if (ln == 0.0) {
+    out[0] = out[1] = out[2] = 0.0;
+    return 0;
+  }
+  if (mu == 0.0) {
+    out[0] = ln;
+    out[1] = out[2] = 0.0;
+    return 0;
+  }
+  if (k.bad & 2) return CNB_E_SINGULAR_BLOCK;
+  const double dln = ln - ln_old;
+  const double dt0 = fma(k.htn0, dln, d[1]);
+  const double dt1 = fma(k.htn1, dln, d[2]);
+  double lt0 = l[1] - fma(k.it00, dt0, k.it01 * dt1);
+  double lt1 = l[2] - fma(k.it10, dt0, k.it11 * dt1);
+  const double radius = mu * ln;
+  const double n2 = fma(lt0, lt0, lt1 * lt1);
+  if (n2 > radius * radius) {
+    const double sc = radius * rsqrt(n2);
+    lt0 *= sc;
+    lt1 *= sc;
+  }
+  out[0] = ln;
+  out[1] = lt0;
+  out[2] = lt1;
+  return 0;
+}
+
 // Shared-memory layout of one scene's PGS.
 struct PgsSmem {
   double* lam;     // c
@@ -170,13 +236,18 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
   __syncthreads();
 
   // stage block 0: delta = delta_base (lambda = 0), diagonal tile
+  // asynchronous copy (LDGSTS) of the block's diagonal tile, then the
+  // regularisation shift on its diagonal (solver.py:119-120)
   auto stage_tile = [&](int b) {
     const int64_t r0 = (int64_t)b * kBR;
     const int rows = (int)min((int64_t)kBR, c - r0);
     for (int e = tid; e < rows * rows; e += blockDim.x) {
       int i = e / rows, j = e - i * rows;
-      sm.Wbb[i * kBR + j] = w_reg(s, sm, r0 + i, r0 + j);
+      cp_async8(&sm.Wbb[i * kBR + j], s.W + (r0 + i) * s.ldw + r0 + j, true);
     }
+    cp_async_wait_all();
+    __syncthreads();
+    for (int i = tid; i < rows; i += blockDim.x) sm.Wbb[i * kBR + i] = add(sm.Wbb[i * kBR + i], sm.dshift[(r0 + i) / 3]);
   };
   stage_tile(0);
   for (int i = tid; i < (int)min((int64_t)kBR, c); i += blockDim.x) sm.dnext[i] = s.delta_base[i];
@@ -199,21 +270,24 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
       if (warp == 0) {
         // ---- sequential block solve ----
         const bool mine = lane < ng;
-        if (mine)
+        GroupConst kc;
+        if (mine) {
           for (int a = 0; a < 3; ++a) {
             lm[a] = sm.lam[3 * (g0 + lane) + a];
             dl_[a] = sm.dnext[3 * lane + a];
           }
+          double Wd[9];
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) Wd[3 * i + j] = sm.Wbb[(3 * lane + i) * kBR + 3 * lane + j];
+          group_const(Wd, h2, kc);
+        }
         int err = 0;
         for (int g = 0; g < ng; ++g) {
           double d0 = 0, d1 = 0, d2 = 0;
           int any = 0;
           if (lane == g) {
-            double Wd[9];
-            for (int i = 0; i < 3; ++i)
-              for (int j = 0; j < 3; ++j) Wd[3 * i + j] = sm.Wbb[(3 * g + i) * kBR + 3 * g + j];
             double nw[3];
-            err = local_solve_dev(dl_, lm, Wd, s.mu, h2, nw);
+            err = local_solve_fast(dl_, lm, kc, s.mu, nw);
             if (!err) {
               d0 = sub(nw[0], lm[0]);
               d1 = sub(nw[1], lm[1]);
@@ -226,7 +300,7 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
                 lm[2] = nw[2];
               }
             } else {
-              raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), Wd[0]);
+              raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), 1.0 / kc.ihw);
             }
           }
           if (__shfl_sync(0xffffffffu, err, g)) {

@@ -63,6 +63,10 @@ def gpu_run(args):
     it_ms = [1e3 * (r + p + c) for rep in reps for r, p, c in
              zip(rep.rebuild_times, rep.pgs_times, rep.correction_times)]
     pgs_ms = [1e3 * p for rep in reps for p in rep.pgs_times]
+    phases = {f"{k}_ms": 1e3 * statistics.median(getattr(r, k) for r in reps) for k in
+              ("t_detect", "t_assemble", "t_free", "t_constraints", "t_build_wg", "t_rebuild_w", "t_pgs",
+               "t_correction", "t_final_correction", "t_step")}
+    print(json.dumps({"phases_median": {k: round(v, 3) for k, v in phases.items()}}), flush=True)
     return dict(ms_per_step=wall, ms_per_newton_iter=statistics.median(it_ms), pgs_ms_median=statistics.median(pgs_ms),
                 pgs_sweeps_per_step=statistics.mean(r.pgs_iterations_total for r in reps),
                 groups=statistics.mean(r.c_groups for r in reps), t_detect_ms=1e3 * statistics.median(
