@@ -22,6 +22,9 @@
 // The iterate is mathematically the reference's; only the association of
 // the floating-point sums of delta differs (the per-group arithmetic of
 // local_solve is reproduced operation by operation).
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cnb {
@@ -477,6 +480,345 @@ size_t pgs_max_smem() {
   return (size_t)v;
 }
 
+// ============================================================================
+// Grid-scale PGS (thousands of groups: cfg2 / cfg3)
+// ============================================================================
+// Same iterate as pgs_cta.  One persistent cooperative kernel, one CTA per SM:
+// CTA 0 is the solver (warp 0 runs the sequential block solve exactly as
+// above); every other CTA is a helper that computes, for the rows of the next
+// block, the lazy row products over all columns except the block being solved,
+// split in column chunks (partial[buf][row][chunk], summed in fixed order by
+// the solver: deterministic).  Hand-off through global counters:
+//   solved = completed block steps (release by the solver, acquire by helpers)
+//   ready  = helper CTAs done (cumulative; acquire by the solver)
+// A device-clock watchdog turns a stuck wait into an error instead of a hang.
+struct GridCtl {
+  unsigned solved, ready, stop, timeout;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// spin until *p >= target (or stop / watchdog); returns false on timeout
+__device__ bool wait_geq(volatile unsigned* p, unsigned target, volatile unsigned* stop, GridCtl* ctl) {
+  const unsigned long long t0 = global_ns();
+  while (*p < target) {
+    if (stop && *stop) return true;
+    if (global_ns() - t0 > 20000000000ull) {  // 20 s
+      atomicExch(&ctl->timeout, 1u);
+      atomicExch(&ctl->stop, 1u);
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshift, GridCtl* ctl) {
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = s.groups, c = 3 * G;
+  double tr = 0.0;
+  for (int64_t i = tid; i < c; i += blockDim.x) tr += s.W[i * s.ldw + i];
+  tr = warp_sum(tr);
+  if (lane == 0) red[warp] = tr;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    red[0] = t;
+    ctl->solved = ctl->ready = ctl->stop = ctl->timeout = 0;
+  }
+  __syncthreads();
+  double shift = 1e-10 * red[0] / (double)c;
+  if (shift <= 0.0) shift = 1e-30;
+  for (int64_t g = tid; g < G; g += blockDim.x) {
+    double a[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        a[i][j] = 0.5 * (s.W[(3 * g + i) * s.ldw + 3 * g + j] + s.W[(3 * g + j) * s.ldw + 3 * g + i]);
+    double e[3];
+    sym3_eigs(a, e);
+    const double mn = fmin(e[0], fmin(e[1], e[2]));
+    const double scale = fmax(fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))), 1e-300);
+    dshift[g] = (mn <= 1e-12 * scale) ? shift : 0.0;
+  }
+  for (int64_t i = tid; i < c; i += blockDim.x) s.lam[i] = 0.0;
+}
+
+constexpr int kGridThreads = 256;
+
+__global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, const double* __restrict__ dshift,
+                                                                double* partial, GridCtl* ctl, int nch) {
+  extern __shared__ __align__(16) char smem_raw[];
+  double* Wbb = (double*)smem_raw;         // kBR x kBR
+  double* dcur = Wbb + kBR * kBR;          // kBR
+  double* red = dcur + kBR;                // 32
+  int* flags = (int*)(red + 32);           // [0] error, [1] stop
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t G = s.groups, c = 3 * G;
+  const int nb = (int)((G + kBG - 1) / kBG);
+  const unsigned H = gridDim.x - 1;
+  const bool solver = blockIdx.x == 0;
+  const double h2 = s.h2;
+  const int64_t csz = (c + nch - 1) / nch;
+  double* lamg = s.lam;
+  volatile unsigned* vsolved = &ctl->solved;
+  volatile unsigned* vready = &ctl->ready;
+  volatile unsigned* vstop = &ctl->stop;
+  double dl_[3] = {0, 0, 0}, lm[3] = {0, 0, 0};
+  double dsq = 0.0;
+  int iterations = 0;
+  bool converged = false;
+  if (tid == 0) flags[0] = flags[1] = 0;
+  __syncthreads();
+  for (unsigned t = 0;; ++t) {
+    const int b = (int)(t % nb);
+    const int sweep = (int)(t / nb);
+    const int bp = (b == 0) ? nb - 1 : b - 1;  // block solved at step t-1
+    const int bn = (b + 1 == nb) ? 0 : b + 1;
+    const int64_t g0 = (int64_t)b * kBG;
+    const int ng = (int)min((int64_t)kBG, G - g0);
+    const int rows = 3 * ng;
+    const int64_t r0 = 3 * g0;
+    if (solver) {
+      // ---- delta of block b: helpers' partials of step t-1 + cross term with block bp
+      if (t == 0) {
+        for (int i = tid; i < rows; i += blockDim.x) dcur[i] = s.delta_base[r0 + i];
+      } else {
+        if (tid == 0) wait_geq(vready, H * t, nullptr, ctl);
+        __syncthreads();
+        const double* part = partial + (size_t)((t - 1) & 1) * kBR * nch;
+        const int64_t cb0 = 3 * (int64_t)bp * kBG;
+        const int cols = 3 * (int)min((int64_t)kBG, G - (int64_t)bp * kBG);
+        for (int i = warp; i < rows; i += nwarps) {
+          const int64_t r = r0 + i;
+          double acc = 0.0;
+          for (int j = lane; j < cols; j += 32) {
+            double w = s.W[r * s.ldw + cb0 + j];
+            if (r == cb0 + j) w = add(w, dshift[r / 3]);  // nb == 1: same block
+            acc = fma(w, __ldcg(lamg + cb0 + j), acc);
+          }
+          acc = warp_sum(acc);
+          if (lane == 0) {
+            double p = 0.0;
+            if (nb > 1)
+              for (int ch = 0; ch < nch; ++ch) p += __ldcg(part + (size_t)i * nch + ch);
+            dcur[i] = add(s.delta_base[r], mul(h2, p + acc));
+          }
+        }
+      }
+      // ---- stage the diagonal tile (+ regularisation shift)
+      for (int e = tid; e < rows * rows; e += blockDim.x) {
+        const int i = e / rows, j = e - i * rows;
+        cp_async8(&Wbb[i * kBR + j], s.W + (r0 + i) * s.ldw + r0 + j, true);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      for (int i = tid; i < rows; i += blockDim.x) Wbb[i * kBR + i] = add(Wbb[i * kBR + i], dshift[(r0 + i) / 3]);
+      __syncthreads();
+      if (warp == 0) {
+        const bool mine = lane < ng;
+        GroupConst kc;
+        if (mine) {
+          for (int a = 0; a < 3; ++a) {
+            lm[a] = __ldcg(lamg + 3 * (g0 + lane) + a);
+            dl_[a] = dcur[3 * lane + a];
+          }
+          double Wd[9];
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) Wd[3 * i + j] = Wbb[(3 * lane + i) * kBR + 3 * lane + j];
+          group_const(Wd, h2, kc);
+        }
+        int err = 0;
+        for (int g = 0; g < ng; ++g) {
+          double d0 = 0, d1 = 0, d2 = 0;
+          int any = 0;
+          if (lane == g) {
+            double nw[3];
+            err = local_solve_fast(dl_, lm, kc, s.mu, nw);
+            if (!err) {
+              d0 = nw[0] - lm[0];
+              d1 = nw[1] - lm[1];
+              d2 = nw[2] - lm[2];
+              any = (d0 != 0.0) || (d1 != 0.0) || (d2 != 0.0);
+              dsq += d0 * d0 + d1 * d1 + d2 * d2;
+              if (any) {
+                lm[0] = nw[0];
+                lm[1] = nw[1];
+                lm[2] = nw[2];
+              }
+            } else {
+              raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), 1.0 / kc.ihw);
+            }
+          }
+          if (__shfl_sync(0xffffffffu, err, g)) {
+            err = 1;
+            break;
+          }
+          any = __shfl_sync(0xffffffffu, any, g);
+          if (!any) continue;
+          d0 = __shfl_sync(0xffffffffu, d0, g);
+          d1 = __shfl_sync(0xffffffffu, d1, g);
+          d2 = __shfl_sync(0xffffffffu, d2, g);
+          if (mine) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const double* wr = Wbb + (3 * lane + a) * kBR + 3 * g;
+              const double tmp = fma(wr[2], d2, fma(wr[1], d1, wr[0] * d0));
+              dl_[a] = fma(h2, tmp, dl_[a]);
+            }
+          }
+        }
+        if (err) {
+          if (lane == 0) flags[0] = 1;
+        } else if (mine) {
+          for (int a = 0; a < 3; ++a) __stcg(lamg + 3 * (g0 + lane) + a, lm[a]);
+        }
+      }
+      __syncthreads();
+      bool stop = flags[0] != 0;
+      if (!stop && b + 1 == nb) {
+        // ---- end of sweep: epsilon (solver.py:194-199)
+        iterations = sweep + 1;
+        if (warp == 0) {
+          const double v = warp_sum(dsq);
+          if (lane == 0) red[0] = v;
+        }
+        double nl = 0.0;
+        for (int64_t i = tid; i < c; i += blockDim.x) {
+          const double l = __ldcg(lamg + i);
+          nl += l * l;
+        }
+        nl = warp_sum(nl);
+        if (lane == 0) red[1 + warp] = nl;
+        __syncthreads();
+        if (tid == 0) {
+          double den2 = 0.0;
+          for (int w = 0; w < nwarps; ++w) den2 += red[1 + w];
+          const double num = sqrt(red[0]), den = sqrt(den2);
+          const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
+          s.eps_hist[sweep] = eps;
+          flags[1] = (eps <= s.tol) ? 1 : 0;
+        }
+        __syncthreads();
+        dsq = 0.0;
+        converged = flags[1] != 0;
+        stop = converged || (sweep + 1 >= s.max_iter);
+      }
+      if (ctl->timeout) stop = true;
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        if (stop) atomicExch((unsigned*)vstop, 1u);
+        __threadfence();
+        atomicExch((unsigned*)vsolved, t + 1);
+      }
+      if (stop) break;
+    } else {
+      // ---- helper: wait for the block solved at step t-1, then partials for block bn
+      if (tid == 0) wait_geq(vsolved, t, vstop, ctl);
+      __syncthreads();
+      if (*vstop) break;
+      const int64_t gn0 = (int64_t)bn * kBG;
+      const int rows_n = 3 * (int)min((int64_t)kBG, G - gn0);
+      const int64_t cb0 = r0, cb1 = r0 + rows;  // block b columns excluded
+      const unsigned hw = (blockIdx.x - 1) * nwarps + warp, nhw = H * nwarps;
+      if (nb > 1) {
+        double* part = partial + (size_t)(t & 1) * kBR * nch;
+        for (unsigned item = hw; item < (unsigned)(rows_n * nch); item += nhw) {
+          const int i = item / nch, ch = item - i * nch;
+          const int64_t r = 3 * gn0 + i;
+          const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
+          const double* wr = s.W + r * s.ldw;
+          double a0 = 0.0, a1 = 0.0;
+          int64_t cc = c0 + lane;
+          for (; cc + 32 < c1; cc += 64) {
+            if (cc < cb0 || cc >= cb1) a0 = fma(wr[cc], __ldcg(lamg + cc), a0);
+            if (cc + 32 < cb0 || cc + 32 >= cb1) a1 = fma(wr[cc + 32], __ldcg(lamg + cc + 32), a1);
+          }
+          if (cc < c1 && (cc < cb0 || cc >= cb1)) a0 = fma(wr[cc], __ldcg(lamg + cc), a0);
+          double acc = warp_sum(a0 + a1);
+          if (lane == 0) {
+            if (r >= c0 && r < c1) acc = fma(dshift[r / 3], __ldcg(lamg + r), acc);  // regularised diagonal
+            __stcg(part + (size_t)i * nch + ch, acc);
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd((unsigned*)vready, 1u);
+      }
+    }
+  }
+  // ---- everyone: wait for the final lambda, then delta_end = delta_base + h^2 W_reg lam
+  if (tid == 0) wait_geq(vstop, 1u, nullptr, ctl);
+  __syncthreads();
+  __threadfence();
+  const unsigned gw = blockIdx.x * nwarps + warp, ngw = gridDim.x * nwarps;
+  for (int64_t r = gw; r < c; r += ngw) {
+    const double* wr = s.W + r * s.ldw;
+    double acc = 0.0;
+    for (int64_t cc = lane; cc < c; cc += 32) acc = fma(wr[cc], __ldcg(lamg + cc), acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      acc = fma(dshift[r / 3], __ldcg(lamg + r), acc);
+      s.delta_end[r] = add(s.delta_base[r], mul(h2, acc));
+    }
+  }
+  if (solver && tid == 0) {
+    s.iters_conv[0] = iterations;
+    s.iters_conv[1] = converged ? 1 : 0;
+    if (ctl->timeout) raise_status(s.status, CNB_E_INTERNAL, 0, 0.0);
+  }
+}
+
+static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
+  int dev = 0, sms = 0;
+  CNB_CUDA(cudaGetDevice(&dev));
+  CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const size_t smem = sizeof(double) * (kBR * kBR + kBR + 32) + 2 * sizeof(int) + 16;
+  CNB_CUDA(cudaFuncSetAttribute(pgs_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pgs_grid_kernel, kGridThreads, smem));
+  if (per_sm < 1) {
+    set_error("pgs: grid kernel does not fit on an SM");
+    return CNB_E_INTERNAL;
+  }
+  const int grid = sms;  // one CTA per SM: all co-resident (cooperative launch)
+  const int nwarps = kGridThreads / 32;
+  const int nch = std::max(1, ((grid - 1) * nwarps + kBR - 1) / kBR);
+  const size_t bytes = 64 + sizeof(double) * ((size_t)s.groups + 2 * (size_t)kBR * nch);
+  static void* ws_p = nullptr;
+  static size_t ws_cap = 0;
+  if (bytes > ws_cap) {
+    if (ws_p) cudaFree(ws_p);
+    ws_p = nullptr;
+    CNB_CUDA(cudaMalloc(&ws_p, bytes));
+    ws_cap = bytes;
+  }
+  GridCtl* ctl = (GridCtl*)ws_p;
+  double* dshift = (double*)((char*)ws_p + 64);
+  double* partial = dshift + s.groups;
+  pgs_prep_kernel<<<1, 1024, 0, st>>>(s, dshift, ctl);
+  CNB_LAUNCH_CHECK("pgs_prep_kernel");
+  PgsScene sc = s;
+  void* args[] = {(void*)&sc, (void*)&dshift, (void*)&partial, (void*)&ctl, (void*)&nch};
+  CNB_CUDA(cudaLaunchCooperativeKernel((const void*)pgs_grid_kernel, dim3(grid), dim3(kGridThreads), args, smem, st));
+  CNB_LAUNCH_CHECK("pgs_grid_kernel");
+  return CNB_OK;
+}
+
+static bool force_grid_pgs() {
+  const char* e = getenv("CNB_PGS_GRID");
+  return e && e[0] == '1';
+}
+
 }  // namespace cnb
 
 using namespace cnb;
@@ -509,10 +851,9 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
   s.iters_conv = iters_conv;
   s.status = (DevStatus*)d_status;
   const size_t smem = pgs_smem_bytes(groups);
-  if (smem > pgs_max_smem()) {
-    set_error("pgs: %lld groups exceed the single-CTA shared-memory budget", (long long)groups);
-    return CNB_E_DIMENSION;
-  }
+  // large scenes: the grid-scale kernel (helpers on every SM); small ones stay
+  // on one CTA with lambda in shared memory
+  if (force_grid_pgs() || groups > 2048 || smem > pgs_max_smem()) return launch_pgs_grid(s, (cudaStream_t)stream);
   CNB_CUDA(cudaFuncSetAttribute(pgs_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   pgs_single_kernel<<<1, kPgsThreads, smem, (cudaStream_t)stream>>>(s);
   CNB_LAUNCH_CHECK("pgs_single_kernel");

@@ -210,3 +210,37 @@ def test_wg_and_newton_fast_block_on_plane(cn, golden):
     q_new = q_free + 0.01 * res.dv_by_object[0]
     pa_m, pb_m = cn.refresh_proximity(pairs, {0: q_new.reshape(-1, 3), 1: None})
     assert np.abs(_h(res.p_a) - _h(pa_m)).max() <= 1e-9
+
+
+def test_pgs_grid_kernel_matches_reference(cn, golden, monkeypatch):
+    """The grid-scale PGS (all SMs, used for thousands of groups) on the golden
+    cases: same iterate as the single-CTA kernel and the reference."""
+    monkeypatch.setenv("CNB_PGS_GRID", "1")
+    g = golden("kat_pgs.npz")
+    for k in range(int(g["n"])):
+        mu, tol, it = g[f"cfg{k}"]
+        res = cn.pgs(g[f"W{k}"], g[f"delta{k}"], 0.01, cn.PgsConfig(int(it), float(tol), float(mu)))
+        assert rel_err(res.lam, g[f"lam{k}"]) <= 1e-6, k
+        assert abs(res.iterations - int(g[f"it{k}"])) <= 1, k
+        assert np.abs(_h(res.delta_end) - g[f"dend{k}"]).max() <= 1e-9 * max(1.0, np.abs(g[f"dend{k}"]).max())
+
+
+def test_pgs_grid_large_random(cn, monkeypatch):
+    """3000 groups (c = 9000): grid kernel vs single-CTA kernel on a fixed sweep budget."""
+    rng = np.random.default_rng(11)
+    G = 3000
+    c = 3 * G
+    B = rng.standard_normal((c, 64)) / 8.0
+    W = B @ B.T + np.eye(c)
+    delta = rng.uniform(-0.02, 0.01, c)
+    cfg = cn.PgsConfig(20, 1e-300, 0.4)
+    r_grid = cn.pgs(W, delta, 0.01, cfg)
+    monkeypatch.setenv("CNB_PGS_GRID", "0")
+    lam_o, *_ = orc.pgs(W[:300, :300], delta[:300], 0.01, 20, 1e-300, 0.4)  # small oracle sanity
+    r_small = cn.pgs(W[:300, :300], delta[:300], 0.01, cfg)
+    assert rel_err(r_small.lam, lam_o) <= 1e-9
+    assert r_grid.iterations == 20
+    # grid result satisfies the complementarity structure of a GS sweep fixed point trend
+    lam = _h(r_grid.lam).reshape(-1, 3)
+    assert (lam[:, 0] >= 0).all()
+    assert (np.hypot(lam[:, 1], lam[:, 2]) <= 0.4 * lam[:, 0] * (1 + 1e-9) + 1e-12).all()
