@@ -216,6 +216,10 @@ int cnb_csr_spmv(int64_t rows, const int64_t* rowptr, const int64_t* col, const 
 /* Number of kernels this library has launched in the process so far. */
 long long cnb_launch_count(void);
 
+/* Cycles per dependent op (out: host, 6): DFMA, DADD, fp64 div, fp64 sqrt,
+ * 64-bit shuffle, FFMA. */
+int cnb_bench_latency(double* out, void* stream);
+
 /* fp64 MMA (DMMA) throughput of the whole GPU in TFLOP/s (out: host). */
 int cnb_bench_dmma(int32_t iters, double* out, void* stream);
 

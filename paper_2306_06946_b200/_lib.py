@@ -52,6 +52,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_chol_solve": [P, P, I64, P, I64, I64, P],
     "cnb_chol_compliance": [P, I64, P, P, P, P, I64, P, I32, I32, P],
     "cnb_bench_dmma": [I32, P, P],
+    "cnb_bench_latency": [P, P],
     "cnb_launch_count": [],
 }
 _RESTYPES = {

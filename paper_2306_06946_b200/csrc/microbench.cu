@@ -21,11 +21,60 @@ __global__ void __launch_bounds__(256) dmma_peak_kernel(int iters, double* out) 
   if (s == 12345.678) out[0] = s;  // keep the work alive
 }
 
+// Dependent-chain latencies (cycles per op) measured by one thread:
+// out[0] DFMA, out[1] DADD, out[2] fp64 division, out[3] fp64 sqrt,
+// out[4] 64-bit shuffle round trip, out[5] FFMA (fp32) for reference.
+__global__ void latency_kernel(int n, double seed, double* out, long long* cyc) {
+  double x = seed, y = 1.0000001, z = 1e-9;
+  float xf = (float)seed;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) x = fma(x, y, z);
+  long long t1 = clock64();
+  for (int i = 0; i < n; ++i) x = x + z;
+  long long t2 = clock64();
+  for (int i = 0; i < n; ++i) x = y / x;
+  long long t3 = clock64();
+  for (int i = 0; i < n; ++i) x = sqrt(x + 1.0);
+  long long t4 = clock64();
+  for (int i = 0; i < n; ++i) x = __shfl_sync(0xffffffffu, x, (threadIdx.x + 1) & 31) + z;
+  long long t5 = clock64();
+  for (int i = 0; i < n; ++i) xf = fmaf(xf, 1.0000001f, 1e-9f);
+  long long t6 = clock64();
+  if (threadIdx.x == 0) {
+    cyc[0] = t1 - t0;
+    cyc[1] = t2 - t1;
+    cyc[2] = t3 - t2;
+    cyc[3] = t4 - t3;
+    cyc[4] = t5 - t4;
+    cyc[5] = t6 - t5;
+    out[0] = x + xf;
+  }
+}
+
 }  // namespace cnb
 
 using namespace cnb;
 
 extern "C" {
+
+// out (host, 6 doubles): cycles per dependent op, see latency_kernel.
+int cnb_bench_latency(double* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  double* d = nullptr;
+  long long* c = nullptr;
+  CNB_CUDA(cudaMalloc(&d, sizeof(double)));
+  CNB_CUDA(cudaMalloc(&c, 6 * sizeof(long long)));
+  const int n = 4096;
+  latency_kernel<<<1, 32, 0, st>>>(n, 1.5, d, c);
+  CNB_LAUNCH_CHECK("latency_kernel");
+  long long h[6];
+  CNB_CUDA(cudaMemcpyAsync(h, c, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CNB_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k < 6; ++k) out[k] = (double)h[k] / n;
+  cudaFree(d);
+  cudaFree(c);
+  return CNB_OK;
+}
 
 // TFLOP/s of DMMA over the whole GPU (result written to host out[0]).
 int cnb_bench_dmma(int32_t iters, double* out, void* stream) {

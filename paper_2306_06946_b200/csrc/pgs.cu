@@ -186,6 +186,29 @@ __device__ __forceinline__ int local_solve_fast(const double d[3], const double 
   return 0;
 }
 
+// Lane-strided partial dot product  sum_{j in [lo,hi), j = lo+lane mod 32} w[j] x[j]
+// with four independent accumulators and the loads of four iterations issued
+// before their FMAs (in-order issue would otherwise stall on every load).
+template <bool CG>
+__device__ __forceinline__ double lane_dot(const double* __restrict__ w, const double* __restrict__ x, int64_t lo,
+                                           int64_t hi, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t j = lo + lane;
+  for (; j + 96 < hi; j += 128) {
+    const double w0 = w[j], w1 = w[j + 32], w2 = w[j + 64], w3 = w[j + 96];
+    const double x0 = CG ? __ldcg(x + j) : x[j];
+    const double x1 = CG ? __ldcg(x + j + 32) : x[j + 32];
+    const double x2 = CG ? __ldcg(x + j + 64) : x[j + 64];
+    const double x3 = CG ? __ldcg(x + j + 96) : x[j + 96];
+    a0 = fma(w0, x0, a0);
+    a1 = fma(w1, x1, a1);
+    a2 = fma(w2, x2, a2);
+    a3 = fma(w3, x3, a3);
+  }
+  for (; j < hi; j += 32) a0 = fma(w[j], CG ? __ldcg(x + j) : x[j], a0);
+  return (a0 + a1) + (a2 + a3);
+}
+
 // Shared-memory layout of one scene's PGS.
 struct PgsSmem {
   double* lam;     // c
@@ -337,11 +360,7 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
         for (int i = warp - 1; i < rows; i += nwarps - 1) {
           const int64_t r = rn0 + i;
           const double* wr = s.W + r * s.ldw;
-          double acc = 0.0;
-          for (int64_t cc = lane; cc < c; cc += 32) {
-            if (cc >= cb0 && cc < cb1) continue;
-            acc = fma(wr[cc], sm.lam[cc], acc);
-          }
+          double acc = lane_dot<false>(wr, sm.lam, 0, cb0, lane) + lane_dot<false>(wr, sm.lam, cb1, c, lane);
           acc = warp_sum(acc);
           if (lane == 0) {
             // regularised diagonal of row r (inside block bn, never block b
@@ -387,7 +406,7 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
           const int64_t r = rn0 + i;
           double acc = 0.0;
           if (nb > 1) {
-            for (int j = lane; j < cols; j += 32) acc = fma(s.W[r * s.ldw + cb0 + j], sm.lam[cb0 + j], acc);
+            acc = lane_dot<false>(s.W + r * s.ldw + cb0, sm.lam + cb0, 0, cols, lane);
           } else {
             for (int j = lane; j < cols; j += 32) acc = fma(w_reg(s, sm, r, cb0 + j), sm.lam[cb0 + j], acc);
           }
@@ -404,8 +423,7 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
   // ---- delta_end = delta_base + h^2 W_reg lam (solver.py:201) ----
   for (int64_t r = warp; r < c; r += nwarps) {
     const double* wr = s.W + r * s.ldw;
-    double acc = 0.0;
-    for (int64_t cc = lane; cc < c; cc += 32) acc = fma(wr[cc], sm.lam[cc], acc);
+    double acc = lane_dot<false>(wr, sm.lam, 0, c, lane);
     acc = warp_sum(acc);
     if (lane == 0) {
       acc = fma(sm.dshift[r / 3], sm.lam[r], acc);
@@ -598,18 +616,18 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
         for (int i = warp; i < rows; i += nwarps) {
           const int64_t r = r0 + i;
           double acc = 0.0;
-          for (int j = lane; j < cols; j += 32) {
-            double w = s.W[r * s.ldw + cb0 + j];
-            if (r == cb0 + j) w = add(w, dshift[r / 3]);  // nb == 1: same block
-            acc = fma(w, __ldcg(lamg + cb0 + j), acc);
+          if (nb > 1) {
+            acc = lane_dot<true>(s.W + r * s.ldw + cb0, lamg + cb0, 0, cols, lane);
+            for (int ch = lane; ch < nch; ch += 32) acc += __ldcg(part + (size_t)i * nch + ch);
+          } else {
+            for (int j = lane; j < cols; j += 32) {
+              double w = s.W[r * s.ldw + cb0 + j];
+              if (r == cb0 + j) w = add(w, dshift[r / 3]);  // nb == 1: same block
+              acc = fma(w, __ldcg(lamg + cb0 + j), acc);
+            }
           }
           acc = warp_sum(acc);
-          if (lane == 0) {
-            double p = 0.0;
-            if (nb > 1)
-              for (int ch = 0; ch < nch; ++ch) p += __ldcg(part + (size_t)i * nch + ch);
-            dcur[i] = add(s.delta_base[r], mul(h2, p + acc));
-          }
+          if (lane == 0) dcur[i] = add(s.delta_base[r], mul(h2, acc));
         }
       }
       // ---- stage the diagonal tile (+ regularisation shift)
@@ -735,14 +753,9 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
           const int64_t r = 3 * gn0 + i;
           const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
           const double* wr = s.W + r * s.ldw;
-          double a0 = 0.0, a1 = 0.0;
-          int64_t cc = c0 + lane;
-          for (; cc + 32 < c1; cc += 64) {
-            if (cc < cb0 || cc >= cb1) a0 = fma(wr[cc], __ldcg(lamg + cc), a0);
-            if (cc + 32 < cb0 || cc + 32 >= cb1) a1 = fma(wr[cc + 32], __ldcg(lamg + cc + 32), a1);
-          }
-          if (cc < c1 && (cc < cb0 || cc >= cb1)) a0 = fma(wr[cc], __ldcg(lamg + cc), a0);
-          double acc = warp_sum(a0 + a1);
+          // [c0, c1) minus the columns of block b, as two branch-free ranges
+          double acc = lane_dot<true>(wr, lamg, c0, min(c1, cb0), lane) + lane_dot<true>(wr, lamg, max(c0, cb1), c1, lane);
+          acc = warp_sum(acc);
           if (lane == 0) {
             if (r >= c0 && r < c1) acc = fma(dshift[r / 3], __ldcg(lamg + r), acc);  // regularised diagonal
             __stcg(part + (size_t)i * nch + ch, acc);
@@ -764,7 +777,7 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
   for (int64_t r = gw; r < c; r += ngw) {
     const double* wr = s.W + r * s.ldw;
     double acc = 0.0;
-    for (int64_t cc = lane; cc < c; cc += 32) acc = fma(wr[cc], __ldcg(lamg + cc), acc);
+    acc = lane_dot<true>(wr, lamg, 0, c, lane);
     acc = warp_sum(acc);
     if (lane == 0) {
       acc = fma(dshift[r / 3], __ldcg(lamg + r), acc);
@@ -853,7 +866,7 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
   const size_t smem = pgs_smem_bytes(groups);
   // large scenes: the grid-scale kernel (helpers on every SM); small ones stay
   // on one CTA with lambda in shared memory
-  if (force_grid_pgs() || groups > 2048 || smem > pgs_max_smem()) return launch_pgs_grid(s, (cudaStream_t)stream);
+  if (force_grid_pgs() || groups > 512 || smem > pgs_max_smem()) return launch_pgs_grid(s, (cudaStream_t)stream);
   CNB_CUDA(cudaFuncSetAttribute(pgs_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   pgs_single_kernel<<<1, kPgsThreads, smem, (cudaStream_t)stream>>>(s);
   CNB_LAUNCH_CHECK("pgs_single_kernel");
