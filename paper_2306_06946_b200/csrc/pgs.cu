@@ -192,21 +192,21 @@ __device__ __forceinline__ int local_solve_fast(const double d[3], const double 
 template <bool CG>
 __device__ __forceinline__ double lane_dot(const double* __restrict__ w, const double* __restrict__ x, int64_t lo,
                                            int64_t hi, int lane) {
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  double a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = 0.0;
   int64_t j = lo + lane;
-  for (; j + 96 < hi; j += 128) {
-    const double w0 = w[j], w1 = w[j + 32], w2 = w[j + 64], w3 = w[j + 96];
-    const double x0 = CG ? __ldcg(x + j) : x[j];
-    const double x1 = CG ? __ldcg(x + j + 32) : x[j + 32];
-    const double x2 = CG ? __ldcg(x + j + 64) : x[j + 64];
-    const double x3 = CG ? __ldcg(x + j + 96) : x[j + 96];
-    a0 = fma(w0, x0, a0);
-    a1 = fma(w1, x1, a1);
-    a2 = fma(w2, x2, a2);
-    a3 = fma(w3, x3, a3);
+  for (; j + 224 < hi; j += 256) {
+    double wv[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) wv[u] = w[j + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[u] = CG ? __ldcg(x + j + 32 * u) : x[j + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = fma(wv[u], xv[u], a[u]);
   }
-  for (; j < hi; j += 32) a0 = fma(w[j], CG ? __ldcg(x + j) : x[j], a0);
-  return (a0 + a1) + (a2 + a3);
+  for (; j < hi; j += 32) a[0] = fma(w[j], CG ? __ldcg(x + j) : x[j], a[0]);
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 }
 
 // Shared-memory layout of one scene's PGS.
@@ -567,14 +567,19 @@ __global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshi
   for (int64_t i = tid; i < c; i += blockDim.x) s.lam[i] = 0.0;
 }
 
-constexpr int kGridThreads = 256;
+constexpr int kGridThreads = 512;
 
 __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, const double* __restrict__ dshift,
-                                                                double* partial, GridCtl* ctl, int nch) {
+                                                                double* partial, GridCtl* ctl, int nch,
+                                                                int lam_in_smem) {
   extern __shared__ __align__(16) char smem_raw[];
-  double* Wbb = (double*)smem_raw;         // kBR x kBR
-  double* dcur = Wbb + kBR * kBR;          // kBR
-  double* red = dcur + kBR;                // 32
+  double* lams = (double*)smem_raw;        // helpers: resident copy of lambda (aliases the tiles)
+  double* Wbb0 = (double*)smem_raw;        // kBR x kBR diagonal tiles, double-buffered
+  double* Wbb1 = Wbb0 + kBR * kBR;
+  double* Wx = Wbb1 + kBR * kBR;           // kBR x kBR cross tile W[next rows, current cols]
+  double* dcur = Wx + kBR * kBR;           // kBR
+  double* lamx = dcur + kBR;               // kBR
+  double* red = lamx + kBR;                // 32
   int* flags = (int*)(red + 32);           // [0] error, [1] stop
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -604,41 +609,56 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
     const int rows = 3 * ng;
     const int64_t r0 = 3 * g0;
     if (solver) {
-      // ---- delta of block b: helpers' partials of step t-1 + cross term with block bp
+      // Tiles: Wcur = diagonal tile of block b (prefetched during step t-1 by
+      // warps 1..7), Wx = W[rows of b, cols of bp] (same), both raw W.
+      double* Wcur = (nb == 1 || !(t & 1)) ? Wbb0 : Wbb1;
+      double* Wnxt = (t & 1) ? Wbb0 : Wbb1;
       if (t == 0) {
-        for (int i = tid; i < rows; i += blockDim.x) dcur[i] = s.delta_base[r0 + i];
-      } else {
-        if (tid == 0) wait_geq(vready, H * t, nullptr, ctl);
-        __syncthreads();
-        const double* part = partial + (size_t)((t - 1) & 1) * kBR * nch;
-        const int64_t cb0 = 3 * (int64_t)bp * kBG;
-        const int cols = 3 * (int)min((int64_t)kBG, G - (int64_t)bp * kBG);
-        for (int i = warp; i < rows; i += nwarps) {
-          const int64_t r = r0 + i;
-          double acc = 0.0;
-          if (nb > 1) {
-            acc = lane_dot<true>(s.W + r * s.ldw + cb0, lamg + cb0, 0, cols, lane);
-            for (int ch = lane; ch < nch; ch += 32) acc += __ldcg(part + (size_t)i * nch + ch);
-          } else {
-            for (int j = lane; j < cols; j += 32) {
-              double w = s.W[r * s.ldw + cb0 + j];
-              if (r == cb0 + j) w = add(w, dshift[r / 3]);  // nb == 1: same block
-              acc = fma(w, __ldcg(lamg + cb0 + j), acc);
-            }
-          }
-          acc = warp_sum(acc);
-          if (lane == 0) dcur[i] = add(s.delta_base[r], mul(h2, acc));
+        for (int e = tid; e < rows * rows; e += blockDim.x) {
+          const int i = e / rows, j = e - i * rows;
+          cp_async8(&Wcur[i * kBR + j], s.W + (r0 + i) * s.ldw + r0 + j, true);
         }
-      }
-      // ---- stage the diagonal tile (+ regularisation shift)
-      for (int e = tid; e < rows * rows; e += blockDim.x) {
-        const int i = e / rows, j = e - i * rows;
-        cp_async8(&Wbb[i * kBR + j], s.W + (r0 + i) * s.ldw + r0 + j, true);
+        for (int i = tid; i < rows; i += blockDim.x) dcur[i] = s.delta_base[r0 + i];
+      } else if (tid == 0) {
+        wait_geq(vready, H * t, nullptr, ctl);
       }
       cp_async_wait_all();
       __syncthreads();
-      for (int i = tid; i < rows; i += blockDim.x) Wbb[i * kBR + i] = add(Wbb[i * kBR + i], dshift[(r0 + i) / 3]);
+      if (t == 0 || nb > 1)  // regularisation shift (solver.py:119-120) on the fresh tile
+        for (int i = tid; i < rows; i += blockDim.x) Wcur[i * kBR + i] = add(Wcur[i * kBR + i], dshift[(r0 + i) / 3]);
+      if (t > 0) {
+        // ---- delta of block b: helpers' partials of step t-1 + cross term with block bp
+        const double* part = partial + (size_t)((t - 1) & 1) * kBR * nch;
+        const int64_t cb0 = 3 * (int64_t)bp * kBG;
+        const int cols = 3 * (int)min((int64_t)kBG, G - (int64_t)bp * kBG);
+        for (int j = tid; j < cols; j += blockDim.x) lamx[j] = __ldcg(lamg + cb0 + j);
+        __syncthreads();
+        const double* X = (nb > 1) ? Wx : Wcur;  // nb == 1: the block itself (regularised)
+        for (int i = warp; i < rows; i += nwarps) {
+          double acc = 0.0;
+          for (int j = lane; j < cols; j += 32) acc = fma(X[i * kBR + j], lamx[j], acc);
+          if (nb > 1)
+            for (int ch = lane; ch < nch; ch += 32) acc += __ldcg(part + (size_t)i * nch + ch);
+          acc = warp_sum(acc);
+          if (lane == 0) dcur[i] = add(s.delta_base[r0 + i], mul(h2, acc));
+        }
+      }
       __syncthreads();
+      double* Wbb = Wcur;
+      if (warp != 0 && nb > 1) {
+        // ---- warps 1..7: prefetch the next block's tiles while warp 0 solves
+        const int64_t rn0 = 3 * (int64_t)bn * kBG;
+        const int rows_n = 3 * (int)min((int64_t)kBG, G - (int64_t)bn * kBG);
+        const int pt = tid - 32, np = blockDim.x - 32;
+        for (int e = pt; e < rows_n * rows_n; e += np) {
+          const int i = e / rows_n, j = e - i * rows_n;
+          cp_async8(&Wnxt[i * kBR + j], s.W + (rn0 + i) * s.ldw + rn0 + j, true);
+        }
+        for (int e = pt; e < rows_n * rows; e += np) {
+          const int i = e / rows, j = e - i * rows;
+          cp_async8(&Wx[i * kBR + j], s.W + (rn0 + i) * s.ldw + r0 + j, true);
+        }
+      }
       if (warp == 0) {
         const bool mine = lane < ng;
         GroupConst kc;
@@ -742,6 +762,17 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
       if (tid == 0) wait_geq(vsolved, t, vstop, ctl);
       __syncthreads();
       if (*vstop) break;
+      if (lam_in_smem) {
+        // helpers keep lambda in shared memory: only the block solved at step t-1 changed
+        if (t == 0) {
+          for (int64_t j = tid; j < c; j += blockDim.x) lams[j] = 0.0;
+        } else {
+          const int64_t pb0 = 3 * (int64_t)bp * kBG;
+          const int pcols = 3 * (int)min((int64_t)kBG, G - (int64_t)bp * kBG);
+          for (int j = tid; j < pcols; j += blockDim.x) lams[pb0 + j] = __ldcg(lamg + pb0 + j);
+        }
+        __syncthreads();
+      }
       const int64_t gn0 = (int64_t)bn * kBG;
       const int rows_n = 3 * (int)min((int64_t)kBG, G - gn0);
       const int64_t cb0 = r0, cb1 = r0 + rows;  // block b columns excluded
@@ -754,10 +785,12 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
           const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
           const double* wr = s.W + r * s.ldw;
           // [c0, c1) minus the columns of block b, as two branch-free ranges
-          double acc = lane_dot<true>(wr, lamg, c0, min(c1, cb0), lane) + lane_dot<true>(wr, lamg, max(c0, cb1), c1, lane);
+          double acc = lam_in_smem
+                           ? lane_dot<false>(wr, lams, c0, min(c1, cb0), lane) + lane_dot<false>(wr, lams, max(c0, cb1), c1, lane)
+                           : lane_dot<true>(wr, lamg, c0, min(c1, cb0), lane) + lane_dot<true>(wr, lamg, max(c0, cb1), c1, lane);
           acc = warp_sum(acc);
           if (lane == 0) {
-            if (r >= c0 && r < c1) acc = fma(dshift[r / 3], __ldcg(lamg + r), acc);  // regularised diagonal
+            if (r >= c0 && r < c1) acc = fma(dshift[r / 3], lam_in_smem ? lams[r] : __ldcg(lamg + r), acc);
             __stcg(part + (size_t)i * nch + ch, acc);
           }
         }
@@ -770,6 +803,7 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
     }
   }
   // ---- everyone: wait for the final lambda, then delta_end = delta_base + h^2 W_reg lam
+  cp_async_wait_all();  // drain prefetches issued for a block that was never solved
   if (tid == 0) wait_geq(vstop, 1u, nullptr, ctl);
   __syncthreads();
   __threadfence();
@@ -795,7 +829,10 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   int dev = 0, sms = 0;
   CNB_CUDA(cudaGetDevice(&dev));
   CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const size_t smem = sizeof(double) * (kBR * kBR + kBR + 32) + 2 * sizeof(int) + 16;
+  const size_t tiles = sizeof(double) * (3 * kBR * kBR + 2 * kBR + 32) + 2 * sizeof(int) + 16;
+  const size_t lam_bytes = sizeof(double) * (size_t)(3 * s.groups);
+  const int lam_in_smem = lam_bytes <= pgs_max_smem() ? 1 : 0;
+  const size_t smem = std::max(tiles, lam_in_smem ? lam_bytes : (size_t)0);
   CNB_CUDA(cudaFuncSetAttribute(pgs_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   CNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pgs_grid_kernel, kGridThreads, smem));
@@ -821,7 +858,8 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   pgs_prep_kernel<<<1, 1024, 0, st>>>(s, dshift, ctl);
   CNB_LAUNCH_CHECK("pgs_prep_kernel");
   PgsScene sc = s;
-  void* args[] = {(void*)&sc, (void*)&dshift, (void*)&partial, (void*)&ctl, (void*)&nch};
+  int lis = lam_in_smem;
+  void* args[] = {(void*)&sc, (void*)&dshift, (void*)&partial, (void*)&ctl, (void*)&nch, (void*)&lis};
   CNB_CUDA(cudaLaunchCooperativeKernel((const void*)pgs_grid_kernel, dim3(grid), dim3(kGridThreads), args, smem, st));
   CNB_LAUNCH_CHECK("pgs_grid_kernel");
   return CNB_OK;
