@@ -56,7 +56,9 @@ from .solver import (
     PgsResult,
     StepContext,
     local_solve,
+    newton,
     newton_fast,
+    newton_standard,
     pgs,
     regularize,
 )

@@ -4,8 +4,9 @@ fast proximity update.
 Mirrors /root/reference/pkg/src/contactnewton/constraints.py.  All dense
 operators live on the GPU: ``rebuild_W_fast`` (3x3 block congruence,
 bit-identical to the reference's naive gemm), ``compute_violation``,
-``fast_update_proximity`` and ``assemble_Wg`` (sparse-RHS forward solve on
-the supernodal factor + blocked Gram product, csrc/wg.cu).
+``fast_update_proximity``, and ``assemble_Wg`` / ``assemble_W_standard``
+(sparse-RHS forward solve on the supernodal factor + blocked Gram product,
+csrc/solve.cu via wg.py).
 """
 
 from __future__ import annotations
@@ -42,7 +43,10 @@ class DirectionMatrix:
     def as_sparse(self) -> sp.csr_matrix:
         if self.n_groups == 0:
             return sp.csr_matrix((0, 0))
-        return sp.block_diag(list(dv.host(self.blocks)), format="csr")
+        m = self.n_groups
+        cols = (3 * np.arange(m)[:, None, None] + np.arange(3)[None, None, :]).repeat(3, axis=1)
+        return sp.csr_matrix((dv.host(self.blocks).reshape(-1), cols.reshape(-1), np.arange(0, 9 * m + 1, 3)),
+                             shape=(3 * m, 3 * m))
 
     def apply(self, rel) -> torch.Tensor:
         """D @ rel for a stacked (3p,) relative vector (constraints.py:58-60)."""
@@ -187,24 +191,54 @@ def assemble_H(D: DirectionMatrix, G) -> sp.csr_matrix:
     return (D.as_sparse() @ Gm).tocsr()
 
 
-def assemble_W_standard(H_by_object: dict, F_by_object: dict) -> Delassus:
-    """W = sum_o H A^-1 H^T via multi-RHS solves on the GPU factor (constraints.py:132-152)."""
+def _as_mapping(G) -> SignedMapping:
+    """Wrap a host CSR (3p x n) as a SignedMapping; participation = pairs with stored rows."""
+    if isinstance(G, SignedMapping):
+        return G
+    csr = sp.csr_matrix(G)
+    csr.sort_indices()
+    nz = np.diff(csr.indptr).reshape(-1, 3).sum(axis=1) > 0 if csr.shape[0] else np.zeros(0, bool)
+    idx = np.flatnonzero(nz).astype(np.int64)
+    return SignedMapping(csr, idx, np.ones(len(idx), dtype=np.int8))
+
+
+def _sum_compliance(parts: list, dim: int) -> torch.Tensor:
+    """sum_o of the per-object parts expanded to dim x dim, ascending object id."""
+    if not parts:
+        return dv.zeros((dim, dim))
+    total = None
+    for comp in parts:
+        if total is None:
+            total = comp.dense(dim).clone() if len(parts) > 1 else comp.dense(dim)
+        elif comp.full:
+            total += comp.U
+        elif len(comp.idx):
+            rows = (3 * comp.idx[:, None] + torch.arange(3, device=total.device)).reshape(-1)
+            total[rows[:, None], rows[None, :]] += comp.U
+    return total
+
+
+def assemble_W_standard(H_by_object: dict, F_by_object: dict, group=None) -> Delassus:
+    """W = sum_o H_o A_o^-1 H_o^T (constraints.py:132-152).
+
+    The reference forms X = A^-1 H^T with a dense multi-RHS solve and multiplies
+    by H; here H^T's columns go through the same sparse-RHS forward solve + Gram
+    product as W_g (wg.py), since H_o = D S_o has S_o's sparsity per pair.
+    """
+    from .wg import object_compliance
+
     ids = sorted(H_by_object)
     if not ids:
         return Delassus(dv.zeros((0, 0)))
     c = H_by_object[ids[0]].shape[0]
-    W = dv.zeros((c, c))
+    parts = []
     for oid in ids:
-        H = H_by_object[oid]
+        H = _as_mapping(H_by_object[oid])
         F = F_by_object[oid]
         if H.shape[1] != F.dim:
             raise DimensionMismatchError(f"object {oid}: H has {H.shape[1]} columns, factorization dim {F.dim}")
-        if H.nnz == 0:
-            continue
-        X = F.solve_multi(H.T.toarray())
-        Hd = dv.f64(H.toarray())
-        W += Hd @ X
-    return Delassus(W)
+        parts.append(object_compliance(H, F, c, group=group))
+    return Delassus(_sum_compliance(parts, c))
 
 
 def assemble_Wg(S_by_object: dict, F_by_object: dict, group=None) -> MappingDelassus:
@@ -221,24 +255,14 @@ def assemble_Wg(S_by_object: dict, F_by_object: dict, group=None) -> MappingDela
     if not ids:
         return MappingDelassus(dv.zeros((0, 0)), {})
     dim = S_by_object[ids[0]].shape[0]
-    wg = None
     per = {}
     for oid in ids:
         S = S_by_object[oid]
         F = F_by_object[oid]
         if S.shape[1] != F.dim:
             raise DimensionMismatchError(f"object {oid}: S has {S.shape[1]} columns, factorization dim {F.dim}")
-        comp = object_compliance(S, F, dim, group=group)
-        per[oid] = comp
-        if wg is None:
-            wg = comp.dense(dim).clone() if len(ids) > 1 else comp.dense(dim)
-        else:
-            if comp.full:
-                wg += comp.U
-            else:
-                rows = (3 * comp.idx[:, None] + torch.arange(3, device=wg.device)).reshape(-1)
-                wg[rows[:, None], rows[None, :]] += comp.U
-    return MappingDelassus(wg, per)
+        per[oid] = object_compliance(S, F, dim, group=group)
+    return MappingDelassus(_sum_compliance([per[o] for o in ids], dim), per)
 
 
 def rebuild_W_fast(D: DirectionMatrix, wg: MappingDelassus, out: torch.Tensor | None = None) -> Delassus:

@@ -3,7 +3,7 @@
 Mirrors /root/reference/pkg/src/contactnewton/solver.py: ``PgsConfig`` /
 ``NewtonConfig`` (52-79), ``regularize`` (99-121), ``local_solve`` (124-165),
 ``pgs`` (168-202), ``StepContext`` / ``CorrectionResult`` (208-242),
-``newton_fast`` (314-367).
+``newton_standard`` (260-311), ``newton_fast`` (314-367).
 
 ``newton_fast`` keeps the whole loop on the device: re-linearisation, the
 W rebuild, the violation, PGS, the proximity update and the impulse
@@ -314,3 +314,83 @@ def newton_fast(ctx: StepContext, ncfg: NewtonConfig, pcfg: PgsConfig) -> Correc
                               final_correction_time=timer.secs(e4, e5))
     result.p_a, result.p_b = p_a, p_b
     return result
+
+
+def newton_standard(ctx: StepContext, ncfg: NewtonConfig, pcfg: PgsConfig, group=None) -> CorrectionResult:
+    """Standard recursive correction (paper Alg. 2; solver.py:260-311).
+
+    Every iteration rebuilds W = sum_o H_o A_o^-1 H_o^T with H_o = D S_o from
+    the factorizations (sparse-RHS forward solve + Gram, assemble_W_standard),
+    runs PGS, solves dv_k = h A^-1 S^T D^T lam per object and refreshes the
+    proximity points through ``ctx.refresh`` (positions g(q_free + h dv)).
+    The "single" scheme is this loop with one iteration and no
+    re-linearisation (scene.py:701-703).  H_o is formed on the host from the
+    iteration's directions (one 9m-double read per iteration).
+    """
+    from .constraints import assemble_H, assemble_W_standard
+
+    if ctx.refresh is None:
+        raise ValidationError("standard scheme needs ctx.refresh (positions from a velocity correction)")
+    D = frames_tensor(ctx.detection_frames).clone()
+    m = D.shape[0]
+    c = 3 * m
+    p_a = dv.f64(ctx.p_a0).reshape(-1, 3).clone()
+    p_b = dv.f64(ctx.p_b0).reshape(-1, 3).clone()
+    dv_tot = {oid: dv.zeros(S.shape[1]) for oid, S in sorted(ctx.S_by_object.items())}
+    acc = dv.zeros(c)
+    delta = dv.empty(c)
+    rot = dv.zeros(1)
+    timer = _Timer()
+    recs = []
+    lam_history = []
+    status = _lib.status(acc.device)
+    for k in range(ncfg.max_iterations):
+        rot_rec = None
+        if k > 0 and ncfg.relinearize:
+            D, _ = relinearize_device(p_a, p_b, D, rot)
+            rot_rec = rot.clone()
+            if float(rot) <= ncfg.rotation_tol:
+                break
+        e0 = timer.mark()
+        Dm = DirectionMatrix(D)
+        H = {oid: assemble_H(Dm, S) for oid, S in sorted(ctx.S_by_object.items())}
+        W = assemble_W_standard(H, ctx.F_by_object, group=group).W
+        e1 = timer.mark()
+        compute_violation(Dm, p_a, p_b, out=delta)
+        res = pgs_device(W, delta, ctx.h, pcfg, PgsWorkspace(c, pcfg.max_iterations))
+        e2 = timer.mark()
+        t = dv.empty(c)
+        _lib.call("cnb_apply_dt", m, D.data_ptr(), res.lam.data_ptr(), t.data_ptr(), acc.data_ptr(), _lib.stream())
+        dv_k = mechanical_correction(ctx, t)
+        for oid in dv_tot:
+            dv_tot[oid] = dv_tot[oid] + dv_k[oid]
+        p_a, p_b = ctx.refresh(dv_tot)
+        p_a, p_b = p_a.reshape(-1, 3), p_b.reshape(-1, 3)
+        e3 = timer.mark()
+        pen = _penetration_device(res.delta_end)
+        lam_history.append(res.lam)
+        recs.append((e0, e1, e2, e3, res, pen, rot_rec))
+        if float(pen) <= ncfg.penetration_tol:
+            break
+    torch.cuda.current_stream().synchronize()
+    status.raise_if_set("newton_standard")
+    iters = []
+    for e0, e1, e2, e3, res, pen, rot_rec in recs:
+        iters.append(IterationStats(
+            rebuild_time=timer.secs(e0, e1), pgs_time=timer.secs(e1, e2), correction_time=timer.secs(e2, e3),
+            pgs_iterations=res.iterations, pgs_eps=res.eps_history[-1] if res.eps_history else 0.0,
+            penetration=float(pen), rotation=float(rot_rec) if rot_rec is not None else 0.0))
+    lam_last = lam_history[-1] if lam_history else dv.zeros(c)
+    result = CorrectionResult(dv_tot, lam_history, LambdaState(lam_last, acc), iters, final_frames=D)
+    result.p_a, result.p_b = p_a, p_b
+    return result
+
+
+def newton(ctx: StepContext, ncfg: NewtonConfig, pcfg: PgsConfig) -> CorrectionResult:
+    """Dispatch on ``ncfg.scheme`` like Simulation.step (scene.py:696-703)."""
+    if ncfg.scheme == "fast":
+        return newton_fast(ctx, ncfg, pcfg)
+    if ncfg.scheme == "standard":
+        return newton_standard(ctx, ncfg, pcfg)
+    from dataclasses import replace
+    return newton_standard(ctx, replace(ncfg, max_iterations=1, relinearize=False), pcfg)

@@ -205,6 +205,30 @@ def scenes():
         save(f"{name}.npz", **out)
 
 
+def scenes_standard():
+    """Reference runs of the standard (Alg. 2) and single schemes on block_on_plane."""
+    from dataclasses import replace
+
+    ref_scenes = "/root/reference/pkg/scenes"
+    base = rsc.load_scene(os.path.join(ref_scenes, "block_on_plane.scn"))
+    for scheme, iters in (("standard", 3), ("single", 1)):
+        cfg = replace(base, newton=replace(base.newton, scheme=scheme, max_iterations=iters, penetration_tol=-1.0,
+                                           rotation_tol=-1.0),
+                      pgs=replace(base.pgs, max_iterations=300, tolerance=1e-10),
+                      output=rsc.OutputConfig(snapshots=False, metrics=False))
+        sim = rsc.Simulation(cfg)
+        out = {}
+        for s in range(2):
+            rep = sim.step()
+            out[f"s{s}_npairs"] = rep.c_groups
+            out[f"s{s}_newton"] = rep.newton_iterations
+            out[f"s{s}_lam"] = sim.last_lam.copy()
+            for obj in sim.dynamic_objects:
+                out[f"s{s}_q{obj.oid}"] = obj.state.q.copy()
+            print(scheme, "step", s, "pairs", rep.c_groups, "newton", rep.newton_iterations)
+        save(f"block_on_plane_{scheme}.npz", **out)
+
+
 def kat_linalg():
     rng = np.random.default_rng(400)
     mesh = cn.box_mesh((0.1, 0.1, 0.1), (2, 2, 2), (0.0, 0.05, 0.0))
@@ -228,3 +252,4 @@ if __name__ == "__main__":
     kat_frames()
     kat_linalg()
     scenes()
+    scenes_standard()

@@ -113,3 +113,45 @@ def test_corotational_rigid_rotation_has_no_elastic_force(cn):
     # K(q) = R K0 R^T blockwise -> symmetric
     K = cor.stiffness().toarray()
     assert np.abs(K - K.T).max() <= 1e-9 * np.abs(K).max()
+
+
+@pytest.mark.parametrize("scheme,iters", [("standard", 3), ("single", 1)])
+def test_block_on_plane_schemes(cn, golden, scheme, iters):
+    """Alg. 2 (standard) and the single corrective motion against reference runs."""
+    from dataclasses import replace
+
+    g = golden("block_on_plane.npz")
+    gs = golden(f"block_on_plane_{scheme}.npz")
+    cfg = _config(cn, g, 1, 0.01, iters, 300, 1e-10)
+    cfg = replace(cfg, newton=replace(cfg.newton, scheme=scheme))
+    sim = cn.Simulation(cfg)
+    for s in range(2):
+        rep = sim.step()
+        assert rep.c_groups == int(gs[f"s{s}_npairs"])
+        assert rep.newton_iterations == int(gs[f"s{s}_newton"])
+        lam, ref = _h(sim.last_lam), gs[f"s{s}_lam"]
+        assert np.abs(lam - ref).max() <= 1e-6 * max(np.abs(ref).max(), 1e-9)  # last lambda may be 0
+        q, qo = gs[f"s{s}_q0"], _h(sim.objects[0].state.q)
+        assert np.abs(qo - q).max() <= 1e-6 * np.abs(q).max()
+
+
+def test_scheme_equivalence_frozen_frames(cn, golden):
+    """With frames frozen, the standard and fast schemes compute the same lambda
+    sequence and correction (reference tests/test_solver.py:312-326, verify.py:106-140)."""
+    from dataclasses import replace
+
+    g = golden("two_body_press.npz")
+    cfg = _config(cn, g, 2, 0.01, 3, 150, 1e-10)
+    sim = cn.Simulation(cfg)
+    ctx, free, states, pen, timings, t_next = sim.prepare_step(build_wg=True)
+    assert ctx.pairs
+    ncfg = replace(cfg.newton, relinearize=False)
+    fast = cn.newton_fast(ctx, ncfg, cfg.pgs)
+    std = cn.newton_standard(ctx, ncfg, cfg.pgs)
+    assert len(fast.lam_history) == len(std.lam_history) == 3
+    scale = max(max(float(x.abs().max()) for x in std.lam_history), 1e-12)
+    for lf, ls in zip(fast.lam_history, std.lam_history):
+        assert float((lf - ls).abs().max()) <= 1e-8 * scale
+    for oid in fast.dv_by_object:
+        a, b = fast.dv_by_object[oid], std.dv_by_object[oid]
+        assert float((a - b).abs().max()) <= 1e-8 * max(float(a.abs().max()), 1e-300)
