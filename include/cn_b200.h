@@ -114,6 +114,20 @@ int cnb_signed_gaps(int64_t m, const int8_t* kind, const int32_t* obj, const int
                     const double* ref_normal, const double* const* views, const double* poses, double* gaps,
                     double* pen, void* stream);
 
+/* Narrow phase, vertex vs triangle mesh (replaces _vertex_vs_mesh
+ * collision.py:222-260 with closest_points_on_triangles 138-184 and
+ * triangle_normals 187-190).  For each query vertex vids[q] (row of pts_a,
+ * n x 3) against every triangle of (tris (nt x 3, int64), pts_b): the
+ * lowest triangle index within 1e-9 of the minimum distance -> best[q];
+ * out[12 q + ...] = signed distance, distance, barycentric (u, v, w),
+ * closest point (3), unit triangle normal (3), hit (1.0 when
+ * signed <= threshold).  Same operation order as numpy (bit-exact
+ * decisions).  work: cnb_detect_work_bytes(nv, nt) bytes of device memory. */
+int64_t cnb_detect_work_bytes(int64_t nv, int64_t nt);
+int cnb_detect_vertex_mesh(int64_t nv, const int64_t* vids, const double* pts_a, int64_t nt, const int64_t* tris,
+                           const double* pts_b, double threshold, void* work, int64_t* best, double* out,
+                           void* stream);
+
 /* ---- projected Gauss-Seidel (contactnewton/solver.py) -------------------- */
 
 /* Workspace bytes needed by cnb_pgs for c = 3*groups rows. */

@@ -35,6 +35,8 @@ _SIGNATURES: dict[str, list] = {
     "cnb_relinearize": [I64, P, P, P, P, P, P],
     "cnb_refresh_proximity": [I64, P, P, P, P, P, P, P, P, P, P, P],
     "cnb_signed_gaps": [I64, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "cnb_detect_work_bytes": [I64, I64],
+    "cnb_detect_vertex_mesh": [I64, P, P, I64, P, P, F64, P, P, P, P],
     "cnb_pgs_work_bytes": [I64],
     "cnb_pgs": [I64, P, I64, P, F64, F64, F64, I32, P, P, P, P, P, P, P],
     "cnb_local_solve": [I64, I64, P, I64, P, P, F64, F64, P, P, P],
@@ -59,6 +61,7 @@ _RESTYPES = {
     "cnb_launch_count": ctypes.c_longlong,
     "cnb_last_error": ctypes.c_char_p,
     "cnb_pgs_work_bytes": I64,
+    "cnb_detect_work_bytes": I64,
     "cnb_chol_export_bytes": I64,
 }
 

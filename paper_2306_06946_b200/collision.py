@@ -3,8 +3,9 @@
 Mirrors the public surface of the reference module
 /root/reference/pkg/src/contactnewton/collision.py.  Frames, re-linearisation,
 proximity refresh and signed gaps run on the GPU (contact.cu, pairs.cu);
-detection runs once per step before the hot path and is host-side here
-(SURVEY.md §8f #1 lists GPU detection as the next item).
+detection's all-pairs closest-point scan runs on the GPU (detect.cu) with
+the reference's selection rule reproduced bit for bit; plane contacts and the
+pair records are built on the host.
 """
 
 from __future__ import annotations
@@ -104,6 +105,7 @@ class MeshGeometry:
     deformable: bool
     dynamic: bool
     pose: Pose = field(default_factory=Pose.identity)
+    points_dev: torch.Tensor | None = None  # device copy of ``points`` when already resident
 
 
 @dataclass
@@ -394,7 +396,7 @@ def signed_gaps(pairs, views: dict):
 
 
 # --------------------------------------------------------------------------
-# detection (host; once per step, before the hot path)
+# detection (once per step, before the hot path)
 # --------------------------------------------------------------------------
 
 def closest_points_on_triangles(tris: np.ndarray, p: np.ndarray):
@@ -449,27 +451,45 @@ def _mesh_side(geom: MeshGeometry, vertex=None, triangle=None, bary=None, point=
                       local_normal=None if normal is None else geom.pose.rotation.T @ normal)
 
 
+def _device_points(geom: MeshGeometry) -> torch.Tensor:
+    if geom.points_dev is not None:
+        return dv.f64(geom.points_dev).reshape(-1, 3)
+    return dv.f64(np.ascontiguousarray(geom.points, dtype=np.float64)).reshape(-1, 3)
+
+
 def _vertex_vs_mesh(ga: MeshGeometry, gb: MeshGeometry, threshold: float):
-    tri_pts = gb.points[gb.triangles]
-    normals = triangle_normals(tri_pts)
-    out = []
-    for vid in ga.vertex_ids:
-        p = ga.points[vid]
-        cps, bary = closest_points_on_triangles(tri_pts, p)
-        diff = p - cps
-        dist = np.linalg.norm(diff, axis=1)
-        signed = np.where(np.einsum("ij,ij->i", diff, normals) >= 0, dist, -dist)
-        best = int(np.flatnonzero(dist <= dist.min() + _TIE_EPS).min())
-        if signed[best] > threshold:
-            continue
-        out.append(ProximityPair(
+    """Best pair per surface vertex of A against B's triangles (collision.py:222-260).
+
+    The all-pairs closest-point scan runs on the GPU (csrc/detect.cu, numpy's
+    operation order, bit-exact selection); the host builds the pair records of
+    the vertices that pass the threshold gate.
+    """
+    nv, nt = len(ga.vertex_ids), len(gb.triangles)
+    if nv == 0 or nt == 0:
+        return []
+    d = dv.device()
+    vids = torch.as_tensor(np.ascontiguousarray(ga.vertex_ids, dtype=np.int64), device=d)
+    tris = torch.as_tensor(np.ascontiguousarray(gb.triangles, dtype=np.int64), device=d)
+    pa, pb = _device_points(ga), _device_points(gb)
+    work = torch.empty((int(_lib.lib().cnb_detect_work_bytes(nv, nt)) + 7) // 8, dtype=torch.float64, device=d)
+    best = torch.empty(nv, dtype=torch.int64, device=d)
+    out = torch.empty((nv, 12), dtype=torch.float64, device=d)
+    _lib.call("cnb_detect_vertex_mesh", nv, vids.data_ptr(), pa.data_ptr(), nt, tris.data_ptr(), pb.data_ptr(),
+              float(threshold), work.data_ptr(), best.data_ptr(), out.data_ptr(), _lib.stream())
+    best_h, out_h = best.cpu().numpy(), out.cpu().numpy()
+    pts_a = np.asarray(ga.points, dtype=np.float64).reshape(-1, 3)
+    res = []
+    for q in np.flatnonzero(out_h[:, 11] > 0.0):
+        vid, t = int(ga.vertex_ids[q]), int(best_h[q])
+        row = out_h[q]
+        p, cp, nrm = pts_a[vid], row[5:8].copy(), row[8:11].copy()
+        res.append(ProximityPair(
             object_a=ga.object_id, object_b=gb.object_id,
             attach_a=_mesh_side(ga, vertex=vid, point=p),
-            attach_b=_mesh_side(gb, triangle=gb.triangles[best], bary=bary[best], point=cps[best],
-                                normal=normals[best]),
-            p_a=p.copy(), p_b=cps[best].copy(), ref_normal=normals[best].copy(),
-            signed_distance=float(signed[best]), vertex_id=int(vid), element_id=best))
-    return out
+            attach_b=_mesh_side(gb, triangle=gb.triangles[t], bary=row[2:5].copy(), point=cp, normal=nrm),
+            p_a=p.copy(), p_b=cp.copy(), ref_normal=nrm.copy(), signed_distance=float(row[0]), vertex_id=vid,
+            element_id=t))
+    return res
 
 
 def _vertex_vs_plane(geom: MeshGeometry, plane: PlaneGeometry, threshold: float):

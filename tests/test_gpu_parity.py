@@ -244,3 +244,37 @@ def test_pgs_grid_large_random(cn, monkeypatch):
     lam = _h(r_grid.lam).reshape(-1, 3)
     assert (lam[:, 0] >= 0).all()
     assert (np.hypot(lam[:, 1], lam[:, 2]) <= 0.4 * lam[:, 0] * (1 + 1e-9) + 1e-12).all()
+
+
+def _oracle_mesh(oid, nodes, tris):
+    return dict(id=oid, points=nodes, triangles=tris, vertex_ids=np.unique(tris), deformable=True, dynamic=True)
+
+
+@pytest.mark.parametrize("shape_a,shape_b,dy,jitter", [
+    ((6, 3, 5), (7, 3, 6), 0.0203, 0.0),      # grid-aligned: exact distance ties everywhere
+    ((9, 4, 9), (10, 5, 10), 0.0395, 2e-4),   # upper block sunk 0.5 mm into the lower one
+    ((14, 4, 12), (16, 5, 16), 0.0380, 1e-3), # jittered, deeper overlap, several triangle slices
+])
+def test_detect_vertex_mesh_matches_oracle(cn, shape_a, shape_b, dy, jitter):
+    """GPU all-pairs closest-point scan vs the oracle (collision.py:222-260): pair keys,
+    attachments and floats bit-identical, including lowest-index tie breaks."""
+    from paper_2306_06946_b200.mesh import five_tet_grid
+
+    rng = np.random.default_rng(7)
+    lower = five_tet_grid(shape_b, 0.01)
+    upper = five_tet_grid(shape_a, 0.01, (0.0125, dy, 0.0075))
+    nodes = [upper.nodes + jitter * rng.standard_normal(upper.nodes.shape),
+             lower.nodes + jitter * rng.standard_normal(lower.nodes.shape)]
+    tris = [cn.surface_triangles(upper.tets), cn.surface_triangles(lower.tets)]
+    geoms = [cn.MeshGeometry(i, nodes[i], tris[i], np.unique(tris[i]), True, True) for i in range(2)]
+    pairs = cn.detect(geoms, 0.005)
+    ref = orc.detect([_oracle_mesh(i, nodes[i], tris[i]) for i in range(2)], [], 0.005)
+    assert len(pairs) == len(ref["vertex_id"]) > 0
+    keys = np.array([(p.object_a, p.object_b, p.vertex_id, p.element_id) for p in pairs])
+    rkeys = np.stack([ref["obj_a"], ref["obj_b"], ref["vertex_id"], ref["element_id"]], 1)
+    assert np.array_equal(keys, rkeys)
+    assert np.array_equal(np.stack([p.attach_b.triangle for p in pairs]), ref["tri_b"])
+    assert np.array_equal(np.stack([p.attach_b.weights for p in pairs]), ref["w_b"])
+    assert np.array_equal(np.stack([p.p_b for p in pairs]), ref["p_b"])
+    assert np.array_equal(np.stack([p.ref_normal for p in pairs]), ref["ref_normal"])
+    assert np.array_equal(np.array([p.signed_distance for p in pairs]), ref["signed"])
