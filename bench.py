@@ -96,6 +96,35 @@ def make_pairs(cn, inp):
     return pairs
 
 
+# cfg3 (BASELINE configs[3]): two corotational 5-tet blocks, 50 x 50 x CFG3_NZ
+# nodes at 1 cm (CFG3_NZ = 30 -> 450 000 DoF, the north star's "450k-DoF"
+# figure; 50x50x20 as literally written gives 300 000), the
+# lower block (E=1e4) on a ground plane, the upper block (E=2e3) resting on it
+# and sliding at 0.5 m/s, nu=0.4, mu=0.4, 10 forced fast-scheme iterations,
+# PGS 30 sweeps / tol 1e-6 (the reference default budget).
+# Contacts: upper vertices vs lower triangles, lower vertices vs upper
+# triangles, lower vertices vs the ground.
+CFG3_NXZ = 50
+CFG3_NZ = 30
+
+
+def make_cfg3_config(cn, nxz=CFG3_NXZ, ny=CFG3_NZ):
+    from paper_2306_06946_b200.mesh import five_tet_grid
+
+    lower = five_tet_grid((nxz, ny, nxz), 0.01)
+    top = float(lower.nodes[:, 1].max())
+    upper = five_tet_grid((nxz, ny, nxz), 0.01, (0.0, top, 0.0))
+    objs = [cn.SoftSpec(name="lower", mesh=lower, young=1e4, poisson=0.4, density=1000.0, material="corotational"),
+            cn.SoftSpec(name="upper", mesh=upper, young=2e3, poisson=0.4, density=1000.0, velocity=(0.5, 0.0, 0.0),
+                        material="corotational"),
+            cn.PlaneSpec(name="ground", normal=(0.0, 1.0, 0.0), offset=0.0)]
+    return cn.SceneConfig(objects=objs, h=H, threshold=0.005,
+                          pgs=cn.PgsConfig(max_iterations=30, tolerance=1e-6, friction=0.4),
+                          newton=cn.NewtonConfig(scheme="fast", max_iterations=10, penetration_tol=-1.0,
+                                                 rotation_tol=-1.0),
+                          output=cn.OutputConfig(snapshots=False, metrics=False))
+
+
 # ----------------------------------------------------------------------------
 # GPU arm
 # ----------------------------------------------------------------------------

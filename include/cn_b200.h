@@ -133,6 +133,17 @@ int cnb_detect_vertex_mesh(int64_t nv, const int64_t* vids, const double* pts_a,
 /* Workspace bytes needed by cnb_pgs for c = 3*groups rows. */
 int64_t cnb_pgs_work_bytes(int64_t groups);
 
+/* Diagnostics of the grid-scale PGS kernel (env CNB_PGS_PROFILE=1): summed
+ * nanoseconds per phase since the last call, out[8]: solver wait, delta,
+ * group solves, epilogue, helper wait, helper partials, helper hand-off,
+ * sequential group loop. */
+int cnb_pgs_profile(double* out);
+
+/* Cycles per group of the sequential warp block solve of the PGS kernels on a
+ * resident synthetic tile (diagnostic microbenchmark; variant selects the
+ * update / projection form), out[0] cycles per group, out[1] checksum. */
+int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stream);
+
 /* PGS with Signorini + isotropic Coulomb disk in the reference's canonical
  * group order.  Replaces pgs solver.py:168-202, local_solve 124-165 and
  * regularize 99-121.

@@ -85,6 +85,18 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n)
                : "memory");
 }
+// L1-bypassing (L2-coherent) asynchronous copy of 16 bytes, for data other
+// SMs rewrite while the kernel runs.  Both addresses 16-byte aligned.
+__device__ __forceinline__ void cp_async16_cg(double* smem, const double* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// n doubles gmem -> smem through L2 only (16-byte chunks + an odd tail);
+// threads [0, nt) of the caller's numbering participate with index k.
+__device__ __forceinline__ void copy_cg(double* smem, const double* gmem, int n, int k, int nt) {
+  for (int e = k; 2 * e + 1 < n; e += nt) cp_async16_cg(smem + 2 * e, gmem + 2 * e);
+  if ((n & 1) && k == 0) smem[n - 1] = __ldcg(gmem + n - 1);
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __device__ __forceinline__ double warp_sum(double v) {

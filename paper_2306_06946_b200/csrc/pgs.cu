@@ -31,6 +31,7 @@ namespace cnb {
 
 constexpr int kBG = 32;         // groups per block (one per solver lane)
 constexpr int kBR = 3 * kBG;    // rows per block
+constexpr int kLDT = kBR + 1;   // shared tile row stride: odd, so lane l's rows 3l.. fall in distinct banks
 constexpr int kPgsThreads = 256;
 
 struct PgsScene {
@@ -186,6 +187,100 @@ __device__ __forceinline__ int local_solve_fast(const double d[3], const double 
   return 0;
 }
 
+// Branch-free local_solve_fast: every lane evaluates its own group with the
+// same instruction stream (no divergence in the sequential chain); the
+// caller keeps only the result of the lane whose turn it is.  Same values as
+// local_solve_fast (the unprojected branch multiplies by exactly 1.0).
+// fp64 1/sqrt(x) for x > 0 without the library's special-case branch: the
+// hardware approximation (rsqrt.approx.f64) refined by two Newton steps.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  return y;
+}
+
+template <int V = 0>
+__device__ __forceinline__ int local_solve_sel(const double d[3], const double l[3], const GroupConst& k,
+                                               double mu, double out[3]) {
+  const double ln_old = l[0];
+  const double x = fma(-d[0], k.ihw, ln_old);
+  const double ln = x > 0.0 ? x : 0.0;
+  const double dln = ln - ln_old;
+  const double dt0 = fma(k.htn0, dln, d[1]);
+  const double dt1 = fma(k.htn1, dln, d[2]);
+  double lt0 = l[1] - fma(k.it00, dt0, k.it01 * dt1);
+  double lt1 = l[2] - fma(k.it10, dt0, k.it11 * dt1);
+  const double radius = mu * ln;
+  const double n2 = fma(lt0, lt0, lt1 * lt1);
+  double sc;
+  if (V & 2) {  // branch-free: evaluate the projection scale unconditionally
+    const double rs = radius * rsqrt_nr(fmax(n2, 1e-300));
+    sc = n2 > radius * radius ? rs : 1.0;
+  } else {
+    sc = n2 > radius * radius ? radius * rsqrt(n2) : 1.0;
+  }
+  lt0 *= sc;
+  lt1 *= sc;
+  const bool zero = ln == 0.0, nofric = mu == 0.0;
+  out[0] = ln;
+  out[1] = (zero || nofric) ? 0.0 : lt0;
+  out[2] = (zero || nofric) ? 0.0 : lt1;
+  return ((k.bad & 1) || (!zero && !nofric && (k.bad & 2))) ? 1 : 0;
+}
+
+// Sequential Gauss-Seidel over one block of ng <= 32 groups by one warp,
+// lane l <-> group l.  Wt: the block's regularised diagonal tile (row stride
+// kLDT).  Per group: all lanes run local_solve_sel, lane g's change is
+// broadcast (3 shuffles) and every lane applies the rank-3 update of its
+// delta; W entries are loaded ahead of the chain.  EXACT selects the
+// reference's unfused association (a*b rounded, then the add) for the
+// update, otherwise fused multiply-adds.  err: lane-local flag for the
+// group the lane owns; dsq: sum of squared lambda changes of the lane.
+// V bit 0: the tile holds h^2 W (the update is three fused multiply-adds);
+// V bit 1: branch-free projection scale (rsqrt_nr).
+template <bool EXACT, int V = 0>
+__device__ __forceinline__ void block_solve(const double* __restrict__ Wt, int ng, int lane, double dl_[3],
+                                            double lm[3], const GroupConst& kc, double mu, double h2, double& dsq,
+                                            int& err) {
+  const double* wrow = Wt + 3 * lane * kLDT;
+#pragma unroll 2
+  for (int g = 0; g < ng; ++g) {
+    double w[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[3 * a + c] = wrow[a * kLDT + 3 * g + c];
+    double nw[3];
+    const int e = local_solve_sel<V>(dl_, lm, kc, mu, nw);
+    const bool me = lane == g;
+    double d0 = nw[0] - lm[0], d1 = nw[1] - lm[1], d2 = nw[2] - lm[2];
+    if (me) {
+      err |= e;
+      dsq += d0 * d0 + d1 * d1 + d2 * d2;
+      lm[0] = nw[0];
+      lm[1] = nw[1];
+      lm[2] = nw[2];
+    }
+    d0 = __shfl_sync(0xffffffffu, d0, g);
+    d1 = __shfl_sync(0xffffffffu, d1, g);
+    d2 = __shfl_sync(0xffffffffu, d2, g);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (EXACT) {
+        const double tmp = add(add(mul(w[3 * a], d0), mul(w[3 * a + 1], d1)), mul(w[3 * a + 2], d2));
+        dl_[a] = add(dl_[a], mul(h2, tmp));
+      } else if (V & 1) {
+        dl_[a] = fma(w[3 * a + 2], d2, fma(w[3 * a + 1], d1, fma(w[3 * a], d0, dl_[a])));
+      } else {
+        const double tmp = fma(w[3 * a + 2], d2, fma(w[3 * a + 1], d1, w[3 * a] * d0));
+        dl_[a] = fma(h2, tmp, dl_[a]);
+      }
+    }
+  }
+}
+
 // Lane-strided partial dot product  sum_{j in [lo,hi), j = lo+lane mod 32} w[j] x[j]
 // with four independent accumulators and the loads of four iterations issued
 // before their FMAs (in-order issue would otherwise stall on every load).
@@ -269,11 +364,11 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
     const int rows = (int)min((int64_t)kBR, c - r0);
     for (int e = tid; e < rows * rows; e += blockDim.x) {
       int i = e / rows, j = e - i * rows;
-      cp_async8(&sm.Wbb[i * kBR + j], s.W + (r0 + i) * s.ldw + r0 + j, true);
+      cp_async8(&sm.Wbb[i * kLDT + j], s.W + (r0 + i) * s.ldw + r0 + j, true);
     }
     cp_async_wait_all();
     __syncthreads();
-    for (int i = tid; i < rows; i += blockDim.x) sm.Wbb[i * kBR + i] = add(sm.Wbb[i * kBR + i], sm.dshift[(r0 + i) / 3]);
+    for (int i = tid; i < rows; i += blockDim.x) sm.Wbb[i * kLDT + i] = add(sm.Wbb[i * kLDT + i], sm.dshift[(r0 + i) / 3]);
   };
   stage_tile(0);
   for (int i = tid; i < (int)min((int64_t)kBR, c); i += blockDim.x) sm.dnext[i] = s.delta_base[i];
@@ -296,7 +391,7 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
       if (warp == 0) {
         // ---- sequential block solve ----
         const bool mine = lane < ng;
-        GroupConst kc;
+        GroupConst kc{};
         if (mine) {
           for (int a = 0; a < 3; ++a) {
             lm[a] = sm.lam[3 * (g0 + lane) + a];
@@ -304,50 +399,15 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
           }
           double Wd[9];
           for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) Wd[3 * i + j] = sm.Wbb[(3 * lane + i) * kBR + 3 * lane + j];
+            for (int j = 0; j < 3; ++j) Wd[3 * i + j] = sm.Wbb[(3 * lane + i) * kLDT + 3 * lane + j];
           group_const(Wd, h2, kc);
         }
         int err = 0;
-        for (int g = 0; g < ng; ++g) {
-          double d0 = 0, d1 = 0, d2 = 0;
-          int any = 0;
-          if (lane == g) {
-            double nw[3];
-            err = local_solve_fast(dl_, lm, kc, s.mu, nw);
-            if (!err) {
-              d0 = sub(nw[0], lm[0]);
-              d1 = sub(nw[1], lm[1]);
-              d2 = sub(nw[2], lm[2]);
-              any = (d0 != 0.0) || (d1 != 0.0) || (d2 != 0.0);
-              dsq += d0 * d0 + d1 * d1 + d2 * d2;
-              if (any) {
-                lm[0] = nw[0];
-                lm[1] = nw[1];
-                lm[2] = nw[2];
-              }
-            } else {
-              raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), 1.0 / kc.ihw);
-            }
-          }
-          if (__shfl_sync(0xffffffffu, err, g)) {
-            err = 1;
-            break;
-          }
-          any = __shfl_sync(0xffffffffu, any, g);
-          if (!any) continue;
-          d0 = __shfl_sync(0xffffffffu, d0, g);
-          d1 = __shfl_sync(0xffffffffu, d1, g);
-          d2 = __shfl_sync(0xffffffffu, d2, g);
-          if (mine) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              const double* wr = sm.Wbb + (3 * lane + a) * kBR + 3 * g;
-              double tmp = add(add(mul(wr[0], d0), mul(wr[1], d1)), mul(wr[2], d2));
-              dl_[a] = add(dl_[a], mul(h2, tmp));
-            }
-          }
-        }
-        if (err) {
+        block_solve<true>(sm.Wbb, ng, lane, dl_, lm, kc, s.mu, h2, dsq, err);
+        const unsigned bad = __ballot_sync(0xffffffffu, mine && err);
+        if (bad) {
+          const int g = __ffs(bad) - 1;  // first failing group in Gauss-Seidel order
+          if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), 1.0 / kc.ihw);
           if (lane == 0) sm.flags[0] = CNB_E_SINGULAR_BLOCK;
         } else if (mine) {
           for (int a = 0; a < 3; ++a) sm.lam[3 * (g0 + lane) + a] = lm[a];
@@ -438,7 +498,7 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
 }
 
 __host__ __device__ inline size_t pgs_smem_bytes(int64_t groups) {
-  return sizeof(double) * (size_t)(3 * groups + groups + kBR * kBR + 2 * kBR + 32) + 2 * sizeof(int) + 16;
+  return sizeof(double) * (size_t)(3 * groups + groups + kBR * kLDT + 2 * kBR + 32) + 2 * sizeof(int) + 16;
 }
 
 __device__ __forceinline__ PgsSmem carve(char* base, int64_t groups) {
@@ -449,7 +509,7 @@ __device__ __forceinline__ PgsSmem carve(char* base, int64_t groups) {
   sm.dshift = p;
   p += groups;
   sm.Wbb = p;
-  p += kBR * kBR;
+  p += kBR * kLDT;
   sm.P = p;
   p += kBR;
   sm.dnext = p;
@@ -535,7 +595,10 @@ __device__ bool wait_geq(volatile unsigned* p, unsigned target, volatile unsigne
   return true;
 }
 
-__global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshift, GridCtl* ctl) {
+// Regularisation shift (solver.py:99-121) and the per-group constants of the
+// regularised diagonal blocks, once per PGS call; lambda <- 0.
+constexpr int kKC = 8;  // doubles per packed GroupConst
+__global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshift, double* kconst, GridCtl* ctl) {
   __shared__ double red[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t G = s.groups, c = 3 * G;
@@ -554,33 +617,91 @@ __global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshi
   double shift = 1e-10 * red[0] / (double)c;
   if (shift <= 0.0) shift = 1e-30;
   for (int64_t g = tid; g < G; g += blockDim.x) {
-    double a[3][3];
+    double a[3][3], Wd[9];
     for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j)
+      for (int j = 0; j < 3; ++j) {
+        Wd[3 * i + j] = s.W[(3 * g + i) * s.ldw + 3 * g + j];
         a[i][j] = 0.5 * (s.W[(3 * g + i) * s.ldw + 3 * g + j] + s.W[(3 * g + j) * s.ldw + 3 * g + i]);
+      }
     double e[3];
     sym3_eigs(a, e);
     const double mn = fmin(e[0], fmin(e[1], e[2]));
     const double scale = fmax(fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))), 1e-300);
-    dshift[g] = (mn <= 1e-12 * scale) ? shift : 0.0;
+    const double sh = (mn <= 1e-12 * scale) ? shift : 0.0;
+    dshift[g] = sh;
+    for (int i = 0; i < 3; ++i) Wd[4 * i] = add(Wd[4 * i], sh);
+    GroupConst kc;
+    group_const(Wd, s.h2, kc);
+    double* o = kconst + kKC * g;
+    o[0] = kc.ihw;
+    o[1] = kc.htn0;
+    o[2] = kc.htn1;
+    o[3] = kc.it00;
+    o[4] = kc.it01;
+    o[5] = kc.it10;
+    o[6] = kc.it11;
+    o[7] = (double)kc.bad;
   }
   for (int64_t i = tid; i < c; i += blockDim.x) s.lam[i] = 0.0;
 }
 
 constexpr int kGridThreads = 512;
+constexpr int kHelpPre = 32;  // W values per lane a helper warp holds in registers (32 x 32 columns)
+
+// Shared memory of the solver CTA (helpers reuse the space for lambda):
+//   T0, T1 : diagonal tiles (double-buffered), Wx: cross tile W[b rows, bp cols]
+//            (all kBR x kLDT; T[(t+1)&1] also stages the helpers' partials)
+//   dcur   : delta of the block being solved
+//   lamx   : lambda of the block solved in the previous step
+//   lamn[2], kcn[2]: next block's lambda / group constants (prefetched)
+struct GridSmem {
+  double *T0, *T1, *Wx, *dcur, *lamx, *lamn, *kcn, *red;
+  int* flags;
+};
+
+__host__ __device__ inline size_t grid_smem_bytes() {
+  return sizeof(double) * (size_t)(3 * kBR * kLDT + 2 * kBR + 2 * kBR + 2 * kKC * kBG + 32) + 4 * sizeof(int);
+}
+
+__device__ __forceinline__ GridSmem grid_carve(char* base) {
+  GridSmem g;
+  double* p = (double*)base;
+  g.T0 = p;
+  p += kBR * kLDT;
+  g.T1 = p;
+  p += kBR * kLDT;
+  g.Wx = p;
+  p += kBR * kLDT;
+  g.dcur = p;
+  p += kBR;
+  g.lamx = p;
+  p += kBR;
+  g.lamn = p;
+  p += 2 * kBR;
+  g.kcn = p;
+  p += 2 * kKC * kBG;
+  g.red = p;
+  p += 32;
+  g.flags = (int*)p;
+  return g;
+}
 
 __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, const double* __restrict__ dshift,
-                                                                double* partial, GridCtl* ctl, int nch,
-                                                                int lam_in_smem) {
+                                                                const double* __restrict__ kconst, double* partial,
+                                                                GridCtl* ctl, int nch, int lam_in_smem,
+                                                                unsigned long long* prof) {
+  // prof (optional, CNB_PGS_PROFILE=1): summed ns per phase, see cnb_pgs_profile
+  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp = 0;
+  auto stamp = [&](int k) {
+    if (prof && threadIdx.x == 0) {
+      const unsigned long long now = global_ns();
+      if (k >= 0) pf[k] += now - tp;
+      tp = now;
+    }
+  };
   extern __shared__ __align__(16) char smem_raw[];
-  double* lams = (double*)smem_raw;        // helpers: resident copy of lambda (aliases the tiles)
-  double* Wbb0 = (double*)smem_raw;        // kBR x kBR diagonal tiles, double-buffered
-  double* Wbb1 = Wbb0 + kBR * kBR;
-  double* Wx = Wbb1 + kBR * kBR;           // kBR x kBR cross tile W[next rows, current cols]
-  double* dcur = Wx + kBR * kBR;           // kBR
-  double* lamx = dcur + kBR;               // kBR
-  double* red = lamx + kBR;                // 32
-  int* flags = (int*)(red + 32);           // [0] error, [1] stop
+  GridSmem sm = grid_carve(smem_raw);
+  double* lams = (double*)smem_raw;  // helpers: resident copy of lambda
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
   const int64_t G = s.groups, c = 3 * G;
@@ -597,8 +718,28 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
   double dsq = 0.0;
   int iterations = 0;
   bool converged = false;
-  if (tid == 0) flags[0] = flags[1] = 0;
+  if (tid == 0) sm.flags[0] = sm.flags[1] = 0;
+  auto rows_of = [&](int blk) { return 3 * (int)min((int64_t)kBG, G - (int64_t)blk * kBG); };
+  // prefetch (cp.async) of block `blk`'s diagonal tile into T, its lambda and
+  // group constants into slot `slot`, and W[blk rows, cols of block `xb`] into
+  // Wx; threads [t0, t0 + nt) participate.
+  auto prefetch = [&](int blk, int xb, double* T, int slot, int t0, int nt) {
+    const int64_t rb0 = 3 * (int64_t)blk * kBG, xb0 = 3 * (int64_t)xb * kBG;
+    const int rws = rows_of(blk), xcols = rows_of(xb);
+    const int tw = (tid - t0) >> 5, ntw = nt >> 5;
+    for (int i = tw; i < rws; i += ntw) {
+      const double* src = s.W + (rb0 + i) * s.ldw;
+      for (int j = lane; j < rws; j += 32) cp_async8(&T[i * kLDT + j], src + rb0 + j, true);
+      if (xb >= 0)
+        for (int j = lane; j < xcols; j += 32) cp_async8(&sm.Wx[i * kLDT + j], src + xb0 + j, true);
+    }
+    copy_cg(&sm.lamn[slot * kBR], lamg + rb0, rws, tid - t0, nt);  // rewritten every sweep: bypass L1
+    for (int e = tid - t0; e < kKC * rws / 3; e += nt)
+      cp_async8(&sm.kcn[slot * kKC * kBG + e], kconst + kKC * (rb0 / 3) + e, true);
+  };
   __syncthreads();
+  stamp(-1);
+  if (solver) prefetch(0, -1, sm.T0, 0, 0, blockDim.x);
   for (unsigned t = 0;; ++t) {
     const int b = (int)(t % nb);
     const int sweep = (int)(t / nb);
@@ -609,123 +750,104 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
     const int rows = 3 * ng;
     const int64_t r0 = 3 * g0;
     if (solver) {
-      // Tiles: Wcur = diagonal tile of block b (prefetched during step t-1 by
-      // warps 1..7), Wx = W[rows of b, cols of bp] (same), both raw W.
-      double* Wcur = (nb == 1 || !(t & 1)) ? Wbb0 : Wbb1;
-      double* Wnxt = (t & 1) ? Wbb0 : Wbb1;
-      if (t == 0) {
-        for (int e = tid; e < rows * rows; e += blockDim.x) {
-          const int i = e / rows, j = e - i * rows;
-          cp_async8(&Wcur[i * kBR + j], s.W + (r0 + i) * s.ldw + r0 + j, true);
-        }
-        for (int i = tid; i < rows; i += blockDim.x) dcur[i] = s.delta_base[r0 + i];
-      } else if (tid == 0) {
+      const int slot = (nb == 1) ? 0 : (int)(t & 1);
+      double* Tc = slot ? sm.T1 : sm.T0;  // this block's diagonal tile
+      double* Tn = slot ? sm.T0 : sm.T1;  // next block's tile / partial staging
+      if (t > 0 && tid == 0) {
+        stamp(3);  // epilogue of step t-1 -> here
         wait_geq(vready, H * t, nullptr, ctl);
       }
+      stamp(0);  // wait for helpers
+      __syncthreads();
+      // delta_base of the block and (t > 0, nb > 1) the helpers' partials
+      for (int i = tid; i < rows; i += blockDim.x) cp_async8(&sm.dcur[i], s.delta_base + r0 + i, true);
+      const double* part = partial + (size_t)((t - 1) & 1) * kBR * nch;
+      if (t > 0 && nb > 1) copy_cg(Tn, part, rows * nch, tid, blockDim.x);  // written by other SMs
       cp_async_wait_all();
       __syncthreads();
       if (t == 0 || nb > 1)  // regularisation shift (solver.py:119-120) on the fresh tile
-        for (int i = tid; i < rows; i += blockDim.x) Wcur[i * kBR + i] = add(Wcur[i * kBR + i], dshift[(r0 + i) / 3]);
+        for (int i = tid; i < rows; i += blockDim.x) Tc[i * kLDT + i] = add(Tc[i * kLDT + i], dshift[(r0 + i) / 3]);
+      if (nb == 1) __syncthreads();
       if (t > 0) {
-        // ---- delta of block b: helpers' partials of step t-1 + cross term with block bp
-        const double* part = partial + (size_t)((t - 1) & 1) * kBR * nch;
-        const int64_t cb0 = 3 * (int64_t)bp * kBG;
-        const int cols = 3 * (int)min((int64_t)kBG, G - (int64_t)bp * kBG);
-        for (int j = tid; j < cols; j += blockDim.x) lamx[j] = __ldcg(lamg + cb0 + j);
-        __syncthreads();
-        const double* X = (nb > 1) ? Wx : Wcur;  // nb == 1: the block itself (regularised)
-        for (int i = warp; i < rows; i += nwarps) {
-          double acc = 0.0;
-          for (int j = lane; j < cols; j += 32) acc = fma(X[i * kBR + j], lamx[j], acc);
+        // ---- delta of block b = delta_base + h^2 (partials + W[b, bp] lam_bp), thread per row
+        const int xcols = rows_of(bp);
+        const double* X = (nb > 1) ? sm.Wx : Tc;  // nb == 1: the block itself (regularised)
+        for (int i = tid; i < rows; i += blockDim.x) {
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          const double* xr = X + i * kLDT;
+          int j = 0;
+          for (; j + 4 <= xcols; j += 4) {
+            a0 = fma(xr[j], sm.lamx[j], a0);
+            a1 = fma(xr[j + 1], sm.lamx[j + 1], a1);
+            a2 = fma(xr[j + 2], sm.lamx[j + 2], a2);
+            a3 = fma(xr[j + 3], sm.lamx[j + 3], a3);
+          }
+          for (; j < xcols; ++j) a0 = fma(xr[j], sm.lamx[j], a0);
+          double acc = (a0 + a1) + (a2 + a3);
           if (nb > 1)
-            for (int ch = lane; ch < nch; ch += 32) acc += __ldcg(part + (size_t)i * nch + ch);
-          acc = warp_sum(acc);
-          if (lane == 0) dcur[i] = add(s.delta_base[r0 + i], mul(h2, acc));
+            for (int ch = 0; ch < nch; ++ch) acc += Tn[i * nch + ch];
+          sm.dcur[i] = add(sm.dcur[i], mul(h2, acc));
         }
       }
       __syncthreads();
-      double* Wbb = Wcur;
+      stamp(1);  // delta of block b
       if (warp != 0 && nb > 1) {
-        // ---- warps 1..7: prefetch the next block's tiles while warp 0 solves
-        const int64_t rn0 = 3 * (int64_t)bn * kBG;
-        const int rows_n = 3 * (int)min((int64_t)kBG, G - (int64_t)bn * kBG);
-        const int pt = tid - 32, np = blockDim.x - 32;
-        for (int e = pt; e < rows_n * rows_n; e += np) {
-          const int i = e / rows_n, j = e - i * rows_n;
-          cp_async8(&Wnxt[i * kBR + j], s.W + (rn0 + i) * s.ldw + rn0 + j, true);
-        }
-        for (int e = pt; e < rows_n * rows; e += np) {
-          const int i = e / rows, j = e - i * rows;
-          cp_async8(&Wx[i * kBR + j], s.W + (rn0 + i) * s.ldw + r0 + j, true);
-        }
+        // ---- warps 1..15: prefetch the next block while warp 0 solves
+        prefetch(bn, b, Tn, slot ^ 1, 32, blockDim.x - 32);
       }
       if (warp == 0) {
         const bool mine = lane < ng;
-        GroupConst kc;
+        GroupConst kc{};
         if (mine) {
-          for (int a = 0; a < 3; ++a) {
-            lm[a] = __ldcg(lamg + 3 * (g0 + lane) + a);
-            dl_[a] = dcur[3 * lane + a];
+          const double* kk = sm.kcn + slot * kKC * kBG + kKC * lane;
+          kc.ihw = kk[0];
+          kc.htn0 = kk[1];
+          kc.htn1 = kk[2];
+          kc.it00 = kk[3];
+          kc.it01 = kk[4];
+          kc.it10 = kk[5];
+          kc.it11 = kk[6];
+          kc.bad = (int)kk[7];
+          for (int a = 0; a < 3; ++a) {  // nb == 1: the block's own lambda from the previous step
+            lm[a] = (nb == 1 && t > 0) ? sm.lamx[3 * lane + a] : sm.lamn[slot * kBR + 3 * lane + a];
+            dl_[a] = sm.dcur[3 * lane + a];
           }
-          double Wd[9];
-          for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) Wd[3 * i + j] = Wbb[(3 * lane + i) * kBR + 3 * lane + j];
-          group_const(Wd, h2, kc);
+        } else {
+          kc.ihw = 1.0;
+          lm[0] = lm[1] = lm[2] = dl_[0] = dl_[1] = dl_[2] = 0.0;
         }
         int err = 0;
-        for (int g = 0; g < ng; ++g) {
-          double d0 = 0, d1 = 0, d2 = 0;
-          int any = 0;
-          if (lane == g) {
-            double nw[3];
-            err = local_solve_fast(dl_, lm, kc, s.mu, nw);
-            if (!err) {
-              d0 = nw[0] - lm[0];
-              d1 = nw[1] - lm[1];
-              d2 = nw[2] - lm[2];
-              any = (d0 != 0.0) || (d1 != 0.0) || (d2 != 0.0);
-              dsq += d0 * d0 + d1 * d1 + d2 * d2;
-              if (any) {
-                lm[0] = nw[0];
-                lm[1] = nw[1];
-                lm[2] = nw[2];
-              }
-            } else {
-              raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), 1.0 / kc.ihw);
-            }
-          }
-          if (__shfl_sync(0xffffffffu, err, g)) {
-            err = 1;
-            break;
-          }
-          any = __shfl_sync(0xffffffffu, any, g);
-          if (!any) continue;
-          d0 = __shfl_sync(0xffffffffu, d0, g);
-          d1 = __shfl_sync(0xffffffffu, d1, g);
-          d2 = __shfl_sync(0xffffffffu, d2, g);
-          if (mine) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              const double* wr = Wbb + (3 * lane + a) * kBR + 3 * g;
-              const double tmp = fma(wr[2], d2, fma(wr[1], d1, wr[0] * d0));
-              dl_[a] = fma(h2, tmp, dl_[a]);
-            }
+        block_solve<false>(Tc, ng, lane, dl_, lm, kc, s.mu, h2, dsq, err);
+        stamp(7);  // the sequential loop itself (+ kc / lambda loads)
+        const unsigned bad = __ballot_sync(0xffffffffu, mine && err);
+        if (bad) {
+          const int g = __ffs(bad) - 1;  // first failing group in Gauss-Seidel order
+          if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), 1.0 / kc.ihw);
+          if (lane == 0) sm.flags[0] = 1;
+        } else if (mine) {
+          for (int a = 0; a < 3; ++a) {
+            __stcg(lamg + 3 * (g0 + lane) + a, lm[a]);
+            sm.lamx[3 * lane + a] = lm[a];
           }
         }
-        if (err) {
-          if (lane == 0) flags[0] = 1;
-        } else if (mine) {
-          for (int a = 0; a < 3; ++a) __stcg(lamg + 3 * (g0 + lane) + a, lm[a]);
+        __syncwarp();
+        // early hand-off: helpers may start on this block's lambda before the
+        // rest of the CTA reaches the barrier (a stop decided below is seen by
+        // them at their next wait)
+        if (lane == 0 && !bad) {
+          __threadfence();
+          atomicExch((unsigned*)vsolved, t + 1);
         }
       }
       __syncthreads();
-      bool stop = flags[0] != 0;
+      stamp(2);  // group solves (+ next-block prefetch)
+      bool stop = sm.flags[0] != 0;
       if (!stop && b + 1 == nb) {
         // ---- end of sweep: epsilon (solver.py:194-199)
         iterations = sweep + 1;
         if (warp == 0) {
           const double v = warp_sum(dsq);
-          if (lane == 0) red[0] = v;
+          if (lane == 0) sm.red[0] = v;
         }
         double nl = 0.0;
         for (int64_t i = tid; i < c; i += blockDim.x) {
@@ -733,33 +855,52 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
           nl += l * l;
         }
         nl = warp_sum(nl);
-        if (lane == 0) red[1 + warp] = nl;
+        if (lane == 0) sm.red[1 + warp] = nl;
         __syncthreads();
         if (tid == 0) {
           double den2 = 0.0;
-          for (int w = 0; w < nwarps; ++w) den2 += red[1 + w];
-          const double num = sqrt(red[0]), den = sqrt(den2);
+          for (int w = 0; w < nwarps; ++w) den2 += sm.red[1 + w];
+          const double num = sqrt(sm.red[0]), den = sqrt(den2);
           const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
           s.eps_hist[sweep] = eps;
-          flags[1] = (eps <= s.tol) ? 1 : 0;
+          sm.flags[1] = (eps <= s.tol) ? 1 : 0;
         }
         __syncthreads();
         dsq = 0.0;
-        converged = flags[1] != 0;
+        converged = sm.flags[1] != 0;
         stop = converged || (sweep + 1 >= s.max_iter);
       }
       if (ctl->timeout) stop = true;
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        if (stop) atomicExch((unsigned*)vstop, 1u);
-        __threadfence();
-        atomicExch((unsigned*)vsolved, t + 1);
+      if (stop) {
+        if (tid == 0) {
+          __threadfence();
+          atomicExch((unsigned*)vstop, 1u);
+        }
+        break;
       }
-      if (stop) break;
     } else {
-      // ---- helper: wait for the block solved at step t-1, then partials for block bn
+      // ---- helper: partials for the rows of block bn over all columns except
+      // block b, with lambda as of the end of step t-1.  The W slice of this
+      // step is loaded into registers before waiting for the solver.
+      const int64_t gn0 = (int64_t)bn * kBG;
+      const int rows_n = 3 * (int)min((int64_t)kBG, G - gn0);
+      const int64_t cb0 = r0, cb1 = r0 + rows;  // block b columns excluded
+      const unsigned hw = (blockIdx.x - 1) * nwarps + warp;
+      const bool has_item = nb > 1 && hw < (unsigned)(rows_n * nch);
+      const int i = has_item ? (int)(hw / nch) : 0, ch = has_item ? (int)(hw % nch) : 0;
+      const int64_t r = 3 * gn0 + i;
+      const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
+      const double* wr = s.W + r * s.ldw;
+      double wv[kHelpPre];
+#pragma unroll
+      for (int u = 0; u < kHelpPre; ++u) {
+        const int64_t j = c0 + lane + 32 * u;
+        const bool ok = has_item && j < c1 && (j < cb0 || j >= cb1);
+        wv[u] = ok ? wr[j] : 0.0;
+      }
+      if (blockIdx.x == 1) stamp(6);  // helper: ready -> next wait start
       if (tid == 0) wait_geq(vsolved, t, vstop, ctl);
+      if (blockIdx.x == 1) stamp(4);  // helper: wait for the solver
       __syncthreads();
       if (*vstop) break;
       if (lam_in_smem) {
@@ -768,34 +909,34 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
           for (int64_t j = tid; j < c; j += blockDim.x) lams[j] = 0.0;
         } else {
           const int64_t pb0 = 3 * (int64_t)bp * kBG;
-          const int pcols = 3 * (int)min((int64_t)kBG, G - (int64_t)bp * kBG);
+          const int pcols = rows_of(bp);
           for (int j = tid; j < pcols; j += blockDim.x) lams[pb0 + j] = __ldcg(lamg + pb0 + j);
         }
         __syncthreads();
       }
-      const int64_t gn0 = (int64_t)bn * kBG;
-      const int rows_n = 3 * (int)min((int64_t)kBG, G - gn0);
-      const int64_t cb0 = r0, cb1 = r0 + rows;  // block b columns excluded
-      const unsigned hw = (blockIdx.x - 1) * nwarps + warp, nhw = H * nwarps;
-      if (nb > 1) {
-        double* part = partial + (size_t)(t & 1) * kBR * nch;
-        for (unsigned item = hw; item < (unsigned)(rows_n * nch); item += nhw) {
-          const int i = item / nch, ch = item - i * nch;
-          const int64_t r = 3 * gn0 + i;
-          const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
-          const double* wr = s.W + r * s.ldw;
-          // [c0, c1) minus the columns of block b, as two branch-free ranges
-          double acc = lam_in_smem
-                           ? lane_dot<false>(wr, lams, c0, min(c1, cb0), lane) + lane_dot<false>(wr, lams, max(c0, cb1), c1, lane)
-                           : lane_dot<true>(wr, lamg, c0, min(c1, cb0), lane) + lane_dot<true>(wr, lamg, max(c0, cb1), c1, lane);
-          acc = warp_sum(acc);
-          if (lane == 0) {
-            if (r >= c0 && r < c1) acc = fma(dshift[r / 3], lam_in_smem ? lams[r] : __ldcg(lamg + r), acc);
-            __stcg(part + (size_t)i * nch + ch, acc);
+      if (has_item) {
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < kHelpPre; ++u) {
+          const int64_t j = min(c0 + lane + 32 * u, c - 1);
+          a[u & 3] = fma(wv[u], lam_in_smem ? lams[j] : __ldcg(lamg + j), a[u & 3]);
+        }
+        for (int64_t j0 = c0 + 32 * kHelpPre; j0 < c1; j0 += 32 * kHelpPre) {  // slices wider than the registers
+#pragma unroll 8
+          for (int u = 0; u < kHelpPre; ++u) {
+            const int64_t j = j0 + lane + 32 * u;
+            if (j < c1 && (j < cb0 || j >= cb1))
+              a[u & 3] = fma(wr[j], lam_in_smem ? lams[j] : __ldcg(lamg + j), a[u & 3]);
           }
+        }
+        double acc = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
+        if (lane == 0) {
+          if (r >= c0 && r < c1) acc = fma(dshift[r / 3], lam_in_smem ? lams[r] : __ldcg(lamg + r), acc);
+          __stcg(partial + (size_t)(t & 1) * kBR * nch + (size_t)i * nch + ch, acc);
         }
       }
       __syncthreads();
+      if (blockIdx.x == 1) stamp(5);  // helper: lambda refresh + partials
       if (tid == 0) {
         __threadfence();
         atomicAdd((unsigned*)vready, 1u);
@@ -810,14 +951,15 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
   const unsigned gw = blockIdx.x * nwarps + warp, ngw = gridDim.x * nwarps;
   for (int64_t r = gw; r < c; r += ngw) {
     const double* wr = s.W + r * s.ldw;
-    double acc = 0.0;
-    acc = lane_dot<true>(wr, lamg, 0, c, lane);
+    double acc = lane_dot<true>(wr, lamg, 0, c, lane);
     acc = warp_sum(acc);
     if (lane == 0) {
       acc = fma(dshift[r / 3], __ldcg(lamg + r), acc);
       s.delta_end[r] = add(s.delta_base[r], mul(h2, acc));
     }
   }
+  if (prof && tid == 0 && blockIdx.x <= 1)
+    for (int k = 0; k < 8; ++k) atomicAdd(prof + k, pf[k]);
   if (solver && tid == 0) {
     s.iters_conv[0] = iterations;
     s.iters_conv[1] = converged ? 1 : 0;
@@ -825,14 +967,76 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
   }
 }
 
+template <int V>
+__global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double* out) {
+  extern __shared__ __align__(16) char bsm[];
+  double* T = (double*)bsm;
+  const int lane = threadIdx.x;
+  for (int i = 0; i < kBR; ++i)
+    for (int j = lane; j < kBR; j += 32) {
+      const double v = (i == j) ? 4.0 : 0.05 * sin(0.37 * i + 0.91 * j + 0.13 * i * j) / (1.0 + fabs(i - j));
+      T[i * kLDT + j] = v;
+    }
+  __syncwarp();
+  for (int i = 0; i < kBR; ++i)  // symmetrise
+    for (int j = lane; j < i; j += 32) T[j * kLDT + i] = T[i * kLDT + j];
+  __syncwarp();
+  const double h2 = 1e-4;
+  double Wd[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) Wd[3 * a + b] = T[(3 * lane + a) * kLDT + 3 * lane + b];
+  GroupConst kc;
+  group_const(Wd, h2, kc);
+  if (V & 1) {
+    for (int i = 0; i < kBR; ++i)
+      for (int j = lane; j < kBR; j += 32) T[i * kLDT + j] *= h2;
+    __syncwarp();
+  }
+  double dl_[3], lm[3] = {0.0, 0.0, 0.0}, dsq = 0.0;
+  int err = 0;
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    dl_[0] = -1e-4 * (1.0 + 0.01 * lane);
+    dl_[1] = ((V & 4) ? 3e-4 : 3e-5) * sin(1.0 * lane);  // V bit 2: tangential loads outside the cone
+    dl_[2] = ((V & 4) ? 3e-4 : 3e-5) * cos(1.0 * lane);
+    block_solve<false, (V & 3)>(T, kBG, lane, dl_, lm, kc, 0.4, h2, dsq, err);
+  }
+  long long t1 = clock64();
+  const double s = warp_sum(lm[0] + lm[1] + lm[2] + dsq);
+  if (lane == 0) {
+    out[0] = (double)(t1 - t0) / ((double)reps * kBG);
+    out[1] = s;
+  }
+}
+
+// CNB_PGS_PROFILE=1: per-phase nanosecond sums of the grid kernel (device
+// buffer, read back with cnb_pgs_profile)
+static unsigned long long* pgs_profile_buffer() {
+  static unsigned long long* buf = nullptr;
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CNB_PGS_PROFILE");
+    on = (e && e[0] == '1') ? 1 : 0;
+    if (on && cudaMalloc(&buf, 8 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(buf, 0, 8 * sizeof(unsigned long long));
+    else
+      buf = nullptr;
+  }
+  return buf;
+}
+
 static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   int dev = 0, sms = 0;
   CNB_CUDA(cudaGetDevice(&dev));
   CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const size_t tiles = sizeof(double) * (3 * kBR * kBR + 2 * kBR + 32) + 2 * sizeof(int) + 16;
+  const size_t tiles = grid_smem_bytes();
   const size_t lam_bytes = sizeof(double) * (size_t)(3 * s.groups);
   const int lam_in_smem = lam_bytes <= pgs_max_smem() ? 1 : 0;
   const size_t smem = std::max(tiles, lam_in_smem ? lam_bytes : (size_t)0);
+  if (smem > pgs_max_smem()) {
+    set_error("pgs: grid kernel needs %zu bytes of shared memory", smem);
+    return CNB_E_INTERNAL;
+  }
   CNB_CUDA(cudaFuncSetAttribute(pgs_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   CNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pgs_grid_kernel, kGridThreads, smem));
@@ -842,8 +1046,10 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   }
   const int grid = sms;  // one CTA per SM: all co-resident (cooperative launch)
   const int nwarps = kGridThreads / 32;
-  const int nch = std::max(1, ((grid - 1) * nwarps + kBR - 1) / kBR);
-  const size_t bytes = 64 + sizeof(double) * ((size_t)s.groups + 2 * (size_t)kBR * nch);
+  // one (row, column-slice) item per helper warp; the partials of a block are
+  // staged in a kBR x kLDT tile by the solver
+  const int nch = std::max(1, std::min(((grid - 1) * nwarps) / kBR, kLDT));
+  const size_t bytes = 64 + sizeof(double) * ((size_t)s.groups * (1 + kKC) + 1 + 2 * (size_t)kBR * nch);
   static void* ws_p = nullptr;
   static size_t ws_cap = 0;
   if (bytes > ws_cap) {
@@ -854,12 +1060,16 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   }
   GridCtl* ctl = (GridCtl*)ws_p;
   double* dshift = (double*)((char*)ws_p + 64);
-  double* partial = dshift + s.groups;
-  pgs_prep_kernel<<<1, 1024, 0, st>>>(s, dshift, ctl);
+  double* kconst = dshift + s.groups;
+  double* partial = kconst + kKC * s.groups + (s.groups & 1);  // 16-byte aligned (copy_cg)
+  pgs_prep_kernel<<<1, 1024, 0, st>>>(s, dshift, kconst, ctl);
   CNB_LAUNCH_CHECK("pgs_prep_kernel");
   PgsScene sc = s;
   int lis = lam_in_smem;
-  void* args[] = {(void*)&sc, (void*)&dshift, (void*)&partial, (void*)&ctl, (void*)&nch, (void*)&lis};
+  int nchv = nch;
+  unsigned long long* prof = pgs_profile_buffer();
+  void* args[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
+                  (void*)&nchv, (void*)&lis, (void*)&prof};
   CNB_CUDA(cudaLaunchCooperativeKernel((const void*)pgs_grid_kernel, dim3(grid), dim3(kGridThreads), args, smem, st));
   CNB_LAUNCH_CHECK("pgs_grid_kernel");
   return CNB_OK;
@@ -877,6 +1087,54 @@ using namespace cnb;
 extern "C" {
 
 int64_t cnb_pgs_work_bytes(int64_t groups) { (void)groups; return 0; }
+
+// Cycles per group of the warp block solve (diagnostic): variant v of block_solve on a
+// resident synthetic tile, reps repetitions.  out[0] = cycles / group.
+int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stream) {
+  double* d = nullptr;
+  CNB_CUDA(cudaMalloc(&d, 2 * sizeof(double)));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int sm = (int)(sizeof(double) * kBR * kLDT);
+#define CNB_BBS(V)                                                                                  \
+  CNB_CUDA(cudaFuncSetAttribute(bench_block_solve_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+  bench_block_solve_kernel<V><<<1, 32, sm, st>>>(reps, d);
+  switch (variant) {
+    case 0: CNB_BBS(0) break;
+    case 1: CNB_BBS(1) break;
+    case 2: CNB_BBS(2) break;
+    case 3: CNB_BBS(3) break;
+    case 4: CNB_BBS(4) break;
+    case 5: CNB_BBS(5) break;
+    case 6: CNB_BBS(6) break;
+    default: CNB_BBS(7) break;
+  }
+#undef CNB_BBS
+  CNB_LAUNCH_CHECK("bench_block_solve_kernel");
+  double h[2];
+  CNB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CNB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d);
+  out[0] = h[0];
+  out[1] = h[1];
+  return CNB_OK;
+}
+
+// Phase sums (ns) of the grid PGS kernel since the last call (CNB_PGS_PROFILE=1):
+// out[0] solver wait, [1] delta, [2] solves, [3] epilogue, [4] helper wait,
+// [5] helper partials, [6] helper hand-off, [7] the sequential group loop.
+// Returns CNB_E_VALIDATION if off.
+int cnb_pgs_profile(double* out) {
+  unsigned long long* b = pgs_profile_buffer();
+  if (!b) {
+    set_error("pgs profile: set CNB_PGS_PROFILE=1");
+    return CNB_E_VALIDATION;
+  }
+  unsigned long long h[8];
+  CNB_CUDA(cudaMemcpy(h, b, sizeof(h), cudaMemcpyDeviceToHost));
+  CNB_CUDA(cudaMemset(b, 0, sizeof(h)));
+  for (int k = 0; k < 8; ++k) out[k] = (double)h[k];
+  return CNB_OK;
+}
 
 int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_base, double h, double mu,
             double tol, int32_t max_iter, double* lam, double* delta_end, double* eps_hist,
