@@ -967,6 +967,396 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
   }
 }
 
+// ============================================================================
+// Pipelined grid PGS (lookahead 2)
+// ============================================================================
+// Same iterate as pgs_cta / pgs_grid_kernel, restructured so that the solver
+// warp's sequential block solve is the only thing on the critical path.
+// Step t solves block b = t mod nb.
+//
+//   helpers (CTAs 1..H), step t: once lambda of block b-1 is published, the
+//     lazy row products of block b+2 over every column except blocks b and
+//     b+1 (whose lambda is not final yet).  They have two block solves of
+//     slack instead of one, so the inter-SM hand-off latency is hidden.
+//   solver CTA, step t:
+//     warp 0      : sequential block solve of b (lane = group);
+//     warps 1..15 : concurrently, publish lambda_{b-1}; prefetch T(b+1),
+//                   W[b+1, b] and lambda(b+1) (cp.async); the cross term
+//                   X2 = W[b+1, b-1] lambda_{b-1} from registers loaded one
+//                   step earlier; the helpers' partials of block b+1 (step
+//                   t-1) summed in fixed order; ||lambda||^2 of the sweep so far;
+//     then all    : delta(b+1) = delta_base + h^2 (partials + X2 + W[b+1, b] lambda_b)
+//                   (one 96 x 96 GEMV from shared memory), two barriers.
+// Every sum is taken in a fixed order: the result is bitwise repeatable.
+constexpr int kPipeThreads = 512;
+constexpr int kAuxWarps = kPipeThreads / 32 - 1;
+constexpr int kX2Rows = (kBR + kAuxWarps - 1) / kAuxWarps;
+constexpr int kPartBufs = 3;
+
+struct PipeSmem {
+  double *T0, *T1, *Wx, *dcur, *pacc, *lamx, *lamn, *kcn, *red;
+  int* flags;
+};
+
+__host__ __device__ inline size_t pipe_smem_bytes() {
+  return sizeof(double) * (size_t)(3 * kBR * kLDT + kBR + kBR + 2 * kBR + 2 * kBR + kKC * kBG + 32) +
+         4 * sizeof(int);
+}
+
+__device__ __forceinline__ PipeSmem pipe_carve(char* base) {
+  PipeSmem g;
+  double* p = (double*)base;
+  g.T0 = p;
+  p += kBR * kLDT;
+  g.T1 = p;
+  p += kBR * kLDT;
+  g.Wx = p;
+  p += kBR * kLDT;
+  g.dcur = p;
+  p += kBR;
+  g.pacc = p;
+  p += kBR;
+  g.lamx = p;
+  p += 2 * kBR;
+  g.lamn = p;
+  p += 2 * kBR;
+  g.kcn = p;
+  p += kKC * kBG;
+  g.red = p;
+  p += 32;
+  g.flags = (int*)p;
+  return g;
+}
+
+// group constants of one group from a packed record (global or shared)
+__device__ __forceinline__ void load_group_const(GroupConst& k, const double* kk, bool valid) {
+  if (valid) {
+    k.ihw = kk[0];
+    k.htn0 = kk[1];
+    k.htn1 = kk[2];
+    k.it00 = kk[3];
+    k.it01 = kk[4];
+    k.it10 = kk[5];
+    k.it11 = kk[6];
+    k.bad = (int)kk[7];
+  } else {
+    k.ihw = 1.0;
+    k.htn0 = k.htn1 = k.it00 = k.it01 = k.it10 = k.it11 = 0.0;
+    k.bad = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, const double* __restrict__ dshift,
+                                                                const double* __restrict__ kconst, double* partial,
+                                                                GridCtl* ctl, int nch, int lam_in_smem,
+                                                                unsigned long long* prof) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = s.groups, c = 3 * G;
+  const int nb = (int)((G + kBG - 1) / kBG);
+  const unsigned H = gridDim.x - 1;
+  const double h2 = s.h2;
+  double* lamg = s.lam;
+  volatile unsigned* vsolved = &ctl->solved;
+  volatile unsigned* vready = &ctl->ready;
+  volatile unsigned* vstop = &ctl->stop;
+  const size_t pstride = (size_t)kBR * nch;
+  auto rows_of = [&](int blk) { return 3 * (int)min((int64_t)kBG, G - (int64_t)blk * kBG); };
+  auto wrap = [&](int blk) { return blk >= nb ? blk - nb : blk; };
+  // CNB_PGS_PROFILE=1: [0] solver idle at B1, [1] phase B, [2] block solve,
+  // [3] aux wait for partials, [4] helper wait, [5] helper work, [6] aux phase A
+  unsigned long long tp = 0;
+  const bool stamper = prof && (tid == 0 || tid == 32) && blockIdx.x <= 1;
+  auto stamp = [&](int k) {
+    if (stamper) {
+      const unsigned long long now = global_ns();
+      if (k >= 0) atomicAdd(prof + k, now - tp);  // fire-and-forget RED
+      tp = now;
+    }
+  };
+
+  if (blockIdx.x == 0) {
+    PipeSmem sm = pipe_carve(smem_raw);
+    if (tid == 0) sm.flags[0] = sm.flags[1] = 0;
+    {
+      const int r0 = rows_of(0);
+      for (int i = warp; i < r0; i += kPipeThreads / 32)
+        for (int j = lane; j < r0; j += 32) cp_async8(&sm.T0[i * kLDT + j], s.W + i * s.ldw + j, true);
+      cp_async_wait_all();
+    }
+    for (int i = tid; i < kBR; i += blockDim.x) {
+      sm.dcur[i] = i < rows_of(0) ? s.delta_base[i] : 0.0;
+      sm.lamn[i] = sm.lamn[kBR + i] = 0.0;  // lambda starts at zero (prep zeroed the global copy)
+      sm.lamx[i] = sm.lamx[kBR + i] = 0.0;
+    }
+    __syncthreads();
+    for (int i = tid; i < rows_of(0); i += blockDim.x)
+      sm.T0[i * kLDT + i] = add(sm.T0[i * kLDT + i], dshift[i / 3]);
+    // solver warp state
+    GroupConst kc{};
+    double dsq = 0.0;
+    if (warp == 0) load_group_const(kc, kconst + kKC * lane, lane < rows_of(0) / 3);
+    // aux state: W[b+2 rows, b cols] for the next step's cross term (rows
+    // (warp-1) + kAuxWarps*k, columns lane + 32u); phase-B row owner's delta_base
+    double xw[kX2Rows][3];
+#pragma unroll
+    for (int k = 0; k < kX2Rows; ++k) xw[k][0] = xw[k][1] = xw[k][2] = 0.0;  // step 0: lambda_{-1} = 0
+    double dbase = 0.0, sumsq = 0.0;
+    const bool rowner = tid >= 32 && tid < 32 + 4 * kBR;
+    const int ri = (tid - 32) >> 2, rq = (tid - 32) & 3;
+    __syncthreads();
+    stamp(-1);
+    int iterations = 0;
+    bool converged = false;
+    for (unsigned t = 0;; ++t) {
+      const int b = (int)(t % nb), sweep = (int)(t / nb);
+      const int b1 = wrap(b + 1), b2 = wrap(b + 2), bm = (b == 0) ? nb - 1 : b - 1;
+      const int rows = rows_of(b), rows1 = rows_of(b1), rowsm = rows_of(bm);
+      const int slot = (int)(t & 1);
+      double* Tc = slot ? sm.T1 : sm.T0;
+      double* Tn = slot ? sm.T0 : sm.T1;
+      double* lamc = sm.lamx + slot * kBR;         // lambda_b (this solve)
+      double* lamp = sm.lamx + (slot ^ 1) * kBR;   // lambda_{b-1}
+      const int64_t rb = 3 * (int64_t)b * kBG, rb1 = 3 * (int64_t)b1 * kBG, rbm = 3 * (int64_t)bm * kBG;
+      if (warp == 0) {
+        // ---- sequential block solve ----
+        const int ng = rows / 3;
+        const bool mine = lane < ng;
+        double lm[3], dl[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          lm[a] = mine ? sm.lamn[slot * kBR + 3 * lane + a] : 0.0;
+          dl[a] = mine ? sm.dcur[3 * lane + a] : 0.0;
+        }
+        int err = 0;
+        block_solve<false>(Tc, ng, lane, dl, lm, kc, s.mu, h2, dsq, err);
+        const unsigned bad = __ballot_sync(0xffffffffu, mine && err);
+        if (bad) {
+          const int g = __ffs(bad) - 1;  // first failing group in Gauss-Seidel order
+          if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(rb / 3 + g), 1.0 / kc.ihw);
+          if (lane == 0) sm.flags[0] = 1;
+        }
+        if (mine)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) lamc[3 * lane + a] = lm[a];
+        if (b == nb - 1) {  // end of sweep: ||dlam||^2 and this block's ||lambda||^2
+          const double l2 = mine ? (lm[0] * lm[0] + lm[1] * lm[1]) + lm[2] * lm[2] : 0.0;
+          const double sl = warp_sum(l2), sd = warp_sum(dsq);
+          if (lane == 0) {
+            sm.red[0] = sd;
+            sm.red[1] = sl;
+          }
+          dsq = 0.0;
+        }
+        stamp(2);
+      } else {
+        // ---- aux warps ----
+        if (warp == 1 && t > 0) {  // publish lambda_{b-1}
+          for (int j = lane; j < rowsm; j += 32) __stcg(lamg + rbm + j, lamp[j]);
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicExch((unsigned*)vsolved, t);
+        }
+        // prefetch T(b+1), W[b+1, b], lambda(b+1)
+        for (int i = warp - 1; i < rows1; i += kAuxWarps) {
+          const double* src = s.W + (rb1 + i) * s.ldw;
+          for (int j = lane; j < rows1; j += 32) cp_async8(&Tn[i * kLDT + j], src + rb1 + j, true);
+          for (int j = lane; j < rows; j += 32) cp_async8(&sm.Wx[i * kLDT + j], src + rb + j, true);
+        }
+        for (int j = tid - 32; j < rows1; j += kPipeThreads - 32) sm.lamn[(slot ^ 1) * kBR + j] = __ldcg(lamg + rb1 + j);
+        for (int e = tid - 32; e < kKC * rows1 / 3; e += kPipeThreads - 32)
+          cp_async8(&sm.kcn[e], kconst + kKC * (rb1 / 3) + e, true);
+        if (rowner && rq == 0 && ri < rows1) dbase = __ldg(s.delta_base + rb1 + ri);
+        // X2 = W[b+1, b-1] lambda_{b-1}
+        double x2[kX2Rows];
+#pragma unroll
+        for (int k = 0; k < kX2Rows; ++k) {
+          double a = fma(xw[k][0], lamp[lane], 0.0);
+          a = fma(xw[k][1], lamp[lane + 32], a);
+          a = fma(xw[k][2], lamp[lane + 64], a);
+          x2[k] = warp_sum(a);
+        }
+        // W[b+2, b] for the next step
+        {
+          const int rows2 = rows_of(b2);
+          const int64_t rb2 = 3 * (int64_t)b2 * kBG;
+#pragma unroll
+          for (int k = 0; k < kX2Rows; ++k) {
+            const int i = (warp - 1) + kAuxWarps * k;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+              const int j = lane + 32 * u;
+              xw[k][u] = (i < rows2 && j < rows) ? __ldg(s.W + (rb2 + i) * s.ldw + rb + j) : 0.0;
+            }
+          }
+        }
+        // ||lambda||^2 of the blocks solved so far in this sweep (fixed order)
+        if (warp == 2) {
+          if (b == 0) {
+            sumsq = 0.0;
+          } else {
+            double v = 0.0;
+            for (int j = lane; j < rowsm; j += 32) v = fma(lamp[j], lamp[j], v);
+            sumsq += warp_sum(v);
+          }
+          if (b == nb - 1 && lane == 0) sm.red[2] = sumsq;
+        }
+        stamp(6);
+        // partials of block b+1 (helpers, step t-1), summed in fixed order
+        if (t > 0) {
+          if (tid == 32) {
+            wait_geq(vready, H * t, nullptr, ctl);
+            __threadfence();
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(kPipeThreads - 32));
+        }
+        stamp(3);
+        const double* part = partial + (size_t)((t + kPartBufs - 1) % kPartBufs) * pstride;
+#pragma unroll
+        for (int k = 0; k < kX2Rows; ++k) {
+          const int i = (warp - 1) + kAuxWarps * k;
+          if (i < rows1) {
+            double v = 0.0;
+            if (t > 0)
+              for (int ch = lane; ch < nch; ch += 32) v += __ldcg(part + (size_t)i * nch + ch);
+            v = warp_sum(v);
+            if (lane == 0) sm.pacc[i] = x2[k] + v;
+          }
+        }
+        cp_async_wait_all();
+      }
+      __syncthreads();  // B1
+      stamp(0);
+      // ---- phase B: delta(b+1), shift of T(b+1)'s diagonal, sweep-end epsilon ----
+      if (rowner) {
+        double a0 = 0.0, a1 = 0.0;
+        if (ri < rows1) {
+          const double* xr = sm.Wx + ri * kLDT;
+          int j = rq;
+          for (; j + 4 < rows; j += 8) {
+            a0 = fma(xr[j], lamc[j], a0);
+            a1 = fma(xr[j + 4], lamc[j + 4], a1);
+          }
+          if (j < rows) a0 = fma(xr[j], lamc[j], a0);
+        }
+        double a = a0 + a1;
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        if (rq == 0 && ri < rows1) sm.dcur[ri] = add(dbase, mul(h2, sm.pacc[ri] + a));
+      } else if (tid >= 32 + 4 * kBR) {
+        for (int i = tid - (32 + 4 * kBR); i < rows1; i += kPipeThreads - (32 + 4 * kBR))
+          Tn[i * kLDT + i] = add(Tn[i * kLDT + i], dshift[(rb1 + i) / 3]);
+      } else {  // warp 0
+        load_group_const(kc, sm.kcn + kKC * lane, lane < rows1 / 3);
+        if (b == nb - 1 && lane == 0 && !sm.flags[0]) {
+          const double num = sqrt(sm.red[0]), den = sqrt(sm.red[1] + sm.red[2]);
+          const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
+          s.eps_hist[sweep] = eps;
+          sm.flags[1] = (eps <= s.tol) ? 1 : ((sweep + 1 >= s.max_iter) ? 2 : 0);
+        }
+      }
+      __syncthreads();  // B2
+      stamp(1);
+      if (b == nb - 1) {
+        iterations = sweep + 1;
+        converged = sm.flags[1] == 1;
+      }
+      if (sm.flags[0] || sm.flags[1] || ctl->timeout) {
+        // publish the last block, then release everyone
+        for (int j = tid; j < rows; j += blockDim.x) __stcg(lamg + rb + j, lamc[j]);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) atomicExch((unsigned*)vstop, 1u);
+        break;
+      }
+    }
+    if (tid == 0) {
+      s.iters_conv[0] = iterations;
+      s.iters_conv[1] = converged ? 1 : 0;
+    }
+  } else {
+    // ---- helpers ----
+    double* lams = (double*)smem_raw;
+    const unsigned hw = (blockIdx.x - 1) * (kPipeThreads / 32) + warp;
+    const int64_t csz = (c + nch - 1) / nch;
+    for (unsigned t = 0;; ++t) {
+      const int b = (int)(t % nb), b1 = wrap(b + 1), b2 = wrap(b + 2), bm = (b == 0) ? nb - 1 : b - 1;
+      const int rows2 = rows_of(b2);
+      const bool has = hw < (unsigned)(rows2 * nch);
+      const int i = has ? (int)(hw / nch) : 0, ch = has ? (int)(hw % nch) : 0;
+      const int64_t r = 3 * (int64_t)b2 * kBG + i;
+      const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
+      const int64_t e0 = 3 * (int64_t)b * kBG, e1 = e0 + rows_of(b);     // excluded: block b
+      const int64_t f0 = 3 * (int64_t)b1 * kBG, f1 = f0 + rows_of(b1);  // excluded: block b+1
+      const double* wr = s.W + r * s.ldw;
+      double wv[kHelpPre];
+#pragma unroll
+      for (int u = 0; u < kHelpPre; ++u) {
+        const int64_t j = c0 + lane + 32 * u;
+        const bool ok = has && j < c1 && (j < e0 || j >= e1) && (j < f0 || j >= f1);
+        wv[u] = ok ? wr[j] : 0.0;
+      }
+      stamp(5);
+      if (tid == 0) wait_geq(vsolved, t, vstop, ctl);
+      __syncthreads();
+      stamp(4);
+      if (*vstop) break;
+      if (lam_in_smem) {
+        if (t == 0) {
+          for (int64_t j = tid; j < c; j += blockDim.x) lams[j] = 0.0;
+        } else {
+          const int64_t pb0 = 3 * (int64_t)bm * kBG;
+          const int pcols = rows_of(bm);
+          for (int j = tid; j < pcols; j += blockDim.x) lams[pb0 + j] = __ldcg(lamg + pb0 + j);
+        }
+        __syncthreads();
+      }
+      if (has) {
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < kHelpPre; ++u) {
+          const int64_t j = min(c0 + lane + 32 * u, c - 1);
+          a[u & 3] = fma(wv[u], lam_in_smem ? lams[j] : __ldcg(lamg + j), a[u & 3]);
+        }
+        for (int64_t j0 = c0 + 32 * kHelpPre; j0 < c1; j0 += 32 * kHelpPre) {  // slices wider than the registers
+#pragma unroll 8
+          for (int u = 0; u < kHelpPre; ++u) {
+            const int64_t j = j0 + lane + 32 * u;
+            if (j < c1 && (j < e0 || j >= e1) && (j < f0 || j >= f1))
+              a[u & 3] = fma(wr[j], lam_in_smem ? lams[j] : __ldcg(lamg + j), a[u & 3]);
+          }
+        }
+        double acc = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
+        if (lane == 0) {
+          if (r >= c0 && r < c1) acc = fma(dshift[r / 3], lam_in_smem ? lams[r] : __ldcg(lamg + r), acc);
+          __stcg(partial + (size_t)(t % kPartBufs) * pstride + (size_t)i * nch + ch, acc);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd((unsigned*)vready, 1u);
+      }
+    }
+  }
+  // ---- everyone: wait for the final lambda, then delta_end = delta_base + h^2 W_reg lam
+  cp_async_wait_all();
+  if (tid == 0) wait_geq(vstop, 1u, nullptr, ctl);
+  __syncthreads();
+  __threadfence();
+  const unsigned gw = blockIdx.x * (kPipeThreads / 32) + warp, ngw = gridDim.x * (kPipeThreads / 32);
+  for (int64_t r = gw; r < c; r += ngw) {
+    const double* wr = s.W + r * s.ldw;
+    double acc = lane_dot<true>(wr, lamg, 0, c, lane);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      acc = fma(dshift[r / 3], __ldcg(lamg + r), acc);
+      s.delta_end[r] = add(s.delta_base[r], mul(h2, acc));
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0 && ctl->timeout) raise_status(s.status, CNB_E_INTERNAL, 0, 0.0);
+}
+
 template <int V>
 __global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double* out) {
   extern __shared__ __align__(16) char bsm[];
@@ -1025,11 +1415,23 @@ static unsigned long long* pgs_profile_buffer() {
   return buf;
 }
 
+// CNB_PGS_KERNEL=grid selects the one-step-lookahead kernel (pgs_grid_kernel);
+// the default is the pipelined lookahead-2 kernel (pgs_pipe_kernel), which
+// needs at least four blocks.
+static bool use_pipe_kernel(int64_t groups) {
+  const char* e = getenv("CNB_PGS_KERNEL");
+  if (e && e[0] == 'g') return false;
+  return (groups + kBG - 1) / kBG >= 4;
+}
+
 static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   int dev = 0, sms = 0;
   CNB_CUDA(cudaGetDevice(&dev));
   CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const size_t tiles = grid_smem_bytes();
+  const bool pipe = use_pipe_kernel(s.groups);
+  const void* kfn = pipe ? (const void*)pgs_pipe_kernel : (const void*)pgs_grid_kernel;
+  const int nthreads = pipe ? kPipeThreads : kGridThreads;
+  const size_t tiles = pipe ? pipe_smem_bytes() : grid_smem_bytes();
   const size_t lam_bytes = sizeof(double) * (size_t)(3 * s.groups);
   const int lam_in_smem = lam_bytes <= pgs_max_smem() ? 1 : 0;
   const size_t smem = std::max(tiles, lam_in_smem ? lam_bytes : (size_t)0);
@@ -1037,19 +1439,19 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
     set_error("pgs: grid kernel needs %zu bytes of shared memory", smem);
     return CNB_E_INTERNAL;
   }
-  CNB_CUDA(cudaFuncSetAttribute(pgs_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CNB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  CNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pgs_grid_kernel, kGridThreads, smem));
+  CNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthreads, smem));
   if (per_sm < 1) {
     set_error("pgs: grid kernel does not fit on an SM");
     return CNB_E_INTERNAL;
   }
   const int grid = sms;  // one CTA per SM: all co-resident (cooperative launch)
-  const int nwarps = kGridThreads / 32;
+  const int nwarps = nthreads / 32;
   // one (row, column-slice) item per helper warp; the partials of a block are
   // staged in a kBR x kLDT tile by the solver
   const int nch = std::max(1, std::min(((grid - 1) * nwarps) / kBR, kLDT));
-  const size_t bytes = 64 + sizeof(double) * ((size_t)s.groups * (1 + kKC) + 1 + 2 * (size_t)kBR * nch);
+  const size_t bytes = 64 + sizeof(double) * ((size_t)s.groups * (1 + kKC) + 1 + kPartBufs * (size_t)kBR * nch);
   static void* ws_p = nullptr;
   static size_t ws_cap = 0;
   if (bytes > ws_cap) {
@@ -1070,14 +1472,17 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   unsigned long long* prof = pgs_profile_buffer();
   void* args[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
                   (void*)&nchv, (void*)&lis, (void*)&prof};
-  CNB_CUDA(cudaLaunchCooperativeKernel((const void*)pgs_grid_kernel, dim3(grid), dim3(kGridThreads), args, smem, st));
-  CNB_LAUNCH_CHECK("pgs_grid_kernel");
+  CNB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthreads), args, smem, st));
+  CNB_LAUNCH_CHECK(pipe ? "pgs_pipe_kernel" : "pgs_grid_kernel");
   return CNB_OK;
 }
 
-static bool force_grid_pgs() {
+// CNB_PGS_GRID=1 forces the grid-scale kernel, =0 the single-CTA kernel
+// whenever its shared-memory footprint fits; unset: by size.
+static int pgs_grid_override() {
   const char* e = getenv("CNB_PGS_GRID");
-  return e && e[0] == '1';
+  if (!e || !e[0]) return -1;
+  return e[0] == '1' ? 1 : 0;
 }
 
 }  // namespace cnb
@@ -1162,7 +1567,9 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
   const size_t smem = pgs_smem_bytes(groups);
   // large scenes: the grid-scale kernel (helpers on every SM); small ones stay
   // on one CTA with lambda in shared memory
-  if (force_grid_pgs() || groups > 512 || smem > pgs_max_smem()) return launch_pgs_grid(s, (cudaStream_t)stream);
+  const int ov = pgs_grid_override();
+  const bool grid = smem > pgs_max_smem() || (ov < 0 ? groups > 512 : ov == 1);
+  if (grid) return launch_pgs_grid(s, (cudaStream_t)stream);
   CNB_CUDA(cudaFuncSetAttribute(pgs_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   pgs_single_kernel<<<1, kPgsThreads, smem, (cudaStream_t)stream>>>(s);
   CNB_LAUNCH_CHECK("pgs_single_kernel");
