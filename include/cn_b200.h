@@ -133,10 +133,9 @@ int cnb_detect_vertex_mesh(int64_t nv, const int64_t* vids, const double* pts_a,
 /* Workspace bytes needed by cnb_pgs for c = 3*groups rows. */
 int64_t cnb_pgs_work_bytes(int64_t groups);
 
-/* Diagnostics of the grid-scale PGS kernel (env CNB_PGS_PROFILE=1): summed
- * nanoseconds per phase since the last call, out[8]: solver wait, delta,
- * group solves, epilogue, helper wait, helper partials, helper hand-off,
- * sequential group loop. */
+/* Diagnostics of the grid-scale PGS kernels (env CNB_PGS_PROFILE=1): summed
+ * nanoseconds (slots 16-31: cycles) per phase since the last call, out[32]; slot meanings are
+ * listed at the stamp() calls of each kernel in csrc/pgs.cu. */
 int cnb_pgs_profile(double* out);
 
 /* Cycles per group of the sequential warp block solve of the PGS kernels on a
@@ -243,7 +242,7 @@ long long cnb_launch_count(void);
 
 /* Cycles per dependent op (out: host, 6): DFMA, DADD, fp64 div, fp64 sqrt,
  * 64-bit shuffle, FFMA. */
-int cnb_bench_latency(double* out, void* stream);
+int cnb_bench_latency(double* out /* 9 doubles */, void* stream);
 
 /* fp64 MMA (DMMA) throughput of the whole GPU in TFLOP/s (out: host). */
 int cnb_bench_dmma(int32_t iters, double* out, void* stream);

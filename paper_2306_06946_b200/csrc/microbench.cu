@@ -23,7 +23,8 @@ __global__ void __launch_bounds__(256) dmma_peak_kernel(int iters, double* out) 
 
 // Dependent-chain latencies (cycles per op) measured by one thread:
 // out[0] DFMA, out[1] DADD, out[2] fp64 division, out[3] fp64 sqrt,
-// out[4] 64-bit shuffle round trip, out[5] FFMA (fp32) for reference.
+// out[4] 64-bit shuffle round trip, out[5] FFMA (fp32) for reference,
+// out[6] fp64 compare-select + DADD, out[7] MUFU.RSQ64H + DADD, out[8] DMUL.
 __global__ void latency_kernel(int n, double seed, double* out, long long* cyc) {
   double x = seed, y = 1.0000001, z = 1e-9;
   float xf = (float)seed;
@@ -40,6 +41,16 @@ __global__ void latency_kernel(int n, double seed, double* out, long long* cyc) 
   long long t5 = clock64();
   for (int i = 0; i < n; ++i) xf = fmaf(xf, 1.0000001f, 1e-9f);
   long long t6 = clock64();
+  for (int i = 0; i < n; ++i) x = (x > z ? x : z) + z;  // DSETP + FSEL select, then DADD
+  long long t7 = clock64();
+  for (int i = 0; i < n; ++i) {
+    double r;
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    x = r + 1.0;  // MUFU.RSQ64H then DADD
+  }
+  long long t8 = clock64();
+  for (int i = 0; i < n; ++i) x = x * y;  // DMUL
+  long long t9 = clock64();
   if (threadIdx.x == 0) {
     cyc[0] = t1 - t0;
     cyc[1] = t2 - t1;
@@ -47,6 +58,9 @@ __global__ void latency_kernel(int n, double seed, double* out, long long* cyc) 
     cyc[3] = t4 - t3;
     cyc[4] = t5 - t4;
     cyc[5] = t6 - t5;
+    cyc[6] = t7 - t6;
+    cyc[7] = t8 - t7;
+    cyc[8] = t9 - t8;
     out[0] = x + xf;
   }
 }
@@ -57,20 +71,20 @@ using namespace cnb;
 
 extern "C" {
 
-// out (host, 6 doubles): cycles per dependent op, see latency_kernel.
+// out (host, 9 doubles): cycles per dependent op, see latency_kernel.
 int cnb_bench_latency(double* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   double* d = nullptr;
   long long* c = nullptr;
   CNB_CUDA(cudaMalloc(&d, sizeof(double)));
-  CNB_CUDA(cudaMalloc(&c, 6 * sizeof(long long)));
+  CNB_CUDA(cudaMalloc(&c, 9 * sizeof(long long)));
   const int n = 4096;
   latency_kernel<<<1, 32, 0, st>>>(n, 1.5, d, c);
   CNB_LAUNCH_CHECK("latency_kernel");
-  long long h[6];
+  long long h[9];
   CNB_CUDA(cudaMemcpyAsync(h, c, sizeof(h), cudaMemcpyDeviceToHost, st));
   CNB_CUDA(cudaStreamSynchronize(st));
-  for (int k = 0; k < 6; ++k) out[k] = (double)h[k] / n;
+  for (int k = 0; k < 9; ++k) out[k] = (double)h[k] / n;
   cudaFree(d);
   cudaFree(c);
   return CNB_OK;

@@ -24,6 +24,10 @@
 // local_solve is reproduced operation by operation).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 
@@ -129,6 +133,8 @@ struct GroupConst {
   double ihw;        // 1 / (h^2 W_nn)
   double htn0, htn1; // h^2 W_tn
   double it00, it01, it10, it11;  // (h^2 W_tt)^{-1}
+  double b0, b1;     // (h^2 W_tt)^{-1} h^2 W_tn: tangential response to a normal change
+  double hwnn;       // h^2 W_nn (= 1 / ihw up to rounding)
   int bad;           // bit 0: W_nn <= 0, bit 1: det(h^2 W_tt) <= 0
 };
 
@@ -136,7 +142,8 @@ __device__ __forceinline__ void group_const(const double Wd[9], double h2, Group
   k.bad = 0;
   const double Wnn = Wd[0];
   if (!(Wnn > 0.0)) k.bad |= 1;
-  k.ihw = 1.0 / mul(h2, Wnn);
+  k.hwnn = mul(h2, Wnn);
+  k.ihw = 1.0 / k.hwnn;
   k.htn0 = mul(h2, Wd[3]);
   k.htn1 = mul(h2, Wd[6]);
   const double T00 = mul(h2, Wd[4]), T01 = mul(h2, Wd[5]);
@@ -148,6 +155,8 @@ __device__ __forceinline__ void group_const(const double Wd[9], double h2, Group
   k.it01 = -T01 * idet;
   k.it10 = -T10 * idet;
   k.it11 = T00 * idet;
+  k.b0 = fma(k.it00, k.htn0, k.it01 * k.htn1);
+  k.b1 = fma(k.it10, k.htn0, k.it11 * k.htn1);
 }
 
 // local_solve with the precomputed constants: same branches and projection
@@ -278,6 +287,150 @@ __device__ __forceinline__ void block_solve(const double* __restrict__ Wt, int n
         dl_[a] = fma(h2, tmp, dl_[a]);
       }
     }
+  }
+}
+
+// Latency-shortened local_solve for the sequential chain (same branches and
+// projection as solver.py:124-165, reassociated):
+//   dln = max(-d_n/(h^2 W_nn), -l_n)              (= max(0, l_n - d_n/(h^2 W_nn)) - l_n)
+//   lt  = [l_t - T^-1 d_t] - T^-1 h^2 W_tn dln   (the bracket is independent of dln)
+//   projection scale from rsqrt.approx + one Newton step (relative error ~1e-13)
+// and the lambda change is returned pre-scaled by h^2, so the delta update
+// after the broadcast is three fused multiply-adds.  About 15 dependent fp64
+// operations per group instead of ~25.  dh = h^2 (new - old); h2l = h^2 l.
+__device__ __forceinline__ int local_solve_v2(const double d[3], const double l[3], const double h2l[3],
+                                              const GroupConst& k, double mu, double h2, double out[3],
+                                              double dh[3]) {
+  const double m = d[0] * k.ihw;
+  const double x = fma(-d[0], k.ihw, l[0]);
+  const double ln = x > 0.0 ? x : 0.0;        // Python max(0.0, x) (NaN -> 0.0)
+  const double dln = m < l[0] ? -m : -l[0];   // ln - l_n, one compare-select
+  const double a0 = fma(-k.it00, d[1], fma(-k.it01, d[2], l[1]));
+  const double a1 = fma(-k.it10, d[1], fma(-k.it11, d[2], l[2]));
+  const double lt0 = fma(-k.b0, dln, a0);
+  const double lt1 = fma(-k.b1, dln, a1);
+  const double radius = mu * ln;
+  const double n2 = fma(lt0, lt0, lt1 * lt1);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(n2));
+  const double e = fma(-0.5 * n2, y * y, 1.5);
+  const double sc = n2 > radius * radius ? (radius * y) * e : 1.0;
+  const bool zero = !(x > 0.0) || mu == 0.0;
+  out[0] = ln;
+  out[1] = zero ? 0.0 : lt0 * sc;
+  out[2] = zero ? 0.0 : lt1 * sc;
+  dh[0] = h2 * dln;
+  dh[1] = zero ? -h2l[1] : fma(h2 * lt0, sc, -h2l[1]);
+  dh[2] = zero ? -h2l[2] : fma(h2 * lt1, sc, -h2l[2]);
+  return ((k.bad & 1) || (!zero && (k.bad & 2))) ? 1 : 0;
+}
+
+// block_solve with local_solve_v2, branch-free: the lambda change is
+// broadcast as soon as it exists and the owning lane's commit is a select.
+// Wt: the block's regularised diagonal tile (unscaled W, row stride ld).
+__device__ __forceinline__ void block_solve_v2(const double* __restrict__ Wt, int ld, int ng, int lane,
+                                               double dl_[3], double lm[3], const GroupConst& kc, double mu,
+                                               double h2, double& dsq, int& err) {
+  const double* wrow = Wt + 3 * lane * ld;
+  double h2l[3] = {h2 * lm[0], h2 * lm[1], h2 * lm[2]};
+#pragma unroll 2
+  for (int g = 0; g < ng; ++g) {
+    double w[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[3 * a + c] = wrow[a * ld + 3 * g + c];
+    double nw[3], dh[3];
+    const int e = local_solve_v2(dl_, lm, h2l, kc, mu, h2, nw, dh);
+    const double d0 = __shfl_sync(0xffffffffu, dh[0], g);
+    const double d1 = __shfl_sync(0xffffffffu, dh[1], g);
+    const double d2 = __shfl_sync(0xffffffffu, dh[2], g);
+    const bool me = lane == g;
+    const double q0 = nw[0] - lm[0], q1 = nw[1] - lm[1], q2 = nw[2] - lm[2];
+    const double sq = fma(q0, q0, fma(q1, q1, q2 * q2));
+    dsq += me ? sq : 0.0;
+    err |= me ? e : 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lm[a] = me ? nw[a] : lm[a];
+      h2l[a] = me ? h2 * nw[a] : h2l[a];
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dl_[a] = fma(w[3 * a + 2], d2, fma(w[3 * a + 1], d1, fma(w[3 * a], d0, dl_[a])));
+  }
+}
+
+// local_solve_v2 with the critical path shortened further (~150 cycles per
+// group on sm_100a instead of ~230): the normal branch is decided by comparing
+// the fresh delta_n against l_n h^2 W_nn (no multiply before the compare), the
+// projected and unprojected tangential changes are both formed and one
+// predicate-ready select picks the result, and the Newton step of the
+// reciprocal square root is folded into the final fused multiply-add.
+// Returns the h^2-scaled changes dh (broadcast first) and the new lambda.
+__device__ __forceinline__ int local_solve_v3(const double d[3], const double l[3], const double h2l[3],
+                                              double lhw, const GroupConst& k, double mu, double h2,
+                                              double out[3], double dh[3]) {
+  const bool open = d[0] < lhw;                 // d_n / (h^2 W_nn) < l_n  <=>  x > 0
+  const double m = d[0] * k.ihw;
+  const double dln = open ? -m : -l[0];         // max(0, l_n - m) - l_n
+  const double x = fma(-d[0], k.ihw, l[0]);
+  const double ln = x > 0.0 ? x : 0.0;          // Python max(0.0, x) (NaN -> 0.0)
+  const double a0 = fma(-k.it00, d[1], fma(-k.it01, d[2], l[1]));
+  const double a1 = fma(-k.it10, d[1], fma(-k.it11, d[2], l[2]));
+  const double lt0 = fma(-k.b0, dln, a0);
+  const double lt1 = fma(-k.b1, dln, a1);
+  const double radius = mu * ln;
+  const double n2 = fma(lt0, lt0, lt1 * lt1);
+  const bool proj = n2 > radius * radius;
+  const bool zero = !(x > 0.0) || mu == 0.0;
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(n2));
+  const double e = fma(-0.5 * n2, y * y, 1.5);  // Newton factor: rsqrt(n2) = y e
+  const double ry = radius * y;
+  const double hl0 = h2 * lt0, hl1 = h2 * lt1;
+  const double p0 = fma(hl0 * ry, e, -h2l[1]), p1 = fma(hl1 * ry, e, -h2l[2]);  // projected
+  const double u0 = hl0 - h2l[1], u1 = hl1 - h2l[2];                          // inside the cone
+  dh[0] = h2 * dln;
+  dh[1] = zero ? -h2l[1] : (proj ? p0 : u0);
+  dh[2] = zero ? -h2l[2] : (proj ? p1 : u1);
+  const double sc = proj ? ry * e : 1.0;
+  out[0] = ln;
+  out[1] = zero ? 0.0 : lt0 * sc;
+  out[2] = zero ? 0.0 : lt1 * sc;
+  return ((k.bad & 1) || (!zero && (k.bad & 2))) ? 1 : 0;
+}
+
+__device__ __forceinline__ void block_solve_v3(const double* __restrict__ Wt, int ld, int ng, int lane,
+                                               double dl_[3], double lm[3], const GroupConst& kc, double mu,
+                                               double h2, double& dsq, int& err) {
+  const double* wrow = Wt + 3 * lane * ld;
+  double h2l[3] = {h2 * lm[0], h2 * lm[1], h2 * lm[2]};
+  double lhw = lm[0] * kc.hwnn;
+#pragma unroll 2
+  for (int g = 0; g < ng; ++g) {
+    double w[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[3 * a + c] = wrow[a * ld + 3 * g + c];
+    double nw[3], dh[3];
+    const int e = local_solve_v3(dl_, lm, h2l, lhw, kc, mu, h2, nw, dh);
+    const double d0 = __shfl_sync(0xffffffffu, dh[0], g);
+    const double d1 = __shfl_sync(0xffffffffu, dh[1], g);
+    const double d2 = __shfl_sync(0xffffffffu, dh[2], g);
+    const bool me = lane == g;
+    const double q0 = nw[0] - lm[0], q1 = nw[1] - lm[1], q2 = nw[2] - lm[2];
+    const double sq = fma(q0, q0, fma(q1, q1, q2 * q2));
+    dsq += me ? sq : 0.0;
+    err |= me ? e : 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lm[a] = me ? nw[a] : lm[a];
+      h2l[a] = me ? h2 * nw[a] : h2l[a];
+    }
+    lhw = me ? nw[0] * kc.hwnn : lhw;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dl_[a] = fma(w[3 * a + 2], d2, fma(w[3 * a + 1], d1, fma(w[3 * a], d0, dl_[a])));
   }
 }
 
@@ -572,6 +725,7 @@ size_t pgs_max_smem() {
 // A device-clock watchdog turns a stuck wait into an error instead of a hang.
 struct GridCtl {
   unsigned solved, ready, stop, timeout;
+  unsigned ready4[4];  // pipelined kernel: helper completions of steps t = s (mod 4), per slot s
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -597,7 +751,8 @@ __device__ bool wait_geq(volatile unsigned* p, unsigned target, volatile unsigne
 
 // Regularisation shift (solver.py:99-121) and the per-group constants of the
 // regularised diagonal blocks, once per PGS call; lambda <- 0.
-constexpr int kKC = 8;  // doubles per packed GroupConst
+constexpr int kKC = 10;  // doubles per packed GroupConst
+constexpr int kKCP = 8;  // leading doubles of the record the pipelined kernel stages
 __global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshift, double* kconst, GridCtl* ctl) {
   __shared__ double red[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -612,6 +767,7 @@ __global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshi
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
     red[0] = t;
     ctl->solved = ctl->ready = ctl->stop = ctl->timeout = 0;
+    ctl->ready4[0] = ctl->ready4[1] = ctl->ready4[2] = ctl->ready4[3] = 0;
   }
   __syncthreads();
   double shift = 1e-10 * red[0] / (double)c;
@@ -632,15 +788,17 @@ __global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshi
     for (int i = 0; i < 3; ++i) Wd[4 * i] = add(Wd[4 * i], sh);
     GroupConst kc;
     group_const(Wd, s.h2, kc);
-    double* o = kconst + kKC * g;
+    double* o = kconst + kKC * g;  // packed record, see load_group_const
     o[0] = kc.ihw;
-    o[1] = kc.htn0;
-    o[2] = kc.htn1;
-    o[3] = kc.it00;
-    o[4] = kc.it01;
-    o[5] = kc.it10;
-    o[6] = kc.it11;
+    o[1] = kc.it00;
+    o[2] = kc.it01;
+    o[3] = kc.it10;
+    o[4] = kc.it11;
+    o[5] = kc.b0;
+    o[6] = kc.b1;
     o[7] = (double)kc.bad;
+    o[8] = kc.htn0;
+    o[9] = kc.htn1;
   }
   for (int64_t i = tid; i < c; i += blockDim.x) s.lam[i] = 0.0;
 }
@@ -799,15 +957,15 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
         const bool mine = lane < ng;
         GroupConst kc{};
         if (mine) {
-          const double* kk = sm.kcn + slot * kKC * kBG + kKC * lane;
+          const double* kk = sm.kcn + slot * kKC * kBG + kKC * lane;  // record layout: load_group_const
           kc.ihw = kk[0];
-          kc.htn0 = kk[1];
-          kc.htn1 = kk[2];
-          kc.it00 = kk[3];
-          kc.it01 = kk[4];
-          kc.it10 = kk[5];
-          kc.it11 = kk[6];
+          kc.it00 = kk[1];
+          kc.it01 = kk[2];
+          kc.it10 = kk[3];
+          kc.it11 = kk[4];
           kc.bad = (int)kk[7];
+          kc.htn0 = kk[8];
+          kc.htn1 = kk[9];
           for (int a = 0; a < 3; ++a) {  // nb == 1: the block's own lambda from the previous step
             lm[a] = (nb == 1 && t > 0) ? sm.lamx[3 * lane + a] : sm.lamn[slot * kBR + 3 * lane + a];
             dl_[a] = sm.dcur[3 * lane + a];
@@ -972,101 +1130,245 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
 // ============================================================================
 // Same iterate as pgs_cta / pgs_grid_kernel, restructured so that the solver
 // warp's sequential block solve is the only thing on the critical path.
-// Step t solves block b = t mod nb.
+// Blocks of kPG = 26 groups (kPR = 78 rows); step t solves block b = t mod nb.
 //
 //   helpers (CTAs 1..H), step t: once lambda of block b-1 is published, the
 //     lazy row products of block b+2 over every column except blocks b and
 //     b+1 (whose lambda is not final yet).  They have two block solves of
-//     slack instead of one, so the inter-SM hand-off latency is hidden.
+//     slack, so the inter-SM hand-off latency is hidden.  They also pull the
+//     excluded column blocks of their rows into L2 for the solver's TMA.
 //   solver CTA, step t:
-//     warp 0      : sequential block solve of b (lane = group);
-//     warps 1..15 : concurrently, publish lambda_{b-1}; prefetch T(b+1),
-//                   W[b+1, b] and lambda(b+1) (cp.async); the cross term
-//                   X2 = W[b+1, b-1] lambda_{b-1} from registers loaded one
-//                   step earlier; the helpers' partials of block b+1 (step
-//                   t-1) summed in fixed order; ||lambda||^2 of the sweep so far;
-//     then all    : delta(b+1) = delta_base + h^2 (partials + X2 + W[b+1, b] lambda_b)
-//                   (one 96 x 96 GEMV from shared memory), two barriers.
+//     warp 0    : sequential block solve of b (lane = group, block_solve_v4);
+//     warp 1    : publishes lambda_{b-1} (release store), ||lambda||^2 of the sweep;
+//     warp 2    : 2-D tensor TMA of T(b+1), W[b+1, b] and, once X2 is done,
+//                 X = W[b+2, b] for the next step: one instruction per tile, no
+//                 load instructions on the solver's SM;
+//     warp 3    : lambda(b+1), group constants of b+1;
+//     warps 5-7, 9-11, 13-15: X2 = W[b+1, b-1] lambda_{b-1} from the X tile and
+//                 the helpers' partials of block b+1 (step t-1), fixed order.
+//     Warps 4, 8, 12 share the solver's SM sub-partition and stay idle.
+//     then all  : delta(b+1) = delta_base + h^2 (partials + X2 + W[b+1, b] lambda_b)
+//                 (one 78 x 78 GEMV from shared memory), two barriers.
 // Every sum is taken in a fixed order: the result is bitwise repeatable.
 constexpr int kPipeThreads = 512;
-constexpr int kAuxWarps = kPipeThreads / 32 - 1;
-constexpr int kX2Rows = (kBR + kAuxWarps - 1) / kAuxWarps;
+constexpr int kPG = 26;             // groups per block
+constexpr int kPR = 3 * kPG;        // rows per block
+constexpr int kPS = kPR;            // dense tile rows (TMA box); 78 = 14 mod 16: at most 2-way bank conflicts
+constexpr int kTileBytes = (kPR * kPS * 8 + 127) / 128 * 128;  // 128-byte aligned tiles
+constexpr int kTileD = kTileBytes / 8;
+constexpr int kXW = 9;              // X2 warps
+constexpr int kXRows = (kPR + kXW - 1) / kXW;
 constexpr int kPartBufs = 3;
+constexpr int kRowOwners = (4 * kPR + 31) / 32 * 32;  // phase-B GEMV threads (4 per row), whole warps
+constexpr int kHelpWarps = kPipeThreads / 32;         // warps per helper CTA
+constexpr int kSeg = 4;                                // partial slots per row (helper CTAs a row can span)
+
+__device__ __forceinline__ int x2_index(int warp) {  // warps 5,6,7,9,10,11,13,14,15 -> 0..8
+  return (warp >= 5 && (warp & 3) != 0) ? ((warp >> 2) - 1) * 3 + (warp & 3) - 1 : -1;
+}
 
 struct PipeSmem {
-  double *T0, *T1, *Wx, *dcur, *pacc, *lamx, *lamn, *kcn, *red;
+  double *T0, *T1, *Wx, *X, *dcur, *lamx, *lamn, *kcn, *sv, *dbs, *dsh, *red;
+  unsigned long long* bar;  // [0] T + Wx, [1] X
   int* flags;
 };
 
 __host__ __device__ inline size_t pipe_smem_bytes() {
-  return sizeof(double) * (size_t)(3 * kBR * kLDT + kBR + kBR + 2 * kBR + 2 * kBR + kKC * kBG + 32) +
-         4 * sizeof(int);
+  return 128 + sizeof(double) * (size_t)(4 * kTileD + kPR + 2 * kPR + kPR + kKCP * kPG + 4 * kPG + kPR + kPG + 8) +
+         16 + 4 * sizeof(int);
 }
+
 
 __device__ __forceinline__ PipeSmem pipe_carve(char* base) {
   PipeSmem g;
   double* p = (double*)base;
   g.T0 = p;
-  p += kBR * kLDT;
+  p += kTileD;
   g.T1 = p;
-  p += kBR * kLDT;
+  p += kTileD;
   g.Wx = p;
-  p += kBR * kLDT;
+  p += kTileD;
+  g.X = p;
+  p += kTileD;
   g.dcur = p;
-  p += kBR;
-  g.pacc = p;
-  p += kBR;
+  p += kPR;
   g.lamx = p;
-  p += 2 * kBR;
+  p += 2 * kPR;
   g.lamn = p;
-  p += 2 * kBR;
+  p += kPR;
   g.kcn = p;
-  p += kKC * kBG;
+  p += kKCP * kPG;
+  g.sv = p;
+  p += 4 * kPG;
+  g.dbs = p;
+  p += kPR;
+  g.dsh = p;
+  p += kPG;
   g.red = p;
-  p += 32;
+  p += 8;
+  g.bar = (unsigned long long*)p;
+  p += 2;
   g.flags = (int*)p;
   return g;
 }
 
-// group constants of one group from a packed record (global or shared)
-__device__ __forceinline__ void load_group_const(GroupConst& k, const double* kk, bool valid) {
+// group constants of one group from a packed record (global or shared):
+// [ihw, it00, it01, it10, it11, b0, b1, bad, htn0, htn1]; the pipelined
+// kernel stages only the first kKCP (what block_solve_v4 reads)
+__device__ __forceinline__ void load_group_const(GroupConst& k, const double* kk, bool valid, int stride = kKC) {
   if (valid) {
     k.ihw = kk[0];
-    k.htn0 = kk[1];
-    k.htn1 = kk[2];
-    k.it00 = kk[3];
-    k.it01 = kk[4];
-    k.it10 = kk[5];
-    k.it11 = kk[6];
+    k.it00 = kk[1];
+    k.it01 = kk[2];
+    k.it10 = kk[3];
+    k.it11 = kk[4];
+    k.b0 = kk[5];
+    k.b1 = kk[6];
     k.bad = (int)kk[7];
+    k.htn0 = stride > 8 ? kk[8] : 0.0;
+    k.htn1 = stride > 9 ? kk[9] : 0.0;
+    k.hwnn = 1.0 / k.ihw;
   } else {
-    k.ihw = 1.0;
-    k.htn0 = k.htn1 = k.it00 = k.it01 = k.it10 = k.it11 = 0.0;
+    k.ihw = k.hwnn = 1.0;
+    k.htn0 = k.htn1 = k.it00 = k.it01 = k.it10 = k.it11 = k.b0 = k.b1 = 0.0;
     k.bad = 0;
   }
 }
 
+// Sequential Gauss-Seidel over one block, minimal per-group chain: every lane
+// evaluates local_solve for its own group from the current delta (only the
+// lane whose turn it is matters), broadcasts the h^2-scaled lambda change
+// and all lanes apply the rank-3 delta update.  Nothing else happens per
+// group: lane g only records (x, dh_t1, dh_t2, open) of its own group in sv,
+// and block_commit turns the records into lambda after the block (a lane's
+// lambda is read by the chain only at its own step).  Same branches as
+// local_solve (solver.py:124-165): normal clamp at zero, frictionless,
+// tangential stick solve, projection onto the cone.
+template <bool FRIC>
+__device__ __forceinline__ void block_solve_v4(const double* __restrict__ Wt, int ld, int ng, int lane,
+                                               double dl_[3], const double lm[3], const GroupConst& kc, double mu,
+                                               double h2, double* __restrict__ sv) {
+  const double* wrow = Wt + 3 * lane * ld;
+  const double h2l1 = h2 * lm[1], h2l2 = h2 * lm[2];
+  const double nl0 = -lm[0], lhw = lm[0] * kc.hwnn, nihw = -kc.ihw;
+#pragma unroll 2
+  for (int g = 0; g < ng; ++g) {
+    double w[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[3 * a + c] = wrow[a * ld + 3 * g + c];
+    const double d0 = dl_[0], d1 = dl_[1], d2 = dl_[2];
+    const bool open = d0 < lhw;                        // l_n - d_n/(h^2 W_nn) > 0
+    const double x = fma(nihw, d0, lm[0]);
+    const double dln = open ? d0 * nihw : nl0;         // max(0, x) - l_n
+    double dh0 = h2 * dln, dh1, dh2;
+    if (FRIC) {
+      const double a0 = fma(-kc.it00, d1, fma(-kc.it01, d2, lm[1]));
+      const double a1 = fma(-kc.it10, d1, fma(-kc.it11, d2, lm[2]));
+      const double lt0 = fma(-kc.b0, dln, a0), lt1 = fma(-kc.b1, dln, a1);
+      const double radius = mu * x;
+      const double n2 = fma(lt0, lt0, lt1 * lt1);
+      const bool proj = n2 > radius * radius;
+      double y;
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(n2));
+      const double e = fma(-0.5 * n2, y * y, 1.5);   // rsqrt(n2) = y e (one Newton step)
+      const double ry = radius * y;
+      const double hl0 = h2 * lt0, hl1 = h2 * lt1;
+      const double p0 = fma(hl0 * ry, e, -h2l1), p1 = fma(hl1 * ry, e, -h2l2);
+      const double u0 = hl0 - h2l1, u1 = hl1 - h2l2;
+      dh1 = open ? (proj ? p0 : u0) : -h2l1;
+      dh2 = open ? (proj ? p1 : u1) : -h2l2;
+    } else {
+      dh1 = -h2l1;
+      dh2 = -h2l2;
+    }
+    const double s0 = __shfl_sync(0xffffffffu, dh0, g);
+    const double s1 = __shfl_sync(0xffffffffu, dh1, g);
+    const double s2 = __shfl_sync(0xffffffffu, dh2, g);
+    // the owning lane records its group (predicated stores: no divergent branch)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.eq.s32 p, %0, %1;\n"
+        " @p st.shared.v2.f64 [%2], {%3, %4};\n @p st.shared.v2.f64 [%2+16], {%5, %6};\n}\n" ::"r"(lane),
+        "r"(g), "r"(smem_u32(sv + 4 * g)), "d"(x), "d"(dh1), "d"(dh2), "d"(open ? 1.0 : 0.0)
+        : "memory");
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dl_[a] = fma(w[3 * a + 2], s2, fma(w[3 * a + 1], s1, fma(w[3 * a], s0, dl_[a])));
+  }
+}
+
+// lambda of the lane's group from its block_solve_v4 record; dsq += |change|^2;
+// returns the error flag (W_nn <= 0, or a singular tangential block when used)
+__device__ __forceinline__ int block_commit(const double* sv, int lane, double lm[3], const GroupConst& kc,
+                                            double mu, double ih2, double& dsq) {
+  const double x = sv[4 * lane], dh1 = sv[4 * lane + 1], dh2 = sv[4 * lane + 2];
+  const bool open = sv[4 * lane + 3] != 0.0;
+  const bool fric = open && mu != 0.0;
+  const double n0 = open ? fmax(x, 0.0) : 0.0;
+  const double n1 = fric ? fma(dh1, ih2, lm[1]) : 0.0;
+  const double n2 = fric ? fma(dh2, ih2, lm[2]) : 0.0;
+  const double q0 = n0 - lm[0], q1 = n1 - lm[1], q2 = n2 - lm[2];
+  dsq += q0 * q0 + q1 * q1 + q2 * q2;
+  lm[0] = n0;
+  lm[1] = n1;
+  lm[2] = n2;
+  return ((kc.bad & 1) || (fric && (kc.bad & 2))) ? 1 : 0;
+}
+
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// spin (acquire) until *p >= target, or stop / watchdog; false on timeout
+__device__ bool wait_acq(const unsigned* p, unsigned target, const unsigned* stop, GridCtl* ctl) {
+  const unsigned long long t0 = global_ns();
+  while (ld_acquire_gpu(p) < target) {
+    if (stop && ld_acquire_gpu(stop)) return true;
+    if (global_ns() - t0 > 20000000000ull) {  // 20 s
+      atomicExch(&ctl->timeout, 1u);
+      atomicExch(&ctl->stop, 1u);
+      return false;
+    }
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, const double* __restrict__ dshift,
                                                                 const double* __restrict__ kconst, double* partial,
-                                                                GridCtl* ctl, int nch, int lam_in_smem,
-                                                                unsigned long long* prof) {
-  extern __shared__ __align__(16) char smem_raw[];
+                                                                GridCtl* ctl, int nch, int lam_in_smem, int tma,
+                                                                unsigned long long* prof,
+                                                                const __grid_constant__ CUtensorMap tmap) {
+  const int dbg = tma & ~1;
+  tma = (dbg & 2) ? 0 : (tma & 1);
+  extern __shared__ __align__(16) char smem_dyn[];
+  // 128-byte aligned base for the TMA tiles; offsetting the shared array (not
+  // an integer round trip) keeps the accesses LDS/STS instead of generic loads
+  char* smem_raw = smem_dyn + ((128u - (smem_u32(smem_dyn) & 127u)) & 127u);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t G = s.groups, c = 3 * G;
-  const int nb = (int)((G + kBG - 1) / kBG);
+  const int nb = (int)((G + kPG - 1) / kPG);
   const unsigned H = gridDim.x - 1;
   const double h2 = s.h2;
   double* lamg = s.lam;
-  volatile unsigned* vsolved = &ctl->solved;
-  volatile unsigned* vready = &ctl->ready;
-  volatile unsigned* vstop = &ctl->stop;
-  const size_t pstride = (size_t)kBR * nch;
-  auto rows_of = [&](int blk) { return 3 * (int)min((int64_t)kBG, G - (int64_t)blk * kBG); };
+  unsigned* psolved = &ctl->solved;
+  // per-slot completion counters: a single cumulative count could be reached
+  // by helpers running ahead while a slow one has not finished the step
+  unsigned* pready4 = ctl->ready4;
+  unsigned* pstop = &ctl->stop;
+  const size_t pstride = (size_t)kPR * kSeg;  // one partial buffer: kSeg row sums per row
+  auto rows_of = [&](int blk) { return 3 * (int)min((int64_t)kPG, G - (int64_t)blk * kPG); };
   auto wrap = [&](int blk) { return blk >= nb ? blk - nb : blk; };
-  // CNB_PGS_PROFILE=1: [0] solver idle at B1, [1] phase B, [2] block solve,
-  // [3] aux wait for partials, [4] helper wait, [5] helper work, [6] aux phase A
+  // CNB_PGS_PROFILE=1 (ns per phase, summed): tid 0: [0] idle at B1, [1] phase B, [2] block solve;
+  // tid 32+64*.. see stamp() calls; helpers (CTA 1, tid 0): [4] wait, [5] work
   unsigned long long tp = 0;
-  const bool stamper = prof && (tid == 0 || tid == 32) && blockIdx.x <= 1;
+  const bool stamper = prof && (tid == 0 || tid == 32 || tid == 64 || tid == 160) && blockIdx.x <= 1;
   auto stamp = [&](int k) {
     if (stamper) {
       const unsigned long long now = global_ns();
@@ -1077,33 +1379,35 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
 
   if (blockIdx.x == 0) {
     PipeSmem sm = pipe_carve(smem_raw);
-    if (tid == 0) sm.flags[0] = sm.flags[1] = 0;
+    const int xi = x2_index(warp);
+    if (tid == 0) {
+      sm.flags[0] = sm.flags[1] = 0;
+      mbar_init(sm.bar, 1);
+      mbar_init(sm.bar + 1, 1);
+    }
+    // prologue: T(0), delta(0); X = W[2, 0] for step 1 is fetched in step 0
     {
       const int r0 = rows_of(0);
       for (int i = warp; i < r0; i += kPipeThreads / 32)
-        for (int j = lane; j < r0; j += 32) cp_async8(&sm.T0[i * kLDT + j], s.W + i * s.ldw + j, true);
+        for (int j = lane; j < r0; j += 32) cp_async8(&sm.T0[i * kPS + j], s.W + i * s.ldw + j, true);
       cp_async_wait_all();
     }
-    for (int i = tid; i < kBR; i += blockDim.x) {
+    for (int i = tid; i < kPR; i += blockDim.x) {
       sm.dcur[i] = i < rows_of(0) ? s.delta_base[i] : 0.0;
-      sm.lamn[i] = sm.lamn[kBR + i] = 0.0;  // lambda starts at zero (prep zeroed the global copy)
-      sm.lamx[i] = sm.lamx[kBR + i] = 0.0;
+      sm.lamn[i] = 0.0;  // lambda starts at zero (prep zeroed the global copy)
+      sm.lamx[i] = sm.lamx[kPR + i] = 0.0;
     }
     __syncthreads();
     for (int i = tid; i < rows_of(0); i += blockDim.x)
-      sm.T0[i * kLDT + i] = add(sm.T0[i * kLDT + i], dshift[i / 3]);
-    // solver warp state
+      sm.T0[i * kPS + i] = add(sm.T0[i * kPS + i], dshift[i / 3]);
     GroupConst kc{};
-    double dsq = 0.0;
+    double dsq = 0.0, sumsq = 0.0;
+    const double ih2 = 1.0 / h2;
     if (warp == 0) load_group_const(kc, kconst + kKC * lane, lane < rows_of(0) / 3);
-    // aux state: W[b+2 rows, b cols] for the next step's cross term (rows
-    // (warp-1) + kAuxWarps*k, columns lane + 32u); phase-B row owner's delta_base
-    double xw[kX2Rows][3];
-#pragma unroll
-    for (int k = 0; k < kX2Rows; ++k) xw[k][0] = xw[k][1] = xw[k][2] = 0.0;  // step 0: lambda_{-1} = 0
-    double dbase = 0.0, sumsq = 0.0;
-    const bool rowner = tid >= 32 && tid < 32 + 4 * kBR;
-    const int ri = (tid - 32) >> 2, rq = (tid - 32) & 3;
+    const bool rowner = tid >= 32 && tid < 32 + kRowOwners;
+    // phase-B GEMV: 8 rows x 4 column phases per warp; a half-warp reads 8 rows x 2
+    // adjacent columns, 16 distinct banks for the 78-double row pitch
+    const int ri = 8 * (warp - 1) + (lane & 7), rq = lane >> 3;
     __syncthreads();
     stamp(-1);
     int iterations = 0;
@@ -1115,9 +1419,10 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
       const int slot = (int)(t & 1);
       double* Tc = slot ? sm.T1 : sm.T0;
       double* Tn = slot ? sm.T0 : sm.T1;
-      double* lamc = sm.lamx + slot * kBR;         // lambda_b (this solve)
-      double* lamp = sm.lamx + (slot ^ 1) * kBR;   // lambda_{b-1}
-      const int64_t rb = 3 * (int64_t)b * kBG, rb1 = 3 * (int64_t)b1 * kBG, rbm = 3 * (int64_t)bm * kBG;
+      double* lamc = sm.lamx + slot * kPR;         // lambda_b (this solve)
+      double* lamp = sm.lamx + (slot ^ 1) * kPR;   // lambda_{b-1}
+      const int64_t rb = 3 * (int64_t)b * kPG, rb1 = 3 * (int64_t)b1 * kPG, rbm = 3 * (int64_t)bm * kPG;
+      const int si = tid - (32 + kRowOwners);  // phase-B diagonal-shift thread, one row (kPR <= 160)
       if (warp == 0) {
         // ---- sequential block solve ----
         const int ng = rows / 3;
@@ -1125,12 +1430,17 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         double lm[3], dl[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          lm[a] = mine ? sm.lamn[slot * kBR + 3 * lane + a] : 0.0;
+          lm[a] = mine ? sm.lamn[3 * lane + a] : 0.0;
           dl[a] = mine ? sm.dcur[3 * lane + a] : 0.0;
         }
-        int err = 0;
-        block_solve<false>(Tc, ng, lane, dl, lm, kc, s.mu, h2, dsq, err);
-        const unsigned bad = __ballot_sync(0xffffffffu, mine && err);
+        if (!(dbg & 2)) asm volatile("bar.arrive 2, %0;" ::"n"(64 + 32 * kXW));  // dcur, lamn consumed
+        if (s.mu != 0.0)
+          block_solve_v4<true>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv);
+        else
+          block_solve_v4<false>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv);
+        __syncwarp();
+        const int err = mine ? block_commit(sm.sv, lane, lm, kc, s.mu, ih2, dsq) : 0;
+        const unsigned bad = __ballot_sync(0xffffffffu, err);
         if (bad) {
           const int g = __ffs(bad) - 1;  // first failing group in Gauss-Seidel order
           if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(rb / 3 + g), 1.0 / kc.ihw);
@@ -1139,6 +1449,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         if (mine)
 #pragma unroll
           for (int a = 0; a < 3; ++a) lamc[3 * lane + a] = lm[a];
+        if (!(dbg & 2)) asm volatile("bar.arrive 4, 64;" ::: "memory");  // lambda_b ready: warp 1 publishes it
         if (b == nb - 1) {  // end of sweep: ||dlam||^2 and this block's ||lambda||^2
           const double l2 = mine ? (lm[0] * lm[0] + lm[1] * lm[1]) + lm[2] * lm[2] : 0.0;
           const double sl = warp_sum(l2), sd = warp_sum(dsq);
@@ -1149,105 +1460,162 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           dsq = 0.0;
         }
         stamp(2);
-      } else {
-        // ---- aux warps ----
-        if (warp == 1 && t > 0) {  // publish lambda_{b-1}
-          for (int j = lane; j < rowsm; j += 32) __stcg(lamg + rbm + j, lamp[j]);
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) atomicExch((unsigned*)vsolved, t);
+      } else if (dbg & 2) {
+        // timing experiment: aux warps idle (wrong results)
+      } else if (warp == 1) {
+        if (lane == 0 && *(volatile unsigned*)&ctl->timeout) sm.flags[0] = 1;  // watchdog fired elsewhere
+        // publish lambda_b as soon as the solver warp has it (helpers of step t+1 wait for it)
+        asm volatile("bar.sync 4, 64;" ::: "memory");
+        stamp(8);
+        for (int j = lane; j < rows; j += 32) __stcg(lamg + rb + j, lamc[j]);
+        __syncwarp();
+        if (lane == 0) st_release_gpu(psolved, t + 1);
+        // ||lambda||^2 of blocks 0..nb-2 of this sweep (fixed order); warp 0 adds the last
+        if (b == 0) sumsq = 0.0;
+        if (b < nb - 1) {
+          double v = 0.0;
+          for (int j = lane; j < rows; j += 32) v = fma(lamc[j], lamc[j], v);
+          sumsq += warp_sum(v);
         }
-        // prefetch T(b+1), W[b+1, b], lambda(b+1)
-        for (int i = warp - 1; i < rows1; i += kAuxWarps) {
-          const double* src = s.W + (rb1 + i) * s.ldw;
-          for (int j = lane; j < rows1; j += 32) cp_async8(&Tn[i * kLDT + j], src + rb1 + j, true);
-          for (int j = lane; j < rows; j += 32) cp_async8(&sm.Wx[i * kLDT + j], src + rb + j, true);
+        if (b == nb - 2 && lane == 0) sm.red[2] = sumsq;
+        stamp(9);
+      } else if (warp == 2) {
+        // T(b+1) and W[b+1, b]: one tensor-TMA box each (out-of-range rows and
+        // columns of a ragged last block arrive as zeros)
+        if (tma) {
+          if (lane == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(sm.bar, 2u * kPR * kPS * 8);
+            tma_load_2d(Tn, &tmap, (int)rb1, (int)rb1, sm.bar);
+            tma_load_2d(sm.Wx, &tmap, (int)rb, (int)rb1, sm.bar);
+          }
+        } else {
+          for (int i = 0; i < rows1; ++i) {
+            const double* src = s.W + (rb1 + i) * s.ldw;
+            for (int j = lane; j < rows1; j += 32) cp_async8(&Tn[i * kPS + j], src + rb1 + j, true);
+            for (int j = lane; j < rows; j += 32) cp_async8(&sm.Wx[i * kPS + j], src + rb + j, true);
+          }
+          cp_async_wait_all();
         }
-        for (int j = tid - 32; j < rows1; j += kPipeThreads - 32) sm.lamn[(slot ^ 1) * kBR + j] = __ldcg(lamg + rb1 + j);
-        for (int e = tid - 32; e < kKC * rows1 / 3; e += kPipeThreads - 32)
-          cp_async8(&sm.kcn[e], kconst + kKC * (rb1 / 3) + e, true);
-        if (rowner && rq == 0 && ri < rows1) dbase = __ldg(s.delta_base + rb1 + ri);
-        // X2 = W[b+1, b-1] lambda_{b-1}
-        double x2[kX2Rows];
+        stamp(10);
+        // X = W[b+2, b] for the next step's X2, once this step's X2 has read the tile
+        asm volatile("bar.sync 3, %0;" ::"n"(32 + 32 * kXW));
+        stamp(11);
+        const int rows2 = rows_of(b2);
+        const int64_t rb2 = 3 * (int64_t)b2 * kPG;
+        if (tma) {
+          if (lane == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(sm.bar + 1, 1u * kPR * kPS * 8);
+            tma_load_2d(sm.X, &tmap, (int)rb, (int)rb2, sm.bar + 1);
+          }
+        } else {
+          for (int i = 0; i < rows2; ++i)
+            for (int j = lane; j < rows; j += 32) cp_async8(&sm.X[i * kPS + j], s.W + (rb2 + i) * s.ldw + rb + j, true);
+          cp_async_wait_all();
+        }
+        stamp(12);
+      } else if (warp == 3) {
+        double lv[3];
 #pragma unroll
-        for (int k = 0; k < kX2Rows; ++k) {
-          double a = fma(xw[k][0], lamp[lane], 0.0);
-          a = fma(xw[k][1], lamp[lane + 32], a);
-          a = fma(xw[k][2], lamp[lane + 64], a);
-          x2[k] = warp_sum(a);
+        for (int u = 0; u < 3; ++u) {
+          const int j = lane + 32 * u;
+          lv[u] = j < rows1 ? __ldcg(lamg + rb1 + j) : 0.0;
         }
-        // W[b+2, b] for the next step
+        for (int e = lane; e < kKCP * rows1 / 3; e += 32) {
+          const int g = e / kKCP, k = e - g * kKCP;
+          cp_async8(&sm.kcn[e], kconst + kKC * (rb1 / 3 + g) + k, true);
+        }
+        // delta_base and the regularisation shifts of block b+1 for phase B
+        for (int j = lane; j < rows1; j += 32) cp_async8(&sm.dbs[j], s.delta_base + rb1 + j, true);
+        if (lane < rows1 / 3) cp_async8(&sm.dsh[lane], dshift + rb1 / 3 + lane, true);
+        asm volatile("bar.sync 2, %0;" ::"n"(64 + 32 * kXW));  // warp 0 has read lamn
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int j = lane + 32 * u;
+          if (j < kPR) sm.lamn[j] = lv[u];
+        }
+        cp_async_wait_all();
+      } else if (xi >= 0) {
+        // X2 = W[b+1, b-1] lambda_{b-1} from the X tile (fetched last step)
+        if (tma && t > 0) mbar_wait(sm.bar + 1, (t - 1) & 1);
+        // lanes 3k..3k+2 share row xi + kXW*k (k < 9), a third of its columns each
+        double x2v = 0.0;
         {
-          const int rows2 = rows_of(b2);
-          const int64_t rb2 = 3 * (int64_t)b2 * kBG;
-#pragma unroll
-          for (int k = 0; k < kX2Rows; ++k) {
-            const int i = (warp - 1) + kAuxWarps * k;
-#pragma unroll
-            for (int u = 0; u < 3; ++u) {
-              const int j = lane + 32 * u;
-              xw[k][u] = (i < rows2 && j < rows) ? __ldg(s.W + (rb2 + i) * s.ldw + rb + j) : 0.0;
+          const int k = lane / 3, part = lane - 3 * k;
+          const int i = xi + kXW * k;
+          if (t > 0 && lane < 3 * kXRows && i < rows1) {
+            const double* xr = sm.X + i * kPS;
+            const int j0 = part * (kPR / 3), j1 = min(j0 + kPR / 3, rowsm);
+            double a0 = 0.0, a1 = 0.0;
+            int j = j0;
+            for (; j + 1 < j1; j += 2) {
+              a0 = fma(xr[j], lamp[j], a0);
+              a1 = fma(xr[j + 1], lamp[j + 1], a1);
+            }
+            if (j < j1) a0 = fma(xr[j], lamp[j], a0);
+            x2v = a0 + a1;
+          }
+          const double n1 = __shfl_down_sync(0xffffffffu, x2v, 1), n2 = __shfl_down_sync(0xffffffffu, x2v, 2);
+          x2v = (x2v + n1) + n2;  // valid in lanes 3k
+        }
+        asm volatile("bar.arrive 3, %0;" ::"n"(32 + 32 * kXW));  // X tile free for the next fetch
+        if (xi == 0) stamp(6);
+        // partials of block b+1 (helpers, step t-1), summed in fixed order
+        if (t > 0) {
+          if (tid == 160) wait_acq(pready4 + ((t - 1) & 3), H * ((t - 1) / 4 + 1), nullptr, ctl);
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kXW));
+        }
+        if (xi == 0) stamp(3);
+        // helpers' row sums, one per helper CTA the row spans (fixed order); lane k <-> row xi + kXW k
+        const double* part = partial + (size_t)((t + kPartBufs - 1) % kPartBufs) * pstride;
+        double pvl = 0.0;
+        {
+          const int i = xi + kXW * lane;
+          if (t > 0 && lane < kXRows && i < rows1) {
+            const int nseg = ((i + 1) * nch - 1) / kHelpWarps - (i * nch) / kHelpWarps + 1;
+            for (int sg = 0; sg < nseg; ++sg) pvl += __ldcg(part + (size_t)i * kSeg + sg);
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(64 + 32 * kXW));  // warp 0 has read dcur
+        const double pk = __shfl_sync(0xffffffffu, pvl, lane / 3);  // lane 3k picks up row k's sum
+        {
+          const int k = lane / 3, i = xi + kXW * k;
+          if (lane == 3 * k && k < kXRows && i < rows1) sm.dcur[i] = x2v + pk;  // partial sums of block b+1
+        }
+        if (xi == 0) stamp(7);
+      }
+      __syncthreads();  // B1
+      if (warp == 0 || warp == 5) stamp(0); else stamp(-1);
+      const long long pb0 = clock64();
+      // ---- phase B: delta(b+1), shift of T(b+1)'s diagonal, sweep-end epsilon ----
+      if (rowner) {
+        if (tma) mbar_wait(sm.bar, t & 1);
+        if (warp == 1) stamp(13);
+        double a0 = 0.0, a1 = 0.0;
+        if (ri < rows1) {  // column pairs 2rq + 8k: 16-byte loads, a quarter-warp reads 8 rows
+          const double* xr = sm.Wx + ri * kPS;
+          for (int j = 2 * rq; j < rows; j += 8) {
+            if (j + 1 < rows) {
+              const double2 x = *reinterpret_cast<const double2*>(xr + j);
+              const double2 l = *reinterpret_cast<const double2*>(lamc + j);
+              a0 = fma(x.x, l.x, a0);
+              a1 = fma(x.y, l.y, a1);
+            } else {
+              a0 = fma(xr[j], lamc[j], a0);
             }
           }
         }
-        // ||lambda||^2 of the blocks solved so far in this sweep (fixed order)
-        if (warp == 2) {
-          if (b == 0) {
-            sumsq = 0.0;
-          } else {
-            double v = 0.0;
-            for (int j = lane; j < rowsm; j += 32) v = fma(lamp[j], lamp[j], v);
-            sumsq += warp_sum(v);
-          }
-          if (b == nb - 1 && lane == 0) sm.red[2] = sumsq;
-        }
-        stamp(6);
-        // partials of block b+1 (helpers, step t-1), summed in fixed order
-        if (t > 0) {
-          if (tid == 32) {
-            wait_geq(vready, H * t, nullptr, ctl);
-            __threadfence();
-          }
-          asm volatile("bar.sync 1, %0;" ::"n"(kPipeThreads - 32));
-        }
-        stamp(3);
-        const double* part = partial + (size_t)((t + kPartBufs - 1) % kPartBufs) * pstride;
-#pragma unroll
-        for (int k = 0; k < kX2Rows; ++k) {
-          const int i = (warp - 1) + kAuxWarps * k;
-          if (i < rows1) {
-            double v = 0.0;
-            if (t > 0)
-              for (int ch = lane; ch < nch; ch += 32) v += __ldcg(part + (size_t)i * nch + ch);
-            v = warp_sum(v);
-            if (lane == 0) sm.pacc[i] = x2[k] + v;
-          }
-        }
-        cp_async_wait_all();
-      }
-      __syncthreads();  // B1
-      stamp(0);
-      // ---- phase B: delta(b+1), shift of T(b+1)'s diagonal, sweep-end epsilon ----
-      if (rowner) {
-        double a0 = 0.0, a1 = 0.0;
-        if (ri < rows1) {
-          const double* xr = sm.Wx + ri * kLDT;
-          int j = rq;
-          for (; j + 4 < rows; j += 8) {
-            a0 = fma(xr[j], lamc[j], a0);
-            a1 = fma(xr[j + 4], lamc[j + 4], a1);
-          }
-          if (j < rows) a0 = fma(xr[j], lamc[j], a0);
-        }
         double a = a0 + a1;
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        if (rq == 0 && ri < rows1) sm.dcur[ri] = add(dbase, mul(h2, sm.pacc[ri] + a));
-      } else if (tid >= 32 + 4 * kBR) {
-        for (int i = tid - (32 + 4 * kBR); i < rows1; i += kPipeThreads - (32 + 4 * kBR))
-          Tn[i * kLDT + i] = add(Tn[i * kLDT + i], dshift[(rb1 + i) / 3]);
+        a += __shfl_xor_sync(0xffffffffu, a, 8);
+        a += __shfl_xor_sync(0xffffffffu, a, 16);
+        if (rq == 0 && ri < rows1) sm.dcur[ri] = add(sm.dbs[ri], mul(h2, sm.dcur[ri] + a));
+        if (warp == 1) stamp(15);
+      } else if (tid >= 32 + kRowOwners) {
+        if (tma) mbar_wait(sm.bar, t & 1);
+        if (si < rows1) Tn[si * kPS + si] = add(Tn[si * kPS + si], sm.dsh[si / 3]);
       } else {  // warp 0
-        load_group_const(kc, sm.kcn + kKC * lane, lane < rows1 / 3);
+        load_group_const(kc, sm.kcn + kKCP * lane, lane < rows1 / 3, kKCP);
         if (b == nb - 1 && lane == 0 && !sm.flags[0]) {
           const double num = sqrt(sm.red[0]), den = sqrt(sm.red[1] + sm.red[2]);
           const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
@@ -1255,18 +1623,19 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           sm.flags[1] = (eps <= s.tol) ? 1 : ((sweep + 1 >= s.max_iter) ? 2 : 0);
         }
       }
+      if (prof && lane == 0) atomicAdd(prof + 16 + warp, (unsigned long long)(clock64() - pb0));  // phase-B cycles per warp
       __syncthreads();  // B2
-      stamp(1);
+      if (warp == 0 || warp == 5) stamp(1); else if (warp == 1) stamp(14); else stamp(-1);
       if (b == nb - 1) {
         iterations = sweep + 1;
         converged = sm.flags[1] == 1;
       }
-      if (sm.flags[0] || sm.flags[1] || ctl->timeout) {
+      if (sm.flags[0] || sm.flags[1]) {
         // publish the last block, then release everyone
+        if (tma && warp == 2) mbar_wait(sm.bar + 1, t & 1);  // drain the X fetch in flight
         for (int j = tid; j < rows; j += blockDim.x) __stcg(lamg + rb + j, lamc[j]);
-        __threadfence();
         __syncthreads();
-        if (tid == 0) atomicExch((unsigned*)vstop, 1u);
+        if (tid == 0) st_release_gpu(pstop, 1u);
         break;
       }
     }
@@ -1277,17 +1646,20 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
   } else {
     // ---- helpers ----
     double* lams = (double*)smem_raw;
+    __shared__ unsigned hflag;
+    __shared__ double hp[kHelpWarps];
     const unsigned hw = (blockIdx.x - 1) * (kPipeThreads / 32) + warp;
     const int64_t csz = (c + nch - 1) / nch;
+    if (stamper) tp = global_ns();
     for (unsigned t = 0;; ++t) {
       const int b = (int)(t % nb), b1 = wrap(b + 1), b2 = wrap(b + 2), bm = (b == 0) ? nb - 1 : b - 1;
       const int rows2 = rows_of(b2);
       const bool has = hw < (unsigned)(rows2 * nch);
       const int i = has ? (int)(hw / nch) : 0, ch = has ? (int)(hw % nch) : 0;
-      const int64_t r = 3 * (int64_t)b2 * kBG + i;
+      const int64_t r = 3 * (int64_t)b2 * kPG + i;
       const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
-      const int64_t e0 = 3 * (int64_t)b * kBG, e1 = e0 + rows_of(b);     // excluded: block b
-      const int64_t f0 = 3 * (int64_t)b1 * kBG, f1 = f0 + rows_of(b1);  // excluded: block b+1
+      const int64_t e0 = 3 * (int64_t)b * kPG, e1 = e0 + rows_of(b);     // excluded: block b
+      const int64_t f0 = 3 * (int64_t)b1 * kPG, f1 = f0 + rows_of(b1);  // excluded: block b+1
       const double* wr = s.W + r * s.ldw;
       double wv[kHelpPre];
 #pragma unroll
@@ -1296,16 +1668,47 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         const bool ok = has && j < c1 && (j < e0 || j >= e1) && (j < f0 || j >= f1);
         wv[u] = ok ? wr[j] : 0.0;
       }
+      {
+        // pull into L2, two steps ahead, what the solver CTA will fetch for
+        // block q = b+3: W[q, b+1] (its X tile at step t+1), W[q, b+2] (its
+        // Wx tile at step t+2), lambda(q), delta_base(q), group constants(q);
+        // T(q) is streamed by these helpers themselves at step t+1
+        const int q = (b + 3) % nb;
+        const int rq = rows_of(q);
+        const int64_t q0 = 3 * (int64_t)q * kPG;
+        if (hw < (unsigned)rq) {
+          const double* qr = s.W + (q0 + hw) * s.ldw;
+          const int64_t cb = (lane < 8) ? f0 : 3 * (int64_t)wrap(b1 + 1) * kPG;
+          const int64_t j = cb + 16 * (lane & 7);
+          if (lane < 16 && 16 * (lane & 7) < kPR + 15 && j < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(qr + j));
+        } else if (hw == (unsigned)rq) {
+          const int64_t g0 = q0 / 3;
+          const int64_t jl = q0 + 16 * lane, jd = q0 + 16 * (lane - 6), jk = kKC * g0 + 16 * (lane - 12);
+          if (lane < 6) {
+            if (jl < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(lamg + jl));
+          } else if (lane < 12) {
+            if (jd < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(s.delta_base + jd));
+          } else if (lane < 30 && jk < kKC * G) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(kconst + jk));
+          }
+        }
+      }
       stamp(5);
-      if (tid == 0) wait_geq(vsolved, t, vstop, ctl);
+      // one thread decides stop and broadcasts it (threads reading the flag
+      // themselves could disagree and split the CTA at the next barrier)
+      if (tid == 0) {
+        wait_acq(psolved, t, pstop, ctl);
+        hflag = ld_acquire_gpu(pstop);
+      }
       __syncthreads();
+      const unsigned hstop = hflag;
       stamp(4);
-      if (*vstop) break;
+      if (hstop) break;
       if (lam_in_smem) {
         if (t == 0) {
           for (int64_t j = tid; j < c; j += blockDim.x) lams[j] = 0.0;
         } else {
-          const int64_t pb0 = 3 * (int64_t)bm * kBG;
+          const int64_t pb0 = 3 * (int64_t)bm * kPG;
           const int pcols = rows_of(bm);
           for (int j = tid; j < pcols; j += blockDim.x) lams[pb0 + j] = __ldcg(lamg + pb0 + j);
         }
@@ -1329,21 +1732,33 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         double acc = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
         if (lane == 0) {
           if (r >= c0 && r < c1) acc = fma(dshift[r / 3], lam_in_smem ? lams[r] : __ldcg(lamg + r), acc);
-          __stcg(partial + (size_t)(t % kPartBufs) * pstride + (size_t)i * nch + ch, acc);
+          hp[warp] = acc;
         }
       }
       __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd((unsigned*)vready, 1u);
+      // one sum per (row, CTA): the first warp of each row in this CTA adds its
+      // successors in warp order and stores it in the row's segment slot
+      if (tid < kHelpWarps) {
+        const unsigned hw0 = (blockIdx.x - 1) * kHelpWarps, hwt = hw0 + tid;
+        const unsigned nitems = (unsigned)(rows2 * nch);
+        if (hwt < nitems) {
+          const unsigned ir = hwt / nch;
+          if (tid == 0 || (hwt - 1) / nch != ir) {
+            double v = hp[tid];
+            for (unsigned w = tid + 1; w < (unsigned)kHelpWarps && hw0 + w < nitems && (hw0 + w) / nch == ir; ++w) v += hp[w];
+            const int seg = (int)(blockIdx.x - 1) - (int)((ir * nch) / kHelpWarps);
+            __stcg(partial + (size_t)(t % kPartBufs) * pstride + (size_t)ir * kSeg + seg, v);
+          }
+        }
       }
+      __syncthreads();
+      if (tid == 0) red_release_gpu_add(pready4 + (t & 3), 1u);
     }
   }
   // ---- everyone: wait for the final lambda, then delta_end = delta_base + h^2 W_reg lam
   cp_async_wait_all();
-  if (tid == 0) wait_geq(vstop, 1u, nullptr, ctl);
+  if (tid == 0) wait_acq(pstop, 1u, nullptr, ctl);
   __syncthreads();
-  __threadfence();
   const unsigned gw = blockIdx.x * (kPipeThreads / 32) + warp, ngw = gridDim.x * (kPipeThreads / 32);
   for (int64_t r = gw; r < c; r += ngw) {
     const double* wr = s.W + r * s.ldw;
@@ -1389,12 +1804,25 @@ __global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double*
     dl_[0] = -1e-4 * (1.0 + 0.01 * lane);
     dl_[1] = ((V & 4) ? 3e-4 : 3e-5) * sin(1.0 * lane);  // V bit 2: tangential loads outside the cone
     dl_[2] = ((V & 4) ? 3e-4 : 3e-5) * cos(1.0 * lane);
-    block_solve<false, (V & 3)>(T, kBG, lane, dl_, lm, kc, 0.4, h2, dsq, err);
+    if (V & 64) {
+      block_solve_v4<true>(T, kPR, kPG, lane, dl_, lm, kc, 0.4, h2, T + kBR * kLDT);
+      __syncwarp();
+      err |= block_commit(T + kBR * kLDT, lane, lm, kc, 0.4, 1.0 / h2, dsq);
+    } else if (V & 32) {
+      block_solve_v4<true>(T, kLDT, kBG, lane, dl_, lm, kc, 0.4, h2, T + kBR * kLDT);
+      __syncwarp();
+      err |= block_commit(T + kBR * kLDT, lane, lm, kc, 0.4, 1.0 / h2, dsq);
+    } else if (V & 16)
+      block_solve_v3(T, kLDT, kBG, lane, dl_, lm, kc, 0.4, h2, dsq, err);
+    else if (V & 8)
+      block_solve_v2(T, kLDT, kBG, lane, dl_, lm, kc, 0.4, h2, dsq, err);
+    else
+      block_solve<false, (V & 3)>(T, kBG, lane, dl_, lm, kc, 0.4, h2, dsq, err);
   }
   long long t1 = clock64();
   const double s = warp_sum(lm[0] + lm[1] + lm[2] + dsq);
   if (lane == 0) {
-    out[0] = (double)(t1 - t0) / ((double)reps * kBG);
+    out[0] = (double)(t1 - t0) / ((double)reps * ((V & 64) ? kPG : kBG));
     out[1] = s;
   }
 }
@@ -1407,8 +1835,8 @@ static unsigned long long* pgs_profile_buffer() {
   if (on < 0) {
     const char* e = getenv("CNB_PGS_PROFILE");
     on = (e && e[0] == '1') ? 1 : 0;
-    if (on && cudaMalloc(&buf, 8 * sizeof(unsigned long long)) == cudaSuccess)
-      cudaMemset(buf, 0, 8 * sizeof(unsigned long long));
+    if (on && cudaMalloc(&buf, 32 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(buf, 0, 32 * sizeof(unsigned long long));
     else
       buf = nullptr;
   }
@@ -1421,7 +1849,7 @@ static unsigned long long* pgs_profile_buffer() {
 static bool use_pipe_kernel(int64_t groups) {
   const char* e = getenv("CNB_PGS_KERNEL");
   if (e && e[0] == 'g') return false;
-  return (groups + kBG - 1) / kBG >= 4;
+  return (groups + kPG - 1) / kPG >= 4;
 }
 
 static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
@@ -1432,7 +1860,7 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   const void* kfn = pipe ? (const void*)pgs_pipe_kernel : (const void*)pgs_grid_kernel;
   const int nthreads = pipe ? kPipeThreads : kGridThreads;
   const size_t tiles = pipe ? pipe_smem_bytes() : grid_smem_bytes();
-  const size_t lam_bytes = sizeof(double) * (size_t)(3 * s.groups);
+  const size_t lam_bytes = sizeof(double) * (size_t)(3 * s.groups) + (pipe ? 128 : 0);  // + alignment slack
   const int lam_in_smem = lam_bytes <= pgs_max_smem() ? 1 : 0;
   const size_t smem = std::max(tiles, lam_in_smem ? lam_bytes : (size_t)0);
   if (smem > pgs_max_smem()) {
@@ -1450,8 +1878,11 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   const int nwarps = nthreads / 32;
   // one (row, column-slice) item per helper warp; the partials of a block are
   // staged in a kBR x kLDT tile by the solver
-  const int nch = std::max(1, std::min(((grid - 1) * nwarps) / kBR, kLDT));
-  const size_t bytes = 64 + sizeof(double) * ((size_t)s.groups * (1 + kKC) + 1 + kPartBufs * (size_t)kBR * nch);
+  // pipe: a row spans at most kSeg helper CTAs, so nch <= (kSeg - 1) * kHelpWarps
+  const int nch = std::max(1, std::min(((grid - 1) * nwarps) / (pipe ? kPR : kBR),
+                                       pipe ? (kSeg - 1) * kHelpWarps : kLDT));
+  const size_t bytes =
+      64 + sizeof(double) * ((size_t)s.groups * (1 + kKC) + 1 + kPartBufs * (size_t)kBR * std::max(nch, kSeg));
   static void* ws_p = nullptr;
   static size_t ws_cap = 0;
   if (bytes > ws_cap) {
@@ -1470,9 +1901,41 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   int lis = lam_in_smem;
   int nchv = nch;
   unsigned long long* prof = pgs_profile_buffer();
-  void* args[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
-                  (void*)&nchv, (void*)&lis, (void*)&prof};
-  CNB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthreads), args, smem, st));
+  // tensor TMA needs a 16-byte aligned base and row pitch (even ldw)
+  int tma = (((uintptr_t)s.W & 15) == 0 && (s.ldw & 1) == 0) ? 1 : 0;
+  int dbg = 0;
+  {
+    const char* e = getenv("CNB_PGS_TMA");
+    if (e && e[0] == '0') tma = 0;
+    const char* d = getenv("CNB_PGS_DEBUG");
+    if (d) dbg = atoi(d) & ~1;
+  }
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (pipe && tma) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)(3 * s.groups), (cuuint64_t)(3 * s.groups)};  // {columns, rows}
+    const cuuint64_t pitch[1] = {(cuuint64_t)s.ldw * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)kPR, (cuuint32_t)kPR};
+    const cuuint32_t estr[2] = {1, 1};
+    if (!encode || encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)s.W, dims, pitch, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      tma = 0;  // fall back to cp.async staging
+  }
+  void* args_grid[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
+                       (void*)&nchv, (void*)&lis, (void*)&prof};
+  int tma_arg = tma | dbg;
+  void* args_pipe[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
+                       (void*)&nchv, (void*)&lis, (void*)&tma_arg, (void*)&prof, (void*)&tmap};
+  CNB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthreads), pipe ? args_pipe : args_grid, smem, st));
   CNB_LAUNCH_CHECK(pipe ? "pgs_pipe_kernel" : "pgs_grid_kernel");
   return CNB_OK;
 }
@@ -1499,7 +1962,7 @@ int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stre
   double* d = nullptr;
   CNB_CUDA(cudaMalloc(&d, 2 * sizeof(double)));
   cudaStream_t st = (cudaStream_t)stream;
-  const int sm = (int)(sizeof(double) * kBR * kLDT);
+  const int sm = (int)(sizeof(double) * (kBR * kLDT + 4 * kBG));
 #define CNB_BBS(V)                                                                                  \
   CNB_CUDA(cudaFuncSetAttribute(bench_block_solve_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
   bench_block_solve_kernel<V><<<1, 32, sm, st>>>(reps, d);
@@ -1511,7 +1974,14 @@ int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stre
     case 4: CNB_BBS(4) break;
     case 5: CNB_BBS(5) break;
     case 6: CNB_BBS(6) break;
-    default: CNB_BBS(7) break;
+    case 7: CNB_BBS(7) break;
+    case 8: CNB_BBS(8) break;
+    case 9: CNB_BBS(12) break;
+    case 10: CNB_BBS(16) break;
+    case 11: CNB_BBS(20) break;
+    case 12: CNB_BBS(32) break;
+    case 13: CNB_BBS(36) break;
+    default: CNB_BBS(100) break;
   }
 #undef CNB_BBS
   CNB_LAUNCH_CHECK("bench_block_solve_kernel");
@@ -1534,10 +2004,10 @@ int cnb_pgs_profile(double* out) {
     set_error("pgs profile: set CNB_PGS_PROFILE=1");
     return CNB_E_VALIDATION;
   }
-  unsigned long long h[8];
+  unsigned long long h[32];
   CNB_CUDA(cudaMemcpy(h, b, sizeof(h), cudaMemcpyDeviceToHost));
   CNB_CUDA(cudaMemset(b, 0, sizeof(h)));
-  for (int k = 0; k < 8; ++k) out[k] = (double)h[k];
+  for (int k = 0; k < 32; ++k) out[k] = (double)h[k];
   return CNB_OK;
 }
 

@@ -13,8 +13,9 @@ from paper_2306_06946_b200 import _lib  # noqa: E402
 torch.cuda.init()
 out = (ctypes.c_double * 2)()
 res = {}
-for v, name in enumerate(["fma-update", "h2-prescaled", "branchless-rsqrt", "both",
-                          "proj:fma-update", "proj:h2-prescaled", "proj:branchless-rsqrt", "proj:both"]):
+names = ["fma-update", "h2-prescaled", "branchless-rsqrt", "both",
+         "proj:fma-update", "proj:h2-prescaled", "proj:branchless-rsqrt", "proj:both", "v2", "proj:v2", "v3", "proj:v3", "v4", "proj:v4", "proj:v4-26x78"]
+for v, name in enumerate(names):
     _lib.call("cnb_bench_block_solve", v, 50, out, _lib.stream())
     _lib.call("cnb_bench_block_solve", v, 2000, out, _lib.stream())
     res[name] = round(out[0], 1)

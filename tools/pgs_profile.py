@@ -38,7 +38,7 @@ def main():
         cfg = cn.PgsConfig(args.sweeps, 1e-300, 0.4)
         pgs_device(W, delta, 0.01, cfg)  # warm-up
         torch.cuda.synchronize()
-        prof = (ctypes.c_double * 8)()
+        prof = (ctypes.c_double * 32)()
         have_prof = _lib.lib().cnb_pgs_profile(prof) == 0
         times = []
         for _ in range(args.reps):
@@ -49,7 +49,7 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
         sweeps = res.iterations
-        nb = (G + 31) // 32
+        nb = (G + 31) // 32 if os.environ.get("CNB_PGS_KERNEL", "pipe").startswith("g") else (G + 25) // 26
         out = {"groups": G, "sweeps": sweeps, "ms": round(min(times), 3),
                "ms_per_sweep": round(min(times) / sweeps, 4),
                "us_per_block_step": round(min(times) * 1e3 / (sweeps * nb), 3),
@@ -57,8 +57,8 @@ def main():
         if have_prof:
             _lib.lib().cnb_pgs_profile(prof)
             steps = args.reps * sweeps * nb
-            names = ["solver_wait", "delta", "solves", "epilogue", "helper_wait", "helper_partials", "helper_handoff", "solve_loop"]
-            out["us_per_step"] = {n: round(prof[k] / steps / 1e3, 3) for k, n in enumerate(names)}
+            names = [str(k) for k in range(32)]
+            out["us_per_step"] = {n: round(prof[k] / steps / 1e3, 3) for k, n in enumerate(names) if prof[k]}
         print(json.dumps(out), flush=True)
         del W
 
