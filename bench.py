@@ -523,7 +523,7 @@ def run_gpu_cfg3(args, rank, world):
     pgs_s = reps[-1].t_pgs
     bytes_sweep = 8.0 * c * c
     ach = sweeps * bytes_sweep / pgs_s / 1e9
-    roof = {"kernel": "pgs_grid_kernel (exact-order projected Gauss-Seidel, dense W)", "bound": "hbm",
+    roof = {"kernel": "pgs_pipe_kernel (exact-order projected Gauss-Seidel, dense W, lookahead-2 pipeline)", "bound": "hbm",
             "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
             "traffic": None, "peak_source": src, "algorithmic_bytes_per_sweep": bytes_sweep, "sweeps_per_step": sweeps,
             "ms_per_sweep": round(pgs_s * 1e3 / max(sweeps, 1), 4)}

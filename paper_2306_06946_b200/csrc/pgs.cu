@@ -1159,7 +1159,7 @@ constexpr int kTileD = kTileBytes / 8;
 constexpr int kXW = 9;              // X2 warps
 constexpr int kXRows = (kPR + kXW - 1) / kXW;
 constexpr int kPartBufs = 3;
-constexpr int kRowOwners = (4 * kPR + 31) / 32 * 32;  // phase-B GEMV threads (4 per row), whole warps
+constexpr int kRowOwners = (4 * kPR + 31) / 32 * 32;  // phase-B GEMV threads (4 per row), whole warps (2..11)
 constexpr int kHelpWarps = kPipeThreads / 32;         // warps per helper CTA
 constexpr int kSeg = 4;                                // partial slots per row (helper CTAs a row can span)
 
@@ -1175,7 +1175,7 @@ struct PipeSmem {
 
 __host__ __device__ inline size_t pipe_smem_bytes() {
   return 128 + sizeof(double) * (size_t)(4 * kTileD + kPR + 2 * kPR + kPR + kKCP * kPG + 4 * kPG + kPR + kPG + 8) +
-         16 + 4 * sizeof(int);
+         16 + 8 * sizeof(int);
 }
 
 
@@ -1340,10 +1340,40 @@ __device__ bool wait_acq(const unsigned* p, unsigned target, const unsigned* sto
   return true;
 }
 
+// Tagged records ("LL" style): a double split into two 8-byte words, each
+// carrying 32 data bits and the 32-bit tag of the step that wrote it.  An
+// 8-byte store is single-copy atomic, so a word whose tag matches carries that
+// step's data: the consumer polls the record itself, no fence or counter.
+__device__ __forceinline__ void ll_store(double* slot, double v, unsigned tag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long w0 = (b & 0xffffffffull) | ((unsigned long long)tag << 32);
+  const unsigned long long w1 = (b >> 32) | ((unsigned long long)tag << 32);
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(slot), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ double ll_load(const double* slot, unsigned tag, GridCtl* ctl) {
+  unsigned long long w0, w1;
+  unsigned long long t0 = 0;
+  for (unsigned n = 0;; ++n) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
+    if ((unsigned)(w0 >> 32) == tag && (unsigned)(w1 >> 32) == tag) break;
+    __nanosleep(64);  // polling loads share the SM's memory pipe with the solver warp
+    if ((n & 1023) == 0) {  // watchdog
+      const unsigned long long now = global_ns();
+      if (n == 0) t0 = now;
+      else if (now - t0 > 20000000000ull) {
+        atomicExch(&ctl->timeout, 1u);
+        atomicExch(&ctl->stop, 1u);
+        return 0.0;
+      }
+    }
+  }
+  return __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
+}
+
 __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, const double* __restrict__ dshift,
                                                                 const double* __restrict__ kconst, double* partial,
                                                                 GridCtl* ctl, int nch, int lam_in_smem, int tma,
-                                                                unsigned long long* prof,
+                                                                unsigned long long* prof, unsigned tag0,
                                                                 const __grid_constant__ CUtensorMap tmap) {
   const int dbg = tma & ~1;
   tma = (dbg & 2) ? 0 : (tma & 1);
@@ -1358,9 +1388,6 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
   const double h2 = s.h2;
   double* lamg = s.lam;
   unsigned* psolved = &ctl->solved;
-  // per-slot completion counters: a single cumulative count could be reached
-  // by helpers running ahead while a slow one has not finished the step
-  unsigned* pready4 = ctl->ready4;
   unsigned* pstop = &ctl->stop;
   const size_t pstride = (size_t)kPR * kSeg;  // one partial buffer: kSeg row sums per row
   auto rows_of = [&](int blk) { return 3 * (int)min((int64_t)kPG, G - (int64_t)blk * kPG); };
@@ -1401,17 +1428,23 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
     for (int i = tid; i < rows_of(0); i += blockDim.x)
       sm.T0[i * kPS + i] = add(sm.T0[i * kPS + i], dshift[i / 3]);
     GroupConst kc{};
-    double dsq = 0.0, sumsq = 0.0;
+    double dsq = 0.0;
     const double ih2 = 1.0 / h2;
     if (warp == 0) load_group_const(kc, kconst + kKC * lane, lane < rows_of(0) / 3);
-    const bool rowner = tid >= 32 && tid < 32 + kRowOwners;
-    // phase-B GEMV: 8 rows x 4 column phases per warp; a half-warp reads 8 rows x 2
-    // adjacent columns, 16 distinct banks for the 78-double row pitch
-    const int ri = 8 * (warp - 1) + (lane & 7), rq = lane >> 3;
+    const bool rowner = tid >= 64 && tid < 64 + kRowOwners;
+    // phase-B GEMV (warps 2..11): 8 rows x 4 column phases per warp; a quarter-warp
+    // reads 8 rows of 16-byte pairs, distinct banks for the 78-double row pitch
+    const int ri = 8 * (warp - 2) + (lane & 7), rq = lane >> 3;
+    volatile unsigned* vcnt = (volatile unsigned*)(sm.flags + 4);  // [0] lambda in smem, [1] published (steps)
+    if (tid == 0) {
+      sm.flags[2] = 0;
+      vcnt[0] = vcnt[1] = 0;
+    }
     __syncthreads();
     stamp(-1);
     int iterations = 0;
     bool converged = false;
+    if (warp != 1) {
     for (unsigned t = 0;; ++t) {
       const int b = (int)(t % nb), sweep = (int)(t / nb);
       const int b1 = wrap(b + 1), b2 = wrap(b + 2), bm = (b == 0) ? nb - 1 : b - 1;
@@ -1422,7 +1455,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
       double* lamc = sm.lamx + slot * kPR;         // lambda_b (this solve)
       double* lamp = sm.lamx + (slot ^ 1) * kPR;   // lambda_{b-1}
       const int64_t rb = 3 * (int64_t)b * kPG, rb1 = 3 * (int64_t)b1 * kPG, rbm = 3 * (int64_t)bm * kPG;
-      const int si = tid - (32 + kRowOwners);  // phase-B diagonal-shift thread, one row (kPR <= 160)
+      const int si = tid - (64 + kRowOwners);  // phase-B diagonal-shift thread, one row (kPR <= 128)
       if (warp == 0) {
         // ---- sequential block solve ----
         const int ng = rows / 3;
@@ -1446,10 +1479,15 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(rb / 3 + g), 1.0 / kc.ihw);
           if (lane == 0) sm.flags[0] = 1;
         }
+        if (t >= 2 && !(dbg & 2))  // the publisher has read this slot's previous lambda (step t-2)
+          while (vcnt[1] + 1 < t) {
+          }
         if (mine)
 #pragma unroll
           for (int a = 0; a < 3; ++a) lamc[3 * lane + a] = lm[a];
-        if (!(dbg & 2)) asm volatile("bar.arrive 4, 64;" ::: "memory");  // lambda_b ready: warp 1 publishes it
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) vcnt[0] = t + 1;  // lambda_b in shared memory: the publisher takes it
         if (b == nb - 1) {  // end of sweep: ||dlam||^2 and this block's ||lambda||^2
           const double l2 = mine ? (lm[0] * lm[0] + lm[1] * lm[1]) + lm[2] * lm[2] : 0.0;
           const double sl = warp_sum(l2), sd = warp_sum(dsq);
@@ -1462,23 +1500,6 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         stamp(2);
       } else if (dbg & 2) {
         // timing experiment: aux warps idle (wrong results)
-      } else if (warp == 1) {
-        if (lane == 0 && *(volatile unsigned*)&ctl->timeout) sm.flags[0] = 1;  // watchdog fired elsewhere
-        // publish lambda_b as soon as the solver warp has it (helpers of step t+1 wait for it)
-        asm volatile("bar.sync 4, 64;" ::: "memory");
-        stamp(8);
-        for (int j = lane; j < rows; j += 32) __stcg(lamg + rb + j, lamc[j]);
-        __syncwarp();
-        if (lane == 0) st_release_gpu(psolved, t + 1);
-        // ||lambda||^2 of blocks 0..nb-2 of this sweep (fixed order); warp 0 adds the last
-        if (b == 0) sumsq = 0.0;
-        if (b < nb - 1) {
-          double v = 0.0;
-          for (int j = lane; j < rows; j += 32) v = fma(lamc[j], lamc[j], v);
-          sumsq += warp_sum(v);
-        }
-        if (b == nb - 2 && lane == 0) sm.red[2] = sumsq;
-        stamp(9);
       } else if (warp == 2) {
         // T(b+1) and W[b+1, b]: one tensor-TMA box each (out-of-range rows and
         // columns of a ragged last block arrive as zeros)
@@ -1561,20 +1582,16 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         }
         asm volatile("bar.arrive 3, %0;" ::"n"(32 + 32 * kXW));  // X tile free for the next fetch
         if (xi == 0) stamp(6);
-        // partials of block b+1 (helpers, step t-1), summed in fixed order
-        if (t > 0) {
-          if (tid == 160) wait_acq(pready4 + ((t - 1) & 3), H * ((t - 1) / 4 + 1), nullptr, ctl);
-          asm volatile("bar.sync 1, %0;" ::"n"(32 * kXW));
-        }
+        // partials of block b+1 (helpers, step t-1): the tagged row sums, one per
+        // helper CTA the row spans, added in fixed order; lane k <-> row xi + kXW k
         if (xi == 0) stamp(3);
-        // helpers' row sums, one per helper CTA the row spans (fixed order); lane k <-> row xi + kXW k
-        const double* part = partial + (size_t)((t + kPartBufs - 1) % kPartBufs) * pstride;
+        const double* part = partial + 2 * (size_t)((t + kPartBufs - 1) % kPartBufs) * pstride;
         double pvl = 0.0;
         {
           const int i = xi + kXW * lane;
           if (t > 0 && lane < kXRows && i < rows1) {
             const int nseg = ((i + 1) * nch - 1) / kHelpWarps - (i * nch) / kHelpWarps + 1;
-            for (int sg = 0; sg < nseg; ++sg) pvl += __ldcg(part + (size_t)i * kSeg + sg);
+            for (int sg = 0; sg < nseg; ++sg) pvl += ll_load(part + 2 * ((size_t)i * kSeg + sg), tag0 + t - 1, ctl);
           }
         }
         asm volatile("bar.sync 2, %0;" ::"n"(64 + 32 * kXW));  // warp 0 has read dcur
@@ -1585,13 +1602,11 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         }
         if (xi == 0) stamp(7);
       }
-      __syncthreads();  // B1
+      asm volatile("bar.sync 5, %0;" ::"n"(kPipeThreads - 32) : "memory");  // B1 (all but the publisher)
       if (warp == 0 || warp == 5) stamp(0); else stamp(-1);
-      const long long pb0 = clock64();
       // ---- phase B: delta(b+1), shift of T(b+1)'s diagonal, sweep-end epsilon ----
       if (rowner) {
         if (tma) mbar_wait(sm.bar, t & 1);
-        if (warp == 1) stamp(13);
         double a0 = 0.0, a1 = 0.0;
         if (ri < rows1) {  // column pairs 2rq + 8k: 16-byte loads, a quarter-warp reads 8 rows
           const double* xr = sm.Wx + ri * kPS;
@@ -1610,89 +1625,163 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         a += __shfl_xor_sync(0xffffffffu, a, 8);
         a += __shfl_xor_sync(0xffffffffu, a, 16);
         if (rq == 0 && ri < rows1) sm.dcur[ri] = add(sm.dbs[ri], mul(h2, sm.dcur[ri] + a));
-        if (warp == 1) stamp(15);
-      } else if (tid >= 32 + kRowOwners) {
+      } else if (tid >= 64 + kRowOwners) {
         if (tma) mbar_wait(sm.bar, t & 1);
         if (si < rows1) Tn[si * kPS + si] = add(Tn[si * kPS + si], sm.dsh[si / 3]);
       } else {  // warp 0
         load_group_const(kc, sm.kcn + kKCP * lane, lane < rows1 / 3, kKCP);
         if (b == nb - 1 && lane == 0 && !sm.flags[0]) {
+          while (vcnt[1] < t) {  // the publisher's sum of blocks 0..nb-2 (step t-1) is in red[2]
+          }
           const double num = sqrt(sm.red[0]), den = sqrt(sm.red[1] + sm.red[2]);
           const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
           s.eps_hist[sweep] = eps;
           sm.flags[1] = (eps <= s.tol) ? 1 : ((sweep + 1 >= s.max_iter) ? 2 : 0);
         }
       }
-      if (prof && lane == 0) atomicAdd(prof + 16 + warp, (unsigned long long)(clock64() - pb0));  // phase-B cycles per warp
-      __syncthreads();  // B2
-      if (warp == 0 || warp == 5) stamp(1); else if (warp == 1) stamp(14); else stamp(-1);
+      asm volatile("bar.sync 6, %0;" ::"n"(kPipeThreads - 32) : "memory");  // B2 (all but the publisher)
+      if (warp == 0 || warp == 5) stamp(1); else stamp(-1);
       if (b == nb - 1) {
         iterations = sweep + 1;
         converged = sm.flags[1] == 1;
       }
       if (sm.flags[0] || sm.flags[1]) {
-        // publish the last block, then release everyone
         if (tma && warp == 2) mbar_wait(sm.bar + 1, t & 1);  // drain the X fetch in flight
-        for (int j = tid; j < rows; j += blockDim.x) __stcg(lamg + rb + j, lamc[j]);
-        __syncthreads();
-        if (tid == 0) st_release_gpu(pstop, 1u);
+        if (tid == 0) sm.flags[2] = 1;                       // the publisher stops after this step
         break;
       }
     }
+    } else {
+      // ---- warp 1: publisher.  Copies each solved block's lambda to global
+      // memory and releases the helpers (psolved = steps published), keeps
+      // ||lambda||^2 of the sweep; decoupled from the step barriers, so the
+      // release fence never delays the solver.
+      double sumsq = 0.0;
+      for (unsigned t = 0;; ++t) {
+        if (lane == 0) {
+          while (vcnt[0] < t + 1 && !*(volatile int*)&sm.flags[2]) __nanosleep(20);
+          if (*(volatile unsigned*)&ctl->timeout) sm.flags[0] = 1;  // watchdog fired elsewhere
+        }
+        const unsigned go = __shfl_sync(0xffffffffu, vcnt[0] >= t + 1 ? 1u : 0u, 0);
+        if (!go) break;
+        __threadfence_block();
+        const int b = (int)(t % nb), rows = rows_of(b);
+        const int64_t rb = 3 * (int64_t)b * kPG;
+        const double* lamc = sm.lamx + (t & 1) * kPR;
+        double v = 0.0;
+        for (int j = lane; j < rows; j += 32) {
+          const double l = lamc[j];
+          __stcg(lamg + rb + j, l);
+          v = fma(l, l, v);
+        }
+        __syncwarp();
+        if (lane == 0) st_release_gpu(psolved, t + 1);
+        // ||lambda||^2 of blocks 0..nb-2 of this sweep (fixed order); warp 0 adds the last
+        if (b == 0) sumsq = 0.0;
+        if (b < nb - 1) sumsq += warp_sum(v);
+        if (b == nb - 2 && lane == 0) sm.red[2] = sumsq;
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) vcnt[1] = t + 1;
+      }
+    }
+    // everyone (publisher included): last lambda block is in global memory; release the grid
+    __syncthreads();
     if (tid == 0) {
+      st_release_gpu(pstop, 1u);
       s.iters_conv[0] = iterations;
       s.iters_conv[1] = converged ? 1 : 0;
     }
   } else {
     // ---- helpers ----
+    // Each helper warp owns one (row, column chunk) item per step; the chunk
+    // index is fixed, the row moves with the step.  Step t: wait for
+    // lambda_{b-1}, refresh it in shared memory, dot products from registers,
+    // then at once issue the loads of step t+1's W slice (hidden behind the
+    // reduction and the next wait), and warp 0 reduces the CTA's items per row
+    // and stores the sums as tagged records (no fence, no counter).
     double* lams = (double*)smem_raw;
     __shared__ unsigned hflag;
     __shared__ double hp[kHelpWarps];
-    const unsigned hw = (blockIdx.x - 1) * (kPipeThreads / 32) + warp;
-    const int64_t csz = (c + nch - 1) / nch;
-    if (stamper) tp = global_ns();
-    for (unsigned t = 0;; ++t) {
-      const int b = (int)(t % nb), b1 = wrap(b + 1), b2 = wrap(b + 2), bm = (b == 0) ? nb - 1 : b - 1;
-      const int rows2 = rows_of(b2);
-      const bool has = hw < (unsigned)(rows2 * nch);
-      const int i = has ? (int)(hw / nch) : 0, ch = has ? (int)(hw % nch) : 0;
-      const int64_t r = 3 * (int64_t)b2 * kPG + i;
-      const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
-      const int64_t e0 = 3 * (int64_t)b * kPG, e1 = e0 + rows_of(b);     // excluded: block b
-      const int64_t f0 = 3 * (int64_t)b1 * kPG, f1 = f0 + rows_of(b1);  // excluded: block b+1
-      const double* wr = s.W + r * s.ldw;
-      double wv[kHelpPre];
+    const unsigned hw = (blockIdx.x - 1) * kHelpWarps + warp;
+    const int64_t csz = (((c + nch - 1) / nch) + 1) & ~(int64_t)1;  // even: 16-byte column pairs
+    struct Item {
+      bool has;
+      int i, rows2;
+      int64_t r, c0, c1, e0, e1, f0, f1;
+    };
+    auto item_of = [&](unsigned tt) {
+      Item it;
+      const int b = (int)(tt % nb), b1 = wrap(b + 1), b2 = wrap(b + 2);
+      it.rows2 = rows_of(b2);
+      it.has = hw < (unsigned)(it.rows2 * nch);
+      it.i = it.has ? (int)(hw / nch) : 0;
+      const int ch = it.has ? (int)(hw % nch) : 0;
+      it.r = 3 * (int64_t)b2 * kPG + it.i;
+      it.c0 = (int64_t)ch * csz;
+      it.c1 = min(c, it.c0 + csz);
+      it.e0 = 3 * (int64_t)b * kPG;  // excluded: block b
+      it.e1 = it.e0 + rows_of(b);
+      it.f0 = 3 * (int64_t)b1 * kPG;  // excluded: block b+1
+      it.f1 = it.f0 + rows_of(b1);
+      return it;
+    };
+    // W slice in registers: lane holds column pairs (c0 + 2 lane + 64 u, +1); the
+    // pipelined kernel requires an even row pitch, so every pair is 16-byte aligned,
+    // and block boundaries (multiples of 78) never split a pair
+    double2 wv[kHelpPre / 2];
+    auto preload = [&](const Item& it) {
+      const double* wr = s.W + it.r * s.ldw;
 #pragma unroll
-      for (int u = 0; u < kHelpPre; ++u) {
-        const int64_t j = c0 + lane + 32 * u;
-        const bool ok = has && j < c1 && (j < e0 || j >= e1) && (j < f0 || j >= f1);
-        wv[u] = ok ? wr[j] : 0.0;
-      }
-      {
-        // pull into L2, two steps ahead, what the solver CTA will fetch for
-        // block q = b+3: W[q, b+1] (its X tile at step t+1), W[q, b+2] (its
-        // Wx tile at step t+2), lambda(q), delta_base(q), group constants(q);
-        // T(q) is streamed by these helpers themselves at step t+1
-        const int q = (b + 3) % nb;
-        const int rq = rows_of(q);
-        const int64_t q0 = 3 * (int64_t)q * kPG;
-        if (hw < (unsigned)rq) {
-          const double* qr = s.W + (q0 + hw) * s.ldw;
-          const int64_t cb = (lane < 8) ? f0 : 3 * (int64_t)wrap(b1 + 1) * kPG;
-          const int64_t j = cb + 16 * (lane & 7);
-          if (lane < 16 && 16 * (lane & 7) < kPR + 15 && j < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(qr + j));
-        } else if (hw == (unsigned)rq) {
-          const int64_t g0 = q0 / 3;
-          const int64_t jl = q0 + 16 * lane, jd = q0 + 16 * (lane - 6), jk = kKC * g0 + 16 * (lane - 12);
-          if (lane < 6) {
-            if (jl < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(lamg + jl));
-          } else if (lane < 12) {
-            if (jd < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(s.delta_base + jd));
-          } else if (lane < 30 && jk < kKC * G) {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(kconst + jk));
-          }
+      for (int u = 0; u < kHelpPre / 2; ++u) {
+        const int64_t j = it.c0 + 2 * lane + 64 * u;
+        const bool ok = it.has && j < it.c1 && (j < it.e0 || j >= it.e1) && (j < it.f0 || j >= it.f1);
+        if (ok && j + 1 < it.c1) {
+          wv[u] = *reinterpret_cast<const double2*>(wr + j);
+        } else {
+          wv[u].x = ok ? wr[j] : 0.0;
+          wv[u].y = 0.0;
         }
       }
+    };
+    // L2 prefetch, about two steps ahead, of what the solver CTA will fetch for
+    // block q = b+4: W[q, b+2] (its X tile at step t+2), W[q, b+3] (its Wx tile
+    // at step t+3), lambda(q), delta_base(q), group constants(q)
+    auto l2_prefetch = [&](unsigned tt) {
+      const int b = (int)(tt % nb), q = (b + 4) % nb, qa = (b + 2) % nb, qb = (b + 3) % nb;
+      const int rq = rows_of(q);
+      const int64_t q0 = 3 * (int64_t)q * kPG;
+      if (hw < (unsigned)rq) {
+        const double* qr = s.W + (q0 + hw) * s.ldw;
+        const int64_t cb = 3 * (int64_t)((lane < 8) ? qa : qb) * kPG;
+        const int64_t j = cb + 16 * (lane & 7);
+        if (lane < 16 && 16 * (lane & 7) < kPR + 15 && j < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(qr + j));
+      } else if (hw == (unsigned)rq) {
+        const int64_t g0 = q0 / 3;
+        const int64_t jl = q0 + 16 * lane, jd = q0 + 16 * (lane - 6), jk = kKC * g0 + 16 * (lane - 12);
+        if (lane < 6) {
+          if (jl < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(lamg + jl));
+        } else if (lane < 12) {
+          if (jd < c) asm volatile("prefetch.global.L2 [%0];" ::"l"(s.delta_base + jd));
+        } else if (lane < 30 && jk < kKC * G) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kconst + jk));
+        }
+      }
+    };
+    if (stamper) tp = global_ns();
+    long long hc = clock64();
+    auto hstamp = [&](int k) {  // CNB_PGS_PROFILE: cycles per helper phase (CTA 1, thread 0), slots 16..21
+      if (prof && blockIdx.x == 1 && tid == 0) {
+        const long long n = clock64();
+        atomicAdd(prof + k, (unsigned long long)(n - hc));
+        hc = n;
+      }
+    };
+    Item it = item_of(0);
+    preload(it);
+    l2_prefetch(0);
+    for (unsigned t = 0;; ++t) {
+      const int b = (int)(t % nb), bm = (b == 0) ? nb - 1 : b - 1;
       stamp(5);
       // one thread decides stop and broadcasts it (threads reading the flag
       // themselves could disagree and split the CTA at the next barrier)
@@ -1702,6 +1791,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
       }
       __syncthreads();
       const unsigned hstop = hflag;
+      hstamp(16);  // wait for the solver
       stamp(4);
       if (hstop) break;
       if (lam_in_smem) {
@@ -1714,45 +1804,64 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         }
         __syncthreads();
       }
-      if (has) {
+      hstamp(17);  // lambda refresh
+      if (it.has) {
+        const double* wr = s.W + it.r * s.ldw;
         double a[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int u = 0; u < kHelpPre; ++u) {
-          const int64_t j = min(c0 + lane + 32 * u, c - 1);
-          a[u & 3] = fma(wv[u], lam_in_smem ? lams[j] : __ldcg(lamg + j), a[u & 3]);
+        for (int u = 0; u < kHelpPre / 2; ++u) {
+          const int64_t j = min(it.c0 + 2 * lane + 64 * u, (c - 1) & ~(int64_t)1);
+          double2 l;
+          if (lam_in_smem) {
+            l = *reinterpret_cast<const double2*>(lams + j);
+          } else {
+            l.x = __ldcg(lamg + j);
+            l.y = j + 1 < c ? __ldcg(lamg + j + 1) : 0.0;
+          }
+          a[(2 * u) & 3] = fma(wv[u].x, l.x, a[(2 * u) & 3]);
+          a[(2 * u + 1) & 3] = fma(wv[u].y, l.y, a[(2 * u + 1) & 3]);
         }
-        for (int64_t j0 = c0 + 32 * kHelpPre; j0 < c1; j0 += 32 * kHelpPre) {  // slices wider than the registers
+        for (int64_t j0 = it.c0 + 32 * kHelpPre; j0 < it.c1; j0 += 32 * kHelpPre) {  // slices wider than the registers
 #pragma unroll 8
           for (int u = 0; u < kHelpPre; ++u) {
             const int64_t j = j0 + lane + 32 * u;
-            if (j < c1 && (j < e0 || j >= e1) && (j < f0 || j >= f1))
+            if (j < it.c1 && (j < it.e0 || j >= it.e1) && (j < it.f0 || j >= it.f1))
               a[u & 3] = fma(wr[j], lam_in_smem ? lams[j] : __ldcg(lamg + j), a[u & 3]);
           }
         }
         double acc = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
         if (lane == 0) {
-          if (r >= c0 && r < c1) acc = fma(dshift[r / 3], lam_in_smem ? lams[r] : __ldcg(lamg + r), acc);
+          if (it.r >= it.c0 && it.r < it.c1)
+            acc = fma(dshift[it.r / 3], lam_in_smem ? lams[it.r] : __ldcg(lamg + it.r), acc);
           hp[warp] = acc;
         }
       }
+      const Item cur = it;
+      it = item_of(t + 1);  // next step's slice: loads in flight during the reduction and the wait
+      preload(it);
+      l2_prefetch(t + 1);
       __syncthreads();
-      // one sum per (row, CTA): the first warp of each row in this CTA adds its
-      // successors in warp order and stores it in the row's segment slot
-      if (tid < kHelpWarps) {
-        const unsigned hw0 = (blockIdx.x - 1) * kHelpWarps, hwt = hw0 + tid;
-        const unsigned nitems = (unsigned)(rows2 * nch);
-        if (hwt < nitems) {
-          const unsigned ir = hwt / nch;
-          if (tid == 0 || (hwt - 1) / nch != ir) {
-            double v = hp[tid];
-            for (unsigned w = tid + 1; w < (unsigned)kHelpWarps && hw0 + w < nitems && (hw0 + w) / nch == ir; ++w) v += hp[w];
-            const int seg = (int)(blockIdx.x - 1) - (int)((ir * nch) / kHelpWarps);
-            __stcg(partial + (size_t)(t % kPartBufs) * pstride + (size_t)ir * kSeg + seg, v);
-          }
+      hstamp(18);  // dot products + next preload issue
+      // one sum per (row, CTA): segmented reduction over the CTA's warps in
+      // warp order (fixed tree: deterministic), first warp of a row stores it
+      if (warp == 0) {
+        const unsigned hw0 = (blockIdx.x - 1) * kHelpWarps, hwl = hw0 + lane;
+        const unsigned nitems = (unsigned)(cur.rows2 * nch);
+        const bool valid = lane < kHelpWarps && hwl < nitems;
+        const int ir = valid ? (int)(hwl / nch) : -1 - lane;
+        double v = valid ? hp[lane] : 0.0;
+#pragma unroll
+        for (int off = 1; off < kHelpWarps; off <<= 1) {
+          const double u = __shfl_down_sync(0xffffffffu, v, off);
+          const int iu = __shfl_down_sync(0xffffffffu, ir, off);
+          if (lane + off < kHelpWarps && iu == ir) v += u;
+        }
+        if (valid && (lane == 0 || (hwl - 1) / nch != (unsigned)ir)) {
+          const int seg = (int)(blockIdx.x - 1) - (int)(((unsigned)ir * nch) / kHelpWarps);
+          ll_store(partial + 2 * ((size_t)(t % kPartBufs) * pstride + (size_t)ir * kSeg + seg), v, tag0 + t);
         }
       }
-      __syncthreads();
-      if (tid == 0) red_release_gpu_add(pready4 + (t & 3), 1u);
+      hstamp(19);  // row sums
     }
   }
   // ---- everyone: wait for the final lambda, then delta_end = delta_base + h^2 W_reg lam
@@ -1846,17 +1955,18 @@ static unsigned long long* pgs_profile_buffer() {
 // CNB_PGS_KERNEL=grid selects the one-step-lookahead kernel (pgs_grid_kernel);
 // the default is the pipelined lookahead-2 kernel (pgs_pipe_kernel), which
 // needs at least four blocks.
-static bool use_pipe_kernel(int64_t groups) {
+static bool use_pipe_kernel(const PgsScene& s) {
   const char* e = getenv("CNB_PGS_KERNEL");
   if (e && e[0] == 'g') return false;
-  return (groups + kPG - 1) / kPG >= 4;
+  // 16-byte row pairs (helpers) and TMA rows need an even pitch and an aligned base
+  return (s.groups + kPG - 1) / kPG >= 4 && (s.ldw & 1) == 0 && ((uintptr_t)s.W & 15) == 0;
 }
 
 static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   int dev = 0, sms = 0;
   CNB_CUDA(cudaGetDevice(&dev));
   CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const bool pipe = use_pipe_kernel(s.groups);
+  const bool pipe = use_pipe_kernel(s);
   const void* kfn = pipe ? (const void*)pgs_pipe_kernel : (const void*)pgs_grid_kernel;
   const int nthreads = pipe ? kPipeThreads : kGridThreads;
   const size_t tiles = pipe ? pipe_smem_bytes() : grid_smem_bytes();
@@ -1933,8 +2043,14 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   void* args_grid[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
                        (void*)&nchv, (void*)&lis, (void*)&prof};
   int tma_arg = tma | dbg;
+  // record tags: unique across launches (a record left by an earlier call never matches)
+  static unsigned tag_base = 1;
+  const unsigned long long steps = (unsigned long long)((s.groups + kPG - 1) / kPG) * (unsigned)s.max_iter + 8;
+  if ((unsigned long long)tag_base + steps >= 0xffffffffull) tag_base = 1;  // wrap (records are rewritten each call)
+  unsigned tag0 = tag_base;
+  tag_base += (unsigned)steps;
   void* args_pipe[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
-                       (void*)&nchv, (void*)&lis, (void*)&tma_arg, (void*)&prof, (void*)&tmap};
+                       (void*)&nchv, (void*)&lis, (void*)&tma_arg, (void*)&prof, (void*)&tag0, (void*)&tmap};
   CNB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthreads), pipe ? args_pipe : args_grid, smem, st));
   CNB_LAUNCH_CHECK(pipe ? "pgs_pipe_kernel" : "pgs_grid_kernel");
   return CNB_OK;
