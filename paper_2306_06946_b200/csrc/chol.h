@@ -21,6 +21,7 @@ constexpr int kPanel = 32;   // pivot panel width of the dense front factorisati
 constexpr int kTile = 64;    // SYRK / GEMM output tile
 constexpr int kEaCols = 32;  // parent columns per extend-add task
 constexpr int kInvCols = 8;  // columns of L11^{-1} per inversion task
+constexpr int kMaxSnCols = 512;  // widest supernode (wider ones are split into chains)
 
 struct LevelTasks {
   // extend-add: (parent supernode, parent col lo, parent col hi)

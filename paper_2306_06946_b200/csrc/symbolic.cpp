@@ -374,33 +374,50 @@ int analyze(Symbolic& S, int64_t n, const int64_t* rowptr, const int64_t* col, i
       owner[c] = p;
     }
   }
-  // final supernodes in ascending node order
-  std::vector<int64_t> snodes;
-  for (int64_t s = 0; s < ns0; ++s)
-    if (alive[s]) snodes.push_back(s);
-  const int64_t ns = (int64_t)snodes.size();
-  std::vector<int64_t> newid(ns0, -1);
-  for (int64_t k = 0; k < ns; ++k) newid[snodes[k]] = k;
+  // final supernodes in ascending node order; supernodes wider than
+  // kMaxSnCols DoFs are split into a chain of pieces (piece k's parent is
+  // piece k+1, its rows the later columns of the supernode plus the
+  // supernode's own rows).  The factor is unchanged; the inverted diagonal
+  // blocks L11^{-1} of the solves stay at most kMaxSnCols wide (a 6750-wide
+  // separator would otherwise cost nc^3/3 flops to invert).
+  std::vector<int64_t> pf, pl, pend;  // piece first / last node, last node of the supernode
+  const int64_t maxw = std::max<int64_t>(1, kMaxSnCols / bs);
+  for (int64_t s = 0; s < ns0; ++s) {
+    if (!alive[s]) continue;
+    const int64_t a = sfirst_m[s], z = slast_m[s], w = z - a + 1;
+    const int64_t np = (w + maxw - 1) / maxw;
+    for (int64_t k = 0; k < np; ++k) {
+      pf.push_back(a + (w * k) / np);  // near-equal pieces
+      pl.push_back(a + (w * (k + 1)) / np - 1);
+      pend.push_back(z);
+    }
+  }
+  const int64_t ns = (int64_t)pf.size();
   S.ns = ns;
   S.first.assign(ns + 1, 0);
   S.parent.assign(ns, -1);
   S.rows_ptr.assign(ns + 1, 0);
   std::vector<int64_t> node_sn(nv);
   for (int64_t k = 0; k < ns; ++k) {
-    const int64_t s = snodes[k];
-    S.first[k] = bs * sfirst_m[s];
-    for (int64_t i = sfirst_m[s]; i <= slast_m[s]; ++i) node_sn[i] = k;
+    S.first[k] = bs * pf[k];
+    for (int64_t i = pf[k]; i <= pl[k]; ++i) node_sn[i] = k;
   }
   S.first[ns] = bs * nv;
   for (int64_t k = 0; k < ns; ++k) {
-    const int64_t last = slast_m[snodes[k]];
-    S.parent[k] = parent[last] >= 0 ? node_sn[parent[last]] : -1;
-    S.rows_ptr[k + 1] = S.rows_ptr[k] + bs * (int64_t)st[last].size();
+    const int64_t last = pend[k];
+    if (pl[k] < last) {
+      S.parent[k] = k + 1;
+    } else {
+      S.parent[k] = parent[last] >= 0 ? node_sn[parent[last]] : -1;
+    }
+    S.rows_ptr[k + 1] = S.rows_ptr[k] + bs * ((last - pl[k]) + (int64_t)st[last].size());
   }
   S.rows.resize(S.rows_ptr[ns]);
   for (int64_t k = 0; k < ns; ++k) {
     int64_t o = S.rows_ptr[k];
-    for (int64_t j : st[slast_m[snodes[k]]])
+    for (int64_t j = pl[k] + 1; j <= pend[k]; ++j)
+      for (int d = 0; d < bs; ++d) S.rows[o++] = bs * j + d;
+    for (int64_t j : st[pend[k]])
       for (int d = 0; d < bs; ++d) S.rows[o++] = bs * j + d;
   }
   // DoF permutation
