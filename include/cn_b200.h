@@ -61,6 +61,14 @@ const char* cnb_last_error(void);
 int cnb_rebuild_w(int64_t groups, const double* D, const double* Wg, int64_t ldwg,
                   double* W, int64_t ldw, void* stream);
 
+/* U = S C S^T (m x m) for S (m x k) in ELL form, width 4 (ell_col int32, ell_val;
+ * padding entries have value 0), C dense symmetric k x k.  The compact mapping
+ * compliance U_o = S_o A^-1 S_o^T of constraints.py:175-178 is formed as
+ * S_o (E^T A^-1 E) S_o^T, E = unit columns of the k DoFs S_o touches (k < m for
+ * barycentric contacts that share triangle nodes).  k <= 29000. */
+int cnb_sandwich(int64_t m, int64_t k, const int32_t* ell_col, const double* ell_val, const double* C,
+                 int64_t ldc, double* U, int64_t ldu, void* stream);
+
 /* delta = D (p_a - p_b).  Replaces compute_violation constraints.py:208-214. */
 int cnb_violation(int64_t groups, const double* D, const double* p_a, const double* p_b,
                   double* delta, void* stream);

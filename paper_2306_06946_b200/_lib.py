@@ -28,6 +28,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_abi_version": [],
     "cnb_last_error": [],
     "cnb_rebuild_w": [I64, P, P, I64, P, I64, P],
+    "cnb_sandwich": [I64, I64, P, P, P, I64, P, I64, P],
     "cnb_violation": [I64, P, P, P, P, P],
     "cnb_apply_dt": [I64, P, P, P, P, P],
     "cnb_prox_update": [I64, P, I64, P, P, P, F64, P, P, P],

@@ -192,50 +192,92 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
       }
 }
 
-// SYRK trailing update on a 64x64 tile with DMMA:
-// C[rows ti, cols tj] -= P[rows ti, :] * P[rows tj, :]^T, P = panel columns.
+// SYRK update on a 64x64 tile with DMMA, K staged through shared memory in
+// 32-column chunks (cp.async double buffer):
+//   C[rows ti, cols tj] -= P[rows ti, :] * P[rows tj, :]^T,  P = L columns [k0, k0 + kw).
+// mode 0 (in-block): P = panel p (kw <= 32), target columns [t0, block end) of
+//   every row below -- only the block's remaining pivot columns;
+// mode 1 (trailing): P = the whole block of panel p (kw <= 128 columns), target
+//   [block end, f).  The trailing matrix is read and written once per 128
+//   columns, with K = 128 per pass (16 flop per byte of C).
 // 4 warps, each a 32x32 quadrant = 4x4 fragments of 8x8.
 constexpr int kSP = kPanel + 4;  // smem row stride (== 4 mod 16 doubles: conflict-free fragments)
-__global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
+constexpr size_t kSyrkSmem = 2 * 2 * kTile * kSP * sizeof(double);
+__global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode,
                                                    double* __restrict__ front) {
-  __shared__ double Pi[kTile * kSP];
-  __shared__ double Pj[kTile * kSP];
+  extern __shared__ __align__(16) double syrk_sm[];
+  double* Pi = syrk_sm;                  // [2][kTile * kSP]
+  double* Pj = syrk_sm + 2 * kTile * kSP;
   const int64_t s = tasks[3 * blockIdx.x];
   const int ti = tasks[3 * blockIdx.x + 1], tj = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
-  const int kw = (int)min((int64_t)kPanel, nc - k0);
-  const int64_t t0 = k0 + kw;
+  constexpr int64_t blk = (int64_t)kBlkPanels * kPanel;
+  const int64_t k0p = (int64_t)p * kPanel;
+  int64_t k0, kw, t0, cend;
+  if (mode == 0) {
+    k0 = k0p;
+    kw = min((int64_t)kPanel, nc - k0);
+    t0 = k0 + kw;
+    cend = min((k0 / blk + 1) * blk, nc);
+  } else {
+    k0 = (k0p / blk) * blk;
+    const int64_t bend = min(k0 + blk, nc);
+    kw = bend - k0;
+    t0 = bend;
+    cend = f;
+  }
   const int64_t r0 = t0 + (int64_t)ti * kTile, c0 = t0 + (int64_t)tj * kTile;
   double* F = front + S.front_off[s];
-  for (int e = threadIdx.x; e < kTile * kPanel; e += blockDim.x) {
-    const int rr = e % kTile, kk = e / kTile;
-    const bool kin = kk < kw;
-    const int64_t ri = r0 + rr, rj = c0 + rr;
-    cp_async8(&Pi[rr * kSP + kk], F + (int64_t)(k0 + kk) * f + ri, kin && ri < f);
-    cp_async8(&Pj[rr * kSP + kk], F + (int64_t)(k0 + kk) * f + rj, kin && rj < f);
-  }
-  cp_async_wait_all();
-  __syncthreads();
+  auto stage = [&](int buf, int64_t kk0) {
+    double* A = Pi + buf * kTile * kSP;
+    double* B = Pj + buf * kTile * kSP;
+    for (int e = threadIdx.x; e < kTile * kPanel; e += blockDim.x) {
+      const int rr = e % kTile, kc = e / kTile;
+      const bool kin = kk0 + kc < kw;
+      const int64_t ri = r0 + rr, rj = c0 + rr;
+      const double* col = F + (k0 + kk0 + kc) * f;
+      cp_async8(&A[rr * kSP + kc], col + ri, kin && ri < f);
+      cp_async8(&B[rr * kSP + kc], col + rj, kin && rj < cend);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wy = (warp >> 1) * 32, wx = (warp & 1) * 32;
-  if (ti == tj && wx > wy) return;  // strictly-upper quadrant of a diagonal tile
+  const bool skip = ti == tj && wx > wy;  // strictly-upper quadrant of a diagonal tile
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int kk = 0; kk < kw; kk += 4) {
-    double fa[4], fb[4];
+  const int nchunk = (int)((kw + kPanel - 1) / kPanel);
+  stage(0, 0);
+  for (int ck = 0; ck < nchunk; ++ck) {
+    if (ck + 1 < nchunk) {
+      stage((ck + 1) & 1, (int64_t)(ck + 1) * kPanel);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* A = Pi + (ck & 1) * kTile * kSP;
+    const double* B = Pj + (ck & 1) * kTile * kSP;
+    const int kc = (int)min((int64_t)kPanel, kw - (int64_t)ck * kPanel);
+    if (!skip)
+      for (int kk = 0; kk < kc; kk += 4) {
+        double fa[4], fb[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) fa[a] = Pi[(wy + 8 * a + g) * kSP + kk + t];
+        for (int a = 0; a < 4; ++a) fa[a] = A[(wy + 8 * a + g) * kSP + kk + t];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) fb[b] = Pj[(wx + 8 * b + g) * kSP + kk + t];
+        for (int b = 0; b < 4; ++b) fb[b] = B[(wx + 8 * b + g) * kSP + kk + t];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+          for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+      }
+    __syncthreads();
   }
+  if (skip) return;
   // epilogue: issue every C load before the first store (F aliases itself, so
   // the compiler would otherwise serialise load -> subtract -> store)
   double cv[4][4][2];
@@ -247,7 +289,7 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
       for (int h = 0; h < 2; ++h) {
         const int64_t r = r0 + wy + 8 * a + g;
         const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-        cv[a][b][h] = (r < f && c < f && r >= c) ? F[c * f + r] : 0.0;
+        cv[a][b][h] = (r < f && c < cend && r >= c) ? F[c * f + r] : 0.0;
       }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -257,7 +299,7 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
       for (int h = 0; h < 2; ++h) {
         const int64_t r = r0 + wy + 8 * a + g;
         const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-        if (r < f && c < f && r >= c) F[c * f + r] = cv[a][b][h] - acc[a][b][h];
+        if (r < f && c < cend && r >= c) F[c * f + r] = cv[a][b][h] - acc[a][b][h];
       }
 }
 
@@ -290,7 +332,7 @@ static int chol_upload(CholHandle* h) {
     int64_t off, count;
   };
   std::vector<Rec> ea_rec, ti_rec, p2_rec;
-  std::vector<std::vector<Rec>> po_rec, tr_rec, sy_rec;
+  std::vector<std::vector<Rec>> po_rec, tr_rec, sy_rec, so_rec;
   for (int l = 0; l < S.n_levels; ++l) {
     const LevelTasks& T = S.tasks[l];
     ea_rec.push_back({(int64_t)all.size(), (int64_t)T.ea.size() / 3});
@@ -298,6 +340,7 @@ static int chol_upload(CholHandle* h) {
     po_rec.emplace_back();
     tr_rec.emplace_back();
     sy_rec.emplace_back();
+    so_rec.emplace_back();
     for (size_t p = 0; p < T.potrf.size(); ++p) {
       po_rec[l].push_back({(int64_t)all.size(), (int64_t)T.potrf[p].size()});
       all.insert(all.end(), T.potrf[p].begin(), T.potrf[p].end());
@@ -305,6 +348,8 @@ static int chol_upload(CholHandle* h) {
       all.insert(all.end(), T.trsm[p].begin(), T.trsm[p].end());
       sy_rec[l].push_back({(int64_t)all.size(), (int64_t)T.syrk[p].size() / 3});
       all.insert(all.end(), T.syrk[p].begin(), T.syrk[p].end());
+      so_rec[l].push_back({(int64_t)all.size(), (int64_t)T.syrk_out[p].size() / 3});
+      all.insert(all.end(), T.syrk_out[p].begin(), T.syrk_out[p].end());
     }
     // triangular inversion tasks: (s, 16-column chunk of L11^{-1})
     const int64_t off = (int64_t)all.size();
@@ -337,6 +382,7 @@ static int chol_upload(CholHandle* h) {
   h->potrf.assign(S.n_levels, {});
   h->trsm.assign(S.n_levels, {});
   h->syrk.assign(S.n_levels, {});
+  h->syrk_out.assign(S.n_levels, {});
   for (int l = 0; l < S.n_levels; ++l) {
     h->ea.push_back(mk(ea_rec[l]));
     h->trinv.push_back(mk(ti_rec[l]));
@@ -344,12 +390,14 @@ static int chol_upload(CholHandle* h) {
     for (auto& r : po_rec[l]) h->potrf[l].push_back(mk(r));
     for (auto& r : tr_rec[l]) h->trsm[l].push_back(mk(r));
     for (auto& r : sy_rec[l]) h->syrk[l].push_back(mk(r));
+    for (auto& r : so_rec[l]) h->syrk_out[l].push_back(mk(r));
   }
   CNB_CUDA(cudaMalloc((void**)&h->d_front, std::max<int64_t>(1, S.front_off[S.ns]) * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_linv, std::max<int64_t>(1, h->linv_off[S.ns]) * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_p21, std::max<int64_t>(1, h->p21_off[S.ns]) * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_kkinv, std::max<int64_t>(1, S.ns) * kPanel * kPanel * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_vals, std::max<int64_t>(1, S.csr_nnz) * sizeof(double)));
+  CNB_CUDA(cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem));
   h->uploaded = true;
   return CNB_OK;
 }
@@ -420,7 +468,13 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
         CNB_LAUNCH_CHECK("trsm_kernel");
       }
       if (h->syrk[l][p].count) {
-        syrk_kernel<<<(unsigned)h->syrk[l][p].count, 128, 0, st>>>(sym, h->syrk[l][p].ptr, k0, h->d_front);
+        syrk_kernel<<<(unsigned)h->syrk[l][p].count, 128, kSyrkSmem, st>>>(sym, h->syrk[l][p].ptr, (int)p, 0,
+                                                                           h->d_front);
+        CNB_LAUNCH_CHECK("syrk_kernel");
+      }
+      if (h->syrk_out[l][p].count) {
+        syrk_kernel<<<(unsigned)h->syrk_out[l][p].count, 128, kSyrkSmem, st>>>(sym, h->syrk_out[l][p].ptr, (int)p,
+                                                                               1, h->d_front);
         CNB_LAUNCH_CHECK("syrk_kernel");
       }
     }
@@ -472,7 +526,8 @@ int cnb_chol_info(cnb_chol_t hh, int64_t* info, double* fl) {
   for (const LevelTasks& T : S.tasks) {
     fl_launch += (T.ea.empty() ? 0 : 1) + 1;  // extend-add, trinv
     for (size_t p = 0; p < T.potrf.size(); ++p)
-      fl_launch += (T.potrf[p].empty() ? 0 : 1) + (T.trsm[p].empty() ? 0 : 1) + (T.syrk[p].empty() ? 0 : 1);
+      fl_launch += (T.potrf[p].empty() ? 0 : 1) + (T.trsm[p].empty() ? 0 : 1) + (T.syrk[p].empty() ? 0 : 1) +
+                   (T.syrk_out[p].empty() ? 0 : 1);
   }
   info[7] = fl_launch;
   info[8] = 2 + 4 * (int64_t)S.n_levels;

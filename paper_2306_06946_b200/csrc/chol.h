@@ -18,6 +18,8 @@
 namespace cnb {
 
 constexpr int kPanel = 32;   // pivot panel width of the dense front factorisation
+constexpr int kBlkPanels = 4;  // panels per trailing-update block: the trailing matrix is
+                               // updated once per kBlkPanels * kPanel = 128 columns (K = 128)
 constexpr int kTile = 64;    // SYRK / GEMM output tile
 constexpr int kEaCols = 32;  // parent columns per extend-add task
 constexpr int kInvCols = 8;  // columns of L11^{-1} per inversion task
@@ -26,8 +28,10 @@ constexpr int kMaxSnCols = 512;  // widest supernode (wider ones are split into 
 struct LevelTasks {
   // extend-add: (parent supernode, parent col lo, parent col hi)
   std::vector<int32_t> ea;
-  // per panel step p: potrf fronts, trsm (front, row chunk), syrk (front, ti, tj)
-  std::vector<std::vector<int32_t>> potrf, trsm, syrk;
+  // per panel step p: potrf fronts, trsm (front, row chunk), syrk (front, ti, tj):
+  // syrk[p] = in-block update of the block's remaining pivot columns by panel p,
+  // syrk_out[p] = trailing update by the whole block (last panel of a block)
+  std::vector<std::vector<int32_t>> potrf, trsm, syrk, syrk_out;
 };
 
 struct Symbolic {

@@ -95,7 +95,7 @@ struct CholHandle {
   std::vector<int64_t> linv_off, p21_off;
   int32_t* d_tasks = nullptr;
   std::vector<DevTasks> ea, trinv, p21;                  // per level
-  std::vector<std::vector<DevTasks>> potrf, trsm, syrk;  // per level, per panel
+  std::vector<std::vector<DevTasks>> potrf, trsm, syrk, syrk_out;  // per level, per panel
   SolvePlan plan1, plan8;                                // single-RHS / multi-RHS dense solves
   GrowBuf bp, tbuf;                                      // permuted RHS, backward temp
   GrowBuf c_int, c_rhs, c_val, c_y;                      // compliance workspace

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cnb {
@@ -327,6 +329,45 @@ __global__ void csr_spmv_kernel(int64_t rows, const int64_t* __restrict__ rp, co
   y[r] = alpha == 1.0 ? s : alpha * s;
 }
 
+// U = S C S^T for a sparse S (m x k) stored as ELL rows of width 4 (col, val;
+// padding val = 0) and a dense symmetric C (k x k).  One CTA per output row j:
+// t = C^T s_j (<= 4 contiguous rows of C combined, in shared memory), then
+// U[j][i] = sum_e s_ie t[col_ie] for every i (gathers from shared memory),
+// fixed summation order.  Used for the mapping compliance of contact DoFs:
+// U_o = S_o (E^T A^-1 E) S_o^T with E the unit columns of the DoFs S_o touches.
+constexpr int kEll = 4;
+__global__ void __launch_bounds__(256) sandwich_kernel(int64_t m, int64_t k, const int32_t* __restrict__ ecol,
+                                                       const double* __restrict__ eval, const double* __restrict__ C,
+                                                       int64_t ldc, double* __restrict__ U, int64_t ldu) {
+  extern __shared__ double tsm[];
+  const int64_t j = blockIdx.x;
+  int32_t cj[kEll];
+  double vj[kEll];
+#pragma unroll
+  for (int e = 0; e < kEll; ++e) {
+    cj[e] = ecol[kEll * j + e];
+    vj[e] = eval[kEll * j + e];
+  }
+  for (int64_t a = threadIdx.x; a < k; a += blockDim.x) {
+    double t = 0.0;
+#pragma unroll
+    for (int e = 0; e < kEll; ++e) t = fma(vj[e], C[(int64_t)cj[e] * ldc + a], t);
+    tsm[a] = t;
+  }
+  __syncthreads();
+  double* urow = U + j * ldu;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const int4 ci = *reinterpret_cast<const int4*>(ecol + kEll * i);
+    const double2 v01 = *reinterpret_cast<const double2*>(eval + kEll * i);
+    const double2 v23 = *reinterpret_cast<const double2*>(eval + kEll * i + 2);
+    double u = v01.x * tsm[ci.x];
+    u = fma(v01.y, tsm[ci.y], u);
+    u = fma(v23.x, tsm[ci.z], u);
+    u = fma(v23.y, tsm[ci.w], u);
+    urow[i] = u;
+  }
+}
+
 static void split_rows(int64_t rows, dim3& grid, int64_t cols_blocks) {
   // rows across y (<= 65535) and z
   int64_t gy = rows < 65535 ? rows : 65535;
@@ -341,6 +382,27 @@ using namespace cnb;
 extern "C" {
 
 int cnb_abi_version(void) { return 1; }
+
+int cnb_sandwich(int64_t m, int64_t k, const int32_t* ell_col, const double* ell_val, const double* C, int64_t ldc,
+                 double* U, int64_t ldu, void* stream) {
+  if (m < 0 || k < 0 || ldc < k || ldu < m) {
+    set_error("sandwich: invalid sizes (m=%lld, k=%lld)", (long long)m, (long long)k);
+    return CNB_E_DIMENSION;
+  }
+  if (m == 0) return CNB_OK;
+  const size_t smem = sizeof(double) * (size_t)std::max<int64_t>(k, 1);
+  int dev = 0, maxs = 0;
+  CNB_CUDA(cudaGetDevice(&dev));
+  CNB_CUDA(cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (smem > (size_t)maxs) {
+    set_error("sandwich: k=%lld exceeds the shared-memory row buffer", (long long)k);
+    return CNB_E_VALIDATION;
+  }
+  CNB_CUDA(cudaFuncSetAttribute(sandwich_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  sandwich_kernel<<<(unsigned)m, 256, smem, (cudaStream_t)stream>>>(m, k, ell_col, ell_val, C, ldc, U, ldu);
+  CNB_LAUNCH_CHECK("sandwich_kernel");
+  return CNB_OK;
+}
 
 long long cnb_launch_count(void) { return g_launches.load(); }
 

@@ -870,7 +870,6 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
   const int64_t csz = (c + nch - 1) / nch;
   double* lamg = s.lam;
   volatile unsigned* vsolved = &ctl->solved;
-  volatile unsigned* vready = &ctl->ready;
   volatile unsigned* vstop = &ctl->stop;
   double dl_[3] = {0, 0, 0}, lm[3] = {0, 0, 0};
   double dsq = 0.0;
@@ -913,7 +912,9 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
       double* Tn = slot ? sm.T0 : sm.T1;  // next block's tile / partial staging
       if (t > 0 && tid == 0) {
         stamp(3);  // epilogue of step t-1 -> here
-        wait_geq(vready, H * t, nullptr, ctl);
+        // per-slot counters: a cumulative count could be reached by helpers
+        // running a step ahead while a slow one has not finished step t-1
+        wait_geq(&ctl->ready4[(t - 1) & 3], H * ((t - 1) / 4 + 1), nullptr, ctl);
       }
       stamp(0);  // wait for helpers
       __syncthreads();
@@ -1097,7 +1098,7 @@ __global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, cons
       if (blockIdx.x == 1) stamp(5);  // helper: lambda refresh + partials
       if (tid == 0) {
         __threadfence();
-        atomicAdd((unsigned*)vready, 1u);
+        atomicAdd(&ctl->ready4[t & 3], 1u);
       }
     }
   }

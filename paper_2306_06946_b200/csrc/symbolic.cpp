@@ -533,6 +533,8 @@ int analyze(Symbolic& S, int64_t n, const int64_t* rowptr, const int64_t* col, i
     T.potrf.assign(max_panels, {});
     T.trsm.assign(max_panels, {});
     T.syrk.assign(max_panels, {});
+    T.syrk_out.assign(max_panels, {});
+    const int64_t blk = (int64_t)kBlkPanels * kPanel;
     for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
       const int64_t s = S.level_sn[q];
       const int64_t nc = S.nc(s), f = S.f(s);
@@ -544,13 +546,27 @@ int analyze(Symbolic& S, int64_t n, const int64_t* rowptr, const int64_t* col, i
           T.trsm[p].push_back((int32_t)s);
           T.trsm[p].push_back((int32_t)c);
         }
-        const int64_t nt = (below + kTile - 1) / kTile;
-        for (int64_t ti = 0; ti < nt; ++ti)
-          for (int64_t tj = 0; tj <= ti; ++tj) {
-            T.syrk[p].push_back((int32_t)s);
-            T.syrk[p].push_back((int32_t)ti);
-            T.syrk[p].push_back((int32_t)tj);
-          }
+        // in-block update: columns [k0 + kw, block end) of every row below
+        const int64_t bend = std::min<int64_t>((k0 / blk + 1) * blk, nc);
+        const int64_t t0 = k0 + kw;
+        if (t0 < bend) {
+          const int64_t ntr = (f - t0 + kTile - 1) / kTile, ntc = (bend - t0 + kTile - 1) / kTile;
+          for (int64_t ti = 0; ti < ntr; ++ti)
+            for (int64_t tj = 0; tj <= std::min(ti, ntc - 1); ++tj) {
+              T.syrk[p].push_back((int32_t)s);
+              T.syrk[p].push_back((int32_t)ti);
+              T.syrk[p].push_back((int32_t)tj);
+            }
+        } else if (bend < f) {
+          // last panel of a block: trailing update [bend, f) by the block's columns
+          const int64_t nt = (f - bend + kTile - 1) / kTile;
+          for (int64_t ti = 0; ti < nt; ++ti)
+            for (int64_t tj = 0; tj <= ti; ++tj) {
+              T.syrk_out[p].push_back((int32_t)s);
+              T.syrk_out[p].push_back((int32_t)ti);
+              T.syrk_out[p].push_back((int32_t)tj);
+            }
+        }
       }
     }
   }

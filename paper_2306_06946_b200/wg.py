@@ -3,9 +3,15 @@
 Replaces the multi-RHS solve + sparse product of assemble_Wg
 (/root/reference/pkg/src/contactnewton/constraints.py:175-178): instead of
 X = A^-1 S^T (n x 3p dense) and S X, the library forward-solves only the
-elimination paths of S^T's columns (Y = L^-1 P S^T) and forms U = Y^T Y with
-fp64 tensor-core tiles (csrc/chol.cu: fwd_kernel sparse mode, gram_kernel).
-Only the rows/columns of the pairs the object takes part in are formed.
+elimination paths of the right-hand sides (Y = L^-1 P R) and forms Y^T Y with
+fp64 tensor-core tiles (csrc/solve.cu: panel_mma_kernel, gram_kernel).  Only
+the rows/columns of the pairs the object takes part in are formed.
+
+Right-hand sides: when the rows of S_o touch fewer distinct DoFs k than they
+are (barycentric contacts share triangle nodes, a node can carry several
+pairs), R = E, the unit columns of those k DoFs: C = E^T A^-1 E (k x k) and
+U_o = S_o C S_o^T (csrc/contact.cu sandwich_kernel).  Same matrix, k^2
+instead of (3 m_o)^2 Gram work.  Otherwise R = S_o^T directly.
 """
 
 from __future__ import annotations
@@ -17,6 +23,11 @@ import torch
 
 from . import _device as dv
 from . import _lib
+
+
+DOF_REDUCTION_MAX = 0.85  # use the DoF-reduced right-hand sides when k <= 0.85 * 3 m_o
+ELL_WIDTH = 4             # nnz per row of S_o the sandwich kernel takes (barycentric: 3)
+SANDWICH_MAX_K = 29000    # row buffer of the sandwich kernel (227 KB of shared memory)
 
 
 def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, shard: bool = True):
@@ -44,10 +55,34 @@ def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, sha
         rowidx = np.ascontiguousarray(csr.indices[sel], dtype=np.int64)
         vals = np.ascontiguousarray(csr.data[sel], dtype=np.float64)
         fl = (ctypes.c_double * 2)()
-        _lib.call("cnb_chol_compliance", F._h, 3 * mo, colptr.ctypes.data, rowidx.ctypes.data, vals.ctypes.data,
-                  U.data_ptr(), 3 * mo, fl, rank, world, _lib.stream())
-        if world > 1:
-            reduce_shards(U, group)
+        dofs, inv = np.unique(rowidx, return_inverse=True)
+        k = len(dofs)
+        per_row = np.diff(colptr)
+        if k <= DOF_REDUCTION_MAX * 3 * mo and per_row.max(initial=0) <= ELL_WIDTH and k <= SANDWICH_MAX_K:
+            # C = E^T A^-1 E over the k touched DoFs, then U = S C S^T
+            e_ptr = np.arange(k + 1, dtype=np.int64)
+            e_val = np.ones(k)
+            dofs = np.ascontiguousarray(dofs, dtype=np.int64)
+            C = dv.empty((k, k))
+            _lib.call("cnb_chol_compliance", F._h, k, e_ptr.ctypes.data, dofs.ctypes.data, e_val.ctypes.data,
+                      C.data_ptr(), k, fl, rank, world, _lib.stream())
+            if world > 1:
+                reduce_shards(C, group)
+            ell_col = np.zeros((3 * mo, ELL_WIDTH), dtype=np.int32)
+            ell_val = np.zeros((3 * mo, ELL_WIDTH))
+            slot = np.arange(len(rowidx)) - np.repeat(colptr[:-1], per_row)
+            rix = np.repeat(np.arange(3 * mo), per_row)
+            ell_col[rix, slot] = inv
+            ell_val[rix, slot] = vals
+            d_col = torch.as_tensor(ell_col, device=d)
+            d_val = torch.as_tensor(ell_val, device=d)
+            _lib.call("cnb_sandwich", 3 * mo, k, d_col.data_ptr(), d_val.data_ptr(), C.data_ptr(), k, U.data_ptr(),
+                      3 * mo, _lib.stream())
+        else:
+            _lib.call("cnb_chol_compliance", F._h, 3 * mo, colptr.ctypes.data, rowidx.ctypes.data, vals.ctypes.data,
+                      U.data_ptr(), 3 * mo, fl, rank, world, _lib.stream())
+            if world > 1:
+                reduce_shards(U, group)
         if stats is not None:
             stats["fwd_flops"] = stats.get("fwd_flops", 0.0) + fl[0]
             stats["gram_flops"] = stats.get("gram_flops", 0.0) + fl[1]

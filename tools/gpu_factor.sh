@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 300 python tools/factor_profile.py > gpurun_out/factor.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/factor_launches.csv python tools/factor_profile.py --reps 1 > gpurun_out/factor_ncu.log 2>&1
