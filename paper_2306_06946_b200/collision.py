@@ -244,6 +244,103 @@ def attachment_triplets(attachment: Attachment, n_dofs: int, row0: int):
 # device pair table
 # --------------------------------------------------------------------------
 
+class PairSoA:
+    """Structure-of-arrays pair records as detection produces them (canonical order
+    after ``sort``); ``LazyPairs`` turns rows into ``ProximityPair`` objects on demand,
+    ``PairTable.from_soa`` uploads them without building Python objects."""
+
+    FIELDS = ("kind", "obj", "node", "w", "local", "world", "lnormal", "has_ln", "ref", "pa", "pb", "signed",
+              "keys")
+
+    def __init__(self, m: int = 0):
+        self.kind = np.full((m, 2), 4, dtype=np.int8)
+        self.obj = np.zeros((m, 2), dtype=np.int32)
+        self.node = np.full((m, 2, 3), -1, dtype=np.int64)
+        self.w = np.zeros((m, 2, 3))
+        self.local = np.zeros((m, 2, 3))
+        self.world = np.zeros((m, 2, 3))
+        self.lnormal = np.zeros((m, 3))
+        self.has_ln = np.zeros(m, dtype=np.int8)
+        self.ref = np.zeros((m, 3))
+        self.pa = np.zeros((m, 3))
+        self.pb = np.zeros((m, 3))
+        self.signed = np.zeros(m)
+        self.keys = np.zeros((m, 4), dtype=np.int64)
+
+    def __len__(self) -> int:
+        return len(self.keys)
+
+    @staticmethod
+    def concat(parts) -> "PairSoA":
+        out = PairSoA(0)
+        parts = [q for q in parts if len(q)]
+        if parts:
+            for f in PairSoA.FIELDS:
+                setattr(out, f, np.concatenate([getattr(q, f) for q in parts]))
+        return out
+
+    def take(self, order) -> "PairSoA":
+        out = PairSoA(0)
+        for f in PairSoA.FIELDS:
+            setattr(out, f, getattr(self, f)[order])
+        return out
+
+    def sort(self) -> "PairSoA":
+        """Canonical order (collision.py:344): (object_a, object_b, vertex_id, element_id)."""
+        k = self.keys
+        return self.take(np.lexsort((k[:, 3], k[:, 2], k[:, 1], k[:, 0])))
+
+    def attachment(self, i: int, s: int) -> Attachment:
+        kind = int(self.kind[i, s])
+        oid = int(self.obj[i, s])
+        if kind == 0:
+            return Attachment(AttachKind.VERTEX, oid, vertex=int(self.node[i, s, 0]))
+        if kind == 1:
+            return Attachment(AttachKind.BARYCENTRIC, oid, triangle=self.node[i, s].copy(), weights=self.w[i, s].copy())
+        if kind == 3:
+            ln = self.lnormal[i].copy() if (s == 1 and self.has_ln[i]) else None
+            return Attachment(AttachKind.LOCAL, oid, local_point=self.local[i, s].copy(), local_normal=ln)
+        return Attachment(AttachKind.WORLD, oid, world_point=self.world[i, s].copy())
+
+    def pair(self, i: int) -> ProximityPair:
+        k = self.keys[i]
+        return ProximityPair(object_a=int(k[0]), object_b=int(k[1]), attach_a=self.attachment(i, 0),
+                             attach_b=self.attachment(i, 1), p_a=self.pa[i].copy(), p_b=self.pb[i].copy(),
+                             ref_normal=self.ref[i].copy(), signed_distance=float(self.signed[i]),
+                             vertex_id=int(k[2]), element_id=int(k[3]))
+
+
+class LazyPairs:
+    """Read-only sequence of ``ProximityPair`` backed by a ``PairSoA`` (objects are
+    built on first access: a step never needs them)."""
+
+    def __init__(self, soa: PairSoA):
+        self.soa = soa
+        self._cache = {}
+
+    def __len__(self) -> int:
+        return len(self.soa)
+
+    def __bool__(self) -> bool:
+        return len(self.soa) > 0
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        p = self._cache.get(i)
+        if p is None:
+            p = self._cache[i] = self.soa.pair(i)
+        return p
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
 class PairTable:
     """Structure-of-arrays view of a canonical pair list, on the device.
 
@@ -301,6 +398,29 @@ class PairTable:
         self.ref_normal = dv.f64(ref, d)
         self.p_a = dv.f64(pa, d)
         self.p_b = dv.f64(pb, d)
+
+    @classmethod
+    def from_soa(cls, soa: PairSoA) -> "PairTable":
+        """Table straight from detection arrays (no per-pair Python objects)."""
+        self = cls.__new__(cls)
+        self.soa = soa
+        self.pairs = LazyPairs(soa)
+        self.m = len(soa)
+        self.h_kind, self.h_obj, self.h_node, self.h_w = soa.kind, soa.obj, soa.node, soa.w
+        self.h_keys = soa.keys
+        d = dv.device()
+        self.kind = torch.as_tensor(soa.kind, device=d)
+        self.obj = torch.as_tensor(soa.obj, device=d)
+        self.node = torch.as_tensor(soa.node, device=d)
+        self.w = dv.f64(soa.w, d)
+        self.local = dv.f64(soa.local, d)
+        self.world = dv.f64(soa.world, d)
+        self.lnormal = dv.f64(soa.lnormal, d)
+        self.has_ln = torch.as_tensor(soa.has_ln, device=d)
+        self.ref_normal = dv.f64(soa.ref, d)
+        self.p_a = dv.f64(soa.pa, d)
+        self.p_b = dv.f64(soa.pb, d)
+        return self
 
     @staticmethod
     def of(pairs) -> "PairTable":
@@ -457,16 +577,18 @@ def _device_points(geom: MeshGeometry) -> torch.Tensor:
     return dv.f64(np.ascontiguousarray(geom.points, dtype=np.float64)).reshape(-1, 3)
 
 
-def _vertex_vs_mesh(ga: MeshGeometry, gb: MeshGeometry, threshold: float):
+def _vertex_vs_mesh(ga: MeshGeometry, gb: MeshGeometry, threshold: float) -> PairSoA:
     """Best pair per surface vertex of A against B's triangles (collision.py:222-260).
 
     The all-pairs closest-point scan runs on the GPU (csrc/detect.cu, numpy's
-    operation order, bit-exact selection); the host builds the pair records of
-    the vertices that pass the threshold gate.
+    operation order, bit-exact selection); the host gathers the records of the
+    vertices that pass the threshold gate into arrays.
     """
     nv, nt = len(ga.vertex_ids), len(gb.triangles)
     if nv == 0 or nt == 0:
-        return []
+        return PairSoA(0)
+    if (ga.dynamic and not ga.deformable) or (gb.dynamic and not gb.deformable):
+        raise InvalidAttachmentError("dynamic non-deformable meshes are not supported")
     d = dv.device()
     vids = torch.as_tensor(np.ascontiguousarray(ga.vertex_ids, dtype=np.int64), device=d)
     tris = torch.as_tensor(np.ascontiguousarray(gb.triangles, dtype=np.int64), device=d)
@@ -477,47 +599,90 @@ def _vertex_vs_mesh(ga: MeshGeometry, gb: MeshGeometry, threshold: float):
     _lib.call("cnb_detect_vertex_mesh", nv, vids.data_ptr(), pa.data_ptr(), nt, tris.data_ptr(), pb.data_ptr(),
               float(threshold), work.data_ptr(), best.data_ptr(), out.data_ptr(), _lib.stream())
     best_h, out_h = best.cpu().numpy(), out.cpu().numpy()
+    keep = np.flatnonzero(out_h[:, 11] > 0.0)
+    m = len(keep)
+    r = PairSoA(m)
+    if m == 0:
+        return r
     pts_a = np.asarray(ga.points, dtype=np.float64).reshape(-1, 3)
-    res = []
-    for q in np.flatnonzero(out_h[:, 11] > 0.0):
-        vid, t = int(ga.vertex_ids[q]), int(best_h[q])
-        row = out_h[q]
-        p, cp, nrm = pts_a[vid], row[5:8].copy(), row[8:11].copy()
-        res.append(ProximityPair(
-            object_a=ga.object_id, object_b=gb.object_id,
-            attach_a=_mesh_side(ga, vertex=vid, point=p),
-            attach_b=_mesh_side(gb, triangle=gb.triangles[t], bary=row[2:5].copy(), point=cp, normal=nrm),
-            p_a=p.copy(), p_b=cp.copy(), ref_normal=nrm.copy(), signed_distance=float(row[0]), vertex_id=vid,
-            element_id=t))
-    return res
+    vid = np.asarray(ga.vertex_ids, dtype=np.int64)[keep]
+    t = best_h[keep].astype(np.int64)
+    rows = out_h[keep]
+    p, cp, nrm = pts_a[vid], rows[:, 5:8], rows[:, 8:11]
+    r.obj[:, 0], r.obj[:, 1] = ga.object_id, gb.object_id
+    if ga.deformable:
+        r.kind[:, 0] = 0
+        r.node[:, 0, 0] = vid
+        r.w[:, 0, 0] = 1.0
+    else:  # kinematic side: the per-point expressions of _mesh_side (same rounding)
+        r.kind[:, 0] = 3
+        for q in range(m):
+            r.local[q, 0] = ga.pose.inverse_apply(p[q])
+    if gb.deformable:
+        r.kind[:, 1] = 1
+        r.node[:, 1] = np.asarray(gb.triangles, dtype=np.int64)[t]
+        r.w[:, 1] = rows[:, 2:5]
+    else:
+        r.kind[:, 1] = 3
+        for q in range(m):
+            r.local[q, 1] = gb.pose.inverse_apply(cp[q])
+            r.lnormal[q] = gb.pose.rotation.T @ nrm[q]
+        r.has_ln[:] = 1
+    r.pa[:], r.pb[:], r.ref[:] = p, cp, nrm
+    r.signed[:] = rows[:, 0]
+    r.keys[:] = np.stack([np.full(m, ga.object_id), np.full(m, gb.object_id), vid, t], axis=1)
+    return r
 
 
-def _vertex_vs_plane(geom: MeshGeometry, plane: PlaneGeometry, threshold: float):
+def _vertex_vs_plane(geom: MeshGeometry, plane: PlaneGeometry, threshold: float) -> PairSoA:
     n = plane.normal
     pts = geom.points[geom.vertex_ids]
-    signed = pts @ n - plane.offset
-    out = []
-    for k in np.flatnonzero(signed <= threshold):
-        vid = int(geom.vertex_ids[k])
-        p = geom.points[vid]
-        s = float(n @ p - plane.offset)
-        foot = p - s * n
-        out.append(ProximityPair(
-            object_a=geom.object_id, object_b=plane.object_id,
-            attach_a=_mesh_side(geom, vertex=vid, point=p),
-            attach_b=Attachment(AttachKind.WORLD, plane.object_id, world_point=foot),
-            p_a=p.copy(), p_b=foot, ref_normal=n.copy(), signed_distance=s, vertex_id=vid,
-            element_id=-1))
-    return out
+    # vectorised gate with a margin, then the reference's own expression
+    # float(n @ p - offset) per candidate (collision.py:264-270): the kept set
+    # and the distances are the reference's bit for bit
+    approx = pts @ n - plane.offset
+    margin = 1e-12 * (np.abs(pts).max(initial=0.0) * np.abs(n).sum() + abs(plane.offset) + 1.0)
+    cand = np.flatnonzero(approx <= threshold + margin)
+    points = np.asarray(geom.points, dtype=np.float64)
+    vids_all = np.asarray(geom.vertex_ids, dtype=np.int64)
+    exact = np.array([float(n @ points[v] - plane.offset) for v in vids_all[cand]])
+    keep = exact <= threshold
+    m = int(keep.sum())
+    r = PairSoA(m)
+    if m == 0:
+        return r
+    if geom.dynamic and not geom.deformable:
+        raise InvalidAttachmentError("dynamic non-deformable meshes are not supported")
+    vid = vids_all[cand][keep]
+    p = points[vid]
+    s = exact[keep]
+    foot = p - s[:, None] * n
+    r.obj[:, 0], r.obj[:, 1] = geom.object_id, plane.object_id
+    if geom.deformable:
+        r.kind[:, 0] = 0
+        r.node[:, 0, 0] = vid
+        r.w[:, 0, 0] = 1.0
+    else:
+        r.kind[:, 0] = 3
+        for q in range(m):
+            r.local[q, 0] = geom.pose.inverse_apply(p[q])
+    r.kind[:, 1] = 4
+    r.world[:, 1] = foot
+    r.pa[:], r.pb[:] = p, foot
+    r.ref[:] = n
+    r.signed[:] = s
+    r.keys[:] = np.stack([np.full(m, geom.object_id), np.full(m, plane.object_id), vid, np.full(m, -1)], axis=1)
+    return r
 
 
-def detect(geometries, threshold: float) -> list:
-    """Pairs with signed distance <= threshold in canonical order (collision.py:320-345)."""
+def detect_soa(geometries, threshold: float) -> PairSoA:
+    """Pairs with signed distance <= threshold in canonical order (collision.py:320-345),
+    as arrays."""
     if threshold <= 0:
         raise InvalidAttachmentError(f"threshold must be positive, got {threshold}")
     meshes = [g for g in geometries if isinstance(g, MeshGeometry)]
     planes = [g for g in geometries if isinstance(g, PlaneGeometry)]
-    pairs = []
+    parts = []
     for ga in meshes:
         for gb in meshes:
             if ga.object_id == gb.object_id or not (ga.dynamic or gb.dynamic):
@@ -528,9 +693,13 @@ def detect(geometries, threshold: float) -> list:
             lo_b, hi_b = gb.points.min(axis=0), gb.points.max(axis=0)
             if not (np.all(lo_a - threshold <= hi_b) and np.all(lo_b - threshold <= hi_a)):
                 continue
-            pairs.extend(_vertex_vs_mesh(ga, gb, threshold))
+            parts.append(_vertex_vs_mesh(ga, gb, threshold))
         for plane in planes:
             if ga.dynamic:
-                pairs.extend(_vertex_vs_plane(ga, plane, threshold))
-    pairs.sort(key=lambda p: (p.object_a, p.object_b, p.vertex_id, p.element_id))
-    return pairs
+                parts.append(_vertex_vs_plane(ga, plane, threshold))
+    return PairSoA.concat(parts).sort()
+
+
+def detect(geometries, threshold: float) -> list:
+    """Pairs with signed distance <= threshold in canonical order (collision.py:320-345)."""
+    return list(LazyPairs(detect_soa(geometries, threshold)))

@@ -20,7 +20,7 @@ import torch
 from . import _device as dv
 from . import _lib
 from .collision import DOF_KINDS, FrameSet, PairTable, attachment_triplets, frames_tensor
-from .errors import DimensionMismatchError
+from .errors import DimensionMismatchError, InvalidAttachmentError
 
 
 @dataclass
@@ -162,6 +162,8 @@ class SignedMapping:
 
 def build_signed_mapping(pairs, object_id: int, n_dofs: int, fixed_mask=None) -> SignedMapping:
     """+G on A sides, -G on B sides, fixed-DOF columns zeroed (constraints.py:101-120)."""
+    if isinstance(pairs, PairTable) and not (pairs.h_kind == 2).any():
+        return _signed_mapping_table(pairs, object_id, n_dofs, fixed_mask)
     plist = pairs.pairs if isinstance(pairs, PairTable) else list(pairs)
     rows, cols, vals = [], [], []
     idx, side = [], []
@@ -180,6 +182,36 @@ def build_signed_mapping(pairs, object_id: int, n_dofs: int, fixed_mask=None) ->
         S = (S @ sp.diags(np.where(fixed_mask, 0.0, 1.0))).tocsr()
     S.sort_indices()
     return SignedMapping(S, np.asarray(idx, dtype=np.int64), np.asarray(side, dtype=np.int8))
+
+
+def _signed_mapping_table(table: PairTable, object_id: int, n_dofs: int, fixed_mask=None) -> SignedMapping:
+    """build_signed_mapping from the table arrays (vertex / barycentric sides): the
+    same triplets as attachment_triplets, pair by pair, side A before side B."""
+    m = table.m
+    kind, obj, node, w = table.h_kind, table.h_obj, table.h_node, table.h_w
+    mine = (obj == object_id) & ((kind == 0) | (kind == 1))          # (m, 2)
+    ii, ss = np.nonzero(mine)                                        # row-major: pair, then side
+    nn = np.where(kind[ii, ss] == 0, 1, 3)
+    cols_node = node[ii, ss]                                         # (k, 3)
+    used = np.arange(3)[None, :] < nn[:, None]
+    if (used & ((cols_node < 0) | (3 * cols_node + 2 >= n_dofs))).any():
+        raise InvalidAttachmentError("attachment node out of range")
+    sign = np.where(ss == 0, 1.0, -1.0)
+    rows, cols, vals = [], [], []
+    for j in range(3):  # node j of each attachment
+        sel = j < nn
+        for a in range(3):
+            rows.append(3 * ii[sel] + a)
+            cols.append(3 * cols_node[sel, j] + a)
+            vals.append(sign[sel] * w[ii[sel], ss[sel], j])
+    rows = np.concatenate(rows) if rows else np.zeros(0, np.int64)
+    cols = np.concatenate(cols) if cols else np.zeros(0, np.int64)
+    vals = np.concatenate(vals) if vals else np.zeros(0)
+    S = sp.coo_matrix((vals, (rows, cols)), shape=(3 * m, n_dofs)).tocsr()
+    if fixed_mask is not None and np.asarray(fixed_mask).any():
+        S = (S @ sp.diags(np.where(fixed_mask, 0.0, 1.0))).tocsr()
+    S.sort_indices()
+    return SignedMapping(S, ii.astype(np.int64), np.where(ss == 0, 1, -1).astype(np.int8))
 
 
 def assemble_H(D: DirectionMatrix, G) -> sp.csr_matrix:
