@@ -41,3 +41,13 @@ def empty(shape, dev=None, dtype=torch.float64) -> torch.Tensor:
 
 def zeros(shape, dev=None, dtype=torch.float64) -> torch.Tensor:
     return torch.zeros(shape, dtype=dtype, device=dev or device())
+
+
+def upload(a, dtype=None) -> torch.Tensor:
+    """Host array -> device tensor without a stream synchronisation: staged through
+    pinned memory and copied asynchronously on the current stream (the caching
+    host allocator keeps the staging block alive until the copy has run)."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.pin_memory().to(device(), non_blocking=True)

@@ -415,6 +415,7 @@ static void chol_free(CholHandle* h) {
   h->plan1.release();
   h->plan8.release();
   for (GrowBuf* b : {&h->bp, &h->tbuf, &h->c_int, &h->c_rhs, &h->c_val, &h->c_y}) b->release();
+  h->c_pin.release();
 }
 
 static std::map<std::string, std::pair<const void*, size_t>> export_table(const CholHandle* h) {

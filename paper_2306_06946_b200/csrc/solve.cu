@@ -743,12 +743,19 @@ int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_
   if ((rc = h->c_val.ensure(std::max<size_t>(1, P.sc_val.size()) * sizeof(double)))) return rc;
   char* base = (char*)h->c_int.p;
   int64_t* d64 = (int64_t*)base;
-  int32_t* d32 = (int32_t*)(base + ((bytes64 + 15) & ~(size_t)15));
-  CNB_CUDA(cudaMemcpyAsync(d64, ints.data(), bytes64, cudaMemcpyHostToDevice, st));
-  if (bytes32) CNB_CUDA(cudaMemcpyAsync(d32, i32.data(), bytes32, cudaMemcpyHostToDevice, st));
-  if (!P.sc_val.empty())
-    CNB_CUDA(cudaMemcpyAsync(h->c_val.p, P.sc_val.data(), P.sc_val.size() * sizeof(double), cudaMemcpyHostToDevice,
-                             st));
+  const size_t off32 = (bytes64 + 15) & ~(size_t)15;
+  int32_t* d32 = (int32_t*)(base + off32);
+  // stage through pinned memory: the uploads stay asynchronous (no stream sync)
+  const size_t vbytes = P.sc_val.size() * sizeof(double);
+  const size_t offv = (off32 + bytes32 + 15) & ~(size_t)15;
+  if ((rc = h->c_pin.ensure(offv + vbytes + 16))) return rc;
+  char* pin = (char*)h->c_pin.p;
+  memcpy(pin, ints.data(), bytes64);
+  if (bytes32) memcpy(pin + off32, i32.data(), bytes32);
+  if (vbytes) memcpy(pin + offv, P.sc_val.data(), vbytes);
+  CNB_CUDA(cudaMemcpyAsync(base, pin, off32 + bytes32, cudaMemcpyHostToDevice, st));
+  if (vbytes) CNB_CUDA(cudaMemcpyAsync(h->c_val.p, pin + offv, vbytes, cudaMemcpyHostToDevice, st));
+  if ((rc = h->c_pin.mark(st))) return rc;
   double* rhs = (double*)h->c_rhs.p;
   double* Y = (double*)h->c_y.p;
   CNB_CUDA(cudaMemsetAsync(rhs, 0, std::max<int64_t>(1, P.roff[S.ns]) * sizeof(double), st));

@@ -74,8 +74,8 @@ def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, sha
             rix = np.repeat(np.arange(3 * mo), per_row)
             ell_col[rix, slot] = inv
             ell_val[rix, slot] = vals
-            d_col = torch.as_tensor(ell_col, device=d)
-            d_val = torch.as_tensor(ell_val, device=d)
+            d_col = dv.upload(ell_col)
+            d_val = dv.upload(ell_val)
             _lib.call("cnb_sandwich", 3 * mo, k, d_col.data_ptr(), d_val.data_ptr(), C.data_ptr(), k, U.data_ptr(),
                       3 * mo, _lib.stream())
         else:
@@ -86,5 +86,4 @@ def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, sha
         if stats is not None:
             stats["fwd_flops"] = stats.get("fwd_flops", 0.0) + fl[0]
             stats["gram_flops"] = stats.get("gram_flops", 0.0) + fl[1]
-    return ObjectCompliance(U=U, idx=torch.as_tensor(idx, device=d), side=torch.as_tensor(side, device=d),
-                            full=full)
+    return ObjectCompliance(U=U, idx=dv.upload(idx), side=dv.upload(side), full=full)

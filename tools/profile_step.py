@@ -1,4 +1,5 @@
-"""Run the cfg1 bench workload for a few steps (for ncu launch lists / captures)."""
+"""Run the default bench workload (cfg3 Simulation.step) for a few steps, for ncu
+launch lists and captures:  python tools/profile_step.py [steps] [cfg3|cfg1]."""
 import os
 import sys
 
@@ -7,8 +8,9 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 
-steps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-wl = bench.GpuWorkload(bench.make_inputs())
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+which = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
+wl = bench.Cfg3Workload() if which == "cfg3" else bench.GpuWorkload(bench.make_inputs())
 for _ in range(steps):
     wl.step()
 torch.cuda.synchronize()
