@@ -525,7 +525,7 @@ def run_gpu_cfg3(args, rank, world):
     ach = sweeps * bytes_sweep / pgs_s / 1e9
     roof = {"kernel": "pgs_pipe_kernel (exact-order projected Gauss-Seidel, dense W, lookahead-2 pipeline)", "bound": "hbm",
             "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
-            "traffic": None, "peak_source": src, "algorithmic_bytes_per_sweep": bytes_sweep, "sweeps_per_step": sweeps,
+            "traffic": pgs_ncu_traffic_per_sweep(), "traffic_unit": "bytes per sweep (ncu --set full dram read+write)", "peak_source": src, "algorithmic_bytes_per_sweep": bytes_sweep, "sweeps_per_step": sweeps,
             "ms_per_sweep": round(pgs_s * 1e3 / max(sweeps, 1), 4)}
     dmma = dmma_peak_tflops(torch, _lib)
     others = wl.kernel_rooflines(dmma, peaks["hbm_gbs"], reps[-1])
@@ -555,6 +555,25 @@ def run_gpu_cfg3(args, rank, world):
         "clocks": clk.summary(int(os.environ.get("LOCAL_RANK", 0))),
     }
     return line
+
+
+def pgs_ncu_traffic_per_sweep():
+    """dram__bytes_read + dram__bytes_write of one pgs_pipe_kernel launch from the
+    committed ncu --set full capture (profiles/), per W pass (30 sweeps + the
+    delta_end pass at G = 7500, the cfg3 size)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_pgs_pipe_kernel.txt")
+    try:
+        vals = {}
+        for line in open(path):
+            if " = " in line and "[" in line:
+                k, rest = line.split(" [", 1)
+                unit, v = rest.split("] = ")
+                scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, None)
+                if scale:
+                    vals[k] = float(v) * scale
+        return round((vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) / 31.0, 0)
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def roofline(args, wl, torch, _lib, phases):
