@@ -146,6 +146,11 @@ int64_t cnb_pgs_work_bytes(int64_t groups);
  * listed at the stamp() calls of each kernel in csrc/pgs.cu. */
 int cnb_pgs_profile(double* out);
 
+/* Diagnostic: cycles per group of the PGS block solve while the other warps of
+ * the CTA generate load of kind `mode` (0 idle, 1 LDS, 2 SHFL, 3 global polls,
+ * 4 bulk copies into shared memory, 5 fp64 FMA). out[0] = cycles / group. */
+int cnb_bench_contention(int32_t mode, int32_t reps, double* out, void* stream);
+
 /* Cycles per group of the sequential warp block solve of the PGS kernels on a
  * resident synthetic tile (diagnostic microbenchmark; variant selects the
  * update / projection form), out[0] cycles per group, out[1] checksum. */

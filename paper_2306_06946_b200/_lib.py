@@ -41,6 +41,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_pgs_work_bytes": [I64],
     "cnb_pgs_profile": [P],
     "cnb_bench_block_solve": [I32, I32, P, P],
+    "cnb_bench_contention": [I32, I32, P, P],
     "cnb_pgs": [I64, P, I64, P, F64, F64, F64, I32, P, P, P, P, P, P, P],
     "cnb_local_solve": [I64, I64, P, I64, P, P, F64, F64, P, P, P],
     "cnb_gemm_naive": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, P],

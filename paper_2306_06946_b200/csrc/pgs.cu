@@ -1937,6 +1937,104 @@ __global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double*
   }
 }
 
+// Contention experiment (diagnostic): warp 0 runs block_solve_v4 on a
+// 26-group tile (stride 78) while the other warps (except 4, 8, 12, as in
+// pgs_pipe_kernel) generate one kind of load: 0 idle, 1 shared-memory loads,
+// 2 shuffles, 3 global polling loads, 4 bulk copies into shared memory,
+// 5 fp64 FMA chains.  out[0] = solver cycles per group.
+template <int MODE>
+__global__ void __launch_bounds__(512) bench_contention_kernel(int reps, const double* gsrc, double* out) {
+  extern __shared__ __align__(128) double csm[];
+  double* T = csm;                     // 78 x 78 tile
+  double* sv = csm + kPR * kPR;        // 4 * 26 records
+  double* buf = sv + 4 * kPG;          // noise buffer (48 KB)
+  unsigned long long* bar = (unsigned long long*)(buf + 6144);
+  volatile int* done = (volatile int*)(bar + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < kPR * kPR; e += blockDim.x) {
+    const int i = e / kPR, j = e % kPR;
+    T[e] = (i == j) ? 4.0 : 0.05 * sin(0.37 * i + 0.91 * j + 0.13 * i * j) / (1.0 + fabs((double)(i - j)));
+  }
+  for (int e = tid; e < 6144; e += blockDim.x) buf[e] = 1.0 + 1e-3 * e;
+  if (tid == 0) {
+    *done = 0;
+    mbar_init(bar, 1);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const double h2 = 1e-4;
+    double Wd[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) Wd[3 * a + b] = T[(3 * lane + a) * kPR + 3 * lane + b];
+    GroupConst kc;
+    group_const(Wd, h2, kc);
+    double lm[3] = {0.0, 0.0, 0.0}, dl_[3], dsq = 0.0;
+    int err = 0;
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      dl_[0] = -1e-4 * (1.0 + 0.01 * lane);
+      dl_[1] = 3e-4 * sin(1.0 * lane);
+      dl_[2] = 3e-4 * cos(1.0 * lane);
+      block_solve_v4<true>(T, kPR, kPG, lane, dl_, lm, kc, 0.4, h2, sv);
+      __syncwarp();
+      err |= block_commit(sv, lane, lm, kc, 0.4, 1.0 / h2, dsq);
+    }
+    const long long t1 = clock64();
+    const double sres = warp_sum(lm[0] + lm[1] + lm[2] + dsq);
+    if (lane == 0) {
+      out[0] = (double)(t1 - t0) / ((double)reps * kPG);
+      out[1] = sres + err;
+      *done = 1;
+    }
+  } else if ((warp & 3) != 0) {
+    double acc = 0.0;
+    unsigned phase = 0;
+    while (!*done) {
+      if (MODE == 1) {
+        for (int k = 0; k < 64; ++k) acc += T[((warp * 7 + k) % kPR) * kPR + lane + (k & 1) * 32];
+      } else if (MODE == 2) {
+        for (int k = 0; k < 16; ++k) acc = warp_sum(acc + k);
+      } else if (MODE == 3) {
+        unsigned v;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gsrc) : "memory");
+        acc += v;
+        __nanosleep(64);
+      } else if (MODE == 4) {
+        if (warp == 2 && lane == 0) {
+          mbar_arrive_expect_tx(bar, 3 * 16384);
+          for (int q = 0; q < 3; ++q) bulk_g2s(buf + q * 2048, gsrc + q * 2048, 16384, bar);
+          while (!mbar_try_wait(bar, phase)) {
+          }
+          phase ^= 1;
+        }
+      } else if (MODE == 5) {
+        for (int k = 0; k < 64; ++k) acc = fma(acc, 0.999999, 1e-9);
+      } else {
+        __nanosleep(200);
+      }
+    }
+    if (acc == 12345.678) out[1] = acc;
+  }
+}
+
+static int launch_contention(int mode, int reps, const double* g, double* d, cudaStream_t st) {
+  const int sm = (int)(sizeof(double) * (kPR * kPR + 4 * kPG + 6144) + 64);
+#define CNB_CONT(M)                                                                                      \
+  CNB_CUDA(cudaFuncSetAttribute(bench_contention_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+  bench_contention_kernel<M><<<1, 512, sm, st>>>(reps, g, d);
+  switch (mode) {
+    case 0: CNB_CONT(0) break;
+    case 1: CNB_CONT(1) break;
+    case 2: CNB_CONT(2) break;
+    case 3: CNB_CONT(3) break;
+    case 4: CNB_CONT(4) break;
+    default: CNB_CONT(5) break;
+  }
+#undef CNB_CONT
+  CNB_LAUNCH_CHECK("bench_contention_kernel");
+  return CNB_OK;
+}
+
 // CNB_PGS_PROFILE=1: per-phase nanosecond sums of the grid kernel (device
 // buffer, read back with cnb_pgs_profile)
 static unsigned long long* pgs_profile_buffer() {
@@ -2106,6 +2204,26 @@ int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stre
   CNB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
   CNB_CUDA(cudaStreamSynchronize(st));
   cudaFree(d);
+  out[0] = h[0];
+  out[1] = h[1];
+  return CNB_OK;
+}
+
+// Solver-warp cycles per group under one kind of concurrent load in the same
+// CTA (diagnostic, see bench_contention_kernel).  out[0] = cycles / group.
+int cnb_bench_contention(int32_t mode, int32_t reps, double* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  double *d = nullptr, *g = nullptr;
+  CNB_CUDA(cudaMalloc(&d, 2 * sizeof(double)));
+  CNB_CUDA(cudaMalloc(&g, 8192 * sizeof(double)));
+  CNB_CUDA(cudaMemsetAsync(g, 0, 8192 * sizeof(double), st));
+  int rc = launch_contention(mode, reps, g, d, st);
+  if (rc) return rc;
+  double h[2];
+  CNB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CNB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d);
+  cudaFree(g);
   out[0] = h[0];
   out[1] = h[1];
   return CNB_OK;

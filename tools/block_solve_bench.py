@@ -20,3 +20,9 @@ for v, name in enumerate(names):
     _lib.call("cnb_bench_block_solve", v, 2000, out, _lib.stream())
     res[name] = round(out[0], 1)
 print(json.dumps({"cycles_per_group": res}))
+cont = {}
+for mode, name in enumerate(["idle", "lds", "shfl", "global-poll", "bulk-copy", "dfma"]):
+    _lib.call("cnb_bench_contention", mode, 50, out, _lib.stream())
+    _lib.call("cnb_bench_contention", mode, 2000, out, _lib.stream())
+    cont[name] = round(out[0], 1)
+print(json.dumps({"cycles_per_group_under_load": cont}))
