@@ -33,6 +33,10 @@ __global__ void scatter_kernel(int64_t nmap, const int64_t* __restrict__ src, co
 // extend-add: task = (parent p, parent col range [lo, hi)).  For every child
 // c of p (ascending) and every child update column k whose parent column
 // rel[k] lies in [lo, hi): F_p[rel[i], rel[k]] += U_c[i, k], i >= k.
+// Rows are processed in batches of kEaBatch per thread: all loads of a batch
+// are issued before its stores (the parent and child fronts live in one
+// buffer, so the compiler could not reorder them otherwise).
+constexpr int kEaBatch = 8;
 __global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                          double* __restrict__ front) {
   const int32_t p = tasks[3 * blockIdx.x], lo = tasks[3 * blockIdx.x + 1], hi = tasks[3 * blockIdx.x + 2];
@@ -41,7 +45,7 @@ __global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t
   for (int64_t ci = S.child_ptr[p]; ci < S.child_ptr[p + 1]; ++ci) {
     const int64_t c = S.child[ci];
     const int64_t ncc = d_nc(S, c), nrc = d_nr(S, c), fc = ncc + nrc;
-    const int32_t* rel = S.rel + S.rel_ptr[c];
+    const int32_t* __restrict__ rel = S.rel + S.rel_ptr[c];
     int64_t a = 0, b = nrc;
     while (a < b) {
       int64_t m = (a + b) >> 1;
@@ -56,16 +60,31 @@ __global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t
     const int64_t k1 = a;
     const double* Fc = front + S.front_off[c];
     for (int64_t k = k0; k < k1; ++k) {
-      const double* uc = Fc + (ncc + k) * fc + ncc;
+      const double* __restrict__ uc = Fc + (ncc + k) * fc + ncc;
       double* fcol = Fp + (int64_t)rel[k] * fp;
-      for (int64_t i = k + threadIdx.x; i < nrc; i += blockDim.x) fcol[rel[i]] += uc[i];
+      for (int64_t i0 = k + threadIdx.x; i0 < nrc; i0 += (int64_t)kEaBatch * blockDim.x) {
+        int32_t ri[kEaBatch];
+        double u[kEaBatch], v[kEaBatch];
+#pragma unroll
+        for (int q = 0; q < kEaBatch; ++q) {
+          const int64_t i = i0 + (int64_t)q * blockDim.x;
+          ri[q] = i < nrc ? __ldg(rel + i) : -1;
+          u[q] = i < nrc ? uc[i] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < kEaBatch; ++q) v[q] = ri[q] >= 0 ? fcol[ri[q]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kEaBatch; ++q)
+          if (ri[q] >= 0) fcol[ri[q]] = v[q] + u[q];
+      }
     }
     __syncthreads();
   }
 }
 
 // POTRF of the kw x kw diagonal block of panel k0 and the inverse of the
-// resulting L_kk (kept in kkinv[s], 32 x 32 row-major, for the TRSM, which
+// resulting L_kk (kept in kkinv slot kk_off[s] + panel, 32 x 32 row-major, for
+// the TRSM and the inversion of L11 (solve.cu trinv_kernel); the TRSM
 // then is a plain DMMA product).  One CTA per front, one thread per block
 // entry (32 x 32 = 1024 threads): every elimination step is a single
 // parallel update between barriers, and the code stays a compact loop
@@ -134,7 +153,7 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
     y[r][c] = c <= r ? ((v0 + v1) + (v2 + v3)) * rdiag[r] : 0.0;
     __syncwarp();
   }
-  double* Y = kkinv + s * (kPanel * kPanel);
+  double* Y = kkinv + (S.kk_off[s] + k0 / kPanel) * (kPanel * kPanel);  // kept for the TRSM and L11^{-1}
   for (int r = 0; r < kPanel; ++r) Y[r * kPanel + c] = y[r][c];
 }
 
@@ -156,7 +175,7 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
     const int64_t r = r0 + rr;
     cp_async8(&As[rr * LD + k], F + (int64_t)(k0 + k) * f + r, r < f && k < kw);
   }
-  const double* Y = kkinv + s * (kPanel * kPanel);
+  const double* Y = kkinv + (S.kk_off[s] + k0 / kPanel) * (kPanel * kPanel);
   for (int e = threadIdx.x; e < kPanel * kPanel; e += blockDim.x)
     cp_async8(&Is[(e / kPanel) * LD + (e % kPanel)], Y + e, true);
   cp_async_wait_all();
@@ -395,7 +414,10 @@ static int chol_upload(CholHandle* h) {
   CNB_CUDA(cudaMalloc((void**)&h->d_front, std::max<int64_t>(1, S.front_off[S.ns]) * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_linv, std::max<int64_t>(1, h->linv_off[S.ns]) * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_p21, std::max<int64_t>(1, h->p21_off[S.ns]) * sizeof(double)));
-  CNB_CUDA(cudaMalloc((void**)&h->d_kkinv, std::max<int64_t>(1, S.ns) * kPanel * kPanel * sizeof(double)));
+  h->kk_off.assign(S.ns + 1, 0);
+  for (int64_t s = 0; s < S.ns; ++s) h->kk_off[s + 1] = h->kk_off[s] + (S.nc(s) + kPanel - 1) / kPanel;
+  if ((rc = upload_vec(&h->d_kk_off, h->kk_off)) != CNB_OK) return rc;
+  CNB_CUDA(cudaMalloc((void**)&h->d_kkinv, std::max<int64_t>(1, h->kk_off[S.ns]) * kPanel * kPanel * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_vals, std::max<int64_t>(1, S.csr_nnz) * sizeof(double)));
   CNB_CUDA(cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem));
   h->uploaded = true;
@@ -405,7 +427,7 @@ static int chol_upload(CholHandle* h) {
 static void chol_free(CholHandle* h) {
   void* ptrs[] = {h->d_first, h->d_rows_ptr, h->d_rows, h->d_front_off, h->d_child_ptr, h->d_child,
                   h->d_rel_ptr, h->d_rel, h->d_map_src, h->d_map_dst, h->d_perm, h->d_front, h->d_tasks,
-                  h->d_linv, h->d_linv_off, h->d_p21, h->d_p21_off, h->d_kkinv, h->d_vals};
+                  h->d_linv, h->d_linv_off, h->d_p21, h->d_p21_off, h->d_kkinv, h->d_vals, h->d_kk_off};
   if (h->factor_exec) cudaGraphExecDestroy(h->factor_exec);
   h->factor_exec = nullptr;
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);

@@ -21,7 +21,7 @@ constexpr int kPanel = 32;   // pivot panel width of the dense front factorisati
 constexpr int kBlkPanels = 4;  // panels per trailing-update block: the trailing matrix is
                                // updated once per kBlkPanels * kPanel = 128 columns (K = 128)
 constexpr int kTile = 64;    // SYRK / GEMM output tile
-constexpr int kEaCols = 32;  // parent columns per extend-add task
+constexpr int kEaCols = 8;   // parent columns per extend-add task (small: more CTAs in flight)
 constexpr int kInvCols = 8;  // columns of L11^{-1} per inversion task
 constexpr int kMaxSnCols = 512;  // widest supernode (wider ones are split into chains)
 

@@ -21,6 +21,7 @@ struct DevSym {
   const int32_t* rel;
   const int64_t* linv_off;  // offsets of the inverted diagonal blocks L11^{-1}
   const int64_t* p21_off;   // offsets of P21 = L21 L11^{-1} (nr x nc, column-major)
+  const int64_t* kk_off;    // first 32x32 diagonal-block inverse of each supernode (kkinv slots)
 };
 
 __device__ __forceinline__ int64_t d_nc(const DevSym& S, int64_t s) { return S.first[s + 1] - S.first[s]; }
@@ -121,7 +122,9 @@ struct CholHandle {
   double* d_front = nullptr;
   double* d_linv = nullptr;
   double* d_p21 = nullptr;
-  double* d_kkinv = nullptr;  // per supernode: inverse of the current 32x32 panel diagonal block
+  double* d_kkinv = nullptr;  // inverse of every 32x32 panel diagonal block (slot kk_off[s] + panel)
+  int64_t* d_kk_off = nullptr;
+  std::vector<int64_t> kk_off;
   double* d_vals = nullptr;   // CSR values being factorised (fixed address for the graph)
   cudaGraphExec_t factor_exec = nullptr;
   cudaStream_t cap_stream = nullptr;
@@ -139,7 +142,7 @@ struct CholHandle {
 
   DevSym sym() const {
     return DevSym{d_first,   d_rows_ptr, d_rows, d_front_off, d_child_ptr,
-                  d_child,   d_rel_ptr,  d_rel,  d_linv_off,  d_p21_off};
+                  d_child,   d_rel_ptr,  d_rel,  d_linv_off,  d_p21_off, d_kk_off};
   }
 };
 

@@ -46,9 +46,15 @@ __device__ __forceinline__ double panel_entry(const double* __restrict__ P, cons
 }
 
 // ---- L11^{-1}, kInvCols columns per task -----------------------------------------
+// Block forward substitution L11 X = I over 32-row blocks: the diagonal block
+// of block kb is inverted already (D_kb, kept by potrf_kernel), so each block
+// step is y = D_kb v (a small product, no sequential row loop) followed by the
+// update of the rows below with the panel columns of L.
 __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                    const double* __restrict__ front, double* __restrict__ linv) {
-  __shared__ double sL[32][33];
+                                                    const double* __restrict__ front, const double* __restrict__ kkinv,
+                                                    double* __restrict__ linv) {
+  __shared__ double sD[32][33];
+  __shared__ double v[32][kInvCols];
   __shared__ double y[32][kInvCols];
   const int64_t s = tasks[2 * blockIdx.x], j0 = tasks[2 * blockIdx.x + 1];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
@@ -60,33 +66,26 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
     X[(j0 + c) * nc + i] = (i == j0 + c) ? 1.0 : 0.0;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = threadIdx.x & 31, cc = threadIdx.x >> 5;  // (row, column) of the 32 x kInvCols block
   for (int64_t kb = (j0 / 32) * 32; kb < nc; kb += 32) {
     const int bw = (int)min((int64_t)32, nc - kb);
+    const double* D = kkinv + (S.kk_off[s] + kb / 32) * (32 * 32);
     for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
-      const int i = e & 31, j = e >> 5;
-      cp_async8(&sL[i][j], F + (kb + j) * f + kb + i, i < bw && j < bw && i >= j);
+      const int a = e >> 5, b = e & 31;
+      sD[a][b] = (a < bw && b <= a) ? D[e] : 0.0;
     }
-    cp_async_wait_all();
+    if (cc < kInvCols) v[r][cc] = (r < bw && cc < ncols) ? X[(j0 + cc) * nc + kb + r] : 0.0;
     __syncthreads();
-    if (warp == 0) {
-      double v[kInvCols];
-#pragma unroll
-      for (int c = 0; c < kInvCols; ++c) v[c] = (lane < bw && c < ncols) ? X[(j0 + c) * nc + kb + lane] : 0.0;
-      for (int j = 0; j < bw; ++j) {
-        const double rjj = 1.0 / sL[j][j], lij = sL[lane][j];
-#pragma unroll
-        for (int c = 0; c < kInvCols; ++c) {
-          if (lane == j) v[c] *= rjj;
-          const double yj = __shfl_sync(0xffffffffu, v[c], j);
-          if (lane > j) v[c] = fma(-lij, yj, v[c]);
-        }
+    if (cc < kInvCols) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int k = 0; k + 1 <= r; k += 2) {
+        a0 = fma(sD[r][k], v[k][cc], a0);
+        a1 = fma(sD[r][k + 1], v[k + 1][cc], a1);
       }
-#pragma unroll
-      for (int c = 0; c < kInvCols; ++c) {
-        y[lane][c] = lane < bw ? v[c] : 0.0;
-        if (lane < bw && c < ncols) X[(j0 + c) * nc + kb + lane] = v[c];
-      }
+      if ((r & 1) == 0) a0 = fma(sD[r][r], v[r][cc], a0);
+      const double yv = a0 + a1;
+      y[r][cc] = r < bw ? yv : 0.0;
+      if (r < bw && cc < ncols) X[(j0 + cc) * nc + kb + r] = yv;
     }
     __syncthreads();
     for (int64_t i = kb + bw + threadIdx.x; i < nc; i += blockDim.x) {
@@ -409,7 +408,7 @@ __global__ void permute_kernel(int64_t n, int64_t k, const int64_t* __restrict__
 int trinv_level(CholHandle* h, int level, cudaStream_t st) {
   const DevTasks& T = h->trinv[level];
   if (!T.count) return CNB_OK;
-  trinv_kernel<<<(unsigned)T.count, 256, 0, st>>>(h->sym(), T.ptr, h->d_front, h->d_linv);
+  trinv_kernel<<<(unsigned)T.count, 256, 0, st>>>(h->sym(), T.ptr, h->d_front, h->d_kkinv, h->d_linv);
   CNB_LAUNCH_CHECK("trinv_kernel");
   const DevTasks& P = h->p21[level];
   if (P.count) {
