@@ -53,6 +53,50 @@ typedef struct cnb_status {
 int cnb_abi_version(void);
 const char* cnb_last_error(void);
 
+/* ---- batched independent scenes (BASELINE configs[4]) ------------------- */
+/* Copies of one soft body (shared mesh, linear material, one factorisation) on
+ * their own planes.  Q: scene states (ns rows, pitch ldq); all other arrays are
+ * device arrays over the concatenated pairs / packed per-scene matrices, with
+ * exclusive prefix offsets poff (pairs), boff (3x3 blocks, m_s^2), woff
+ * (doubles, (3 m_s)^2).  Replace, per copy: vertex-plane detection
+ * (collision.py:264-287), W_g (constraints.py:155-179, as a gather from the
+ * compliance C = E^T A^-1 E of the candidate surface DoFs), rebuild_W_fast
+ * (constraints.py:182-191, bit-exact order), fast_update_proximity
+ * (constraints.py:217-244), the backward-Euler right-hand side
+ * (dynamics.py:183-211) and S^T acc (solver.py:250-257). */
+int cnb_batch_detect_planes(int32_t ns, int64_t nsurf, const int64_t* vids, const double* Q, int64_t ldq,
+                            const double* normals, const double* offsets, double threshold, int32_t* count,
+                            int32_t* kept, void* stream);
+int cnb_batch_pairs(int32_t ns, int64_t m, int64_t nsurf, const int64_t* poff, const int32_t* kept,
+                    const int64_t* vids, const double* Q, int64_t ldq, const double* normals, const double* offsets,
+                    int32_t* pscene, int32_t* pcand, double* pa, double* pb, double* ref, double* sdist,
+                    void* stream);
+int cnb_batch_gather_pa(int64_t m, const int32_t* pscene, const int32_t* pcand, const int64_t* vids, const double* Q,
+                        int64_t ldq, double* pa, void* stream);
+int cnb_batch_wg_gather(int32_t ns, int64_t nblocks, const int64_t* boff, const int64_t* poff, const int64_t* woff,
+                        const int32_t* pcand, const int64_t* vids, const double* C, int64_t ldc, double* Wg,
+                        void* stream);
+/* C = A B (row-major fp64, DMMA tiles): the batched scenes' multi-RHS solves
+ * against the shared inverse of A (formed once from the sparse factor). */
+int cnb_gemm_dense(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                   double* C, int64_t ldc, void* stream);
+int cnb_batch_rebuild_w(int32_t ns, int64_t nblocks, const int64_t* boff, const int64_t* poff, const int64_t* woff,
+                        const double* D, const double* Wg, double* W, void* stream);
+int cnb_batch_prox(int32_t ns, int64_t m, const int64_t* poff, const int64_t* woff, const double* Wg, const double* t,
+                   double h, double* pa, void* stream);
+int cnb_batch_spmv(int32_t ns, int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+                   const double* x, int64_t ldx, double* y, int64_t ldy, void* stream);
+int cnb_batch_rhs(int32_t ns, int64_t n, const double* fel, const double* Kv, const double* m3, const double* v,
+                  const double* fext, const int8_t* fixed, double h, double alpha, double beta, double* b,
+                  cnb_status_t* d_status, void* stream);
+int cnb_batch_scatter_acc(int64_t m, const int32_t* pscene, const int32_t* pcand, const int64_t* vids,
+                          const double* acc, double* rhs, int64_t ldr, void* stream);
+/* PGS of independent scenes, one CTA each (solver.py:168-202 per scene);
+ * g_off / w_off / mu are HOST arrays (nscenes + 1 / nscenes / nscenes). */
+int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off, const double* mu, const double* W,
+                    const double* delta_base, double h, double tol, int32_t max_iter, double* lam, double* delta_end,
+                    double* eps_hist, int32_t* iters_conv, cnb_status_t* d_status, void* stream);
+
 /* ---- constraint-space operators (contactnewton/constraints.py) ---------- */
 
 /* W = D Wg D^T, D block-diagonal (groups x 3 x 3, rows n,t1,t2).

@@ -29,6 +29,17 @@ _SIGNATURES: dict[str, list] = {
     "cnb_last_error": [],
     "cnb_rebuild_w": [I64, P, P, I64, P, I64, P],
     "cnb_sandwich": [I64, I64, P, P, P, I64, P, I64, P],
+    "cnb_batch_detect_planes": [I32, I64, P, P, I64, P, P, F64, P, P, P],
+    "cnb_batch_pairs": [I32, I64, I64, P, P, P, P, I64, P, P, P, P, P, P, P, P, P],
+    "cnb_batch_gather_pa": [I64, P, P, P, P, I64, P, P],
+    "cnb_batch_wg_gather": [I32, I64, P, P, P, P, P, P, I64, P, P],
+    "cnb_gemm_dense": [I64, I64, I64, P, I64, P, I64, P, I64, P],
+    "cnb_batch_rebuild_w": [I32, I64, P, P, P, P, P, P, P],
+    "cnb_batch_prox": [I32, I64, P, P, P, P, F64, P, P],
+    "cnb_batch_spmv": [I32, I64, P, P, P, P, I64, P, I64, P],
+    "cnb_batch_rhs": [I32, I64, P, P, P, P, P, P, F64, F64, F64, P, P, P],
+    "cnb_batch_scatter_acc": [I64, P, P, P, P, P, I64, P],
+    "cnb_pgs_batched": [I32, P, P, P, P, P, F64, F64, I32, P, P, P, P, P, P],
     "cnb_violation": [I64, P, P, P, P, P],
     "cnb_apply_dt": [I64, P, P, P, P, P],
     "cnb_prox_update": [I64, P, I64, P, P, P, F64, P, P, P],

@@ -49,41 +49,6 @@ struct GrowBuf {
   }
 };
 
-// Pinned host staging for per-call uploads: cudaMemcpyAsync from pageable
-// memory synchronises the stream first, which would serialise the host-side
-// planning of one object with the GPU work of the previous one.  `ready`
-// guards reuse: the previous upload from this buffer must have executed.
-struct PinnedBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  cudaEvent_t ready = nullptr;
-  int ensure(size_t bytes) {
-    if (ready) CNB_CUDA(cudaEventSynchronize(ready));
-    if (bytes <= cap) return CNB_OK;
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    cap = 0;
-    CNB_CUDA(cudaMallocHost(&p, std::max<size_t>(bytes, 4096)));
-    cap = std::max<size_t>(bytes, 4096);
-    return CNB_OK;
-  }
-  int mark(cudaStream_t st) {
-    if (!ready) CNB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    CNB_CUDA(cudaEventRecord(ready, st));
-    return CNB_OK;
-  }
-  void release() {
-    if (ready) {
-      cudaEventSynchronize(ready);
-      cudaEventDestroy(ready);
-    }
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    ready = nullptr;
-    cap = 0;
-  }
-};
-
 template <typename T>
 inline int upload_vec(T** dptr, const std::vector<T>& v) {
   size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);

@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <algorithm>
 #include <string>
 
 #include "../../include/cn_b200.h"
@@ -144,6 +146,41 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+
+// Pinned host staging for per-call uploads: cudaMemcpyAsync from pageable
+// memory synchronises the stream first, which would serialise the host-side
+// planning of one object with the GPU work of the previous one.  `ready`
+// guards reuse: the previous upload from this buffer must have executed.
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ready = nullptr;
+  int ensure(size_t bytes) {
+    if (ready) CNB_CUDA(cudaEventSynchronize(ready));
+    if (bytes <= cap) return CNB_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    CNB_CUDA(cudaMallocHost(&p, std::max<size_t>(bytes, 4096)));
+    cap = std::max<size_t>(bytes, 4096);
+    return CNB_OK;
+  }
+  int mark(cudaStream_t st) {
+    if (!ready) CNB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CNB_CUDA(cudaEventRecord(ready, st));
+    return CNB_OK;
+  }
+  void release() {
+    if (ready) {
+      cudaEventSynchronize(ready);
+      cudaEventDestroy(ready);
+    }
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    ready = nullptr;
+    cap = 0;
+  }
+};
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -2281,6 +2281,63 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
   return CNB_OK;
 }
 
+// Independent scenes (BASELINE configs[4]): one CTA per scene runs pgs_cta on
+// its own W (packed at w_off[s], c_s x c_s), violation, lambda and outputs at
+// the scene's group offset g_off[s].  Host arrays describe the scenes.
+int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off, const double* mu, const double* W,
+                    const double* delta_base, double h, double tol, int32_t max_iter, double* lam, double* delta_end,
+                    double* eps_hist, int32_t* iters_conv, cnb_status_t* d_status, void* stream) {
+  if (nscenes <= 0) return CNB_OK;
+  if (max_iter < 1) {
+    set_error("pgs_batched: max_iter must be positive");
+    return CNB_E_VALIDATION;
+  }
+  static PgsScene* d_sc = nullptr;
+  static size_t cap = 0;
+  static PinnedBuf pin;
+  const size_t bytes = sizeof(PgsScene) * (size_t)nscenes;
+  if (bytes > cap) {
+    if (d_sc) cudaFree(d_sc);
+    d_sc = nullptr;
+    CNB_CUDA(cudaMalloc(&d_sc, bytes));
+    cap = bytes;
+  }
+  int rc = pin.ensure(bytes);
+  if (rc) return rc;
+  PgsScene* hs = (PgsScene*)pin.p;
+  int64_t gmax = 0;
+  for (int i = 0; i < nscenes; ++i) {
+    const int64_t G = g_off[i + 1] - g_off[i];
+    gmax = std::max(gmax, G);
+    PgsScene& sc = hs[i];
+    sc.groups = G;
+    sc.W = W + w_off[i];
+    sc.ldw = 3 * G;
+    sc.delta_base = delta_base + 3 * g_off[i];
+    sc.h2 = h * h;
+    sc.mu = mu[i];
+    sc.tol = tol;
+    sc.max_iter = max_iter;
+    sc.lam = lam + 3 * g_off[i];
+    sc.delta_end = delta_end + 3 * g_off[i];
+    sc.eps_hist = eps_hist + (int64_t)i * max_iter;
+    sc.iters_conv = iters_conv + 2 * i;
+    sc.status = (DevStatus*)d_status;
+  }
+  const size_t smem = pgs_smem_bytes(std::max<int64_t>(gmax, 1));
+  if (smem > pgs_max_smem()) {
+    set_error("pgs_batched: %lld groups in one scene exceed the single-CTA kernel", (long long)gmax);
+    return CNB_E_VALIDATION;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  CNB_CUDA(cudaMemcpyAsync(d_sc, hs, bytes, cudaMemcpyHostToDevice, st));
+  if ((rc = pin.mark(st))) return rc;
+  CNB_CUDA(cudaFuncSetAttribute(pgs_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  pgs_batched_kernel<<<nscenes, kPgsThreads, smem, st>>>(d_sc);
+  CNB_LAUNCH_CHECK("pgs_batched_kernel");
+  return CNB_OK;
+}
+
 int cnb_local_solve(int64_t alpha, int64_t groups, const double* W, int64_t ldw, const double* delta_cur,
                     const double* lam, double mu, double h2, double* out, cnb_status_t* d_status,
                     void* stream) {
