@@ -557,6 +557,272 @@ def run_gpu_cfg3(args, rank, world):
     return line
 
 
+# ----------------------------------------------------------------------------
+# cfg4: batched independent scenes (BASELINE configs[4])
+# ----------------------------------------------------------------------------
+
+CFG4_COPIES = 1024
+CFG4_PREROLL = 12  # steps before the timed region: copies start 2 cm above their planes, contact from step ~7
+
+
+def cfg4_copy_range(rank, world, total=CFG4_COPIES):
+    per = (total + world - 1) // world
+    a = min(total, rank * per)
+    return a, min(total, a + per)
+
+
+class Cfg4Workload:
+    """1024 copies of the cfg0 beam, this rank's share."""
+
+    def __init__(self, rank, world, total=CFG4_COPIES):
+        import torch
+
+        from paper_2306_06946_b200.batch import BatchedPlaneScenes, cfg4_draws
+        from paper_2306_06946_b200.mesh import five_tet_grid
+
+        self.first, last = cfg4_copy_range(rank, world, total)
+        self.ns = last - self.first
+        self.mesh = five_tet_grid((20, 4, 4), 0.01)
+        tilts, mus, jit = cfg4_draws(self.first, self.ns, self.mesh.nodes.size)
+        self.B = BatchedPlaneScenes(self.mesh, tilts, mus, jit, threshold=0.005, clearance=0.02,
+                                    newton_iterations=5, pgs_tolerance=1e-10, pgs_max_iterations=1000)
+        n = self.B.n
+        self.q_host = torch.empty((self.ns, n), dtype=torch.float64).pin_memory()
+        self.v_host = torch.empty((self.ns, n), dtype=torch.float64).pin_memory()
+        self.pairs = 0
+
+    def step(self):
+        self.pairs = self.B.step()
+        return self.pairs
+
+    def snapshot(self):
+        self.q_host.copy_(self.B.Q)
+        self.v_host.copy_(self.B.V)
+
+    def step_e2e(self):
+        """Public API with host buffers: state uploaded from pinned memory, one time
+        step of every copy, the new state read back into the same host buffers (the
+        next step's input)."""
+        import torch
+
+        B = self.B
+        B.Q.copy_(self.q_host, non_blocking=True)
+        B.V.copy_(self.v_host, non_blocking=True)
+        self.pairs = B.step()
+        self.q_host.copy_(B.Q, non_blocking=True)
+        self.v_host.copy_(B.V, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    @property
+    def h2d_bytes(self):
+        return int(2 * self.q_host.numel() * 8)
+
+    @property
+    def d2h_bytes(self):
+        return int(2 * self.q_host.numel() * 8)
+
+
+def run_gpu_cfg4(args, rank, world):
+    import torch
+
+    from paper_2306_06946_b200 import _lib
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    wl = Cfg4Workload(rank, world)
+    for _ in range(max(CFG4_PREROLL - args.warmup, 0) + args.warmup):
+        wl.step()
+    wl.B.check()
+    wl.snapshot()  # state at the start of the timed region: e2e replays the same steps from it
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    pairs, iters = [], []
+    prof = _PgsBatchTimer(torch)
+    with ClockSampler() as clk:
+        torch.cuda.synchronize()
+        launches0 = _lib.lib().cnb_launch_count()
+        for i in range(args.steps):
+            starts[i].record()
+            with prof:
+                pairs.append(wl.step())
+            ends[i].record()
+        torch.cuda.synchronize()
+        launches = _lib.lib().cnb_launch_count() - launches0
+    wl.B.check()
+    sweeps = int(wl.B.last["iters"][:, 0].sum()) if wl.B.last else 0
+    if world > 1:
+        torch.distributed.barrier()
+    total_ms = sum(s_.elapsed_time(e_) for s_, e_ in zip(starts, ends))
+    # e2e: the same steps again from the snapshot, state round-tripping through host memory
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        wl.step_e2e()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    if world > 1:
+        t = torch.tensor([total_ms, e2e_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms, e2e_ms = float(t[0]), float(t[1])
+    ms_step = total_ms / args.steps
+    total = CFG4_COPIES
+    peaks, src = measured_peaks()
+    # dominant kernel: batched PGS, W of every copy read once per sweep (8 c_s^2 bytes)
+    P = wl.B.last["pairs"] if wl.B.last else None
+    it_h = wl.B.last["iters"].cpu().numpy() if wl.B.last else np.zeros((0, 2), dtype=np.int32)
+    cnt = P["cnt"] if P is not None else np.zeros(0)
+    pgs_bytes = float(sum(8.0 * (3 * c) ** 2 * int(k) for c, k in zip(cnt, it_h[:, 0])))
+    pgs_ms = prof.pgs_ms_last_iter()
+    ach = pgs_bytes / (pgs_ms * 1e-3) / 1e9 if pgs_ms > 0 else 0.0
+    roof = {"kernel": "pgs_copy_kernel (one CTA per copy, exact-order projected Gauss-Seidel, dense W)",
+            "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "peak_source": src,
+            "algorithmic_bytes_per_launch": pgs_bytes, "ms_per_launch": round(pgs_ms, 4),
+            "launch": "last Newton iteration of the last timed step"}
+    line = {
+        "metric": "scene-steps per second (cfg4: 1024 independent cfg0 beam copies, 5 corrective iterations)",
+        "value": round(total * args.steps / (total_ms * 1e-3), 1), "unit": "scene-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded per-copy tilt, mu, jitter: np.random.default_rng([4, i]))",
+        "config": {"workload": "cfg4: 1024 copies of the cfg0 beam (20x4x4-node 5-tet grid, 960 DoF, linear, "
+                               "E=5e3 nu=0.45), plane tilt U(0,20) deg, mu U(0.2,0.8), threshold 0.005, 5 forced "
+                               "fast-scheme iterations, PGS tol 1e-10 / 1000 sweeps",
+                   "copies": total, "copies_per_rank": wl.ns, "timed_steps": f"{CFG4_PREROLL}..{CFG4_PREROLL + args.steps - 1}",
+                   "parallelism": f"scene-parallel over {world} GPU(s), no data-path collective",
+                   "l2": "not flushed; per-step working set (W of all copies ~0.5 GB) exceeds L2"},
+        "contacts_per_copy_mean": round(float(np.mean(cnt)) if len(cnt) else 0.0, 1),
+        "contacts_total": int(pairs[-1]) if pairs else 0,
+        "pgs_sweeps_last_iter_max": int(it_h[:, 0].max()) if len(it_h) else 0,
+        "pgs_sweeps_last_iter_total": sweeps,
+        "phases_ms": prof.phases(),
+        "e2e": {"value": round(wl.ns * world / (e2e_ms * 1e-3), 1), "unit": "scene-steps/s",
+                "h2d_bytes_per_step": wl.h2d_bytes, "d2h_bytes_per_step": wl.d2h_bytes},
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(int(os.environ.get("LOCAL_RANK", 0))),
+    }
+    return line
+
+
+class _PgsBatchTimer:
+    """CUDA events around the batched PGS launches of a step (monkey-patched onto the
+    library call so the step code stays the product path)."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.recs = []
+        self.cur = []
+
+    def __enter__(self):
+        from paper_2306_06946_b200 import _lib
+
+        self._orig = _lib.call
+        torch = self.torch
+        cur = self.cur = []
+
+        def call(name, *a):
+            if name == "cnb_pgs_batched":
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                r = self._orig(name, *a)
+                e1.record()
+                cur.append((e0, e1))
+                return r
+            return self._orig(name, *a)
+
+        _lib.call = call
+        import paper_2306_06946_b200.batch as bmod
+
+        bmod._lib.call = call
+        return self
+
+    def __exit__(self, *a):
+        from paper_2306_06946_b200 import _lib
+
+        _lib.call = self._orig
+        self.recs.append(self.cur)
+
+    def pgs_ms_last_iter(self):
+        self.torch.cuda.synchronize()
+        if not self.recs or not self.recs[-1]:
+            return 0.0
+        e0, e1 = self.recs[-1][-1]
+        return e0.elapsed_time(e1)
+
+    def phases(self):
+        self.torch.cuda.synchronize()
+        per = [sum(a.elapsed_time(b) for a, b in r) for r in self.recs if r]
+        return {"pgs_ms_per_step_median": round(statistics.median(per), 3) if per else 0.0}
+
+
+def _cfg4_cpu_worker(arg):
+    """One process: the oracle port of the reference advancing copy i, pre-rolled to
+    the timed region, then ``steps`` timed steps.  Returns seconds per step."""
+    i, steps, preroll = arg
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import cn_oracle as orc
+
+    from paper_2306_06946_b200.batch import cfg4_draws, placement, plane_normals
+    from paper_2306_06946_b200.mesh import five_tet_grid
+
+    mesh = five_tet_grid((20, 4, 4), 0.01)
+    tilts, mus, jit = cfg4_draws(i, 1, mesh.nodes.size)
+    nrm = plane_normals(tilts)[0]
+    rest = placement(mesh.nodes, plane_normals(tilts), 0.02)[0]
+    body = orc.Body(rest, mesh.tets, young=5e3, poisson=0.45, density=1000.0)
+    sc = orc.Scene([body], [dict(normal=nrm, offset=0.0)], threshold=0.005, mu=float(mus[0]), pgs_iter=1000,
+                   pgs_tol=1e-10, newton_iter=5, penetration_tol=-1.0, rotation_tol=-1.0)
+    sc.q[0] = sc.q[0] + jit[0]
+    for _ in range(preroll):
+        sc.step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sc.step()
+    return (time.perf_counter() - t0) / steps
+
+
+def cpu_reference_cfg4(steps=1, procs=None, preroll=CFG4_PREROLL):
+    """Oracle port on all host cores, one process per core (one copy each), SURVEY §8d:
+    scene-steps/s = sum over processes of 1 / (seconds per step)."""
+    import multiprocessing as mp
+
+    procs = procs or (os.cpu_count() or 1)
+    env_keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+    saved = {k: os.environ.get(k) for k in env_keys}
+    for k in env_keys:
+        os.environ[k] = "1"
+    try:
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(procs) as pool:
+            secs = pool.map(_cfg4_cpu_worker, [(i, steps, preroll) for i in range(procs)])
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return sum(1.0 / s for s in secs), procs, secs
+
+
+def run_reference_cfg4(args):
+    steps = max(1, min(args.steps, 3))
+    v, procs, secs = cpu_reference_cfg4(steps=steps)
+    sample = (f"oracle port of the reference, {procs} processes x 1 thread, copy i = process i (cfg4 draws), "
+              f"pre-rolled {CFG4_PREROLL} steps, then {steps} timed step(s) each; throughput = sum 1/t_step")
+    return {"metric": "scene-steps per second (cfg4: 1024 independent cfg0 beam copies, 5 corrective iterations)",
+            "value": round(v, 3), "unit": "scene-steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(CFG4_COPIES / v * 1e3, 1), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded per-copy tilt, mu, jitter: np.random.default_rng([4, i]))",
+            "config": {"workload": "cfg4: 1024 copies of the cfg0 beam, sampled on the host cores"},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(v, 3), "unit": "scene-steps/s", "cores": procs, "kind": "port",
+                             "sample": sample, "s_per_step_median": round(statistics.median(secs), 3)},
+            "e2e": {"value": round(v, 3), "unit": "scene-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def pgs_ncu_traffic_per_sweep():
     """dram__bytes_read + dram__bytes_write of one pgs_pipe_kernel launch from the
     committed ncu --set full capture (profiles/), per W pass (30 sweeps + the
@@ -872,14 +1138,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg1"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg1", "cfg4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         if rank == 0:
-            line = run_reference_cfg3(args) if args.workload == "cfg3" else run_reference(args)
+            line = {"cfg3": run_reference_cfg3, "cfg4": run_reference_cfg4}.get(args.workload, run_reference)(args)
             print(json.dumps(line), flush=True)
         return
     import torch
@@ -888,10 +1154,17 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
-    line = run_gpu_cfg3(args, rank, world) if args.workload == "cfg3" else run_gpu_cfg1(args, rank, world)
+    line = {"cfg3": run_gpu_cfg3, "cfg4": run_gpu_cfg4}.get(args.workload, run_gpu_cfg1)(args, rank, world)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
-            if args.workload == "cfg3":
+            if args.workload == "cfg4":
+                v_, procs, secs = cpu_reference_cfg4(steps=1)
+                line["cpu_baseline"] = {"value": round(v_, 3), "unit": "scene-steps/s", "cores": procs,
+                                        "kind": "port",
+                                        "sample": f"oracle port, {procs} processes x 1 thread, one copy each, "
+                                                  f"pre-rolled {CFG4_PREROLL} steps then 1 timed step",
+                                        "s_per_step_median": round(statistics.median(secs), 3)}
+            elif args.workload == "cfg3":
                 s_, it, det = cpu_reference_sample_cfg3()
                 line["cpu_baseline"] = {"value": round(s_, 1), "unit": "ms/step", "cores": cpu_threads(),
                                         "kind": "port", "extrapolated": True,

@@ -58,7 +58,7 @@ const char* cnb_last_error(void);
  * their own planes.  Q: scene states (ns rows, pitch ldq); all other arrays are
  * device arrays over the concatenated pairs / packed per-scene matrices, with
  * exclusive prefix offsets poff (pairs), boff (3x3 blocks, m_s^2), woff
- * (doubles, (3 m_s)^2).  Replace, per copy: vertex-plane detection
+ * (doubles, ldw_s^2 with the even row stride ldw_s = 3 m_s + (m_s & 1)).  Replace, per copy: vertex-plane detection
  * (collision.py:264-287), W_g (constraints.py:155-179, as a gather from the
  * compliance C = E^T A^-1 E of the candidate surface DoFs), rebuild_W_fast
  * (constraints.py:182-191, bit-exact order), fast_update_proximity

@@ -157,8 +157,10 @@ class BatchedPlaneScenes:
         m = int(poff[-1])
         boff = np.zeros(ns + 1, dtype=np.int64)
         boff[1:] = np.cumsum(cnt * cnt)
-        woff = 9 * boff[:-1]
-        P = dict(m=m, poff_h=poff, boff_h=boff, woff_h=woff, cnt=cnt,
+        ldw = 3 * cnt + (cnt & 1)  # even row stride: 16-byte aligned rows of W_g / W
+        woff = np.zeros(ns + 1, dtype=np.int64)
+        woff[1:] = np.cumsum(ldw * ldw)
+        P = dict(m=m, poff_h=poff, boff_h=boff, woff_h=woff, cnt=cnt, wsize=int(woff[-1]),
                  poff=dv.upload(poff), boff=dv.upload(boff), woff=dv.upload(woff))
         P["scene"] = torch.empty(m, dtype=torch.int32, device=d)
         P["cand"] = torch.empty(m, dtype=torch.int32, device=d)
@@ -190,17 +192,17 @@ class BatchedPlaneScenes:
                       q_free.data_ptr(), n, pa.data_ptr(), st)
             pb = P["pb"]  # world points on the planes
             nblk = int(P["boff_h"][-1])
-            Wg, W = dv.empty(9 * nblk), dv.empty(9 * nblk)
+            Wg, W = dv.empty(P["wsize"]), dv.empty(P["wsize"])
             _lib.call("cnb_batch_wg_gather", ns, nblk, P["boff"].data_ptr(), P["poff"].data_ptr(),
                       P["woff"].data_ptr(), P["cand"].data_ptr(), self.vids.data_ptr(), self.Ainv.data_ptr(), n,
                       Wg.data_ptr(), st)
             delta, t = dv.empty(3 * m), dv.empty(3 * m)
             lam, dend = dv.empty(3 * m), dv.empty(3 * m)
             eps = dv.empty((ns, self.pgs_max))
-            ic = torch.zeros((ns, 2), dtype=torch.int32, device=dv.device())
+            ics = []
             rot = dv.zeros(1)
             g_off = np.ascontiguousarray(P["poff_h"])
-            w_off = np.ascontiguousarray(P["woff_h"])
+            w_off = np.ascontiguousarray(P["woff_h"][:-1])
             mus = np.ascontiguousarray(self.mus)
             Dk = D
             for k in range(self.newton_iterations):
@@ -212,13 +214,15 @@ class BatchedPlaneScenes:
                 _lib.call("cnb_batch_rebuild_w", ns, nblk, P["boff"].data_ptr(), P["poff"].data_ptr(),
                           P["woff"].data_ptr(), Dk.data_ptr(), Wg.data_ptr(), W.data_ptr(), st)
                 _lib.call("cnb_violation", m, Dk.data_ptr(), pa.data_ptr(), pb.data_ptr(), delta.data_ptr(), st)
+                ic = torch.zeros((ns, 2), dtype=torch.int32, device=dv.device())
+                ics.append(ic)
                 _lib.call("cnb_pgs_batched", ns, g_off.ctypes.data, w_off.ctypes.data, mus.ctypes.data, W.data_ptr(),
                           delta.data_ptr(), h, self.pgs_tol, self.pgs_max, lam.data_ptr(), dend.data_ptr(),
                           eps.data_ptr(), ic.data_ptr(), self._status.ptr, st)
                 _lib.call("cnb_apply_dt", m, Dk.data_ptr(), lam.data_ptr(), t.data_ptr(), acc.data_ptr(), st)
                 _lib.call("cnb_batch_prox", ns, m, P["poff"].data_ptr(), P["woff"].data_ptr(), Wg.data_ptr(),
                           t.data_ptr(), h, pa.data_ptr(), st)
-            self.last = dict(pairs=P, lam=lam, frames=Dk, iters=ic, pa=pa)
+            self.last = dict(pairs=P, lam=lam, frames=Dk, iters=ic, iters_all=ics, pa=pa)
         # mechanical correction dv = h A^-1 S^T acc, integration
         rhs = dv.zeros((ns, n))
         if m:

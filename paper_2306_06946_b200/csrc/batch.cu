@@ -118,7 +118,8 @@ __global__ void batch_gather_pa_kernel(int64_t m, const int32_t* __restrict__ ps
   for (int a = 0; a < 3; ++a) pa[3 * i + a] = q[a];
 }
 
-// W_g of every scene (packed at woff[s], c_s x c_s, c_s = 3 m_s): block (I, J)
+// W_g of every scene (packed at woff[s], c_s x c_s, c_s = 3 m_s, row stride
+// c_s rounded up to even so rows are 16-byte aligned): block (I, J)
 // = Ainv[3 v_I .., 3 v_J ..] (vertex rows of S are unit rows, A is shared:
 // S A^-1 S^T is a gather from the inverse).  Thread per 3x3 block, flattened
 // over scenes with the block prefix boff (m_s^2).
@@ -132,7 +133,7 @@ __global__ void batch_wg_gather_kernel(int ns, const int64_t* __restrict__ boff,
   const int64_t ms = poff[s + 1] - poff[s], loc = x - boff[s];
   const int64_t I = loc / ms, J = loc - I * ms;
   const int64_t ki = vids[pcand[poff[s] + I]], kj = vids[pcand[poff[s] + J]];
-  const int64_t c = 3 * ms;
+  const int64_t c = 3 * ms + (ms & 1);  // even row stride
   double* w = Wg + woff[s] + (3 * I) * c + 3 * J;
   const double* src = C + (3 * ki) * ldc + 3 * kj;
 #pragma unroll
@@ -150,7 +151,7 @@ __global__ void batch_rebuild_w_kernel(int ns, const int64_t* __restrict__ boff,
   const int s = scene_of(boff, ns, x);
   const int64_t ms = poff[s + 1] - poff[s], loc = x - boff[s];
   const int64_t I = loc / ms, J = loc - I * ms;
-  const int64_t c = 3 * ms;
+  const int64_t c = 3 * ms + (ms & 1);  // even row stride
   double DI[9], DJ[9], G[9];
 #pragma unroll
   for (int e = 0; e < 9; ++e) DI[e] = __ldg(D + 9 * (poff[s] + I) + e);
@@ -193,8 +194,8 @@ __global__ void __launch_bounds__(256) batch_prox_kernel(int ns, const int64_t* 
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= 3 * poff[ns]) return;
   const int s = scene_of(poff, ns, r / 3);
-  const int64_t c = 3 * (poff[s + 1] - poff[s]), lr = r - 3 * poff[s];
-  const double* row = Wg + woff[s] + lr * c;
+  const int64_t ms = poff[s + 1] - poff[s], c = 3 * ms, lr = r - 3 * poff[s];
+  const double* row = Wg + woff[s] + lr * (c + (ms & 1));
   const double* ts = t + 3 * poff[s];
   double v = 0.0;
   for (int64_t j = lane; j < c; j += 32) v = fma(row[j], ts[j], v);

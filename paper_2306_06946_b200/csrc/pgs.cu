@@ -1882,6 +1882,355 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
   if (blockIdx.x == 0 && tid == 0 && ctl->timeout) raise_status(s.status, CNB_E_INTERNAL, 0, 0.0);
 }
 
+// ============================================================================
+// Batched PGS, one CTA per independent scene (cfg4 copies)
+// ============================================================================
+// The iterate of pgs_cta with the pipelined kernel's per-group chain
+// (block_solve_v4 + block_commit) and warp specialisation inside the CTA,
+// blocks of kCG = 16 groups:
+//   warp 0     : sequential solve of block b from its diagonal tile T(b);
+//   warps 1..7 : meanwhile, cp.async of T(b+1) and Wx = W[b+1, b] into shared
+//                memory, and the lazy row products P = W[b+1, not b] lambda
+//                (+ the regularisation shift) from global memory / L2, all rows
+//                of a warp interleaved so their loads are in flight together;
+//   all        : delta(b+1) = delta_base + h^2 (P + Wx lambda_b) from shared
+//                memory (4 threads per row); two barriers per block.
+// eps = ||dlambda|| / ||lambda|| is accumulated by the solver lanes (every
+// group is visited once per sweep), so a sweep ends without an extra pass.
+constexpr int kCG = 16, kCR = 3 * kCG, kCS = kCR + 2;  // tile stride 50: at most 2-way bank conflicts
+constexpr int kCopyThreads = 256;
+constexpr int kCHelp = kCopyThreads / 32 - 2;       // helper warps: all but the solver and warp 4
+constexpr int kCRW = (kCR + kCHelp - 1) / kCHelp;   // rows per helper warp
+constexpr int kCU = 2;                              // column chunks per load batch
+
+__host__ __device__ inline size_t copy_smem_bytes(int64_t G) {
+  return sizeof(double) * (size_t)(3 * kCR * kCS + 4 * kCG + 8 + 3 * kCR + 3 * G + kKCP * G + G + 1) + 16;
+}
+
+// rows [r0, r0+nr) x cols [c0, c0+nc) of W -> dst (row stride kCS), 16-byte
+// copies (W rows 16-byte aligned, c0 even; an odd nc copies one padding column
+// that nothing reads), zero-filled outside; threads k of nt participate
+__device__ __forceinline__ void copy_stage(double* dst, const double* W, int64_t ld, int64_t r0, int nr, int64_t c0,
+                                           int nc, int k, int nt) {
+  constexpr int kH = kCR / 2;
+  for (int e = k; e < kCR * kH; e += nt) {
+    const int i = e / kH, j = 2 * (e - i * kH);
+    const bool v = i < nr && j < nc;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + i * kCS + j);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(v ? W + (r0 + i) * ld + c0 + j : W),
+                 "r"(v ? 16 : 0)
+                 : "memory");
+  }
+}
+
+// the next block's diagonal tile T and Wx = W[rows, cols of block b] by TMA bulk
+// copies, one row per thread (k < 2 rows), completion on bar; an odd column
+// count copies one padding column more (rows are 16-byte aligned, ld even)
+__device__ __forceinline__ void copy_stage_bulk(double* T, double* X, const double* W, int64_t ld, int64_t rn0,
+                                                int rows, int64_t cb0, int xcols, int k, unsigned long long* bar) {
+  const unsigned bt = (unsigned)((rows + 1) & ~1) * 8u, bx = (unsigned)((xcols + 1) & ~1) * 8u;
+  if (k == 0) mbar_arrive_expect_tx(bar, (unsigned)rows * (bt + bx));
+  if (k < 2 * rows) {
+    fence_proxy_async_smem();  // earlier generic reads / writes of the buffers before the async writes
+    if (k < rows)
+      bulk_g2s(T + k * kCS, W + (rn0 + k) * ld + rn0, bt, bar);
+    else
+      bulk_g2s(X + (k - rows) * kCS, W + (rn0 + k - rows) * ld + cb0, bx, bar);
+  }
+}
+
+// eight per-lane partial sums reduced across the warp at once (9 shuffles): lane
+// L returns the total of value 4 ((L >> 4) & 1) + 2 ((L >> 3) & 1) + ((L >> 2) & 1)
+__device__ __forceinline__ double warp_sum8(const double v[8], int lane) {
+  double a[4], b[2];
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) a[k] = (h16 ? v[k + 4] : v[k]) + __shfl_xor_sync(0xffffffffu, h16 ? v[k] : v[k + 4], 16);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) b[k] = (h8 ? a[k + 2] : a[k]) + __shfl_xor_sync(0xffffffffu, h8 ? a[k] : a[k + 2], 8);
+  double c = (h4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, h4 ? b[0] : b[1], 4);
+  c += __shfl_xor_sync(0xffffffffu, c, 2);
+  c += __shfl_xor_sync(0xffffffffu, c, 1);
+  return c;
+}
+static_assert(kCRW == 8, "helper rows per warp must match warp_sum8");
+
+__global__ void __launch_bounds__(kCopyThreads, 2) pgs_copy_kernel(const PgsScene* scenes, unsigned long long* prof, int exper) {
+  extern __shared__ __align__(16) double pcsm[];
+  const PgsScene s = scenes[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = s.groups, c = 3 * G;
+  if (G == 0) {
+    if (tid == 0) {
+      s.iters_conv[0] = 0;
+      s.iters_conv[1] = 1;
+    }
+    return;
+  }
+  double* p = pcsm;
+  double* T0 = p;
+  p += kCR * kCS;
+  double* T1 = p;
+  p += kCR * kCS;
+  double* Wx = p;
+  p += kCR * kCS;
+  double* sv = p;
+  p += 4 * kCG;
+  double* red = p;
+  p += 8;
+  double* dn = p;
+  p += kCR;
+  double* P = p;
+  p += kCR;
+  double* dbn = p;  // delta_base of the next block
+  p += kCR;
+  double* lam = p;
+  p += 3 * G;
+  double* rec = p;
+  p += kKCP * G;
+  double* dsh = p;
+  p += G;
+  unsigned long long* tbar = (unsigned long long*)p;  // 8-byte aligned (every block above is whole doubles)
+  p += 1;
+  int* flags = (int*)p;
+  const int nb = (int)((G + kCG - 1) / kCG);
+  const double h2 = s.h2, ih2 = 1.0 / h2, mu = s.mu;
+  const double* __restrict__ W = s.W;
+  const int64_t ld = s.ldw;
+
+  // ---- regularize (solver.py:99-121) and the per-group constants ----
+  double tr = 0.0;
+  for (int64_t i = tid; i < c; i += blockDim.x) tr += W[i * ld + i];
+  tr = warp_sum(tr);
+  if (lane == 0) red[warp] = tr;
+  if (tid == 0) {
+    flags[0] = flags[1] = 0;
+    mbar_init(tbar, 1);
+  }
+  __syncthreads();
+  double shift = 0.0;
+  for (int w = 0; w < kCopyThreads / 32; ++w) shift += red[w];
+  shift = 1e-10 * shift / (double)c;
+  if (shift <= 0.0) shift = 1e-30;
+  for (int64_t g = tid; g < G; g += blockDim.x) {
+    double a[3][3], Wd[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        Wd[3 * i + j] = W[(3 * g + i) * ld + 3 * g + j];
+        a[i][j] = 0.5 * (W[(3 * g + i) * ld + 3 * g + j] + W[(3 * g + j) * ld + 3 * g + i]);
+      }
+    double e[3];
+    sym3_eigs(a, e);
+    const double mn = fmin(e[0], fmin(e[1], e[2]));
+    const double scale = fmax(fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))), 1e-300);
+    const double sh = (mn <= 1e-12 * scale) ? shift : 0.0;
+    dsh[g] = sh;
+    for (int i = 0; i < 3; ++i) Wd[4 * i] = add(Wd[4 * i], sh);
+    GroupConst kc;
+    group_const(Wd, h2, kc);
+    double* o = rec + kKCP * g;  // record layout: load_group_const
+    o[0] = kc.ihw;
+    o[1] = kc.it00;
+    o[2] = kc.it01;
+    o[3] = kc.it10;
+    o[4] = kc.it11;
+    o[5] = kc.b0;
+    o[6] = kc.b1;
+    o[7] = (double)kc.bad;
+  }
+  for (int64_t i = tid; i < c; i += blockDim.x) lam[i] = 0.0;
+  {
+    const int r0n = 3 * (int)min((int64_t)kCG, G);
+    copy_stage(T0, W, ld, 0, r0n, 0, r0n, tid, blockDim.x);
+    for (int i = tid; i < r0n; i += blockDim.x) dn[i] = s.delta_base[i];
+    cp_async_wait_all();
+    __syncthreads();
+    for (int i = tid; i < r0n; i += blockDim.x) T0[i * kCS + i] = add(T0[i * kCS + i], dsh[i / 3]);
+    __syncthreads();
+  }
+
+  double dl[3] = {0, 0, 0}, lm[3] = {0, 0, 0}, dsq = 0.0, nl = 0.0;
+  GroupConst kc;
+  double* Tc = T0;
+  double* Tn = T1;
+  int iterations = 0;
+  bool converged = false;
+  // CNB_PGS_PROFILE=1: cycle sums of CTA 0 (solver solve / solver wait / helper
+  // products / helper tile wait / delta phase / blocks)
+  const bool stamp = prof && blockIdx.x == 0 && (tid == 0 || tid == 32);
+  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = 0, t1 = 0;
+  unsigned tph = 0;  // phase of tbar (helper thread 0 only)
+  for (int sweep = 0; sweep < s.max_iter; ++sweep) {
+    iterations = sweep + 1;
+    for (int b = 0; b < nb; ++b) {
+      const int64_t g0 = (int64_t)b * kCG;
+      const int ng = (int)min((int64_t)kCG, G - g0);
+      const int bn = (b + 1 == nb) ? 0 : b + 1;
+      const int64_t gn0 = (int64_t)bn * kCG;
+      const int ngn = (int)min((int64_t)kCG, G - gn0);
+      const int64_t cb0 = 3 * g0, cb1 = cb0 + 3 * ng, rn0 = 3 * gn0;
+      const int rows = 3 * ngn;
+      if (stamp) t0 = clock64();
+      if (warp == 0) {
+        // ---- sequential block solve ----
+        const bool mine = lane < ng;
+        load_group_const(kc, rec + kKCP * (g0 + (mine ? lane : 0)), mine, kKCP);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          lm[a] = mine ? lam[3 * (g0 + lane) + a] : 0.0;
+          dl[a] = mine ? dn[3 * lane + a] : 0.0;
+        }
+        if (mu != 0.0)
+          block_solve_v4<true>(Tc, kCS, ng, lane, dl, lm, kc, mu, h2, sv);
+        else
+          block_solve_v4<false>(Tc, kCS, ng, lane, dl, lm, kc, mu, h2, sv);
+        __syncwarp();
+        int err = 0;
+        if (mine) {
+          err = block_commit(sv, lane, lm, kc, mu, ih2, dsq);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) lam[3 * (g0 + lane) + a] = lm[a];
+          nl = fma(lm[0], lm[0], fma(lm[1], lm[1], fma(lm[2], lm[2], nl)));
+        }
+        const unsigned bad = __ballot_sync(0xffffffffu, err);
+        if (bad) {
+          const int g = __ffs(bad) - 1;  // first failing group in Gauss-Seidel order
+          if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), 1.0 / kc.ihw);
+          if (lane == 0) flags[0] = CNB_E_SINGULAR_BLOCK;
+        }
+        if (stamp) {
+          t1 = clock64();
+          pf[0] += t1 - t0;
+        }
+        if (b + 1 == nb) {
+          // ---- end of sweep: epsilon (solver.py:194-199) ----
+          const double num2 = warp_sum(dsq), den2 = warp_sum(nl);
+          dsq = nl = 0.0;
+          if (lane == 0) {
+            const double num = sqrt(num2), den = sqrt(den2);
+            const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
+            s.eps_hist[sweep] = eps;
+            flags[1] = (eps <= s.tol) ? 1 : 0;
+          }
+        }
+      } else if (nb > 1 && warp != 4) {
+        // ---- helpers: next block's tiles, lazy products over every column but block b ----
+        // (warp 4 shares the solver's SM sub-partition and stays idle)
+        const int hw = warp < 4 ? warp - 1 : warp - 2;
+        const int k = 32 * hw + lane, nt = 32 * kCHelp;
+        if (!(exper & 2)) copy_stage_bulk(Tn, Wx, W, ld, rn0, rows, cb0, 3 * ng, k, tbar);
+        if (!(exper & 4)) {
+          // L2 prefetch of the row panel the helpers read in the next step
+          const int bn2 = (bn + 1 == nb) ? 0 : bn + 1;
+          const int64_t r2 = 3 * (int64_t)bn2 * kCG;
+          const int rows2 = 3 * (int)min((int64_t)kCG, G - (int64_t)bn2 * kCG);
+          const int i = k - 2 * kCR;  // threads past the bulk-copy issuers
+          if (i >= 0 && i < rows2)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(W + (r2 + i) * ld),
+                         "r"((unsigned)(((c + 1) & ~1LL) * 8)));
+        }
+        for (int i = k; i < rows; i += nt) cp_async8(dbn + i, s.delta_base + rn0 + i, true);
+        if (stamp) pf[6] += clock64() - t0;
+        double acc[kCRW];
+#pragma unroll
+        for (int r = 0; r < kCRW; ++r) acc[r] = 0.0;
+        // unconditional loads (rows clamped, excluded / padding columns masked through
+        // lambda = 0) so a batch of kCU x kCRW loads is in flight together
+        const double* rp[kCRW];
+#pragma unroll
+        for (int r = 0; r < kCRW; ++r) rp[r] = W + (rn0 + min(hw + kCHelp * r, rows - 1)) * ld;
+        const int64_t cend = (exper & 1) ? 0 : c;  // diagnostic: skip the products
+        for (int64_t j0 = 0; j0 < cend; j0 += 32 * kCU) {
+          double w[kCU][kCRW], lj[kCU];
+#pragma unroll
+          for (int u = 0; u < kCU; ++u) {
+            const int64_t j = j0 + 32 * u + lane;
+            const int64_t jj = min(j, c - 1);
+            lj[u] = (j < c && (j < cb0 || j >= cb1)) ? lam[jj] : 0.0;
+#pragma unroll
+            for (int r = 0; r < kCRW; ++r) w[u][r] = __ldg(rp[r] + jj);
+          }
+#pragma unroll
+          for (int u = 0; u < kCU; ++u)
+#pragma unroll
+            for (int r = 0; r < kCRW; ++r) acc[r] = fma(w[u][r], lj[u], acc[r]);
+        }
+        if (stamp) pf[7] += clock64() - t0;
+        {
+          const double v = warp_sum8(acc, lane);
+          const int i = hw + kCHelp * (4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1));
+          if ((lane & 3) == 0 && i < rows) P[i] = fma(dsh[(rn0 + i) / 3], lam[rn0 + i], v);
+        }
+        if (stamp) {
+          t1 = clock64();
+          pf[2] += t1 - t0;
+        }
+        cp_async_wait_all();
+        if (k == 0 && !(exper & 2)) {
+          mbar_wait(tbar, tph);
+          tph ^= 1u;
+        }
+        if (stamp) pf[3] += clock64() - t1;
+      }
+      __syncthreads();
+      if (stamp) {
+        const long long t2 = clock64();
+        if (tid == 0) pf[1] += t2 - t1;
+        t1 = t2;
+      }
+      if (flags[0]) break;
+      if (b + 1 == nb && flags[1]) {
+        converged = true;
+        break;
+      }
+      // ---- delta of the next block (4 threads per row) ----
+      {
+        const double* X = nb > 1 ? Wx : Tc;  // one block: its own regularised tile, all columns
+        const int ncol = 3 * ng;
+        const int i = tid >> 2, q = tid & 3;
+        double acc = 0.0;
+        if (i < rows)
+          for (int j = q; j < ncol; j += 4) acc = fma(X[i * kCS + j], lam[cb0 + j], acc);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (q == 0 && i < rows) dn[i] = add(nb > 1 ? dbn[i] : s.delta_base[rn0 + i], mul(h2, (nb > 1 ? P[i] : 0.0) + acc));
+        if (nb > 1)
+          for (int r = tid; r < rows; r += blockDim.x) Tn[r * kCS + r] = add(Tn[r * kCS + r], dsh[(rn0 + r) / 3]);
+      }
+      __syncthreads();
+      if (stamp && tid == 0) {
+        pf[4] += clock64() - t1;
+        pf[5] += 1;
+      }
+      if (nb > 1) {
+        double* t = Tc;
+        Tc = Tn;
+        Tn = t;
+      }
+    }
+    if (flags[0] || converged) break;
+  }
+  __syncthreads();
+  // ---- delta_end = delta_base + h^2 W_reg lam (solver.py:201) ----
+  for (int64_t r = warp; r < c; r += kCopyThreads / 32) {
+    double acc = lane_dot<false>(W + r * ld, lam, 0, c, lane);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      acc = fma(dsh[r / 3], lam[r], acc);
+      s.delta_end[r] = add(s.delta_base[r], mul(h2, acc));
+    }
+  }
+  for (int64_t i = tid; i < c; i += blockDim.x) s.lam[i] = lam[i];
+  if (tid == 0) {
+    s.iters_conv[0] = iterations;
+    s.iters_conv[1] = converged ? 1 : 0;
+  }
+  if (stamp)
+    for (int k = 0; k < 8; ++k)
+      if (pf[k]) atomicAdd(prof + 8 + k, pf[k]);
+}
+
 template <int V>
 __global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double* out) {
   extern __shared__ __align__(16) char bsm[];
@@ -2312,7 +2661,7 @@ int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off,
     PgsScene& sc = hs[i];
     sc.groups = G;
     sc.W = W + w_off[i];
-    sc.ldw = 3 * G;
+    sc.ldw = 3 * G + (G & 1);  // even row stride (16-byte aligned rows)
     sc.delta_base = delta_base + 3 * g_off[i];
     sc.h2 = h * h;
     sc.mu = mu[i];
@@ -2324,7 +2673,12 @@ int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off,
     sc.iters_conv = iters_conv + 2 * i;
     sc.status = (DevStatus*)d_status;
   }
-  const size_t smem = pgs_smem_bytes(std::max<int64_t>(gmax, 1));
+  // per-copy pipelined kernel unless CNB_PGS_BATCHED=cta asks for the plain single-CTA iterate
+  static const bool plain = [] {
+    const char* e = getenv("CNB_PGS_BATCHED");
+    return e && !strcmp(e, "cta");
+  }();
+  const size_t smem = plain ? pgs_smem_bytes(std::max<int64_t>(gmax, 1)) : copy_smem_bytes(std::max<int64_t>(gmax, 1));
   if (smem > pgs_max_smem()) {
     set_error("pgs_batched: %lld groups in one scene exceed the single-CTA kernel", (long long)gmax);
     return CNB_E_VALIDATION;
@@ -2332,9 +2686,17 @@ int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off,
   cudaStream_t st = (cudaStream_t)stream;
   CNB_CUDA(cudaMemcpyAsync(d_sc, hs, bytes, cudaMemcpyHostToDevice, st));
   if ((rc = pin.mark(st))) return rc;
-  CNB_CUDA(cudaFuncSetAttribute(pgs_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  pgs_batched_kernel<<<nscenes, kPgsThreads, smem, st>>>(d_sc);
-  CNB_LAUNCH_CHECK("pgs_batched_kernel");
+  if (plain) {
+    CNB_CUDA(cudaFuncSetAttribute(pgs_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pgs_batched_kernel<<<nscenes, kPgsThreads, smem, st>>>(d_sc);
+    CNB_LAUNCH_CHECK("pgs_batched_kernel");
+  } else {
+    CNB_CUDA(cudaFuncSetAttribute(pgs_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const char* ee = getenv("CNB_PGS_COPY_EXP");  // diagnostic switches (results invalid when set)
+    const int exper = ee ? atoi(ee) : 0;
+    pgs_copy_kernel<<<nscenes, kCopyThreads, smem, st>>>(d_sc, pgs_profile_buffer(), exper);
+    CNB_LAUNCH_CHECK("pgs_copy_kernel");
+  }
   return CNB_OK;
 }
 
