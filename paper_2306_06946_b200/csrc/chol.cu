@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
 __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
                                                    double* __restrict__ front, const double* __restrict__ kkinv) {
   constexpr int LD = kPanel + 4;
-  __shared__ double As[64 * LD];
+  constexpr int LK = 64 + 4;  // k-major rows of the chunk (conflict-free copies and fragments)
+  __shared__ double As[kPanel * LK];
   __shared__ double Is[kPanel * LD];
   const int64_t s = tasks[2 * blockIdx.x];
   const int64_t chunk = tasks[2 * blockIdx.x + 1];
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
   for (int e = threadIdx.x; e < 64 * kPanel; e += blockDim.x) {
     const int rr = e % 64, k = e / 64;
     const int64_t r = r0 + rr;
-    cp_async8(&As[rr * LD + k], F + (int64_t)(k0 + k) * f + r, r < f && k < kw);
+    cp_async8(&As[k * LK + rr], F + (int64_t)(k0 + k) * f + r, r < f && k < kw);
   }
   const double* Y = kkinv + (S.kk_off[s] + k0 / kPanel) * (kPanel * kPanel);
   for (int e = threadIdx.x; e < kPanel * kPanel; e += blockDim.x)
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
   for (int kk = 0; kk < kPanel; kk += 4) {
     double fa[2], fb[4];
 #pragma unroll
-    for (int a = 0; a < 2; ++a) fa[a] = As[(16 * warp + 8 * a + g) * LD + kk + t];
+    for (int a = 0; a < 2; ++a) fa[a] = As[(kk + t) * LK + 16 * warp + 8 * a + g];
 #pragma unroll
     for (int b = 0; b < 4; ++b) fb[b] = Is[(8 * b + g) * LD + kk + t];
 #pragma unroll
@@ -219,14 +220,17 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
 // mode 1 (trailing): P = the whole block of panel p (kw <= 128 columns), target
 //   [block end, f).  The trailing matrix is read and written once per 128
 //   columns, with K = 128 per pass (16 flop per byte of C).
-// 4 warps, each a 32x32 quadrant = 4x4 fragments of 8x8.
-constexpr int kSP = kPanel + 4;  // smem row stride (== 4 mod 16 doubles: conflict-free fragments)
-constexpr size_t kSyrkSmem = 2 * 2 * kTile * kSP * sizeof(double);
+// 4 warps, each a 32x32 quadrant = 4x4 fragments of 8x8.  The staged panels
+// are k-major ([k][row], as in the column-major front), so the asynchronous
+// copies of consecutive rows land in consecutive banks, and the fragment loads
+// are conflict-free with a row stride == 4 mod 16 doubles.
+constexpr int kSK = kTile + 4;  // smem stride of one k column of a staged tile
+constexpr size_t kSyrkSmem = 2 * 2 * kPanel * kSK * sizeof(double);
 __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode,
                                                    double* __restrict__ front) {
   extern __shared__ __align__(16) double syrk_sm[];
-  double* Pi = syrk_sm;                  // [2][kTile * kSP]
-  double* Pj = syrk_sm + 2 * kTile * kSP;
+  double* Pi = syrk_sm;                  // [2][kPanel * kSK]
+  double* Pj = syrk_sm + 2 * kPanel * kSK;
   const int64_t s = tasks[3 * blockIdx.x];
   const int ti = tasks[3 * blockIdx.x + 1], tj = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
@@ -248,15 +252,15 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
   const int64_t r0 = t0 + (int64_t)ti * kTile, c0 = t0 + (int64_t)tj * kTile;
   double* F = front + S.front_off[s];
   auto stage = [&](int buf, int64_t kk0) {
-    double* A = Pi + buf * kTile * kSP;
-    double* B = Pj + buf * kTile * kSP;
+    double* A = Pi + buf * kPanel * kSK;
+    double* B = Pj + buf * kPanel * kSK;
     for (int e = threadIdx.x; e < kTile * kPanel; e += blockDim.x) {
       const int rr = e % kTile, kc = e / kTile;
       const bool kin = kk0 + kc < kw;
       const int64_t ri = r0 + rr, rj = c0 + rr;
       const double* col = F + (k0 + kk0 + kc) * f;
-      cp_async8(&A[rr * kSP + kc], col + ri, kin && ri < f);
-      cp_async8(&B[rr * kSP + kc], col + rj, kin && rj < cend);
+      cp_async8(&A[kc * kSK + rr], col + ri, kin && ri < f);
+      cp_async8(&B[kc * kSK + rr], col + rj, kin && rj < cend);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -279,16 +283,16 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
-    const double* A = Pi + (ck & 1) * kTile * kSP;
-    const double* B = Pj + (ck & 1) * kTile * kSP;
+    const double* A = Pi + (ck & 1) * kPanel * kSK;
+    const double* B = Pj + (ck & 1) * kPanel * kSK;
     const int kc = (int)min((int64_t)kPanel, kw - (int64_t)ck * kPanel);
     if (!skip)
       for (int kk = 0; kk < kc; kk += 4) {
         double fa[4], fb[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) fa[a] = A[(wy + 8 * a + g) * kSP + kk + t];
+        for (int a = 0; a < 4; ++a) fa[a] = A[(kk + t) * kSK + wy + 8 * a + g];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) fb[b] = B[(wx + 8 * b + g) * kSP + kk + t];
+        for (int b = 0; b < 4; ++b) fb[b] = B[(kk + t) * kSK + wx + 8 * b + g];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll

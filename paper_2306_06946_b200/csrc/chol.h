@@ -18,7 +18,7 @@
 namespace cnb {
 
 constexpr int kPanel = 32;   // pivot panel width of the dense front factorisation
-constexpr int kBlkPanels = 4;  // panels per trailing-update block: the trailing matrix is
+constexpr int kBlkPanels = 8;  // panels per trailing-update block: the trailing matrix is
                                // updated once per kBlkPanels * kPanel = 128 columns (K = 128)
 constexpr int kTile = 64;    // SYRK / GEMM output tile
 constexpr int kEaCols = 8;   // parent columns per extend-add task (small: more CTAs in flight)

@@ -28,6 +28,7 @@ constexpr int kBwdRows = 4;     // pivot rows per backward task (warp per row)
 constexpr int kMT = 64;         // DMMA panel tile (rows, cols)
 constexpr int kMK = 32;         // DMMA k-chunk
 constexpr int kMS = kMK + 4;    // smem stride (== 4 mod 16)
+constexpr int kMA = kMT + 4;    // k-major stride of tiles staged from column-major sources
 
 // RHS block of supernode s: R_s = rhs + roff[s], f_s x w_s column-major;
 // global columns [lo_s, lo_s + w_s).
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
                                                         const double* __restrict__ p21,
                                                         const double* __restrict__ linv, double* __restrict__ Y,
                                                         const int64_t* __restrict__ yoff) {
-  __shared__ double As[kMT * kMS];
+  __shared__ double As[kMK * kMA];  // [k][row]
   __shared__ double Bs[kMT * kMS];
   const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
       const int rr = e % kMT, kk = e / kMT;
       const int64_t i = r0 + rr, j = k0 + kk;
       const bool in = i < f && j < nc && (i >= nc || j <= i);
-      cp_async8(&As[rr * kMS + kk], i < nc ? Li + j * nc + i : P + j * nr + (i - nc), in);
+      cp_async8(&As[kk * kMA + rr], i < nc ? Li + j * nc + i : P + j * nr + (i - nc), in);
     }
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int kk = e % kMK, cc = e / kMK;
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
     for (int kk = 0; kk < kMK; kk += 4) {
       double fa[4], fb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) fa[a] = As[(wy + 8 * a + g) * kMS + kk + t];
+      for (int a = 0; a < 4; ++a) fa[a] = As[(kk + t) * kMA + wy + 8 * a + g];
 #pragma unroll
       for (int b = 0; b < 4; ++b) fb[b] = Bs[(wx + 8 * b + g) * kMS + kk + t];
 #pragma unroll
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int3
 __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                   const double* __restrict__ front, const double* __restrict__ linv,
                                                   double* __restrict__ p21) {
-  __shared__ double As[kMT * kMS];
+  __shared__ double As[kMK * kMA];  // [k][row]
   __shared__ double Bs[kMT * kMS];
   const int64_t s = tasks[3 * blockIdx.x], q0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int rr = e % kMT, kk = e / kMT;
       const int64_t q = q0 + rr, k = k0 + kk;
-      cp_async8(&As[rr * kMS + kk], F + k * f + nc + q, q < nr && k < nc);
+      cp_async8(&As[kk * kMA + rr], F + k * f + nc + q, q < nr && k < nc);
     }
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int kk = e % kMK, cc = e / kMK;
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
     for (int kk = 0; kk < kMK; kk += 4) {
       double fa[4], fb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) fa[a] = As[(wy + 8 * a + g) * kMS + kk + t];
+      for (int a = 0; a < 4; ++a) fa[a] = As[(kk + t) * kMA + wy + 8 * a + g];
 #pragma unroll
       for (int b = 0; b < 4; ++b) fb[b] = Bs[(wx + 8 * b + g) * kMS + kk + t];
 #pragma unroll
