@@ -315,7 +315,9 @@ class Cfg3Workload:
         ach = fl / (ms * 1e-3) / 1e12
         out["build_wg"] = {"kernel": "W_g: sparse-RHS forward solve + Gram (2 bodies)", "bound": "tensor",
                            "achieved": round(ach, 3), "peak": round(dmma, 2), "unit": "TFLOP/s",
-                           "frac": round(ach / dmma, 4), "algorithmic_gflop": round(fl / 1e9, 1), "ms": round(ms, 3)}
+                           "frac": round(ach / dmma, 4), "algorithmic_gflop": round(fl / 1e9, 1), "ms": round(ms, 3),
+                           "fwd_gflop": round(st.get("fwd_flops", 0.0) / 1e9, 1),
+                           "gram_gflop": round(st.get("gram_flops", 0.0) / 1e9, 1)}
         return out
 
     def config_json(self, world):

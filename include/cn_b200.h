@@ -189,6 +189,10 @@ int64_t cnb_pgs_work_bytes(int64_t groups);
  * nanoseconds (slots 16-31: cycles) per phase since the last call, out[32]; slot meanings are
  * listed at the stamp() calls of each kernel in csrc/pgs.cu. */
 int cnb_pgs_profile(double* out);
+/* Diagnostic: summed cycles of the POTRF kernel's phases (CTA 0 of every launch)
+ * since the last call: out[0] loads, [1] factor, [2] store L, [3] inverse,
+ * [4] store L^{-1}, out[7] launches. */
+int cnb_potrf_profile(double* out);
 
 /* Diagnostic: cycles per group of the PGS block solve while the other warps of
  * the CTA generate load of kind `mode` (0 idle, 1 LDS, 2 SHFL, 3 global polls,

@@ -90,71 +90,106 @@ __global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t
 // parallel update between barriers, and the code stays a compact loop
 // (a fully unrolled register version thrashes the instruction cache).
 // Rows / columns >= kw are padded with the identity.
+// diagnostic: cycle sums of potrf phases (CTA 0 of every launch), cnb_potrf_profile
+__device__ unsigned long long g_potrf_prof[8];
+
 __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
                                                    double* __restrict__ front, double* __restrict__ kkinv,
                                                    DevStatus* st) {
-  // One warp per front.  Left-looking by columns: at step j lane i (row i)
-  // forms l_ij = (a_ij - sum_{k<j} l_ik l_jk) / l_jj with a rolled dot-product
-  // loop over shared memory (own row + broadcast row j); no block barriers.
+  // One warp per front, right-looking: at step j every lane i > j scales its
+  // l_ij and updates its own row a[i][j+1..i] with the broadcast column j.
+  // The update loops are unrolled by 8 with predication so a lane keeps eight
+  // independent shared loads / FMAs in flight (a single warp has nothing else
+  // to hide latency with).  1/sqrt comes from rsqrt.approx + two Newton steps:
+  // the libm sqrt and the IEEE division are long subroutines on the sequential
+  // chain.  Then Y = L^{-1} by the same scheme, lane c owning column c (in
+  // place: Y starts as the identity).
   __shared__ double a[kPanel][kPanel + 1];
   __shared__ double y[kPanel][kPanel + 1];
-  __shared__ double rdiag[kPanel];
+  __shared__ double rd[kPanel];
   const int64_t s = tasks[blockIdx.x];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
   const int kw = (int)min((int64_t)kPanel, nc - k0);
   double* F = front + S.front_off[s];
   const int i = threadIdx.x;
-  for (int l = 0; l < kPanel; ++l)  // lane i loads column l: coalesced over rows
+  const bool stamp = blockIdx.x == 0 && i == 0;
+  long long ts[6];
+  ts[0] = clock64();
+#pragma unroll 8
+  for (int l = 0; l < kPanel; ++l)  // lane i loads row i, column by column: coalesced over rows
     a[i][l] = (i < kw && l < kw && l <= i) ? F[(int64_t)(k0 + l) * f + k0 + i] : (l == i ? 1.0 : 0.0);
   __syncwarp();
-  for (int j = 0; j < kw; ++j) {
-    // four independent partial sums: dependent fp64 FMA chains are the
-    // latency bottleneck of this kernel
-    double v0 = a[i][j], v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    int k = 0;
-    for (; k + 4 <= j; k += 4) {
-      v0 = fma(-a[i][k], a[j][k], v0);
-      v1 = fma(-a[i][k + 1], a[j][k + 1], v1);
-      v2 = fma(-a[i][k + 2], a[j][k + 2], v2);
-      v3 = fma(-a[i][k + 3], a[j][k + 3], v3);
-    }
-    for (; k < j; ++k) v0 = fma(-a[i][k], a[j][k], v0);
-    const double v = (v0 + v1) + (v2 + v3);
-    const double d = __shfl_sync(0xffffffffu, v, j);
-    if (!(d > 0.0) && i == 0) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
-    const double ljj = d > 0.0 ? sqrt(d) : __longlong_as_double(0x7ff8000000000000LL);
-    const double r = 1.0 / ljj;
+  ts[1] = clock64();
+  for (int j = 0; j < kPanel; ++j) {
+    const double d = a[j][j];
+    const double aij = a[i][j];
+    if (j < kw && !(d > 0.0) && i == 0) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
+    double inv;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(d));
+    inv = inv * fma(-0.5 * d, inv * inv, 1.5);
+    inv = inv * fma(-0.5 * d, inv * inv, 1.5);
+    if (!(d > 0.0)) inv = __longlong_as_double(0x7ff8000000000000LL);
+    const double lij = aij * inv;
+    __syncwarp();
     if (i == j) {
-      a[j][j] = ljj;
-      rdiag[j] = r;
-    } else if (i > j) {
-      a[i][j] = v * r;
+      a[j][j] = d * inv;
+      rd[j] = inv;
+    }
+    if (i > j) a[i][j] = lij;
+    __syncwarp();
+    for (int k0u = j + 1; k0u < kPanel; k0u += 8) {
+      double lk[8], ai[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = min(k0u + u, kPanel - 1);
+        lk[u] = a[k][j];
+        ai[u] = a[i][k];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0u + u;
+        if (k < kPanel && k <= i) a[i][k] = fma(-lij, lk[u], ai[u]);
+      }
     }
     __syncwarp();
   }
-  for (int l = kw; l < kPanel; ++l)
-    if (i == l) rdiag[l] = 1.0;
-  __syncwarp();
+  ts[2] = clock64();
+#pragma unroll 8
   for (int l = 0; l < kw; ++l)
     if (i < kw && l <= i) F[(int64_t)(k0 + l) * f + k0 + i] = a[i][l];
-  // Y = L^{-1}: row by row, lane c owns column c:
-  // Y[r][c] = (delta_rc - sum_{k=c}^{r-1} L[r][k] Y[k][c]) / L[r][r]
+  ts[3] = clock64();
+  // Y = L^{-1}: lane c owns column c; step r: y[r][c] *= 1/L[r][r] (= rd[r]), then
+  // rows below subtract L[q][r] y[r][c]
   const int c = threadIdx.x;
+#pragma unroll 8
+  for (int r = 0; r < kPanel; ++r) y[r][c] = (r == c) ? 1.0 : 0.0;
+  __syncwarp();
   for (int r = 0; r < kPanel; ++r) {
-    double v0 = (r == c) ? 1.0 : 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    int k = c;
-    for (; k + 4 <= r; k += 4) {
-      v0 = fma(-a[r][k], y[k][c], v0);
-      v1 = fma(-a[r][k + 1], y[k + 1][c], v1);
-      v2 = fma(-a[r][k + 2], y[k + 2][c], v2);
-      v3 = fma(-a[r][k + 3], y[k + 3][c], v3);
+    const double yr = y[r][c] * rd[r];
+    y[r][c] = yr;
+    for (int q0 = r + 1; q0 < kPanel; q0 += 8) {
+      double lq[8], yq[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = min(q0 + u, kPanel - 1);
+        lq[u] = a[q][r];
+        yq[u] = y[q][c];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < kPanel) y[q0 + u][c] = fma(-lq[u], yr, yq[u]);
     }
-    for (; k < r; ++k) v0 = fma(-a[r][k], y[k][c], v0);
-    y[r][c] = c <= r ? ((v0 + v1) + (v2 + v3)) * rdiag[r] : 0.0;
-    __syncwarp();
   }
+  __syncwarp();
+  ts[4] = clock64();
   double* Y = kkinv + (S.kk_off[s] + k0 / kPanel) * (kPanel * kPanel);  // kept for the TRSM and L11^{-1}
+#pragma unroll 8
   for (int r = 0; r < kPanel; ++r) Y[r * kPanel + c] = y[r][c];
+  ts[5] = clock64();
+  if (stamp) {
+    for (int k = 0; k < 5; ++k) atomicAdd(&g_potrf_prof[k], (unsigned long long)(ts[k + 1] - ts[k]));
+    atomicAdd(&g_potrf_prof[7], 1ull);
+  }
 }
 
 // TRSM of the rows below the diagonal block: X = B L_kk^{-T} as a DMMA product
@@ -515,6 +550,17 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
 using namespace cnb;
 
 extern "C" {
+
+// diagnostic: summed cycles of the potrf phases since the last call (loads,
+// factor, store L, inverse, store Y) and the launch count in out[7]
+int cnb_potrf_profile(double* out) {
+  unsigned long long h[8];
+  CNB_CUDA(cudaMemcpyFromSymbol(h, g_potrf_prof, sizeof(h)));
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  CNB_CUDA(cudaMemcpyToSymbol(g_potrf_prof, z, sizeof(z)));
+  for (int k = 0; k < 8; ++k) out[k] = (double)h[k];
+  return CNB_OK;
+}
 
 static CholHandle* H(cnb_chol_t h) { return reinterpret_cast<CholHandle*>(h); }
 
