@@ -246,10 +246,82 @@ def kat_linalg():
          K_data=K.data, masses=body.masses())
 
 
+SCENE_IO_TEXT = """\
+# scene-format fixture: soft box on the ground, pushed by a moving plate
+gravity: [0.0, -9.81, 0.0]
+dt: 0.01
+threshold: 0.008
+mu: 0.4
+pgs: {iterations: 150, tolerance: 1.0e-8}
+newton: {scheme: fast, iterations: 3, penetration_tol: -1.0}
+output: {snapshots: true, metrics: true, every: 1}
+objects:
+  - name: cube
+    type: soft
+    mesh: {box: {size: [0.04, 0.04, 0.04], divisions: [3, 3, 3], center: [0.0, 0.0205, 0.0]}}
+    material: {young: 3.0e4, poisson: 0.35, density: 900.0, rayleigh_mass: 0.1, rayleigh_stiffness: 0.05}
+    velocity: [0.1, 0.0, 0.0]
+  - name: ground
+    type: plane
+    normal: [0.0, 1.0, 0.0]
+    offset: 0.0
+  - name: pusher
+    type: kinematic_mesh
+    plate: {center: [0.03, 0.02, 0.0], normal: [-1.0, 0.0, 0.0], size: [0.06, 0.06]}
+    motion: {velocity: [-0.05, 0.0, 0.0]}
+"""
+
+
+def scene_io():
+    """Reference parse of a scene file, its metrics.csv and snapshot files after a
+    3-step run (scene.py:292-354, 541-547, 771-866)."""
+    import json
+    import shutil
+    import tempfile
+
+    tmp = tempfile.mkdtemp()
+    path = os.path.join(tmp, "io.scn")
+    with open(path, "w") as fh:
+        fh.write(SCENE_IO_TEXT)
+    cfg = rsc.load_scene(path)
+    summary = {"h": cfg.h, "threshold": cfg.threshold, "gravity": list(cfg.gravity),
+               "pgs": [cfg.pgs.max_iterations, cfg.pgs.tolerance, cfg.pgs.friction],
+               "newton": [cfg.newton.scheme, cfg.newton.max_iterations, cfg.newton.penetration_tol,
+                          cfg.newton.relinearize],
+               "output": [cfg.output.snapshots, cfg.output.metrics, cfg.output.every], "objects": []}
+    arrays = {}
+    for k, o in enumerate(cfg.objects):
+        d = {"name": o.name, "type": type(o).__name__}
+        if hasattr(o, "mesh"):
+            d.update(young=o.young, poisson=o.poisson, density=o.density, rayleigh_mass=o.rayleigh_mass,
+                     rayleigh_stiffness=o.rayleigh_stiffness, velocity=list(o.velocity))
+            arrays[f"nodes{k}"], arrays[f"tets{k}"] = o.mesh.nodes, o.mesh.tets
+        elif hasattr(o, "points"):
+            d.update(axis=list(o.motion.axis), center=list(o.motion.center),
+                     angular_velocity=o.motion.angular_velocity, velocity=list(o.motion.velocity))
+            arrays[f"points{k}"], arrays[f"triangles{k}"] = o.points, o.triangles
+        else:
+            d.update(normal=list(o.normal), offset=o.offset)
+        summary["objects"].append(d)
+    out_dir = os.path.join(tmp, "out")
+    sim = rsc.Simulation(cfg)
+    reps = rsc.run(sim, 3, out_dir)
+    for r in reps:
+        print("scene_io step", r.step, "pairs", r.c_groups, "newton", r.newton_iterations, "pgs", r.pgs_iterations_total)
+    with open(os.path.join(HERE, "scene_io.scn"), "w") as fh:
+        fh.write(SCENE_IO_TEXT)
+    with open(os.path.join(HERE, "scene_io.json"), "w") as fh:
+        json.dump(summary, fh, indent=1)
+    shutil.copy(os.path.join(out_dir, "metrics.csv"), os.path.join(HERE, "scene_io_metrics.csv"))
+    for st in (0, 2):
+        shutil.copy(os.path.join(out_dir, "snapshots", f"step_{st:06d}.bin"),
+                    os.path.join(HERE, f"scene_io_step_{st:06d}.bin"))
+    save("scene_io.npz", **arrays)
+    shutil.rmtree(tmp)
+
+
 if __name__ == "__main__":
-    kat_rebuild()
-    kat_pgs()
-    kat_frames()
-    kat_linalg()
-    scenes()
-    scenes_standard()
+    which = sys.argv[1:] or ["kat_rebuild", "kat_pgs", "kat_frames", "kat_linalg", "scenes", "scenes_standard",
+                             "scene_io"]
+    for name in which:
+        globals()[name]()

@@ -2,6 +2,8 @@
 trajectories produced by the reference (tests/golden), plus the corotational
 material's own checks (reduction to linear, rigid-rotation invariance)."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -155,3 +157,44 @@ def test_scheme_equivalence_frozen_frames(cn, golden):
     for oid in fast.dv_by_object:
         a, b = fast.dv_by_object[oid], std.dv_by_object[oid]
         assert float((a - b).abs().max()) <= 1e-8 * max(float(a.abs().max()), 1e-300)
+
+
+def test_scene_file_run_outputs_match_reference(cn, tmp_path):
+    """load_scene + run() on the reference-written scene fixture: metrics.csv rows and
+    snapshot files against the reference's own outputs (scene.py:541-547, 771-908)."""
+    import csv
+    import shutil
+
+    from conftest import GOLDEN
+    from paper_2306_06946_b200 import scene as sc
+
+    path = tmp_path / "io.scn"
+    shutil.copy(os.path.join(GOLDEN, "scene_io.scn"), path)
+    sim = cn.Simulation(sc.load_scene(str(path)))
+    sc.run(sim, 3, str(tmp_path / "out"))
+    with open(os.path.join(GOLDEN, "scene_io_metrics.csv")) as fh:
+        ref = list(csv.DictReader(fh))
+    with open(tmp_path / "out" / "metrics.csv") as fh:
+        got = list(csv.DictReader(fh))
+    assert len(got) == len(ref) == 3
+    for g, r in zip(got, ref):
+        for k in ("step", "c_groups", "dofs", "newton_iterations", "pgs_iterations_total"):
+            assert int(g[k]) == int(r[k]), (k, g[k], r[k])
+        assert float(g["time"]) == float(r["time"])
+        for k in ("pen_before", "pen_after", "lambda_n_sum", "lambda_n_max", "lambda_t_max"):
+            a, b = float(g[k]), float(r[k])
+            assert abs(a - b) <= 1e-6 * max(abs(b), 1e-12) + 1e-12, (k, a, b)
+    for step in (0, 2):
+        mine = sc.load_snapshot(str(tmp_path / "out" / "snapshots" / f"step_{step:06d}.bin"))
+        ref_s = sc.load_snapshot(os.path.join(GOLDEN, f"scene_io_step_{step:06d}.bin"))
+        assert (mine.step, mine.time) == (ref_s.step, ref_s.time)
+        assert [(o[0], o[1], len(o[2]), len(o[3])) for o in mine.objects] == \
+            [(o[0], o[1], len(o[2]), len(o[3])) for o in ref_s.objects]
+        for a, b in zip(mine.objects, ref_s.objects):
+            for x, y in ((a[2], b[2]), (a[3], b[3])):
+                if len(y):
+                    assert np.abs(x - y).max() <= 1e-6 * np.abs(y).max()
+        assert [(p[0], p[1]) for p in mine.pairs] == [(p[0], p[1]) for p in ref_s.pairs]
+        for a, b in zip(mine.pairs, ref_s.pairs):
+            for x, y in zip(a[2:], b[2:]):
+                assert np.abs(np.asarray(x) - np.asarray(y)).max() <= 1e-6 * max(np.abs(y).max(), 1e-3)
