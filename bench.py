@@ -679,7 +679,8 @@ def run_gpu_cfg4(args, rank, world):
     ach = pgs_bytes / (pgs_ms * 1e-3) / 1e9 if pgs_ms > 0 else 0.0
     roof = {"kernel": "pgs_copy_kernel (one CTA per copy, exact-order projected Gauss-Seidel, dense W)",
             "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "peak_source": src,
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": cfg4_ncu_traffic_last_launch(), "peak_source": src,
+            "traffic_unit": "dram bytes of the last Newton iteration's launch (profiles/r01_cfg4_pgs_traffic.json)",
             "algorithmic_bytes_per_launch": pgs_bytes, "ms_per_launch": round(pgs_ms, 4),
             "launch": "last Newton iteration of the last timed step"}
     line = {
@@ -706,6 +707,17 @@ def run_gpu_cfg4(args, rank, world):
         "clocks": clk.summary(int(os.environ.get("LOCAL_RANK", 0))),
     }
     return line
+
+
+def cfg4_ncu_traffic_last_launch():
+    """DRAM read+write bytes of the last batched PGS launch of a cfg4 step, from the
+    committed ncu launch list (tools/gpu_ncu_cfg4.sh)."""
+    p = os.path.join(ROOT, "profiles", "r01_cfg4_pgs_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)["launches"][-1]["dram_bytes"]
+    except (OSError, KeyError, IndexError, ValueError):
+        return None
 
 
 class _PgsBatchTimer:
