@@ -55,3 +55,29 @@ def test_gloo_two_rank_shard_reduce_is_exact():
     mp.spawn(_worker, args=(world, port, U, out), nprocs=world, join=True)
     for r in range(world):
         assert np.array_equal(out[r], U)
+
+
+def test_cfg4_copy_partition_covers_every_copy_once():
+    """Scene-parallel cfg4: ranks take contiguous, disjoint copy ranges that cover
+    all copies for every world size the scaling run uses (bench.cfg4_copy_range)."""
+    import bench
+
+    for world in (1, 2, 3, 4, 8):
+        seen = []
+        for rank in range(world):
+            a, b = bench.cfg4_copy_range(rank, world)
+            assert 0 <= a <= b <= bench.CFG4_COPIES
+            seen.extend(range(a, b))
+        assert seen == list(range(bench.CFG4_COPIES))
+
+
+def test_cfg4_draws_are_per_copy_seeded():
+    """Copy i's tilt, mu and jitter depend only on i (rng([4, i])), so any rank
+    split reproduces the same copies."""
+    from paper_2306_06946_b200.batch import cfg4_draws
+
+    t_all, m_all, j_all = cfg4_draws(0, 6, 12)
+    t_part, m_part, j_part = cfg4_draws(3, 3, 12)
+    assert np.array_equal(t_all[3:], t_part) and np.array_equal(m_all[3:], m_part)
+    assert np.array_equal(j_all[3:], j_part)
+    assert (t_all >= 0).all() and (t_all <= 20).all() and (m_all >= 0.2).all() and (m_all <= 0.8).all()
