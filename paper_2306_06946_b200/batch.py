@@ -23,6 +23,7 @@ the data path.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -118,6 +119,7 @@ class BatchedPlaneScenes:
         self._fext = self.body._fext(self.gravity)
         self.time = 0.0
         self.step_index = 0
+        self._prev_sweeps = None
         self._status = _lib.status(d)
         self.last = {}
 
@@ -176,7 +178,13 @@ class BatchedPlaneScenes:
     def step(self):
         ns, n, h = self.ns, self.n, self.h
         st = _lib.stream()
+        if self.last.get("iters_all"):
+            # after the previous step (its kernels are done once detection syncs below)
+            self._pending_sweeps = self.last["iters_all"][0]
         P = self._detect()
+        if getattr(self, "_pending_sweeps", None) is not None:
+            self._prev_sweeps = self._pending_sweeps[:, 0].cpu().numpy().astype(np.float64)
+            self._pending_sweeps = None
         m = P["m"]
         # free motion
         dv_free = self._solve(self._rhs())
@@ -202,6 +210,7 @@ class BatchedPlaneScenes:
             ics = []
             rot = dv.zeros(1)
             g_off = np.ascontiguousarray(P["poff_h"])
+            order = self._launch_order(P["cnt"])
             w_off = np.ascontiguousarray(P["woff_h"][:-1])
             mus = np.ascontiguousarray(self.mus)
             Dk = D
@@ -218,7 +227,7 @@ class BatchedPlaneScenes:
                 ics.append(ic)
                 _lib.call("cnb_pgs_batched", ns, g_off.ctypes.data, w_off.ctypes.data, mus.ctypes.data, W.data_ptr(),
                           delta.data_ptr(), h, self.pgs_tol, self.pgs_max, lam.data_ptr(), dend.data_ptr(),
-                          eps.data_ptr(), ic.data_ptr(), self._status.ptr, st)
+                          eps.data_ptr(), ic.data_ptr(), order.ctypes.data, self._status.ptr, st)
                 _lib.call("cnb_apply_dt", m, Dk.data_ptr(), lam.data_ptr(), t.data_ptr(), acc.data_ptr(), st)
                 _lib.call("cnb_batch_prox", ns, m, P["poff"].data_ptr(), P["woff"].data_ptr(), Wg.data_ptr(),
                           t.data_ptr(), h, pa.data_ptr(), st)
@@ -234,6 +243,17 @@ class BatchedPlaneScenes:
         self.time += h
         self.step_index += 1
         return m
+
+    def _launch_order(self, cnt):
+        """Batched-PGS launch order: expected work (the previous step's first-iteration
+        sweeps, which dominate, times c_s^2) descending, so the longest solves start
+        first; the previous step's counts are complete once this step's detection has
+        synchronised."""
+        prev = self._prev_sweeps
+        if os.environ.get("CNB_BATCH_ORDER", "1") == "0":  # diagnostic: launch in copy order
+            return np.arange(len(cnt), dtype=np.int32)
+        work = cnt.astype(np.float64) ** 2 * (prev if prev is not None else 1.0)
+        return np.ascontiguousarray(np.argsort(-work, kind="stable").astype(np.int32))
 
     def check(self):
         """Raise the reference's exception for a device-side failure (synchronises)."""

@@ -2635,7 +2635,8 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
 // the scene's group offset g_off[s].  Host arrays describe the scenes.
 int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off, const double* mu, const double* W,
                     const double* delta_base, double h, double tol, int32_t max_iter, double* lam, double* delta_end,
-                    double* eps_hist, int32_t* iters_conv, cnb_status_t* d_status, void* stream) {
+                    double* eps_hist, int32_t* iters_conv, const int32_t* order, cnb_status_t* d_status,
+                    void* stream) {
   if (nscenes <= 0) return CNB_OK;
   if (max_iter < 1) {
     set_error("pgs_batched: max_iter must be positive");
@@ -2655,10 +2656,17 @@ int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off,
   if (rc) return rc;
   PgsScene* hs = (PgsScene*)pin.p;
   int64_t gmax = 0;
-  for (int i = 0; i < nscenes; ++i) {
+  for (int k = 0; k < nscenes; ++k) {
+    // launch order: CTA k solves scene order[k] (heaviest expected first, so the
+    // longest solves do not start in the last wave); identity without order
+    const int i = order ? order[k] : k;
+    if (i < 0 || i >= nscenes) {
+      set_error("pgs_batched: order[%d] = %d out of range", k, i);
+      return CNB_E_VALIDATION;
+    }
     const int64_t G = g_off[i + 1] - g_off[i];
     gmax = std::max(gmax, G);
-    PgsScene& sc = hs[i];
+    PgsScene& sc = hs[k];
     sc.groups = G;
     sc.W = W + w_off[i];
     sc.ldw = 3 * G + (G & 1);  // even row stride (16-byte aligned rows)

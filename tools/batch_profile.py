@@ -86,7 +86,7 @@ def main():
         for rep in range(2):
             e0.record()
             _lib.call("cnb_pgs_batched", k, g_off.ctypes.data, w_off.ctypes.data, mus.ctypes.data, W.data_ptr(),
-                      delta.data_ptr(), B.h, 0.0, SW, lam.data_ptr(), dend.data_ptr(), eps.data_ptr(), ic.data_ptr(),
+                      delta.data_ptr(), B.h, 0.0, SW, lam.data_ptr(), dend.data_ptr(), eps.data_ptr(), ic.data_ptr(), None,
                       st.ptr, _lib.stream())
             e1.record()
         torch.cuda.synchronize()
@@ -100,7 +100,7 @@ def main():
         w_off = np.ascontiguousarray(P["woff_h"][:1])
         mus = np.ascontiguousarray(B.mus[:1])
         _lib.call("cnb_pgs_batched", 1, g_off.ctypes.data, w_off.ctypes.data, mus.ctypes.data, W.data_ptr(),
-                  delta.data_ptr(), B.h, 0.0, SW, lam.data_ptr(), dend.data_ptr(), eps.data_ptr(), ic.data_ptr(),
+                  delta.data_ptr(), B.h, 0.0, SW, lam.data_ptr(), dend.data_ptr(), eps.data_ptr(), ic.data_ptr(), None,
                   st.ptr, _lib.stream())
         torch.cuda.synchronize()
         _lib.check(_lib.lib().cnb_pgs_profile(buf), "profile")
