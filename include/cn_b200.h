@@ -196,6 +196,10 @@ int cnb_pgs_profile(double* out);
  * since the last call: out[0] loads, [1] factor, [2] store L, [3] inverse,
  * [4] store L^{-1}, out[7] launches. */
 int cnb_potrf_profile(double* out);
+/* Diagnostic: fp64 DMMA GEMM tile-shape variants, C = A B (row-major; sizes
+ * multiples of the variant's tile). */
+int cnb_bench_gemm(int32_t variant, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                   int64_t ldb, double* C, int64_t ldc, void* stream);
 
 /* Diagnostic: cycles per group of the PGS block solve while the other warps of
  * the CTA generate load of kind `mode` (0 idle, 1 LDS, 2 SHFL, 3 global polls,

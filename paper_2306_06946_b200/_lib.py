@@ -52,6 +52,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_pgs_work_bytes": [I64],
     "cnb_pgs_profile": [P],
     "cnb_potrf_profile": [P],
+    "cnb_bench_gemm": [I32, I64, I64, I64, P, I64, P, I64, P, I64, P],
     "cnb_bench_block_solve": [I32, I32, P, P],
     "cnb_bench_contention": [I32, I32, P, P],
     "cnb_pgs": [I64, P, I64, P, F64, F64, F64, I32, P, P, P, P, P, P, P],

@@ -40,11 +40,11 @@ constexpr int kEaBatch = 8;
 __global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                          double* __restrict__ front) {
   const int32_t p = tasks[3 * blockIdx.x], lo = tasks[3 * blockIdx.x + 1], hi = tasks[3 * blockIdx.x + 2];
-  const int64_t fp = d_nc(S, p) + d_nr(S, p);
+  const int64_t ldp = d_ldf(S, p);
   double* Fp = front + S.front_off[p];
   for (int64_t ci = S.child_ptr[p]; ci < S.child_ptr[p + 1]; ++ci) {
     const int64_t c = S.child[ci];
-    const int64_t ncc = d_nc(S, c), nrc = d_nr(S, c), fc = ncc + nrc;
+    const int64_t ncc = d_nc(S, c), nrc = d_nr(S, c), ldc = d_ldf(S, c);
     const int32_t* __restrict__ rel = S.rel + S.rel_ptr[c];
     int64_t a = 0, b = nrc;
     while (a < b) {
@@ -60,8 +60,8 @@ __global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t
     const int64_t k1 = a;
     const double* Fc = front + S.front_off[c];
     for (int64_t k = k0; k < k1; ++k) {
-      const double* __restrict__ uc = Fc + (ncc + k) * fc + ncc;
-      double* fcol = Fp + (int64_t)rel[k] * fp;
+      const double* __restrict__ uc = Fc + (ncc + k) * ldc + ncc;
+      double* fcol = Fp + (int64_t)rel[k] * ldp;
       for (int64_t i0 = k + threadIdx.x; i0 < nrc; i0 += (int64_t)kEaBatch * blockDim.x) {
         int32_t ri[kEaBatch];
         double u[kEaBatch], v[kEaBatch];
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
   __shared__ double y[kPanel][kPanel + 1];
   __shared__ double rd[kPanel];
   const int64_t s = tasks[blockIdx.x];
-  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldf = d_ldf(S, s);
   const int kw = (int)min((int64_t)kPanel, nc - k0);
   double* F = front + S.front_off[s];
   const int i = threadIdx.x;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
   ts[0] = clock64();
 #pragma unroll 8
   for (int l = 0; l < kPanel; ++l)  // lane i loads row i, column by column: coalesced over rows
-    a[i][l] = (i < kw && l < kw && l <= i) ? F[(int64_t)(k0 + l) * f + k0 + i] : (l == i ? 1.0 : 0.0);
+    a[i][l] = (i < kw && l < kw && l <= i) ? F[(int64_t)(k0 + l) * ldf + k0 + i] : (l == i ? 1.0 : 0.0);
   __syncwarp();
   ts[1] = clock64();
   for (int j = 0; j < kPanel; ++j) {
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
   ts[2] = clock64();
 #pragma unroll 8
   for (int l = 0; l < kw; ++l)
-    if (i < kw && l <= i) F[(int64_t)(k0 + l) * f + k0 + i] = a[i][l];
+    if (i < kw && l <= i) F[(int64_t)(k0 + l) * ldf + k0 + i] = a[i][l];
   ts[3] = clock64();
   // Y = L^{-1}: lane c owns column c; step r: y[r][c] *= 1/L[r][r] (= rd[r]), then
   // rows below subtract L[q][r] y[r][c]
@@ -202,14 +202,14 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
   __shared__ double Is[kPanel * LD];
   const int64_t s = tasks[2 * blockIdx.x];
   const int64_t chunk = tasks[2 * blockIdx.x + 1];
-  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldf = d_ldf(S, s);
   const int kw = (int)min((int64_t)kPanel, nc - k0);
   double* F = front + S.front_off[s];
   const int64_t r0 = k0 + kw + chunk * 64;
   for (int e = threadIdx.x; e < 64 * kPanel; e += blockDim.x) {
     const int rr = e % 64, k = e / 64;
     const int64_t r = r0 + rr;
-    cp_async8(&As[k * LK + rr], F + (int64_t)(k0 + k) * f + r, r < f && k < kw);
+    cp_async8(&As[k * LK + rr], F + (int64_t)(k0 + k) * ldf + r, r < f && k < kw);
   }
   const double* Y = kkinv + (S.kk_off[s] + k0 / kPanel) * (kPanel * kPanel);
   for (int e = threadIdx.x; e < kPanel * kPanel; e += blockDim.x)
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
       for (int hh = 0; hh < 2; ++hh) {
         const int64_t r = r0 + 16 * warp + 8 * a + g;
         const int j = 8 * b + 2 * t + hh;
-        if (r < f && j < kw) F[(int64_t)(k0 + j) * f + r] = acc[a][b][hh];
+        if (r < f && j < kw) F[(int64_t)(k0 + j) * ldf + r] = acc[a][b][hh];
       }
 }
 
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
   double* Pj = syrk_sm + 2 * kPanel * kSK;
   const int64_t s = tasks[3 * blockIdx.x];
   const int ti = tasks[3 * blockIdx.x + 1], tj = tasks[3 * blockIdx.x + 2];
-  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldf = d_ldf(S, s);
   constexpr int64_t blk = (int64_t)kBlkPanels * kPanel;
   const int64_t k0p = (int64_t)p * kPanel;
   int64_t k0, kw, t0, cend;
@@ -286,16 +286,27 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
   }
   const int64_t r0 = t0 + (int64_t)ti * kTile, c0 = t0 + (int64_t)tj * kTile;
   double* F = front + S.front_off[s];
+  // 16-byte copies of row pairs: the front columns are 16-byte aligned (even
+  // stride), so a tile whose first row is odd is staged from the row before
+  // (uniform shift sa / sb inside the staged tile, read back with the fragments)
+  const int sa = (int)(r0 & 1), sb = (int)(c0 & 1);
+  constexpr int kPairs = kTile / 2 + 1;  // 33 pairs cover 64 rows at either parity
+  static_assert(2 * kPairs <= kSK, "staged tile stride too small");
   auto stage = [&](int buf, int64_t kk0) {
     double* A = Pi + buf * kPanel * kSK;
     double* B = Pj + buf * kPanel * kSK;
-    for (int e = threadIdx.x; e < kTile * kPanel; e += blockDim.x) {
-      const int rr = e % kTile, kc = e / kTile;
+    for (int e = threadIdx.x; e < kPanel * kPairs; e += blockDim.x) {
+      const int kc = e / kPairs, rr = 2 * (e - kc * kPairs);
       const bool kin = kk0 + kc < kw;
-      const int64_t ri = r0 + rr, rj = c0 + rr;
-      const double* col = F + (k0 + kk0 + kc) * f;
-      cp_async8(&A[kc * kSK + rr], col + ri, kin && ri < f);
-      cp_async8(&B[kc * kSK + rr], col + rj, kin && rj < cend);
+      const int64_t ri = r0 - sa + rr, rj = c0 - sb + rr;
+      const double* col = F + (k0 + kk0 + kc) * ldf;
+      const bool va = kin && ri < f, vb = kin && rj < f;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(A + kc * kSK + rr)),
+                   "l"(va ? col + ri : F), "r"(va ? 16 : 0)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(B + kc * kSK + rr)),
+                   "l"(vb ? col + rj : F), "r"(vb ? 16 : 0)
+                   : "memory");
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -325,9 +336,9 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
       for (int kk = 0; kk < kc; kk += 4) {
         double fa[4], fb[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) fa[a] = A[(kk + t) * kSK + wy + 8 * a + g];
+        for (int a = 0; a < 4; ++a) fa[a] = A[(kk + t) * kSK + sa + wy + 8 * a + g];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) fb[b] = B[(kk + t) * kSK + wx + 8 * b + g];
+        for (int b = 0; b < 4; ++b) fb[b] = B[(kk + t) * kSK + sb + wx + 8 * b + g];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -347,7 +358,7 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
       for (int h = 0; h < 2; ++h) {
         const int64_t r = r0 + wy + 8 * a + g;
         const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-        cv[a][b][h] = (r < f && c < cend && r >= c) ? F[c * f + r] : 0.0;
+        cv[a][b][h] = (r < f && c < cend && r >= c) ? F[c * ldf + r] : 0.0;
       }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
       for (int h = 0; h < 2; ++h) {
         const int64_t r = r0 + wy + 8 * a + g;
         const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-        if (r < f && c < cend && r >= c) F[c * f + r] = cv[a][b][h] - acc[a][b][h];
+        if (r < f && c < cend && r >= c) F[c * ldf + r] = cv[a][b][h] - acc[a][b][h];
       }
 }
 

@@ -59,6 +59,9 @@ struct Symbolic {
 
   int64_t nc(int64_t s) const { return first[s + 1] - first[s]; }
   int64_t nr(int64_t s) const { return rows_ptr[s + 1] - rows_ptr[s]; }
+  // column stride of front s: f rounded up to even, so every front column starts
+  // 16-byte aligned (16-byte asynchronous copies in the dense kernels)
+  int64_t ldf(int64_t s) const { const int64_t x = nc(s) + nr(s); return x + (x & 1); }
   int64_t f(int64_t s) const { return nc(s) + nr(s); }
 };
 

@@ -26,6 +26,11 @@ struct DevSym {
 
 __device__ __forceinline__ int64_t d_nc(const DevSym& S, int64_t s) { return S.first[s + 1] - S.first[s]; }
 __device__ __forceinline__ int64_t d_nr(const DevSym& S, int64_t s) { return S.rows_ptr[s + 1] - S.rows_ptr[s]; }
+// column stride of front s (f rounded up to even: 16-byte aligned columns), Symbolic::ldf
+__device__ __forceinline__ int64_t d_ldf(const DevSym& S, int64_t s) {
+  const int64_t f = d_nc(S, s) + d_nr(S, s);
+  return f + (f & 1);
+}
 
 struct DevTasks {
   int32_t* ptr = nullptr;

@@ -65,6 +65,126 @@ __global__ void latency_kernel(int n, double seed, double* out, long long* cyc) 
   }
 }
 
+// GEMM tile-shape experiments (C = A B, row-major, fp64 DMMA): BM x BN CTA tile,
+// WM x WN warp tiles, BK-deep k chunks double-buffered with cp.async (8- or
+// 16-byte copies), A staged [m][k], B staged [k][n] (both conflict-free
+// fragment reads with strides == 4 mod 16 doubles); VOL: mma as asm volatile.
+__device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+template <int BM, int BN, int WM, int WN, int BK, bool V16, bool VOL>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32) gemm_var_kernel(int64_t M, int64_t N, int64_t K,
+                                                                             const double* __restrict__ A,
+                                                                             int64_t lda,
+                                                                             const double* __restrict__ B,
+                                                                             int64_t ldb, double* __restrict__ C,
+                                                                             int64_t ldc) {
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  constexpr int SA = BK + 4, SB = BN + 4;
+  extern __shared__ __align__(16) double gv_sm[];
+  double* As = gv_sm;                 // [2][BM][SA]
+  double* Bs = gv_sm + 2 * BM * SA;   // [2][BK][SB]
+  const int64_t r0 = (int64_t)blockIdx.y * BM, c0 = (int64_t)blockIdx.x * BN;
+  auto stage = [&](int buf, int64_t k0) {
+    double* Ab = As + buf * BM * SA;
+    double* Bb = Bs + buf * BK * SB;
+    if (V16) {
+      for (int e = threadIdx.x; e < BM * BK / 2; e += NT) {
+        const int rr = e / (BK / 2), kk = 2 * (e % (BK / 2));
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(Ab + rr * SA + kk);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(A + (r0 + rr) * lda + k0 + kk)
+                     : "memory");
+      }
+      for (int e = threadIdx.x; e < BK * BN / 2; e += NT) {
+        const int kk = e / (BN / 2), cc = 2 * (e % (BN / 2));
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(Bb + kk * SB + cc);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb), "l"(B + (k0 + kk) * ldb + c0 + cc)
+                     : "memory");
+      }
+    } else {
+      for (int e = threadIdx.x; e < BM * BK; e += NT) {
+        const int rr = e / BK, kk = e % BK;
+        cp_async8(Ab + rr * SA + kk, A + (r0 + rr) * lda + k0 + kk, true);
+      }
+      for (int e = threadIdx.x; e < BK * BN; e += NT) {
+        const int kk = e / BN, cc = e % BN;
+        cp_async8(Bb + kk * SB + cc, B + (k0 + kk) * ldb + c0 + cc, true);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  constexpr int WX = BN / WN;
+  const int wy = (warp / WX) * WM, wx = (warp % WX) * WN;
+  constexpr int FA = WM / 8, FB = WN / 8;
+  double acc[FA][FB][2];
+#pragma unroll
+  for (int a = 0; a < FA; ++a)
+#pragma unroll
+    for (int b = 0; b < FB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nk = (int)(K / BK);  // experiment: K, M, N multiples of the tile
+  stage(0, 0);
+  for (int ck = 0; ck < nk; ++ck) {
+    if (ck + 1 < nk) {
+      stage((ck + 1) & 1, (int64_t)(ck + 1) * BK);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* Ab = As + (ck & 1) * BM * SA;
+    const double* Bb = Bs + (ck & 1) * BK * SB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double fa[FA], fb[FB];
+#pragma unroll
+      for (int a = 0; a < FA; ++a) fa[a] = Ab[(wy + 8 * a + g) * SA + kk + t];
+#pragma unroll
+      for (int b = 0; b < FB; ++b) fb[b] = Bb[(kk + t) * SB + wx + 8 * b + g];
+#pragma unroll
+      for (int a = 0; a < FA; ++a)
+#pragma unroll
+        for (int b = 0; b < FB; ++b) {
+          if (VOL)
+            dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+          else
+            dmma_nv(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < FA; ++a)
+#pragma unroll
+    for (int b = 0; b < FB; ++b)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int64_t r = r0 + wy + 8 * a + g, c = c0 + wx + 8 * b + 2 * t + hh;
+        C[r * ldc + c] = acc[a][b][hh];
+      }
+}
+
+template <int BM, int BN, int WM, int WN, int BK, bool V16, bool VOL>
+static int launch_gemm_var(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                           int64_t ldb, double* C, int64_t ldc, cudaStream_t st) {
+  if (M % BM || N % BN || K % BK) {
+    set_error("bench_gemm: sizes must be multiples of the tile");
+    return CNB_E_VALIDATION;
+  }
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  const int smem = (int)(2 * (BM * (BK + 4) + BK * (BN + 4)) * sizeof(double));
+  auto kern = gemm_var_kernel<BM, BN, WM, WN, BK, V16, VOL>;
+  CNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid((unsigned)(N / BN), (unsigned)(M / BM));
+  kern<<<grid, NT, smem, st>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  CNB_LAUNCH_CHECK("gemm_var_kernel");
+  return CNB_OK;
+}
+
 }  // namespace cnb
 
 using namespace cnb;
@@ -88,6 +208,25 @@ int cnb_bench_latency(double* out, void* stream) {
   cudaFree(d);
   cudaFree(c);
   return CNB_OK;
+}
+
+// Diagnostic GEMM tile-shape variants (see gemm_var_kernel): C = A B.
+int cnb_bench_gemm(int32_t variant, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                   int64_t ldb, double* C, int64_t ldc, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (variant) {
+    case 0: return launch_gemm_var<64, 64, 32, 32, 32, false, true>(M, N, K, A, lda, B, ldb, C, ldc, st);
+    case 1: return launch_gemm_var<64, 64, 32, 32, 32, true, true>(M, N, K, A, lda, B, ldb, C, ldc, st);
+    case 2: return launch_gemm_var<64, 64, 32, 32, 32, true, false>(M, N, K, A, lda, B, ldb, C, ldc, st);
+    case 3: return launch_gemm_var<128, 64, 64, 32, 32, true, false>(M, N, K, A, lda, B, ldb, C, ldc, st);
+    case 4: return launch_gemm_var<128, 128, 64, 32, 32, true, false>(M, N, K, A, lda, B, ldb, C, ldc, st);
+    case 5: return launch_gemm_var<128, 128, 64, 32, 16, true, false>(M, N, K, A, lda, B, ldb, C, ldc, st);
+    case 6: return launch_gemm_var<64, 128, 32, 64, 32, true, false>(M, N, K, A, lda, B, ldb, C, ldc, st);
+    case 7: return launch_gemm_var<128, 64, 64, 32, 16, true, false>(M, N, K, A, lda, B, ldb, C, ldc, st);
+    default:
+      set_error("bench_gemm: unknown variant %d", variant);
+      return CNB_E_VALIDATION;
+  }
 }
 
 // TFLOP/s of DMMA over the whole GPU (result written to host out[0]).

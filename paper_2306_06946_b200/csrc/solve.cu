@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
   __shared__ double v[32][kInvCols];
   __shared__ double y[32][kInvCols];
   const int64_t s = tasks[2 * blockIdx.x], j0 = tasks[2 * blockIdx.x + 1];
-  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t nc = d_nc(S, s), ldf = d_ldf(S, s);
   const double* F = front + S.front_off[s];
   double* X = linv + S.linv_off[s];
   const int ncols = (int)min((int64_t)kInvCols, nc - j0);
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
 #pragma unroll
       for (int c = 0; c < kInvCols; ++c) acc[c] = 0.0;
       for (int j = 0; j < bw; ++j) {
-        const double l = F[(kb + j) * f + i];
+        const double l = F[(kb + j) * ldf + i];
 #pragma unroll
         for (int c = 0; c < kInvCols; ++c) acc[c] = fma(l, y[j][c], acc[c]);
       }
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
   __shared__ double As[kMK * kMA];  // [k][row]
   __shared__ double Bs[kMT * kMS];
   const int64_t s = tasks[3 * blockIdx.x], q0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
-  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
+  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), ldf = d_ldf(S, s);
   const double* F = front + S.front_off[s];
   const double* Li = linv + S.linv_off[s];
   double* P = p21 + S.p21_off[s];
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int rr = e % kMT, kk = e / kMT;
       const int64_t q = q0 + rr, k = k0 + kk;
-      cp_async8(&As[kk * kMA + rr], F + k * f + nc + q, q < nr && k < nc);
+      cp_async8(&As[kk * kMA + rr], F + k * ldf + nc + q, q < nr && k < nc);
     }
     for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
       const int kk = e % kMK, cc = e / kMK;

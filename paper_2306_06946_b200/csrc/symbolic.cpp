@@ -460,7 +460,7 @@ int analyze(Symbolic& S, int64_t n, const int64_t* rowptr, const int64_t* col, i
   S.solve_flops_per_rhs = 0.0;
   for (int64_t k = 0; k < ns; ++k) {
     const int64_t f = S.f(k), nc = S.nc(k);
-    S.front_off[k + 1] = S.front_off[k] + f * f;
+    S.front_off[k + 1] = S.front_off[k] + S.ldf(k) * f;
     S.nnz_L += nc * (nc + 1) / 2 + nc * S.nr(k);
     for (int64_t j = 0; j < nc; ++j) {
       const double m = (double)(f - j - 1);
@@ -513,7 +513,7 @@ int analyze(Symbolic& S, int64_t n, const int64_t* rowptr, const int64_t* col, i
         r = S.nc(s) + (it - rs);
       }
       S.map_src.push_back(e);
-      S.map_dst.push_back(S.front_off[s] + c * f + r);
+      S.map_dst.push_back(S.front_off[s] + c * S.ldf(s) + r);
     }
   // per-level task lists
   S.tasks.assign(S.n_levels, LevelTasks());

@@ -48,9 +48,11 @@ def emulate_factor_solve(S, A, b):
     nc = np.diff(S["first"])
     nr = np.diff(S["rows_ptr"])
     f = nc + nr
+    ldf = f + (f & 1)  # front columns are stored with an even stride (16-byte aligned)
+    assert np.array_equal(np.diff(S["front_off"]), ldf * f)
     fronts = np.zeros(S["front_off"][-1])
     fronts[S["map_dst"]] = A.data[S["map_src"]]
-    F = [fronts[S["front_off"][s]:S["front_off"][s + 1]].reshape(f[s], f[s], order="F") for s in range(ns)]
+    F = [fronts[S["front_off"][s]:S["front_off"][s + 1]].reshape(f[s], ldf[s])[:, :f[s]].T.copy() for s in range(ns)]
     children = [S["child"][S["child_ptr"][s]:S["child_ptr"][s + 1]] for s in range(ns)]
     rel = [S["rel"][S["rel_ptr"][s]:S["rel_ptr"][s + 1]] for s in range(ns)]
     for l in range(len(S["level_ptr"]) - 1):
