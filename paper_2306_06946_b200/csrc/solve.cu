@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
         const int64_t c = c0 + wx + 8 * b + 2 * t + hh;
         if (i >= f || c >= ws) continue;
         if (i < nc)
-          Ys[c * nc + i] = acc[a][b][hh];
+          Ys[c * (nc + (nc & 1)) + i] = acc[a][b][hh];
         else
           Rs[c * f + i] -= acc[a][b][hh];
       }
@@ -553,14 +553,31 @@ __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const do
     const int64_t nc = d_nc(S, s);
     const int64_t lo = R.lo[s], w = R.w[s];
     const double* Ys = Y + yoff[s];
+    const int64_t ldy = nc + (nc & 1);  // Y columns 16-byte aligned (panel_mma_kernel)
     for (int64_t k0 = 0; k0 < nc; k0 += kGK) {
       __syncthreads();
-      for (int idx = threadIdx.x; idx < kGK * kGT; idx += blockDim.x) {
-        const int kk = idx % kGK, cc = idx / kGK;
+      // 16-byte copies of k pairs; a pair straddling nc takes its valid element
+      // alone and a zero (the padding entry of Y is never written)
+      for (int idx = threadIdx.x; idx < (kGK / 2) * kGT; idx += blockDim.x) {
+        const int kk = 2 * (idx % (kGK / 2)), cc = idx / (kGK / 2);
         const int64_t k = k0 + kk;
         const int64_t la = ra0 + cc - lo, lb = rb0 + cc - lo;
-        cp_async8(&Ya[cc * kGS + kk], Ys + la * nc + k, k < nc && la >= 0 && la < w);
-        cp_async8(&Yb[cc * kGS + kk], Ys + lb * nc + k, k < nc && lb >= 0 && lb < w);
+        const bool ia = la >= 0 && la < w, ib = lb >= 0 && lb < w;
+        double* da = &Ya[cc * kGS + kk];
+        double* db = &Yb[cc * kGS + kk];
+        if (k + 1 < nc) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(da)),
+                       "l"(ia ? Ys + la * ldy + k : Ys), "r"(ia ? 16 : 0)
+                       : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(db)),
+                       "l"(ib ? Ys + lb * ldy + k : Ys), "r"(ib ? 16 : 0)
+                       : "memory");
+        } else {
+          cp_async8(da, Ys + la * ldy + k, ia && k < nc);
+          cp_async8(db, Ys + lb * ldy + k, ib && k < nc);
+          da[1] = 0.0;
+          db[1] = 0.0;
+        }
       }
       cp_async_wait_all();
       __syncthreads();
@@ -653,7 +670,7 @@ static int build_compliance_plan(const Symbolic& S, int64_t ncols, const int64_t
       P.w[s] = hi[s] - lo[s];
     }
     P.roff[s + 1] = P.roff[s] + S.f(s) * P.w[s];
-    P.yoff[s + 1] = P.yoff[s] + S.nc(s) * P.w[s];
+    P.yoff[s + 1] = P.yoff[s] + (S.nc(s) + (S.nc(s) & 1)) * P.w[s];  // even column stride
     const double nc = (double)S.nc(s), nr = (double)S.nr(s), w = (double)P.w[s];
     P.fwd_flops += w * (nc * nc + 2.0 * nc * nr);
   }
