@@ -36,8 +36,8 @@ __global__ void scatter_kernel(int64_t nmap, const int64_t* __restrict__ src, co
 // Rows are processed in batches of kEaBatch per thread: all loads of a batch
 // are issued before its stores (the parent and child fronts live in one
 // buffer, so the compiler could not reorder them otherwise).
-constexpr int kEaBatch = 8;
-__global__ void __launch_bounds__(256) extend_add_kernel(DevSym S, const int32_t* __restrict__ tasks,
+constexpr int kEaBatch = 4;
+__global__ void __launch_bounds__(256, 6) extend_add_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                          double* __restrict__ front) {
   const int32_t p = tasks[3 * blockIdx.x], lo = tasks[3 * blockIdx.x + 1], hi = tasks[3 * blockIdx.x + 2];
   const int64_t ldp = d_ldf(S, p);
