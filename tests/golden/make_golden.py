@@ -246,6 +246,73 @@ def kat_linalg():
          K_data=K.data, masses=body.masses())
 
 
+def ellipsoid_mesh(semi=(0.05, 0.03, 0.025), spacing=0.008, seed=0):
+    """Small cfg2-style body: jittered lattice inside an ellipsoid, Delaunay tets,
+    centroid-inside / sliver filter, positive orientation."""
+    from scipy.spatial import Delaunay
+
+    rng = np.random.default_rng(seed)
+    a = np.asarray(semi)
+    axes = [np.arange(-ai, ai + 1e-12, spacing) for ai in a]
+    P = np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1).reshape(-1, 3)
+    P = P + rng.uniform(-0.25 * spacing, 0.25 * spacing, P.shape)
+    P = P[((P / a) ** 2).sum(axis=1) <= 1.0]
+    tri = Delaunay(P)
+    T = tri.simplices.astype(np.int64)
+    cen = P[T].mean(axis=1)
+    T = T[((cen / a) ** 2).sum(axis=1) <= 1.0]
+    v = np.einsum("ij,ij->i", np.cross(P[T[:, 1]] - P[T[:, 0]], P[T[:, 2]] - P[T[:, 0]]), P[T[:, 3]] - P[T[:, 0]]) / 6
+    T[v < 0] = T[v < 0][:, [0, 2, 1, 3]]
+    T = T[np.abs(v) >= 1e-3 * spacing ** 3]
+    used = np.unique(T)
+    remap = -np.ones(len(P), dtype=np.int64)
+    remap[used] = np.arange(len(used))
+    return P[used], remap[T]
+
+
+def cylinder_surface(radius=0.015, length=0.06, n_theta=24, n_z=6):
+    """Open cylinder (side surface) along z through the origin, outward wound."""
+    th = np.linspace(0.0, 2 * np.pi, n_theta, endpoint=False)
+    zs = np.linspace(-0.5 * length, 0.5 * length, n_z + 1)
+    pts = np.array([[radius * np.cos(t), radius * np.sin(t), z] for z in zs for t in th])
+    tris = []
+    for k in range(n_z):
+        for j in range(n_theta):
+            a, b = k * n_theta + j, k * n_theta + (j + 1) % n_theta
+            c, d = a + n_theta, b + n_theta
+            tris += [[a, b, d], [a, d, c]]
+    tris = np.array(tris, dtype=np.int64)
+    n0 = np.cross(pts[tris[:, 1]] - pts[tris[:, 0]], pts[tris[:, 2]] - pts[tris[:, 0]])
+    out = pts[tris].mean(axis=1) * np.array([1.0, 1.0, 0.0])
+    flip = np.einsum("ij,ij->i", n0, out) < 0
+    tris[flip] = tris[flip][:, ::-1]
+    return pts, tris
+
+
+def cylinder_press():
+    """cfg2-style reference run: soft ellipsoid with its bottom 5 % fixed, pressed by a
+    rigid cylinder rotating at 1 rad/s about its own axis (kinematic mesh), mu = 0.3,
+    forced fast-scheme iterations with re-linearisation."""
+    nodes, tets = ellipsoid_mesh()
+    fixed = np.argsort(nodes[:, 1], kind="stable")[: max(1, len(nodes) // 20)]
+    top = float(nodes[:, 1].max())
+    pts, tris = cylinder_surface()
+    center = (0.0, top + 0.015 - 0.003, 0.0)  # 3 mm indentation
+    soft = rsc.SoftSpec(name="ellipsoid", mesh=cn.TetMesh(nodes, tets), young=3e3, poisson=0.45, density=1000.0,
+                        fixed_nodes=np.sort(fixed))
+    cyl = rsc.KinematicMeshSpec(name="cylinder", points=pts + np.asarray(center), triangles=tris,
+                                motion=rsc.MotionSpec(axis=(0.0, 0.0, 1.0), center=center, angular_velocity=1.0))
+    cfg = rsc.SceneConfig(objects=[soft, cyl], h=0.01, threshold=0.004,
+                          pgs=rsol.PgsConfig(max_iterations=400, tolerance=1e-10, friction=0.3),
+                          newton=rsol.NewtonConfig(scheme="fast", max_iterations=4, penetration_tol=-1,
+                                                   rotation_tol=-1),
+                          output=rsc.OutputConfig(snapshots=False, metrics=False))
+    out = _run_scene(cfg, 3, {0, 2}, tag="cylinder_press")
+    out.update(nodes=nodes, tets=tets, fixed=np.sort(fixed), cyl_points=pts + np.asarray(center), cyl_tris=tris,
+               center=np.asarray(center))
+    save("cylinder_press.npz", **out)
+
+
 SCENE_IO_TEXT = """\
 # scene-format fixture: soft box on the ground, pushed by a moving plate
 gravity: [0.0, -9.81, 0.0]
@@ -322,6 +389,6 @@ def scene_io():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kat_rebuild", "kat_pgs", "kat_frames", "kat_linalg", "scenes", "scenes_standard",
-                             "scene_io"]
+                             "scene_io", "cylinder_press"]
     for name in which:
         globals()[name]()

@@ -198,3 +198,26 @@ def test_scene_file_run_outputs_match_reference(cn, tmp_path):
         for a, b in zip(mine.pairs, ref_s.pairs):
             for x, y in zip(a[2:], b[2:]):
                 assert np.abs(np.asarray(x) - np.asarray(y)).max() <= 1e-6 * max(np.abs(y).max(), 1e-3)
+
+
+def test_cylinder_press_cfg2_style(cn, golden):
+    """cfg2-style scene against the reference: Delaunay ellipsoid with its bottom 5 %
+    fixed, pressed by a kinematic cylinder rotating about its own axis (mesh-mesh
+    pairs in both directions, LOCAL attachments on the moving collider, forced
+    re-linearised fast iterations), 3 steps."""
+    g = golden("cylinder_press.npz")
+    soft = cn.SoftSpec(name="ellipsoid", mesh=cn.TetMesh(g["nodes"], g["tets"]), young=3e3, poisson=0.45,
+                       density=1000.0, fixed_nodes=g["fixed"])
+    cyl = cn.KinematicMeshSpec(name="cylinder", points=g["cyl_points"], triangles=g["cyl_tris"],
+                               motion=cn.MotionSpec(axis=(0.0, 0.0, 1.0), center=tuple(g["center"]),
+                                                    angular_velocity=1.0))
+    cfg = cn.SceneConfig(objects=[soft, cyl], h=0.01, threshold=0.004,
+                         pgs=cn.PgsConfig(max_iterations=400, tolerance=1e-10, friction=0.3),
+                         newton=cn.NewtonConfig(scheme="fast", max_iterations=4, penetration_tol=-1.0,
+                                                rotation_tol=-1.0),
+                         output=cn.OutputConfig(snapshots=False, metrics=False))
+    sim = cn.Simulation(cfg)
+    _run_and_compare(sim, g, 3, 1)
+    # fixed nodes stay at rest
+    q = _h(sim.objects[0].state.q).reshape(-1, 3)
+    assert np.array_equal(q[g["fixed"]], g["nodes"][g["fixed"]])
