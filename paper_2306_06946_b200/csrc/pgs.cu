@@ -1298,6 +1298,69 @@ __device__ __forceinline__ void block_solve_v4(const double* __restrict__ Wt, in
   }
 }
 
+// block_solve_v4 that also accumulates, for the NEXT block, dn += h^2 W[next, this]
+// (lambda change) group by group from the broadcast changes: Wn holds the rows of
+// the next block (lane l <-> its group l) over the columns of this block, stride
+// ld.  The extra loads / FMAs are independent of the sequential chain.
+template <bool FRIC>
+__device__ __forceinline__ void block_solve_v5(const double* __restrict__ Wt, const double* __restrict__ Wn, int ld,
+                                               int ng, int lane, double dl_[3], double dn[3], const double lm[3],
+                                               const GroupConst& kc, double mu, double h2, double* __restrict__ sv) {
+  const double* wrow = Wt + 3 * lane * ld;
+  const double* nrow = Wn + 3 * lane * ld;
+  const double h2l1 = h2 * lm[1], h2l2 = h2 * lm[2];
+  const double nl0 = -lm[0], lhw = lm[0] * kc.hwnn, nihw = -kc.ihw;
+#pragma unroll 2
+  for (int g = 0; g < ng; ++g) {
+    double w[9], wn[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        w[3 * a + c] = wrow[a * ld + 3 * g + c];
+        wn[3 * a + c] = nrow[a * ld + 3 * g + c];
+      }
+    const double d0 = dl_[0], d1 = dl_[1], d2 = dl_[2];
+    const bool open = d0 < lhw;
+    const double x = fma(nihw, d0, lm[0]);
+    const double dln = open ? d0 * nihw : nl0;
+    double dh0 = h2 * dln, dh1, dh2;
+    if (FRIC) {
+      const double a0 = fma(-kc.it00, d1, fma(-kc.it01, d2, lm[1]));
+      const double a1 = fma(-kc.it10, d1, fma(-kc.it11, d2, lm[2]));
+      const double lt0 = fma(-kc.b0, dln, a0), lt1 = fma(-kc.b1, dln, a1);
+      const double radius = mu * x;
+      const double n2 = fma(lt0, lt0, lt1 * lt1);
+      const bool proj = n2 > radius * radius;
+      double y;
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(n2));
+      const double e = fma(-0.5 * n2, y * y, 1.5);
+      const double ry = radius * y;
+      const double hl0 = h2 * lt0, hl1 = h2 * lt1;
+      const double p0 = fma(hl0 * ry, e, -h2l1), p1 = fma(hl1 * ry, e, -h2l2);
+      const double u0 = hl0 - h2l1, u1 = hl1 - h2l2;
+      dh1 = open ? (proj ? p0 : u0) : -h2l1;
+      dh2 = open ? (proj ? p1 : u1) : -h2l2;
+    } else {
+      dh1 = -h2l1;
+      dh2 = -h2l2;
+    }
+    const double s0 = __shfl_sync(0xffffffffu, dh0, g);
+    const double s1 = __shfl_sync(0xffffffffu, dh1, g);
+    const double s2 = __shfl_sync(0xffffffffu, dh2, g);
+    asm volatile(
+        "{\n .reg .pred p;\n setp.eq.s32 p, %0, %1;\n"
+        " @p st.shared.v2.f64 [%2], {%3, %4};\n @p st.shared.v2.f64 [%2+16], {%5, %6};\n}\n" ::"r"(lane),
+        "r"(g), "r"(smem_u32(sv + 4 * g)), "d"(x), "d"(dh1), "d"(dh2), "d"(open ? 1.0 : 0.0)
+        : "memory");
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      dl_[a] = fma(w[3 * a + 2], s2, fma(w[3 * a + 1], s1, fma(w[3 * a], s0, dl_[a])));
+      dn[a] = fma(wn[3 * a + 2], s2, fma(wn[3 * a + 1], s1, fma(wn[3 * a], s0, dn[a])));
+    }
+  }
+}
+
 // lambda of the lane's group from its block_solve_v4 record; dsq += |change|^2;
 // returns the error flag (W_nn <= 0, or a singular tangential block when used)
 __device__ __forceinline__ int block_commit(const double* sv, int lane, double lm[3], const GroupConst& kc,
@@ -1468,11 +1531,13 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           dl[a] = mine ? sm.dcur[3 * lane + a] : 0.0;
         }
         if (!(dbg & 2)) asm volatile("bar.arrive 2, %0;" ::"n"(64 + 32 * kXW));  // dcur, lamn consumed
+        stamp(13);
         if (s.mu != 0.0)
           block_solve_v4<true>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv);
         else
           block_solve_v4<false>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv);
         __syncwarp();
+        stamp(14);
         const int err = mine ? block_commit(sm.sv, lane, lm, kc, s.mu, ih2, dsq) : 0;
         const unsigned bad = __ballot_sync(0xffffffffu, err);
         if (bad) {
@@ -2263,7 +2328,13 @@ __global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double*
     dl_[0] = -1e-4 * (1.0 + 0.01 * lane);
     dl_[1] = ((V & 4) ? 3e-4 : 3e-5) * sin(1.0 * lane);  // V bit 2: tangential loads outside the cone
     dl_[2] = ((V & 4) ? 3e-4 : 3e-5) * cos(1.0 * lane);
-    if (V & 64) {
+    if (V & 128) {
+      double dn[3] = {0.0, 0.0, 0.0};
+      block_solve_v5<true>(T, T + 3, kPR, kPG, lane, dl_, dn, lm, kc, 0.4, h2, T + kBR * kLDT);
+      __syncwarp();
+      err |= block_commit(T + kBR * kLDT, lane, lm, kc, 0.4, 1.0 / h2, dsq);
+      dsq += dn[0] + dn[1] + dn[2];
+    } else if (V & 64) {
       block_solve_v4<true>(T, kPR, kPG, lane, dl_, lm, kc, 0.4, h2, T + kBR * kLDT);
       __syncwarp();
       err |= block_commit(T + kBR * kLDT, lane, lm, kc, 0.4, 1.0 / h2, dsq);
@@ -2281,7 +2352,7 @@ __global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double*
   long long t1 = clock64();
   const double s = warp_sum(lm[0] + lm[1] + lm[2] + dsq);
   if (lane == 0) {
-    out[0] = (double)(t1 - t0) / ((double)reps * ((V & 64) ? kPG : kBG));
+    out[0] = (double)(t1 - t0) / ((double)reps * ((V & 192) ? kPG : kBG));
     out[1] = s;
   }
 }
@@ -2545,6 +2616,7 @@ int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stre
     case 11: CNB_BBS(20) break;
     case 12: CNB_BBS(32) break;
     case 13: CNB_BBS(36) break;
+    case 14: CNB_BBS(132) break;
     default: CNB_BBS(100) break;
   }
 #undef CNB_BBS

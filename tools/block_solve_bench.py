@@ -14,7 +14,7 @@ torch.cuda.init()
 out = (ctypes.c_double * 2)()
 res = {}
 names = ["fma-update", "h2-prescaled", "branchless-rsqrt", "both",
-         "proj:fma-update", "proj:h2-prescaled", "proj:branchless-rsqrt", "proj:both", "v2", "proj:v2", "v3", "proj:v3", "v4", "proj:v4", "proj:v4-26x78"]
+         "proj:fma-update", "proj:h2-prescaled", "proj:branchless-rsqrt", "proj:both", "v2", "proj:v2", "v3", "proj:v3", "v4", "proj:v4", "proj:v5-26x78-next-block", "proj:v4-26x78"]
 for v, name in enumerate(names):
     _lib.call("cnb_bench_block_solve", v, 50, out, _lib.stream())
     _lib.call("cnb_bench_block_solve", v, 2000, out, _lib.stream())
