@@ -1213,6 +1213,48 @@ __device__ __forceinline__ PipeSmem pipe_carve(char* base) {
   return g;
 }
 
+// Shared-memory layout of the solver CTA with the fused next-block update
+// (pgs_pipe_kernel<true>): double-buffered diagonal tiles T and next-block tiles
+// Wn = W[b+1, b], lambda (new, old) / group constants / delta(b) per step parity.
+struct Pipe5Smem {
+  double *T[2], *Wn[2], *lamx, *lamn, *kcn, *sv, *dpre, *red;
+  unsigned long long* bar;  // [slot]: T(b) and W[b+1, b] of that step parity
+  int* flags;
+};
+
+__host__ __device__ inline size_t pipe5_smem_bytes() {
+  return 128 + sizeof(double) * (size_t)(4 * kTileD + 6 * kPR + 2 * kKCP * kPG + 4 * kPG + 8) + 16 + 8 * sizeof(int);
+}
+
+__device__ __forceinline__ Pipe5Smem pipe5_carve(char* base) {
+  Pipe5Smem g;
+  double* p = (double*)base;
+  g.T[0] = p;
+  p += kTileD;
+  g.T[1] = p;
+  p += kTileD;
+  g.Wn[0] = p;
+  p += kTileD;
+  g.Wn[1] = p;
+  p += kTileD;
+  g.lamx = p;
+  p += 2 * kPR;
+  g.lamn = p;
+  p += 2 * kPR;
+  g.kcn = p;
+  p += 2 * kKCP * kPG;
+  g.sv = p;
+  p += 4 * kPG;
+  g.dpre = p;
+  p += 2 * kPR;
+  g.red = p;
+  p += 8;
+  g.bar = (unsigned long long*)p;
+  p += 2;
+  g.flags = (int*)p;
+  return g;
+}
+
 // group constants of one group from a packed record (global or shared):
 // [ihw, it00, it01, it10, it11, b0, b1, bad, htn0, htn1]; the pipelined
 // kernel stages only the first kKCP (what block_solve_v4 reads)
@@ -1301,13 +1343,16 @@ __device__ __forceinline__ void block_solve_v4(const double* __restrict__ Wt, in
 // block_solve_v4 that also accumulates, for the NEXT block, dn += h^2 W[next, this]
 // (lambda change) group by group from the broadcast changes: Wn holds the rows of
 // the next block (lane l <-> its group l) over the columns of this block, stride
-// ld.  The extra loads / FMAs are independent of the sequential chain.
+// ld.  The extra loads / FMAs are independent of the sequential chain.  Lanes
+// past the tile's groups (> lmax) read row lmax instead (their results are unused).
 template <bool FRIC>
 __device__ __forceinline__ void block_solve_v5(const double* __restrict__ Wt, const double* __restrict__ Wn, int ld,
                                                int ng, int lane, double dl_[3], double dn[3], const double lm[3],
-                                               const GroupConst& kc, double mu, double h2, double* __restrict__ sv) {
-  const double* wrow = Wt + 3 * lane * ld;
-  const double* nrow = Wn + 3 * lane * ld;
+                                               const GroupConst& kc, double mu, double h2, double* __restrict__ sv,
+                                               int lmax) {
+  const int lr = min(lane, lmax);
+  const double* wrow = Wt + 3 * lr * ld;
+  const double* nrow = Wn + 3 * lr * ld;
   const double h2l1 = h2 * lm[1], h2l2 = h2 * lm[2];
   const double nl0 = -lm[0], lhw = lm[0] * kc.hwnn, nihw = -kc.ihw;
 #pragma unroll 2
@@ -1434,6 +1479,7 @@ __device__ __forceinline__ double ll_load(const double* slot, unsigned tag, Grid
   return __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
 }
 
+template <bool V5>
 __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, const double* __restrict__ dshift,
                                                                 const double* __restrict__ kconst, double* partial,
                                                                 GridCtl* ctl, int nch, int lam_in_smem, int tma,
@@ -1468,7 +1514,244 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
     }
   };
 
-  if (blockIdx.x == 0) {
+  if (blockIdx.x == 0 && V5) {
+    // ---- solver CTA with the next-block update folded into the block solve ----
+    // Step t solves block b with block_solve_v5, which also accumulates, lane l
+    // for group l of block b+1, dn = h^2 W[b+1, b] (lambda_b change).  Everything
+    // else delta(b+1) needs is formed off the critical path during the solve:
+    //   X2 warps: dpre(b+1) = delta_base + h^2 (helper partials + W[b+1, b-1]
+    //             lambda_{b-1} (global / L2) + W[b+1, b] lambda_b(old) (tile Wn));
+    //   warp 2:   tensor TMA of T(b+1) and Wn = W[b+2, b+1] for the next step, then
+    //             the regularisation shift of T(b+1)'s diagonal;
+    //   warp 3:   lambda(b+1) and the group constants of b+1;
+    //   warp 1:   publisher (as in the v4 path).
+    // The solver then starts block b+1 from dpre(b+1) + dn right after one
+    // barrier at which the other warps have long arrived: no phase B.
+    Pipe5Smem sm = pipe5_carve(smem_raw);
+    const int xi = x2_index(warp);
+    const int K5 = kKCP * kPG;
+    if (tid == 0) {
+      sm.flags[0] = sm.flags[1] = 0;
+      mbar_init(sm.bar, 1);
+      mbar_init(sm.bar + 1, 1);
+    }
+    for (int i = tid; i < kPR; i += blockDim.x) {
+      sm.lamx[i] = sm.lamx[kPR + i] = 0.0;
+      sm.lamn[i] = sm.lamn[kPR + i] = 0.0;  // lambda starts at zero
+      sm.dpre[i] = i < rows_of(0) ? s.delta_base[i] : 0.0;
+      sm.dpre[kPR + i] = 0.0;
+    }
+    for (int e = tid; e < kKCP * rows_of(0) / 3; e += blockDim.x)
+      sm.kcn[e] = kconst[kKC * (e / kKCP) + (e % kKCP)];
+    __syncthreads();
+    if (tid == 64) {  // T(0) and Wn = W[1, 0] for step 0
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(sm.bar, 2u * kPR * kPS * 8);
+      tma_load_2d(sm.T[0], &tmap, 0, 0, sm.bar);
+      tma_load_2d(sm.Wn[0], &tmap, 0, kPR, sm.bar);
+    }
+    if (warp == 2) {
+      mbar_wait(sm.bar, 0);
+      for (int i = lane; i < rows_of(0); i += 32) sm.T[0][i * kPS + i] = add(sm.T[0][i * kPS + i], dshift[i / 3]);
+    }
+    double dsq = 0.0;
+    const double ih2 = 1.0 / h2;
+    double dn[3] = {0.0, 0.0, 0.0};
+    volatile unsigned* vcnt = (volatile unsigned*)(sm.flags + 4);  // [0] lambda in smem, [1] published (steps)
+    if (tid == 0) {
+      sm.flags[2] = 0;
+      vcnt[0] = vcnt[1] = 0;
+    }
+    __syncthreads();
+    stamp(-1);
+    int iterations = 0;
+    bool converged = false;
+    if (warp != 1) {
+    for (unsigned t = 0;; ++t) {
+      const int b = (int)(t % nb), sweep = (int)(t / nb);
+      const int b1 = wrap(b + 1), b2 = wrap(b + 2), bm = (b == 0) ? nb - 1 : b - 1;
+      const int rows = rows_of(b), rows1 = rows_of(b1), rowsm = rows_of(bm);
+      const int slot = (int)(t & 1);
+      double* Tc = sm.T[slot];
+      double* Tn = sm.T[slot ^ 1];
+      const double* Wc = sm.Wn[slot];
+      double* lamc = sm.lamx + slot * kPR;           // lambda_b (this solve)
+      const double* lamp = sm.lamx + (slot ^ 1) * kPR;  // lambda_{b-1}
+      const double* lamo = sm.lamn + slot * kPR;      // lambda_b before this solve
+      const int64_t rb = 3 * (int64_t)b * kPG, rb1 = 3 * (int64_t)b1 * kPG, rb2 = 3 * (int64_t)b2 * kPG;
+      const int64_t rbm = 3 * (int64_t)bm * kPG;
+      if (warp == 0) {
+        // ---- sequential block solve ----
+        const int ng = rows / 3;
+        const bool mine = lane < ng;
+        GroupConst kc;
+        load_group_const(kc, sm.kcn + slot * K5 + kKCP * lane, mine, kKCP);
+        double lm[3], dl[3];
+        mbar_wait(sm.bar + slot, (t >> 1) & 1u);  // T(b), W[b+1, b] (landed during the previous step)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          lm[a] = mine ? lamo[3 * lane + a] : 0.0;
+          dl[a] = mine ? add(sm.dpre[slot * kPR + 3 * lane + a], dn[a]) : 0.0;
+          dn[a] = 0.0;
+        }
+        stamp(13);
+        if (s.mu != 0.0)
+          block_solve_v5<true>(Tc, Wc, kPS, ng, lane, dl, dn, lm, kc, s.mu, h2, sm.sv, kPG - 1);
+        else
+          block_solve_v5<false>(Tc, Wc, kPS, ng, lane, dl, dn, lm, kc, s.mu, h2, sm.sv, kPG - 1);
+        __syncwarp();
+        stamp(14);
+        const int err = mine ? block_commit(sm.sv, lane, lm, kc, s.mu, ih2, dsq) : 0;
+        const unsigned bad = __ballot_sync(0xffffffffu, err);
+        if (bad) {
+          const int g = __ffs(bad) - 1;  // first failing group in Gauss-Seidel order
+          if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(rb / 3 + g), 1.0 / kc.ihw);
+          if (lane == 0) sm.flags[0] = 1;
+        }
+        if (t >= 2)  // the publisher has read this slot's previous lambda (step t-2)
+          while (vcnt[1] + 1 < t) {
+          }
+        if (mine)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) lamc[3 * lane + a] = lm[a];
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) vcnt[0] = t + 1;  // lambda_b in shared memory: the publisher takes it
+        if (b == nb - 1) {  // end of sweep: ||dlam||^2 and ||lambda||^2 (publisher: blocks 0..nb-2)
+          const double l2 = mine ? (lm[0] * lm[0] + lm[1] * lm[1]) + lm[2] * lm[2] : 0.0;
+          const double sl = warp_sum(l2), sd = warp_sum(dsq);
+          dsq = 0.0;
+          if (lane == 0 && !sm.flags[0]) {
+            while (vcnt[1] < t) {  // the publisher's sum of blocks 0..nb-2 (step t-1) is in red[2]
+            }
+            const double num = sqrt(sd), den = sqrt(sl + sm.red[2]);
+            const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
+            s.eps_hist[sweep] = eps;
+            sm.flags[1] = (eps <= s.tol) ? 1 : ((sweep + 1 >= s.max_iter) ? 2 : 0);
+          }
+        }
+        stamp(2);
+      } else if (warp == 2) {
+        // T(b+1) and Wn = W[b+2, b+1] for the next step, then T(b+1)'s diagonal shift
+        const int ns = slot ^ 1;
+        if (lane == 0) {
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(sm.bar + ns, 2u * kPR * kPS * 8);
+          tma_load_2d(Tn, &tmap, (int)rb1, (int)rb1, sm.bar + ns);
+          tma_load_2d(sm.Wn[ns], &tmap, (int)rb1, (int)rb2, sm.bar + ns);
+        }
+        mbar_wait(sm.bar + ns, ((t + 1) >> 1) & 1u);
+        for (int i = lane; i < rows1; i += 32) Tn[i * kPS + i] = add(Tn[i * kPS + i], dshift[(rb1 + i) / 3]);
+        stamp(10);
+      } else if (warp == 3) {
+        // lambda(b+1) (published in the previous sweep) and the group constants of b+1
+        double* lnx = sm.lamn + (slot ^ 1) * kPR;
+        double* kcx = sm.kcn + (slot ^ 1) * K5;
+        for (int e = lane; e < kKCP * rows1 / 3; e += 32) {
+          const int g = e / kKCP, k = e - g * kKCP;
+          cp_async8(&kcx[e], kconst + kKC * (rb1 / 3 + g) + k, true);
+        }
+        for (int j = lane; j < kPR; j += 32) lnx[j] = j < rows1 ? __ldcg(lamg + rb1 + j) : 0.0;
+        cp_async_wait_all();
+      } else if (xi >= 0) {
+        // dpre(b+1) = delta_base + h^2 ((partials + X2) + W[b+1, b] lambda_b(old)), fixed order;
+        // lanes 3k..3k+2 share row xi + kXW k, a third of the columns each
+        double x2v = 0.0, wov = 0.0;
+        {
+          const int k = lane / 3, part = lane - 3 * k;
+          const int i = xi + kXW * k;
+          if (lane < 3 * kXRows && i < rows1) {
+            const double* wr = s.W + (rb1 + i) * s.ldw + rbm;
+            const int j0 = part * (kPR / 3), j1m = min(j0 + kPR / 3, rowsm), j1 = min(j0 + kPR / 3, rows);
+            double a0 = 0.0, a1 = 0.0;
+            int j = j0;
+            for (; j + 1 < j1m; j += 2) {
+              a0 = fma(__ldg(wr + j), lamp[j], a0);
+              a1 = fma(__ldg(wr + j + 1), lamp[j + 1], a1);
+            }
+            if (j < j1m) a0 = fma(__ldg(wr + j), lamp[j], a0);
+            x2v = a0 + a1;
+            mbar_wait(sm.bar + slot, (t >> 1) & 1u);  // Wn = W[b+1, b]
+            const double* xr = Wc + i * kPS;
+            double c0 = 0.0, c1 = 0.0;
+            for (j = j0; j + 1 < j1; j += 2) {
+              c0 = fma(xr[j], lamo[j], c0);
+              c1 = fma(xr[j + 1], lamo[j + 1], c1);
+            }
+            if (j < j1) c0 = fma(xr[j], lamo[j], c0);
+            wov = c0 + c1;
+          }
+          x2v = (x2v + __shfl_down_sync(0xffffffffu, x2v, 1)) + __shfl_down_sync(0xffffffffu, x2v, 2);
+          wov = (wov + __shfl_down_sync(0xffffffffu, wov, 1)) + __shfl_down_sync(0xffffffffu, wov, 2);
+        }
+        if (xi == 0) stamp(6);
+        // partials of block b+1 (helpers, step t-1), fixed order; lane k <-> row xi + kXW k
+        const double* part = partial + 2 * (size_t)((t + kPartBufs - 1) % kPartBufs) * pstride;
+        double pvl = 0.0;
+        {
+          const int i = xi + kXW * lane;
+          if (t > 0 && lane < kXRows && i < rows1) {
+            const int nseg = ((i + 1) * nch - 1) / kHelpWarps - (i * nch) / kHelpWarps + 1;
+            for (int sg = 0; sg < nseg; ++sg) pvl += ll_load(part + 2 * ((size_t)i * kSeg + sg), tag0 + t - 1, ctl);
+          }
+        }
+        const double pk = __shfl_sync(0xffffffffu, pvl, lane / 3);  // lane 3k picks up row k's sum
+        {
+          const int k = lane / 3, i = xi + kXW * k;
+          if (lane == 3 * k && k < kXRows && i < rows1)
+            sm.dpre[(slot ^ 1) * kPR + i] = add(s.delta_base[rb1 + i], mul(h2, (pk + x2v) + wov));
+        }
+        if (xi == 0) stamp(7);
+      }
+      asm volatile("bar.sync 5, %0;" ::"n"(kPipeThreads - 32) : "memory");  // end of step (all but the publisher)
+      if (warp == 0 || warp == 5) stamp(0); else stamp(-1);
+      if (b == nb - 1) {
+        iterations = sweep + 1;
+        converged = sm.flags[1] == 1;
+      }
+      if (sm.flags[0] || sm.flags[1]) {
+        if (tid == 0) sm.flags[2] = 1;  // the publisher stops after this step
+        break;
+      }
+    }
+    } else {
+      // ---- warp 1: publisher (see the v4 path) ----
+      double sumsq = 0.0;
+      for (unsigned t = 0;; ++t) {
+        if (lane == 0) {
+          while (vcnt[0] < t + 1 && !*(volatile int*)&sm.flags[2]) __nanosleep(20);
+          if (*(volatile unsigned*)&ctl->timeout) sm.flags[0] = 1;  // watchdog fired elsewhere
+        }
+        const unsigned go = __shfl_sync(0xffffffffu, vcnt[0] >= t + 1 ? 1u : 0u, 0);
+        if (!go) break;
+        __threadfence_block();
+        const int b = (int)(t % nb), rows = rows_of(b);
+        const int64_t rb = 3 * (int64_t)b * kPG;
+        const double* lamc = sm.lamx + (t & 1) * kPR;
+        double v = 0.0;
+        for (int j = lane; j < rows; j += 32) {
+          const double l = lamc[j];
+          __stcg(lamg + rb + j, l);
+          v = fma(l, l, v);
+        }
+        __syncwarp();
+        if (lane == 0) st_release_gpu(psolved, t + 1);
+        if (b == 0) sumsq = 0.0;
+        if (b < nb - 1) sumsq += warp_sum(v);
+        if (b == nb - 2 && lane == 0) sm.red[2] = sumsq;
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) vcnt[1] = t + 1;
+      }
+    }
+    // everyone (publisher included): last lambda block is in global memory; release the grid
+    __syncthreads();
+    if (tid == 0) {
+      st_release_gpu(pstop, 1u);
+      s.iters_conv[0] = iterations;
+      s.iters_conv[1] = converged ? 1 : 0;
+    }
+  } else if (blockIdx.x == 0) {
     PipeSmem sm = pipe_carve(smem_raw);
     const int xi = x2_index(warp);
     if (tid == 0) {
@@ -2330,7 +2613,7 @@ __global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double*
     dl_[2] = ((V & 4) ? 3e-4 : 3e-5) * cos(1.0 * lane);
     if (V & 128) {
       double dn[3] = {0.0, 0.0, 0.0};
-      block_solve_v5<true>(T, T + 3, kPR, kPG, lane, dl_, dn, lm, kc, 0.4, h2, T + kBR * kLDT);
+      block_solve_v5<true>(T, T + 3, kPR, kPG, lane, dl_, dn, lm, kc, 0.4, h2, T + kBR * kLDT, kPG - 1);
       __syncwarp();
       err |= block_commit(T + kBR * kLDT, lane, lm, kc, 0.4, 1.0 / h2, dsq);
       dsq += dn[0] + dn[1] + dn[2];
@@ -2486,9 +2769,27 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   CNB_CUDA(cudaGetDevice(&dev));
   CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const bool pipe = use_pipe_kernel(s);
-  const void* kfn = pipe ? (const void*)pgs_pipe_kernel : (const void*)pgs_grid_kernel;
+  // tensor TMA needs a 16-byte aligned base and row pitch (even ldw)
+  int tma = (((uintptr_t)s.W & 15) == 0 && (s.ldw & 1) == 0) ? 1 : 0;
+  int dbg = 0;
+  bool want_v5 = false;
+  {
+    const char* e = getenv("CNB_PGS_TMA");
+    if (e && e[0] == '0') tma = 0;
+    const char* d = getenv("CNB_PGS_DEBUG");
+    if (d) dbg = atoi(d) & ~1;
+    // CNB_PGS_PIPE=v5: experimental solver CTA with the next-block update folded into
+    // the block solve (no delta phase).  Measured slower at cfg3 (8.3 vs 5.3 us per
+    // block step): the overlapped tile fetches and X2 loads contend with the solve
+    // and the next tiles land late, so the default stays the v4 solver CTA.
+    const char* v = getenv("CNB_PGS_PIPE");
+    want_v5 = v && !strcmp(v, "v5");
+  }
+  const bool v5 = pipe && tma && !dbg && want_v5;
+  const void* kfn = pipe ? (v5 ? (const void*)pgs_pipe_kernel<true> : (const void*)pgs_pipe_kernel<false>)
+                         : (const void*)pgs_grid_kernel;
   const int nthreads = pipe ? kPipeThreads : kGridThreads;
-  const size_t tiles = pipe ? pipe_smem_bytes() : grid_smem_bytes();
+  const size_t tiles = pipe ? (v5 ? pipe5_smem_bytes() : pipe_smem_bytes()) : grid_smem_bytes();
   const size_t lam_bytes = sizeof(double) * (size_t)(3 * s.groups) + (pipe ? 128 : 0);  // + alignment slack
   const int lam_in_smem = lam_bytes <= pgs_max_smem() ? 1 : 0;
   const size_t smem = std::max(tiles, lam_in_smem ? lam_bytes : (size_t)0);
@@ -2530,15 +2831,6 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   int lis = lam_in_smem;
   int nchv = nch;
   unsigned long long* prof = pgs_profile_buffer();
-  // tensor TMA needs a 16-byte aligned base and row pitch (even ldw)
-  int tma = (((uintptr_t)s.W & 15) == 0 && (s.ldw & 1) == 0) ? 1 : 0;
-  int dbg = 0;
-  {
-    const char* e = getenv("CNB_PGS_TMA");
-    if (e && e[0] == '0') tma = 0;
-    const char* d = getenv("CNB_PGS_DEBUG");
-    if (d) dbg = atoi(d) & ~1;
-  }
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (pipe && tma) {
@@ -2571,7 +2863,7 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   void* args_pipe[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
                        (void*)&nchv, (void*)&lis, (void*)&tma_arg, (void*)&prof, (void*)&tag0, (void*)&tmap};
   CNB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthreads), pipe ? args_pipe : args_grid, smem, st));
-  CNB_LAUNCH_CHECK(pipe ? "pgs_pipe_kernel" : "pgs_grid_kernel");
+  CNB_LAUNCH_CHECK(pipe ? (v5 ? "pgs_pipe_kernel<v5>" : "pgs_pipe_kernel") : "pgs_grid_kernel");
   return CNB_OK;
 }
 
