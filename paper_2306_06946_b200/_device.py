@@ -13,20 +13,21 @@ def device() -> torch.device:
 
 
 def f64(x, dev=None) -> torch.Tensor:
-    """Contiguous fp64 CUDA tensor view/copy of an array-like."""
+    """Contiguous fp64 CUDA tensor view/copy of an array-like (host data goes
+    through pinned staging without a stream synchronisation, see upload)."""
     dev = dev or device()
     if isinstance(x, torch.Tensor):
         if x.device != dev or x.dtype != torch.float64:
             x = x.to(device=dev, dtype=torch.float64)
         return x.contiguous()
-    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=dev)
+    return upload(np.asarray(x, dtype=np.float64), dev=dev)
 
 
 def i64(x, dev=None) -> torch.Tensor:
     dev = dev or device()
     if isinstance(x, torch.Tensor):
         return x.to(device=dev, dtype=torch.int64).contiguous()
-    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int64), device=dev)
+    return upload(np.asarray(x, dtype=np.int64), dev=dev)
 
 
 def host(x) -> np.ndarray:
@@ -43,11 +44,12 @@ def zeros(shape, dev=None, dtype=torch.float64) -> torch.Tensor:
     return torch.zeros(shape, dtype=dtype, device=dev or device())
 
 
-def upload(a, dtype=None) -> torch.Tensor:
+def upload(a, dtype=None, dev=None) -> torch.Tensor:
     """Host array -> device tensor without a stream synchronisation: staged through
-    pinned memory and copied asynchronously on the current stream (the caching
-    host allocator keeps the staging block alive until the copy has run)."""
+    pinned memory (a copy taken now, so later host writes do not race) and copied
+    asynchronously on the current stream (the caching host allocator keeps the
+    staging block alive until the copy has run)."""
     t = torch.from_numpy(np.ascontiguousarray(a))
     if dtype is not None:
         t = t.to(dtype)
-    return t.pin_memory().to(device(), non_blocking=True)
+    return t.pin_memory().to(dev or device(), non_blocking=True)

@@ -387,14 +387,14 @@ class PairTable:
         self.h_kind, self.h_obj, self.h_node, self.h_w = kind, obj, node, w
         self.h_keys = keys
         d = dv.device()
-        self.kind = torch.as_tensor(kind, device=d)
-        self.obj = torch.as_tensor(obj, device=d)
-        self.node = torch.as_tensor(node, device=d)
+        self.kind = dv.upload(kind)
+        self.obj = dv.upload(obj)
+        self.node = dv.upload(node)
         self.w = dv.f64(w, d)
         self.local = dv.f64(local, d)
         self.world = dv.f64(world, d)
         self.lnormal = dv.f64(lnormal, d)
-        self.has_ln = torch.as_tensor(has_ln, device=d)
+        self.has_ln = dv.upload(has_ln)
         self.ref_normal = dv.f64(ref, d)
         self.p_a = dv.f64(pa, d)
         self.p_b = dv.f64(pb, d)
@@ -409,14 +409,14 @@ class PairTable:
         self.h_kind, self.h_obj, self.h_node, self.h_w = soa.kind, soa.obj, soa.node, soa.w
         self.h_keys = soa.keys
         d = dv.device()
-        self.kind = torch.as_tensor(soa.kind, device=d)
-        self.obj = torch.as_tensor(soa.obj, device=d)
-        self.node = torch.as_tensor(soa.node, device=d)
+        self.kind = dv.upload(soa.kind)
+        self.obj = dv.upload(soa.obj)
+        self.node = dv.upload(soa.node)
         self.w = dv.f64(soa.w, d)
         self.local = dv.f64(soa.local, d)
         self.world = dv.f64(soa.world, d)
         self.lnormal = dv.f64(soa.lnormal, d)
-        self.has_ln = torch.as_tensor(soa.has_ln, device=d)
+        self.has_ln = dv.upload(soa.has_ln)
         self.ref_normal = dv.f64(soa.ref, d)
         self.p_a = dv.f64(soa.pa, d)
         self.p_b = dv.f64(soa.pb, d)
@@ -460,7 +460,7 @@ class PositionViews:
 
     def device(self):
         d = dv.device()
-        return torch.as_tensor(self.ptrs, device=d), dv.f64(self.poses, d)
+        return dv.upload(self.ptrs), dv.f64(self.poses, d)
 
 
 def refresh_proximity_device(table: PairTable, views: PositionViews, p_a=None, p_b=None):
@@ -590,8 +590,8 @@ def _vertex_vs_mesh(ga: MeshGeometry, gb: MeshGeometry, threshold: float) -> Pai
     if (ga.dynamic and not ga.deformable) or (gb.dynamic and not gb.deformable):
         raise InvalidAttachmentError("dynamic non-deformable meshes are not supported")
     d = dv.device()
-    vids = torch.as_tensor(np.ascontiguousarray(ga.vertex_ids, dtype=np.int64), device=d)
-    tris = torch.as_tensor(np.ascontiguousarray(gb.triangles, dtype=np.int64), device=d)
+    vids = dv.upload(np.ascontiguousarray(ga.vertex_ids, dtype=np.int64))
+    tris = dv.upload(np.ascontiguousarray(gb.triangles, dtype=np.int64))
     pa, pb = _device_points(ga), _device_points(gb)
     work = torch.empty((int(_lib.lib().cnb_detect_work_bytes(nv, nt)) + 7) // 8, dtype=torch.float64, device=d)
     best = torch.empty(nv, dtype=torch.int64, device=d)

@@ -146,8 +146,8 @@ class SignedMapping:
             st = self.csr.T.tocsr()
             st.sort_indices()
             d = dv.device()
-            self._dev = (torch.as_tensor(st.indptr.astype(np.int64), device=d),
-                         torch.as_tensor(st.indices.astype(np.int64), device=d), dv.f64(st.data, d))
+            self._dev = (dv.upload(st.indptr.astype(np.int64)),
+                         dv.upload(st.indices.astype(np.int64)), dv.f64(st.data, d))
         return self._dev
 
     def rmatvec(self, t: torch.Tensor, out: torch.Tensor | None = None, alpha: float = 1.0) -> torch.Tensor:
