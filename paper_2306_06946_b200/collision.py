@@ -675,6 +675,25 @@ def _vertex_vs_plane(geom: MeshGeometry, plane: PlaneGeometry, threshold: float)
     return r
 
 
+def _aabbs(meshes):
+    """Bounding box of every mesh, once per detection: on the device when the
+    points live there (one small read-back), else on the host.  Only a pruning
+    gate: it never changes which pairs are found."""
+    out = {}
+    dev = [g for g in meshes if g.points_dev is not None and len(g.points)]
+    if dev:
+        mm = torch.stack([torch.cat(torch.aminmax(dv.f64(g.points_dev).reshape(-1, 3), dim=0)) for g in dev])
+        mm = mm.cpu().numpy()
+        for g, row in zip(dev, mm):
+            out[g.object_id] = (row[:3], row[3:])
+    for g in meshes:
+        if g.object_id not in out:
+            pts = np.asarray(g.points, dtype=np.float64).reshape(-1, 3)
+            out[g.object_id] = (pts.min(axis=0), pts.max(axis=0)) if len(pts) else (np.full(3, np.inf),
+                                                                                  np.full(3, -np.inf))
+    return out
+
+
 def detect_soa(geometries, threshold: float) -> PairSoA:
     """Pairs with signed distance <= threshold in canonical order (collision.py:320-345),
     as arrays."""
@@ -683,14 +702,15 @@ def detect_soa(geometries, threshold: float) -> PairSoA:
     meshes = [g for g in geometries if isinstance(g, MeshGeometry)]
     planes = [g for g in geometries if isinstance(g, PlaneGeometry)]
     parts = []
+    boxes = _aabbs(meshes)
     for ga in meshes:
         for gb in meshes:
             if ga.object_id == gb.object_id or not (ga.dynamic or gb.dynamic):
                 continue
             if len(gb.triangles) == 0:
                 continue
-            lo_a, hi_a = ga.points.min(axis=0), ga.points.max(axis=0)
-            lo_b, hi_b = gb.points.min(axis=0), gb.points.max(axis=0)
+            lo_a, hi_a = boxes[ga.object_id]
+            lo_b, hi_b = boxes[gb.object_id]
             if not (np.all(lo_a - threshold <= hi_b) and np.all(lo_b - threshold <= hi_a)):
                 continue
             parts.append(_vertex_vs_mesh(ga, gb, threshold))
