@@ -37,22 +37,6 @@ struct DevTasks {
   int64_t count = 0;
 };
 
-struct GrowBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  int ensure(size_t bytes) {
-    if (bytes <= cap) return CNB_OK;
-    release();
-    CNB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
-    cap = std::max<size_t>(bytes, 256);
-    return CNB_OK;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-  }
-};
 
 template <typename T>
 inline int upload_vec(T** dptr, const std::vector<T>& v) {

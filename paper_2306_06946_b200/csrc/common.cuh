@@ -147,6 +147,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// Device scratch that only grows (reused across calls on one stream).
+struct GrowBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return CNB_OK;
+    release();
+    CNB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    cap = std::max<size_t>(bytes, 256);
+    return CNB_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
 // Pinned host staging for per-call uploads: cudaMemcpyAsync from pageable
 // memory synchronises the stream first, which would serialise the host-side
 // planning of one object with the GPU work of the previous one.  `ready`

@@ -156,15 +156,18 @@ __global__ void __launch_bounds__(256) prox_update_kernel(int64_t mo, const doub
   const int64_t rows = 3 * mo;
   if (r >= rows) return;
   const double* row = U + r * ldu;
-  double s = 0.0;
-  if (idx == nullptr) {
-    for (int64_t c = lane; c < rows; c += 32) s = fma(__ldcs(row + c), t[c], s);
-  } else {
-    for (int64_t c = lane; c < rows; c += 32) {
-      int64_t k = c / 3;
-      s = fma(__ldcs(row + c), t[3 * idx[k] + (c - 3 * k)], s);
-    }
+  // t is contiguous here (gathered by prox_gather_kernel when the object uses a
+  // subset of the pairs); four independent accumulators, streaming loads
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t c = lane;
+  for (; c + 96 < rows; c += 128) {
+    s0 = fma(__ldcs(row + c), t[c], s0);
+    s1 = fma(__ldcs(row + c + 32), t[c + 32], s1);
+    s2 = fma(__ldcs(row + c + 64), t[c + 64], s2);
+    s3 = fma(__ldcs(row + c + 96), t[c + 96], s3);
   }
+  for (; c < rows; c += 32) s0 = fma(__ldcs(row + c), t[c], s0);
+  double s = (s0 + s1) + (s2 + s3);
   s = warp_sum(s);
   if (lane == 0) {
     const int64_t k = r / 3;
@@ -176,6 +179,15 @@ __global__ void __launch_bounds__(256) prox_update_kernel(int64_t mo, const doub
     else
       pb[3 * pair + d] = sub(pb[3 * pair + d], move);
   }
+}
+
+// tg[c] = t[3 idx[c / 3] + c % 3]: the object's rows of D^T lambda, contiguous
+__global__ void prox_gather_kernel(int64_t mo, const int64_t* __restrict__ idx, const double* __restrict__ t,
+                                   double* __restrict__ tg) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 3 * mo) return;
+  const int64_t k = c / 3;
+  tg[c] = t[3 * idx[k] + (c - 3 * k)];
 }
 
 // ---- frames ---------------------------------------------------------------
@@ -442,9 +454,18 @@ int cnb_apply_dt(int64_t groups, const double* D, const double* lam, double* t, 
 int cnb_prox_update(int64_t mo, const double* U, int64_t ldu, const int64_t* idx, const int8_t* side,
                     const double* t, double h, double* p_a, double* p_b, void* stream) {
   if (mo <= 0) return CNB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double* tv = t;
+  if (idx) {  // gather the object's rows of t once (the GEMV then streams U against a contiguous vector)
+    static GrowBuf tg;
+    int rc = tg.ensure((size_t)(3 * mo) * sizeof(double));
+    if (rc) return rc;
+    prox_gather_kernel<<<grid_for(3 * mo, 256), 256, 0, st>>>(mo, idx, t, (double*)tg.p);
+    CNB_LAUNCH_CHECK("prox_gather_kernel");
+    tv = (const double*)tg.p;
+  }
   const int64_t threads = 3 * mo * 32;
-  prox_update_kernel<<<grid_for(threads, 256), 256, 0, (cudaStream_t)stream>>>(mo, U, ldu, idx, side, t,
-                                                                                 h * h, p_a, p_b);
+  prox_update_kernel<<<grid_for(threads, 256), 256, 0, st>>>(mo, U, ldu, idx, side, tv, h * h, p_a, p_b);
   CNB_LAUNCH_CHECK("prox_update_kernel");
   return CNB_OK;
 }
