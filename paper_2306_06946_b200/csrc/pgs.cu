@@ -753,37 +753,64 @@ __device__ bool wait_geq(volatile unsigned* p, unsigned target, volatile unsigne
 // regularised diagonal blocks, once per PGS call; lambda <- 0.
 constexpr int kKC = 10;  // doubles per packed GroupConst
 constexpr int kKCP = 8;  // leading doubles of the record the pipelined kernel stages
-__global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshift, double* kconst, GridCtl* ctl) {
-  __shared__ double red[32];
+// Regularisation (solver.py:99-121) and the per-group constants of the grid
+// kernels, grid-wide in two passes (a single CTA is latency-bound on the strided
+// diagonal loads): pass 1, one thread per group,
+// reads the group's diagonal block once, keeps the eigenvalue test (independent
+// of the shift) in dshift as 0 / 1 and the CTA's trace partial in part[];
+// pass 2: every CTA sums the partials in the same fixed order (the same shift
+// everywhere) and writes the shifts, the group constants and lambda = 0.
+constexpr int kPrepThreads = 128;
+__global__ void __launch_bounds__(kPrepThreads) pgs_prep1_kernel(PgsScene s, double* dshift, double* part) {
+  __shared__ double red[kPrepThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t G = s.groups, c = 3 * G;
+  const int64_t g = (int64_t)blockIdx.x * kPrepThreads + tid;
   double tr = 0.0;
-  for (int64_t i = tid; i < c; i += blockDim.x) tr += s.W[i * s.ldw + i];
+  if (g < s.groups) {
+    double a[3][3], Wd[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) Wd[3 * i + j] = s.W[(3 * g + i) * s.ldw + 3 * g + j];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) a[i][j] = 0.5 * (Wd[3 * i + j] + Wd[3 * j + i]);
+    tr = (Wd[0] + Wd[4]) + Wd[8];
+    double e[3];
+    sym3_eigs(a, e);
+    const double mn = fmin(e[0], fmin(e[1], e[2]));
+    const double scale = fmax(fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))), 1e-300);
+    dshift[g] = (mn <= 1e-12 * scale) ? 1.0 : 0.0;
+  }
   tr = warp_sum(tr);
   if (lane == 0) red[warp] = tr;
   __syncthreads();
   if (tid == 0) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    red[0] = t;
-    ctl->solved = ctl->ready = ctl->stop = ctl->timeout = 0;
-    ctl->ready4[0] = ctl->ready4[1] = ctl->ready4[2] = ctl->ready4[3] = 0;
+    for (int w = 0; w < kPrepThreads / 32; ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kPrepThreads) pgs_prep2_kernel(PgsScene s, double* dshift, double* kconst,
+                                                                 const double* part, int nparts, GridCtl* ctl) {
+  __shared__ double shs;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    double t = 0.0;
+    for (int k = 0; k < nparts; ++k) t += part[k];
+    double shift = 1e-10 * t / (double)(3 * s.groups);
+    if (shift <= 0.0) shift = 1e-30;
+    shs = shift;
+    if (blockIdx.x == 0) {
+      ctl->solved = ctl->ready = ctl->stop = ctl->timeout = 0;
+      ctl->ready4[0] = ctl->ready4[1] = ctl->ready4[2] = ctl->ready4[3] = 0;
+    }
   }
   __syncthreads();
-  double shift = 1e-10 * red[0] / (double)c;
-  if (shift <= 0.0) shift = 1e-30;
-  for (int64_t g = tid; g < G; g += blockDim.x) {
-    double a[3][3], Wd[9];
+  const int64_t g = (int64_t)blockIdx.x * kPrepThreads + tid;
+  if (g < s.groups) {
+    double Wd[9];
     for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        Wd[3 * i + j] = s.W[(3 * g + i) * s.ldw + 3 * g + j];
-        a[i][j] = 0.5 * (s.W[(3 * g + i) * s.ldw + 3 * g + j] + s.W[(3 * g + j) * s.ldw + 3 * g + i]);
-      }
-    double e[3];
-    sym3_eigs(a, e);
-    const double mn = fmin(e[0], fmin(e[1], e[2]));
-    const double scale = fmax(fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))), 1e-300);
-    const double sh = (mn <= 1e-12 * scale) ? shift : 0.0;
+      for (int j = 0; j < 3; ++j) Wd[3 * i + j] = s.W[(3 * g + i) * s.ldw + 3 * g + j];
+    const double sh = dshift[g] != 0.0 ? shs : 0.0;
     dshift[g] = sh;
     for (int i = 0; i < 3; ++i) Wd[4 * i] = add(Wd[4 * i], sh);
     GroupConst kc;
@@ -799,8 +826,8 @@ __global__ void __launch_bounds__(1024) pgs_prep_kernel(PgsScene s, double* dshi
     o[7] = (double)kc.bad;
     o[8] = kc.htn0;
     o[9] = kc.htn1;
+    for (int a = 0; a < 3; ++a) s.lam[3 * g + a] = 0.0;
   }
-  for (int64_t i = tid; i < c; i += blockDim.x) s.lam[i] = 0.0;
 }
 
 constexpr int kGridThreads = 512;
@@ -2825,8 +2852,18 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   double* dshift = (double*)((char*)ws_p + 64);
   double* kconst = dshift + s.groups;
   double* partial = kconst + kKC * s.groups + (s.groups & 1);  // 16-byte aligned (copy_cg)
-  pgs_prep_kernel<<<1, 1024, 0, st>>>(s, dshift, kconst, ctl);
-  CNB_LAUNCH_CHECK("pgs_prep_kernel");
+  {
+    // regularisation shifts + group constants, grid-wide (two passes)
+    const int nparts = (int)((s.groups + kPrepThreads - 1) / kPrepThreads);
+    static GrowBuf prep_part;
+    int rc = prep_part.ensure((size_t)nparts * sizeof(double));
+    if (rc) return rc;
+    double* part = (double*)prep_part.p;
+    pgs_prep1_kernel<<<nparts, kPrepThreads, 0, st>>>(s, dshift, part);
+    CNB_LAUNCH_CHECK("pgs_prep1_kernel");
+    pgs_prep2_kernel<<<nparts, kPrepThreads, 0, st>>>(s, dshift, kconst, part, nparts, ctl);
+    CNB_LAUNCH_CHECK("pgs_prep2_kernel");
+  }
   PgsScene sc = s;
   int lis = lam_in_smem;
   int nchv = nch;
