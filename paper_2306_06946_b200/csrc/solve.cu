@@ -227,8 +227,11 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
                                                         const double* __restrict__ p21,
                                                         const double* __restrict__ linv, double* __restrict__ Y,
                                                         const int64_t* __restrict__ yoff) {
-  __shared__ double As[kMK * kMA];  // [k][row]
-  __shared__ double Bs[kMT * kMS];
+  // k chunks of 16, double-buffered (cp.async of chunk k+1 overlaps the MMAs of k);
+  // 38 KB of static shared memory keeps four CTAs per SM
+  constexpr int BK = 16, SB = BK + 4;
+  __shared__ double As[2][BK * kMA];  // [k][row]
+  __shared__ double Bs[2][kMT * SB];  // [col][k]
   const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
   const int64_t ws = R.w[s];
@@ -245,33 +248,46 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   // rows of this tile that lie in L11^{-1} only need k <= row
   const int64_t kend = (r0 + kMT <= nc) ? min(nc, r0 + kMT) : nc;
-  for (int64_t k0 = 0; k0 < kend; k0 += kMK) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
+  auto stage = [&](int buf, int64_t k0) {
+    for (int e = threadIdx.x; e < kMT * BK; e += blockDim.x) {
       const int rr = e % kMT, kk = e / kMT;
       const int64_t i = r0 + rr, j = k0 + kk;
       const bool in = i < f && j < nc && (i >= nc || j <= i);
-      cp_async8(&As[kk * kMA + rr], i < nc ? Li + j * nc + i : P + j * nr + (i - nc), in);
+      cp_async8(&As[buf][kk * kMA + rr], i < nc ? Li + j * nc + i : P + j * nr + (i - nc), in);
     }
-    for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
-      const int kk = e % kMK, cc = e / kMK;
+    for (int e = threadIdx.x; e < kMT * BK; e += blockDim.x) {
+      const int kk = e % BK, cc = e / BK;
       const int64_t j = k0 + kk, c = c0 + cc;
-      cp_async8(&Bs[cc * kMS + kk], Rs + c * f + j, j < nc && c < ws);
+      cp_async8(&Bs[buf][cc * SB + kk], Rs + c * f + j, j < nc && c < ws);
     }
-    cp_async_wait_all();
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (kend > 0) stage(0, 0);
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < kend; k0 += BK) {
+    if (k0 + BK < kend) {
+      stage(buf ^ 1, k0 + BK);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncthreads();
+    const double* Ab = As[buf];
+    const double* Bb = Bs[buf];
 #pragma unroll
-    for (int kk = 0; kk < kMK; kk += 4) {
+    for (int kk = 0; kk < BK; kk += 4) {
       double fa[4], fb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) fa[a] = As[(kk + t) * kMA + wy + 8 * a + g];
+      for (int a = 0; a < 4; ++a) fa[a] = Ab[(kk + t) * kMA + wy + 8 * a + g];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) fb[b] = Bs[(wx + 8 * b + g) * kMS + kk + t];
+      for (int b = 0; b < 4; ++b) fb[b] = Bb[(wx + 8 * b + g) * SB + kk + t];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
     }
+    __syncthreads();
+    buf ^= 1;
   }
   double* Ys = Y + yoff[s];
 #pragma unroll
