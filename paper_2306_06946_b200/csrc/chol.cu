@@ -93,26 +93,22 @@ __global__ void __launch_bounds__(256, 6) extend_add_kernel(DevSym S, const int3
 // diagnostic: cycle sums of potrf phases (CTA 0 of every launch), cnb_potrf_profile
 __device__ unsigned long long g_potrf_prof[8];
 
-__global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
-                                                   double* __restrict__ front, double* __restrict__ kkinv,
-                                                   DevStatus* st) {
-  // One warp per front, right-looking: at step j every lane i > j scales its
-  // l_ij and updates its own row a[i][j+1..i] with the broadcast column j.
-  // The update loops are unrolled by 8 with predication so a lane keeps eight
-  // independent shared loads / FMAs in flight (a single warp has nothing else
-  // to hide latency with).  1/sqrt comes from rsqrt.approx + two Newton steps:
-  // the libm sqrt and the IEEE division are long subroutines on the sequential
-  // chain.  Then Y = L^{-1} by the same scheme, lane c owning column c (in
-  // place: Y starts as the identity).
-  __shared__ double a[kPanel][kPanel + 1];
-  __shared__ double y[kPanel][kPanel + 1];
-  __shared__ double rd[kPanel];
-  const int64_t s = tasks[blockIdx.x];
-  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldf = d_ldf(S, s);
+// POTRF of panel k0's diagonal block of front s by one warp (lane = threadIdx.x
+// & 31), right-looking: at step j every lane i > j scales its l_ij and updates
+// its own row a[i][j+1..i] with the broadcast column j.  The update loops are
+// unrolled by 8 with predication so a lane keeps eight independent shared loads /
+// FMAs in flight (a single warp has nothing else to hide latency with).  1/sqrt
+// comes from rsqrt.approx + two Newton steps: the libm sqrt and the IEEE
+// division are long subroutines on the sequential chain.  Then Y = L^{-1} by the
+// same scheme, lane c owning column c (in place: Y starts as the identity).
+// a, y: kPanel x (kPanel + 1) shared scratch, rd: kPanel.
+__device__ void potrf_panel(const DevSym& S, int64_t s, int k0, double* __restrict__ front,
+                            double* __restrict__ kkinv, DevStatus* st, double (*a)[kPanel + 1],
+                            double (*y)[kPanel + 1], double* rd, bool stamp) {
+  const int64_t nc = d_nc(S, s), ldf = d_ldf(S, s);
   const int kw = (int)min((int64_t)kPanel, nc - k0);
   double* F = front + S.front_off[s];
-  const int i = threadIdx.x;
-  const bool stamp = blockIdx.x == 0 && i == 0;
+  const int i = threadIdx.x & 31;
   long long ts[6];
   ts[0] = clock64();
 #pragma unroll 8
@@ -160,7 +156,7 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
   ts[3] = clock64();
   // Y = L^{-1}: lane c owns column c; step r: y[r][c] *= 1/L[r][r] (= rd[r]), then
   // rows below subtract L[q][r] y[r][c]
-  const int c = threadIdx.x;
+  const int c = i;
 #pragma unroll 8
   for (int r = 0; r < kPanel; ++r) y[r][c] = (r == c) ? 1.0 : 0.0;
   __syncwarp();
@@ -186,10 +182,21 @@ __global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __re
 #pragma unroll 8
   for (int r = 0; r < kPanel; ++r) Y[r * kPanel + c] = y[r][c];
   ts[5] = clock64();
-  if (stamp) {
+  if (stamp && i == 0) {
     for (int k = 0; k < 5; ++k) atomicAdd(&g_potrf_prof[k], (unsigned long long)(ts[k + 1] - ts[k]));
     atomicAdd(&g_potrf_prof[7], 1ull);
   }
+}
+
+// POTRF of every front's first panel (later panels are factored at the end of the
+// SYRK update that last touches them, see syrk_kernel)
+__global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
+                                                   double* __restrict__ front, double* __restrict__ kkinv,
+                                                   DevStatus* st) {
+  __shared__ double a[kPanel][kPanel + 1];
+  __shared__ double y[kPanel][kPanel + 1];
+  __shared__ double rd[kPanel];
+  potrf_panel(S, tasks[blockIdx.x], k0, front, kkinv, st, a, y, rd, blockIdx.x == 0);
 }
 
 // TRSM of the rows below the diagonal block: X = B L_kk^{-T} as a DMMA product
@@ -262,7 +269,8 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
 constexpr int kSK = kTile + 4;  // smem stride of one k column of a staged tile
 constexpr size_t kSyrkSmem = 2 * 2 * kPanel * kSK * sizeof(double);
 __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode,
-                                                   double* __restrict__ front) {
+                                                   double* __restrict__ front, double* __restrict__ kkinv,
+                                                   DevStatus* st) {
   extern __shared__ __align__(16) double syrk_sm[];
   double* Pi = syrk_sm;                  // [2][kPanel * kSK]
   double* Pj = syrk_sm + 2 * kPanel * kSK;
@@ -346,30 +354,42 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
       }
     __syncthreads();
   }
-  if (skip) return;
-  // epilogue: issue every C load before the first store (F aliases itself, so
+  // epilogue (not for the strictly-upper quadrant of a diagonal tile): issue every
+  // C load before the first store (F aliases itself, so
   // the compiler would otherwise serialise load -> subtract -> store)
-  double cv[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t r = r0 + wy + 8 * a + g;
-        const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-        cv[a][b][h] = (r < f && c < cend && r >= c) ? F[c * ldf + r] : 0.0;
-      }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t r = r0 + wy + 8 * a + g;
-        const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-        if (r < f && c < cend && r >= c) F[c * ldf + r] = cv[a][b][h] - acc[a][b][h];
-      }
+  if (!skip) {
+    double cv[4][4][2];
+  #pragma unroll
+    for (int a = 0; a < 4; ++a)
+  #pragma unroll
+      for (int b = 0; b < 4; ++b)
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t r = r0 + wy + 8 * a + g;
+          const int64_t c = c0 + wx + 8 * b + 2 * t + h;
+          cv[a][b][h] = (r < f && c < cend && r >= c) ? F[c * ldf + r] : 0.0;
+        }
+  #pragma unroll
+    for (int a = 0; a < 4; ++a)
+  #pragma unroll
+      for (int b = 0; b < 4; ++b)
+  #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t r = r0 + wy + 8 * a + g;
+          const int64_t c = c0 + wx + 8 * b + 2 * t + h;
+          if (r < f && c < cend && r >= c) F[c * ldf + r] = cv[a][b][h] - acc[a][b][h];
+        }
+  }
+  // the tile holding the next panel's diagonal block (this update is the last one
+  // it receives) factors it right away: no separate POTRF launch for panels > 0
+  if (ti == 0 && tj == 0 && t0 < nc) {
+    __syncthreads();  // the tile's stores are visible to the CTA
+    if (warp == 0) {
+      double (*a)[kPanel + 1] = reinterpret_cast<double (*)[kPanel + 1]>(syrk_sm);
+      double (*y)[kPanel + 1] = reinterpret_cast<double (*)[kPanel + 1]>(syrk_sm + kPanel * (kPanel + 1));
+      potrf_panel(S, s, (int)t0, front, kkinv, st, a, y, syrk_sm + 2 * kPanel * (kPanel + 1), false);
+    }
+  }
 }
 
 static int chol_upload(CholHandle* h) {
@@ -530,7 +550,7 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
     }
     for (size_t p = 0; p < h->potrf[l].size(); ++p) {
       const int k0 = (int)(p * kPanel);
-      if (h->potrf[l][p].count) {
+      if (p == 0 && h->potrf[l][p].count) {  // later panels: fused into the preceding SYRK
         potrf_kernel<<<(unsigned)h->potrf[l][p].count, 32, 0, st>>>(sym, h->potrf[l][p].ptr, k0, h->d_front,
                                                                        h->d_kkinv, d_status);
         CNB_LAUNCH_CHECK("potrf_kernel");
@@ -542,12 +562,12 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
       }
       if (h->syrk[l][p].count) {
         syrk_kernel<<<(unsigned)h->syrk[l][p].count, 128, kSyrkSmem, st>>>(sym, h->syrk[l][p].ptr, (int)p, 0,
-                                                                           h->d_front);
+                                                                           h->d_front, h->d_kkinv, d_status);
         CNB_LAUNCH_CHECK("syrk_kernel");
       }
       if (h->syrk_out[l][p].count) {
         syrk_kernel<<<(unsigned)h->syrk_out[l][p].count, 128, kSyrkSmem, st>>>(sym, h->syrk_out[l][p].ptr, (int)p,
-                                                                               1, h->d_front);
+                                                                               1, h->d_front, h->d_kkinv, d_status);
         CNB_LAUNCH_CHECK("syrk_kernel");
       }
     }
