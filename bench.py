@@ -695,6 +695,7 @@ def run_gpu_cfg4(args, rank, world):
                    "copies": total, "copies_per_rank": wl.ns, "timed_steps": f"{CFG4_PREROLL}..{CFG4_PREROLL + args.steps - 1}",
                    "parallelism": f"scene-parallel over {world} GPU(s), no data-path collective",
                    "l2": "not flushed; per-step working set (W of all copies ~0.5 GB) exceeds L2"},
+        "step_ms_each": [round(s_.elapsed_time(e_), 2) for s_, e_ in zip(starts, ends)],
         "contacts_per_copy_mean": round(float(np.mean(cnt)) if len(cnt) else 0.0, 1),
         "contacts_total": int(pairs[-1]) if pairs else 0,
         "pgs_sweeps_last_iter_max": int(it_h[:, 0].max()) if len(it_h) else 0,
