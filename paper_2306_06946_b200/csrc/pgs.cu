@@ -457,6 +457,20 @@ __device__ __forceinline__ double lane_dot(const double* __restrict__ w, const d
   return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 }
 
+// eight per-lane partial sums reduced across the warp at once (9 shuffles): lane
+// L returns the total of value 4 ((L >> 4) & 1) + 2 ((L >> 3) & 1) + ((L >> 2) & 1)
+__device__ __forceinline__ double warp_sum8(const double v[8], int lane) {
+  double a[4], b[2];
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) a[k] = (h16 ? v[k + 4] : v[k]) + __shfl_xor_sync(0xffffffffu, h16 ? v[k] : v[k + 4], 16);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) b[k] = (h8 ? a[k + 2] : a[k]) + __shfl_xor_sync(0xffffffffu, h8 ? a[k] : a[k + 2], 8);
+  double c = (h4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, h4 ? b[0] : b[1], 4);
+  c += __shfl_xor_sync(0xffffffffu, c, 2);
+  c += __shfl_xor_sync(0xffffffffu, c, 1);
+  return c;
+}
 // Shared-memory layout of one scene's PGS.
 struct PgsSmem {
   double* lam;     // c
@@ -1529,13 +1543,14 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
   const size_t pstride = (size_t)kPR * kSeg;  // one partial buffer: kSeg row sums per row
   auto rows_of = [&](int blk) { return 3 * (int)min((int64_t)kPG, G - (int64_t)blk * kPG); };
   auto wrap = [&](int blk) { return blk >= nb ? blk - nb : blk; };
-  // CNB_PGS_PROFILE=1 (ns per phase, summed): tid 0: [0] idle at B1, [1] phase B, [2] block solve;
-  // tid 32+64*.. see stamp() calls; helpers (CTA 1, tid 0): [4] wait, [5] work
+  // CNB_PGS_PROFILE=1 (SM cycles per phase, summed; clock64, the global timer is
+  // too coarse for sub-microsecond phases): tid 0: [0] idle at B1, [1] phase B,
+  // [2] block solve; tid 32+64*.. see stamp() calls; helpers (CTA 1, tid 0): [4] wait, [5] work
   unsigned long long tp = 0;
   const bool stamper = prof && (tid == 0 || tid == 32 || tid == 64 || tid == 160) && blockIdx.x <= 1;
   auto stamp = [&](int k) {
     if (stamper) {
-      const unsigned long long now = global_ns();
+      const unsigned long long now = (unsigned long long)clock64();
       if (k >= 0) atomicAdd(prof + k, now - tp);  // fire-and-forget RED
       tp = now;
     }
@@ -1808,7 +1823,6 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
     const bool rowner = tid >= 64 && tid < 64 + kRowOwners;
     // phase-B GEMV (warps 2..11): 8 rows x 4 column phases per warp; a quarter-warp
     // reads 8 rows of 16-byte pairs, distinct banks for the 78-double row pitch
-    const int ri = 8 * (warp - 2) + (lane & 7), rq = lane >> 3;
     volatile unsigned* vcnt = (volatile unsigned*)(sm.flags + 4);  // [0] lambda in smem, [1] published (steps)
     if (tid == 0) {
       sm.flags[2] = 0;
@@ -1982,25 +1996,40 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
       if (warp == 0 || warp == 5) stamp(0); else stamp(-1);
       // ---- phase B: delta(b+1), shift of T(b+1)'s diagonal, sweep-end epsilon ----
       if (rowner) {
+        if (tid == 64) stamp(-1);
         if (tma) mbar_wait(sm.bar, t & 1);
-        double a0 = 0.0, a1 = 0.0;
-        if (ri < rows1) {  // column pairs 2rq + 8k: 16-byte loads, a quarter-warp reads 8 rows
-          const double* xr = sm.Wx + ri * kPS;
-          for (int j = 2 * rq; j < rows; j += 8) {
-            if (j + 1 < rows) {
-              const double2 x = *reinterpret_cast<const double2*>(xr + j);
-              const double2 l = *reinterpret_cast<const double2*>(lamc + j);
-              a0 = fma(x.x, l.x, a0);
-              a1 = fma(x.y, l.y, a1);
-            } else {
-              a0 = fma(xr[j], lamc[j], a0);
+        if (tid == 64) stamp(15);  // phase B: wait for T(b+1) / W[b+1, b]
+        // W[b+1, b] lambda_b: warp rw (0..9) takes rows rw + 10 k (k < 8), lanes the
+        // column pairs 2 lane and 2 lane + 64: lambda_b is loaded once per lane and
+        // every W row is one contiguous 512-byte read (shared-memory bandwidth is
+        // the limit of this GEMV); one 8-row warp reduction
+        const int rw = warp - 2;
+        const int j0 = 2 * lane, j1 = 2 * lane + 64;
+        double2 l0, l1;
+        l0.x = j0 < rows ? lamc[j0] : 0.0;
+        l0.y = j0 + 1 < rows ? lamc[j0 + 1] : 0.0;
+        l1.x = j1 < rows ? lamc[j1] : 0.0;
+        l1.y = j1 + 1 < rows ? lamc[j1 + 1] : 0.0;
+        double acc8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = rw + 10 * k;
+          double a = 0.0;
+          if (r < rows1) {
+            const double* xr = sm.Wx + r * kPS;
+            const double2 x0 = *reinterpret_cast<const double2*>(xr + j0);
+            a = fma(x0.y, l0.y, x0.x * l0.x);
+            if (j1 < rows) {
+              const double2 x1 = *reinterpret_cast<const double2*>(xr + j1);
+              a = fma(x1.y, l1.y, fma(x1.x, l1.x, a));
             }
           }
+          acc8[k] = a;
         }
-        double a = a0 + a1;
-        a += __shfl_xor_sync(0xffffffffu, a, 8);
-        a += __shfl_xor_sync(0xffffffffu, a, 16);
-        if (rq == 0 && ri < rows1) sm.dcur[ri] = add(sm.dbs[ri], mul(h2, sm.dcur[ri] + a));
+        const double v = warp_sum8(acc8, lane);
+        const int r = rw + 10 * (4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1));
+        if ((lane & 3) == 0 && r < rows1) sm.dcur[r] = add(sm.dbs[r], mul(h2, sm.dcur[r] + v));
+        if (tid == 64) stamp(9);  // phase B GEMV
       } else if (tid >= 64 + kRowOwners) {
         if (tma) mbar_wait(sm.bar, t & 1);
         if (si < rows1) Tn[si * kPS + si] = add(Tn[si * kPS + si], sm.dsh[si / 3]);
@@ -2144,7 +2173,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         }
       }
     };
-    if (stamper) tp = global_ns();
+    if (stamper) tp = (unsigned long long)clock64();
     long long hc = clock64();
     auto hstamp = [&](int k) {  // CNB_PGS_PROFILE: cycles per helper phase (CTA 1, thread 0), slots 16..21
       if (prof && blockIdx.x == 1 && tid == 0) {
@@ -2314,20 +2343,6 @@ __device__ __forceinline__ void copy_stage_bulk(double* T, double* X, const doub
   }
 }
 
-// eight per-lane partial sums reduced across the warp at once (9 shuffles): lane
-// L returns the total of value 4 ((L >> 4) & 1) + 2 ((L >> 3) & 1) + ((L >> 2) & 1)
-__device__ __forceinline__ double warp_sum8(const double v[8], int lane) {
-  double a[4], b[2];
-  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) a[k] = (h16 ? v[k + 4] : v[k]) + __shfl_xor_sync(0xffffffffu, h16 ? v[k] : v[k + 4], 16);
-#pragma unroll
-  for (int k = 0; k < 2; ++k) b[k] = (h8 ? a[k + 2] : a[k]) + __shfl_xor_sync(0xffffffffu, h8 ? a[k] : a[k + 2], 8);
-  double c = (h4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, h4 ? b[0] : b[1], 4);
-  c += __shfl_xor_sync(0xffffffffu, c, 2);
-  c += __shfl_xor_sync(0xffffffffu, c, 1);
-  return c;
-}
 static_assert(kCRW == 8, "helper rows per warp must match warp_sum8");
 
 __global__ void __launch_bounds__(kCopyThreads, 2) pgs_copy_kernel(const PgsScene* scenes, unsigned long long* prof, int exper) {

@@ -58,7 +58,8 @@ def main():
             _lib.lib().cnb_pgs_profile(prof)
             steps = args.reps * sweeps * nb
             names = [str(k) for k in range(32)]
-            out["us_per_step"] = {n: round(prof[k] / steps / 1e3, 3) for k, n in enumerate(names) if prof[k]}
+            # pipe kernel slots are SM cycles (clock64); microseconds at the 1965 MHz clock
+            out["us_per_step"] = {n: round(prof[k] / steps / 1965.0, 3) for k, n in enumerate(names) if prof[k]}
         print(json.dumps(out), flush=True)
         del W
 
