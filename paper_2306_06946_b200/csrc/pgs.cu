@@ -2245,6 +2245,16 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
       it = item_of(t + 1);  // next step's slice: loads in flight during the reduction and the wait
       preload(it);
       l2_prefetch(t + 1);
+      {
+        // the slice of step t+2 into L2 now, so next step's register preload hits L2
+        // (the HBM stream of all helpers is ~14 MB per step at cfg3)
+        const Item it2 = item_of(t + 2);
+        if (it2.has) {
+          const double* wr2 = s.W + it2.r * s.ldw;
+          for (int64_t j = it2.c0 + 16 * lane; j < it2.c1; j += 16 * 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(wr2 + j));
+        }
+      }
       __syncthreads();
       hstamp(18);  // dot products + next preload issue
       // one sum per (row, CTA): segmented reduction over the CTA's warps in
