@@ -2241,6 +2241,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           hp[warp] = acc;
         }
       }
+      hstamp(20);  // dot products (waits for the preloaded slice)
       const Item cur = it;
       it = item_of(t + 1);  // next step's slice: loads in flight during the reduction and the wait
       preload(it);
@@ -2256,7 +2257,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         }
       }
       __syncthreads();
-      hstamp(18);  // dot products + next preload issue
+      hstamp(18);  // next preload issue + prefetches + barrier
       // one sum per (row, CTA): segmented reduction over the CTA's warps in
       // warp order (fixed tree: deterministic), first warp of a row stores it
       if (warp == 0) {
