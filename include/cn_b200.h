@@ -116,6 +116,12 @@ int cnb_rebuild_w(int64_t groups, const double* D, const double* Wg, int64_t ldw
 int cnb_sandwich(int64_t m, int64_t k, const int32_t* ell_col, const double* ell_val, const double* C,
                  int64_t ldc, double* U, int64_t ldu, void* stream);
 
+/* total[3 idx[I] + a][3 idx[J] + b] += U[3I + a][3J + b] for one object's compact
+ * compliance U (3 mo x 3 mo, idx ascending pair indices): the per-object sum of
+ * W_g, constraints.py:175-179. */
+int cnb_scatter_add_compliance(int64_t mo, const double* U, int64_t ldu, const int64_t* idx, double* total,
+                               int64_t ldt, void* stream);
+
 /* delta = D (p_a - p_b).  Replaces compute_violation constraints.py:208-214. */
 int cnb_violation(int64_t groups, const double* D, const double* p_a, const double* p_b,
                   double* delta, void* stream);

@@ -41,6 +41,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_batch_scatter_acc": [I64, P, P, P, P, P, I64, P],
     "cnb_pgs_batched": [I32, P, P, P, P, P, F64, F64, I32, P, P, P, P, P, P, P],
     "cnb_violation": [I64, P, P, P, P, P],
+    "cnb_scatter_add_compliance": [I64, P, I64, P, P, I64, P],
     "cnb_apply_dt": [I64, P, P, P, P, P],
     "cnb_prox_update": [I64, P, I64, P, P, P, F64, P, P, P],
     "cnb_build_frames": [I64, P, P, P, P, P, P],

@@ -98,8 +98,9 @@ class ObjectCompliance:
         if self.full:
             return self.U
         out = dv.zeros((dim, dim))
-        rows = (3 * self.idx[:, None] + torch.arange(3, device=self.idx.device)).reshape(-1)
-        out[rows[:, None], rows[None, :]] = self.U
+        if len(self.idx):  # out = 0 + U at the object's rows (scatter-add kernel)
+            _lib.call("cnb_scatter_add_compliance", int(self.idx.shape[0]), self.U.data_ptr(), self.U.shape[1],
+                      self.idx.data_ptr(), out.data_ptr(), dim, _lib.stream())
         return out
 
 
@@ -245,8 +246,9 @@ def _sum_compliance(parts: list, dim: int) -> torch.Tensor:
         elif comp.full:
             total += comp.U
         elif len(comp.idx):
-            rows = (3 * comp.idx[:, None] + torch.arange(3, device=total.device)).reshape(-1)
-            total[rows[:, None], rows[None, :]] += comp.U
+            mo = int(comp.idx.shape[0])
+            _lib.call("cnb_scatter_add_compliance", mo, comp.U.data_ptr(), comp.U.shape[1], comp.idx.data_ptr(),
+                      total.data_ptr(), total.shape[1], _lib.stream())
     return total
 
 

@@ -190,6 +190,26 @@ __global__ void prox_gather_kernel(int64_t mo, const int64_t* __restrict__ idx, 
   tg[c] = t[3 * idx[k] + (c - 3 * k)];
 }
 
+// total[3 idx[I] + a][3 idx[J] + b] += U[3 I + a][3 J + b]: one object's compact
+// compliance added into W_g (constraints.py:175-179, objects in ascending id
+// order).  Warp per U row: the row is read contiguously, the destination
+// columns ascend with J (idx is sorted).
+__global__ void __launch_bounds__(256) scatter_add_compliance_kernel(int64_t mo, const double* __restrict__ U,
+                                                                     int64_t ldu, const int64_t* __restrict__ idx,
+                                                                     double* __restrict__ total, int64_t ldt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= 3 * mo) return;
+  const int64_t I = r / 3;
+  double* dst = total + (3 * idx[I] + (r - 3 * I)) * ldt;
+  const double* src = U + r * ldu;
+  for (int64_t c = lane; c < 3 * mo; c += 32) {
+    const int64_t J = c / 3;
+    const int64_t col = 3 * __ldg(idx + J) + (c - 3 * J);
+    dst[col] = add(dst[col], __ldcs(src + c));
+  }
+}
+
 // ---- frames ---------------------------------------------------------------
 
 __device__ __forceinline__ double dot3(const double* a, const double* b) {
@@ -467,6 +487,15 @@ int cnb_prox_update(int64_t mo, const double* U, int64_t ldu, const int64_t* idx
   const int64_t threads = 3 * mo * 32;
   prox_update_kernel<<<grid_for(threads, 256), 256, 0, st>>>(mo, U, ldu, idx, side, tv, h * h, p_a, p_b);
   CNB_LAUNCH_CHECK("prox_update_kernel");
+  return CNB_OK;
+}
+
+int cnb_scatter_add_compliance(int64_t mo, const double* U, int64_t ldu, const int64_t* idx, double* total,
+                               int64_t ldt, void* stream) {
+  if (mo <= 0) return CNB_OK;
+  scatter_add_compliance_kernel<<<grid_for(3 * mo * 32, 256), 256, 0, (cudaStream_t)stream>>>(mo, U, ldu, idx, total,
+                                                                                             ldt);
+  CNB_LAUNCH_CHECK("scatter_add_compliance_kernel");
   return CNB_OK;
 }
 
