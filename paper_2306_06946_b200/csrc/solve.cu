@@ -142,10 +142,31 @@ __global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int3
     const int64_t off = R.lo[ch] - los;
     const double* Rc = R.rhs + R.roff[ch];
     const int64_t cc0 = max(c0, off), cc1 = min(c1, off + wc);
-    for (int64_t c = cc0; c < cc1; ++c) {
-      const double* src = Rc + (c - off) * fc + ncc;
-      double* dst = Rs + c * f;
-      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) dst[rel[k]] += src[k];
+    // the child's (column, row) entries flattened over the threads, 4 per thread per
+    // batch: all loads of a batch are issued before its stores (the parent and child
+    // windows share one buffer, so the compiler could not reorder them otherwise)
+    const int nk = (int)(k1 - k0);
+    const int tot = nk * (int)max((int64_t)0, cc1 - cc0);
+    for (int e0 = threadIdx.x; e0 < tot; e0 += 4 * blockDim.x) {
+      double u[4], v[4];
+      double* d[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q * (int)blockDim.x;
+        d[q] = nullptr;
+        u[q] = 0.0;
+        if (e < tot) {
+          const int cq = e / nk, kq = e - cq * nk;
+          const int64_t c = cc0 + cq, k = k0 + kq;
+          u[q] = Rc[(c - off) * fc + ncc + k];
+          d[q] = Rs + c * f + rel[k];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = d[q] ? *d[q] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (d[q]) *d[q] = v[q] + u[q];
     }
     __syncthreads();
   }
