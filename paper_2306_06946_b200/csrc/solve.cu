@@ -346,25 +346,54 @@ __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int3
   const double* lcol = linv + S.linv_off[s] + i * nc;       // L11^{-1}[:, i] = row i of L11^{-T}
   const int64_t* rows = S.rows + S.rows_ptr[s];
   const int64_t first = S.first[s];
-  double acc[NC];
+  // four independent partial sums per column (lane-strided chunks of 128): the
+  // gathers X[rows[q]] of a chunk are all in flight together
+  double acc[4][NC];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-  for (int64_t j = i + lane; j < nc; j += 32) {
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[u][c] = 0.0;
+  int64_t j = i + lane;
+  for (; j + 96 < nc; j += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double l = lcol[j + 32 * u];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c < ncols) acc[u][c] = fma(l, Bp[c * n + first + j + 32 * u], acc[u][c]);
+    }
+  }
+  for (; j < nc; j += 32) {
     const double l = lcol[j];
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      if (c < ncols) acc[c] = fma(l, Bp[c * n + first + j], acc[c]);
+      if (c < ncols) acc[0][c] = fma(l, Bp[c * n + first + j], acc[0][c]);
   }
-  for (int64_t q = lane; q < nr; q += 32) {
-    const double pq = pcol[q];
-    const int64_t rq = rows[q];
+  int64_t q = lane;
+  for (; q + 96 < nr; q += 128) {
+    double pq[4];
+    int64_t rq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pq[u] = pcol[q + 32 * u];
+      rq[u] = rows[q + 32 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c < ncols) acc[u][c] = fma(-pq[u], X[c * n + rq[u]], acc[u][c]);
+  }
+  for (; q < nr; q += 32) {
+    const double pv = pcol[q];
+    const int64_t rv = rows[q];
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      if (c < ncols) acc[c] = fma(-pq, X[c * n + rq], acc[c]);
+      if (c < ncols) acc[0][c] = fma(-pv, X[c * n + rv], acc[0][c]);
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    const double v = warp_sum(acc[c]);
+    const double v = warp_sum((acc[0][c] + acc[1][c]) + (acc[2][c] + acc[3][c]));
     if (lane == 0 && c < ncols) X[c * n + first + i] = v;
   }
 }
