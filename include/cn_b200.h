@@ -64,6 +64,10 @@ const char* cnb_last_error(void);
  * (constraints.py:182-191, bit-exact order), fast_update_proximity
  * (constraints.py:217-244), the backward-Euler right-hand side
  * (dynamics.py:183-211) and S^T acc (solver.py:250-257). */
+/* d_i = float(n @ p_{vids[i]} - offset), bit-identical to the reference's plane
+ * test (collision.py:264-270): numpy's 3-element dot is an FMA chain. */
+int cnb_plane_distances(int64_t nv, const int64_t* vids, const double* pts, double n0, double n1, double n2,
+                        double offset, double* out, void* stream);
 int cnb_batch_detect_planes(int32_t ns, int64_t nsurf, const int64_t* vids, const double* Q, int64_t ldq,
                             const double* normals, const double* offsets, double threshold, int32_t* count,
                             int32_t* kept, void* stream);

@@ -29,6 +29,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_last_error": [],
     "cnb_rebuild_w": [I64, P, P, I64, P, I64, P],
     "cnb_sandwich": [I64, I64, P, P, P, I64, P, I64, P],
+    "cnb_plane_distances": [I64, P, P, F64, F64, F64, F64, P, P],
     "cnb_batch_detect_planes": [I32, I64, P, P, I64, P, P, F64, P, P, P],
     "cnb_batch_pairs": [I32, I64, I64, P, P, P, P, I64, P, P, P, P, P, P, P, P, P],
     "cnb_batch_gather_pa": [I64, P, P, P, P, I64, P, P],

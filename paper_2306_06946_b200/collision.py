@@ -634,18 +634,38 @@ def _vertex_vs_mesh(ga: MeshGeometry, gb: MeshGeometry, threshold: float) -> Pai
     return r
 
 
+def _plane_distances_device(geom: MeshGeometry, plane: PlaneGeometry):
+    """float(n @ p - offset) of every surface vertex on the device, bit for bit the
+    reference's per-vertex expression (numpy's 3-element dot is an FMA chain,
+    csrc/batch.cu plane_distances_kernel); None when the points are host-only."""
+    if geom.points_dev is None or len(geom.vertex_ids) == 0:
+        return None
+    vids = dv.upload(np.ascontiguousarray(geom.vertex_ids, dtype=np.int64))
+    pts = _device_points(geom)
+    out = dv.empty(len(geom.vertex_ids))
+    n = np.asarray(plane.normal, dtype=np.float64)
+    _lib.call("cnb_plane_distances", len(geom.vertex_ids), vids.data_ptr(), pts.data_ptr(), float(n[0]),
+              float(n[1]), float(n[2]), float(plane.offset), out.data_ptr(), _lib.stream())
+    return out.cpu().numpy()
+
+
 def _vertex_vs_plane(geom: MeshGeometry, plane: PlaneGeometry, threshold: float) -> PairSoA:
     n = plane.normal
-    pts = geom.points[geom.vertex_ids]
-    # vectorised gate with a margin, then the reference's own expression
-    # float(n @ p - offset) per candidate (collision.py:264-270): the kept set
-    # and the distances are the reference's bit for bit
-    approx = pts @ n - plane.offset
-    margin = 1e-12 * (np.abs(pts).max(initial=0.0) * np.abs(n).sum() + abs(plane.offset) + 1.0)
-    cand = np.flatnonzero(approx <= threshold + margin)
     points = np.asarray(geom.points, dtype=np.float64)
     vids_all = np.asarray(geom.vertex_ids, dtype=np.int64)
-    exact = np.array([float(n @ points[v] - plane.offset) for v in vids_all[cand]])
+    d_all = _plane_distances_device(geom, plane)
+    if d_all is not None:
+        cand = np.arange(len(vids_all))
+        exact = d_all
+    else:
+        # vectorised gate with a margin, then the reference's own expression
+        # float(n @ p - offset) per candidate (collision.py:264-270): the kept set
+        # and the distances are the reference's bit for bit
+        pts = geom.points[geom.vertex_ids]
+        approx = pts @ n - plane.offset
+        margin = 1e-12 * (np.abs(pts).max(initial=0.0) * np.abs(n).sum() + abs(plane.offset) + 1.0)
+        cand = np.flatnonzero(approx <= threshold + margin)
+        exact = np.array([float(n @ points[v] - plane.offset) for v in vids_all[cand]])
     keep = exact <= threshold
     m = int(keep.sum())
     r = PairSoA(m)

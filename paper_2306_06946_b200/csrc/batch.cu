@@ -32,10 +32,10 @@ __device__ __forceinline__ int scene_of(const int64_t* __restrict__ off, int ns,
   return a;
 }
 
-// numpy's 1-D dot of length 3 (n @ p) as a plain left-to-right loop without
-// contraction; the tests compare the kept sets with the reference's.
+// numpy's 1-D dot of length 3 (n @ p), bit for bit: a fused multiply-add chain
+// fma(a2, b2, fma(a1, b1, a0 b0)) (measured against numpy 2.3 on this image).
 __device__ __forceinline__ double ndot3(const double* a, const double* b) {
-  return add(add(mul(a[0], b[0]), mul(a[1], b[1])), mul(a[2], b[2]));
+  return fma(a[2], b[2], fma(a[1], b[1], mul(a[0], b[0])));
 }
 
 // One CTA per scene: signed distance of every candidate vertex to the scene's
@@ -116,6 +116,18 @@ __global__ void batch_gather_pa_kernel(int64_t m, const int32_t* __restrict__ ps
   const double* q = Q + (int64_t)pscene[i] * ldq + 3 * vids[pcand[i]];
 #pragma unroll
   for (int a = 0; a < 3; ++a) pa[3 * i + a] = q[a];
+}
+
+// Signed distance of surface vertices to a plane, the reference's own float(n @ p
+// - offset) (collision.py:264-270) bit for bit (ndot3 above).
+__global__ void plane_distances_kernel(int64_t nv, const int64_t* __restrict__ vids, const double* __restrict__ P,
+                                       double n0, double n1, double n2, double offset, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const double* p = P + 3 * vids[i];
+  const double n[3] = {n0, n1, n2};
+  const double q[3] = {p[0], p[1], p[2]};
+  out[i] = sub(ndot3(n, q), offset);
 }
 
 // W_g of every scene (packed at woff[s], c_s x c_s, c_s = 3 m_s, row stride
@@ -319,6 +331,14 @@ __global__ void __launch_bounds__(128) batch_gemm_kernel(int64_t M, int64_t N, i
 using namespace cnb;
 
 extern "C" {
+
+int cnb_plane_distances(int64_t nv, const int64_t* vids, const double* pts, double n0, double n1, double n2,
+                        double offset, double* out, void* stream) {
+  if (nv <= 0) return CNB_OK;
+  plane_distances_kernel<<<grid_for(nv, 256), 256, 0, (cudaStream_t)stream>>>(nv, vids, pts, n0, n1, n2, offset, out);
+  CNB_LAUNCH_CHECK("plane_distances_kernel");
+  return CNB_OK;
+}
 
 int cnb_batch_detect_planes(int32_t ns, int64_t nsurf, const int64_t* vids, const double* Q, int64_t ldq,
                             const double* normals, const double* offsets, double threshold, int32_t* count,

@@ -121,3 +121,24 @@ def test_batched_no_contacts_is_free_fall(cn):
     d = _h(B.Q) - B.rest_host
     assert np.abs(d[0] - d[1]).max() <= 1e-12
     assert (d.reshape(2, -1, 3)[:, :, 1] < 0).all()
+
+
+def test_plane_distances_bit_exact(cn):
+    """Device plane distances equal the reference's per-vertex float(n @ p - offset)
+    bit for bit (numpy's 3-element dot is a fused multiply-add chain)."""
+    from paper_2306_06946_b200 import _device as dv
+    from paper_2306_06946_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    pts = rng.uniform(-0.3, 0.3, (5000, 3))
+    vids = np.sort(rng.choice(5000, 3000, replace=False)).astype(np.int64)
+    for _ in range(3):
+        n = rng.standard_normal(3)
+        n /= np.linalg.norm(n)
+        off = float(rng.uniform(-0.01, 0.01))
+        out = dv.empty(len(vids))
+        d_vids, d_pts = dv.upload(vids), dv.f64(pts)  # keep the device copies alive across the launch
+        _lib.call("cnb_plane_distances", len(vids), d_vids.data_ptr(), d_pts.data_ptr(), float(n[0]),
+                  float(n[1]), float(n[2]), off, out.data_ptr(), _lib.stream())
+        ref = np.array([float(n @ pts[v] - off) for v in vids])
+        assert np.array_equal(_h(out), ref)
