@@ -404,8 +404,10 @@ __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int3
 __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                   const double* __restrict__ front, const double* __restrict__ linv,
                                                   double* __restrict__ p21) {
-  __shared__ double As[kMK * kMA];  // [k][row]
-  __shared__ double Bs[kMT * kMS];
+  // k chunks of 16, cp.async double buffer (as panel_mma_kernel)
+  constexpr int BK = 16, SB = BK + 4;
+  __shared__ double As[2][BK * kMA];  // [k][row]
+  __shared__ double Bs[2][kMT * SB];  // [col][k]
   const int64_t s = tasks[3 * blockIdx.x], q0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s), ldf = d_ldf(S, s);
   const double* F = front + S.front_off[s];
@@ -419,32 +421,46 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int64_t k0 = c0; k0 < nc; k0 += kMK) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
+  auto stage = [&](int buf, int64_t k0) {
+    for (int e = threadIdx.x; e < kMT * BK; e += blockDim.x) {
       const int rr = e % kMT, kk = e / kMT;
       const int64_t q = q0 + rr, k = k0 + kk;
-      cp_async8(&As[kk * kMA + rr], F + k * ldf + nc + q, q < nr && k < nc);
+      cp_async8(&As[buf][kk * kMA + rr], F + k * ldf + nc + q, q < nr && k < nc);
     }
-    for (int e = threadIdx.x; e < kMT * kMK; e += blockDim.x) {
-      const int kk = e % kMK, cc = e / kMK;
+    for (int e = threadIdx.x; e < kMT * BK; e += blockDim.x) {
+      const int kk = e % BK, cc = e / BK;
       const int64_t k = k0 + kk, c = c0 + cc;
-      cp_async8(&Bs[cc * kMS + kk], Li + c * nc + k, k < nc && c < nc && k >= c);
+      cp_async8(&Bs[buf][cc * SB + kk], Li + c * nc + k, k < nc && c < nc && k >= c);
     }
-    cp_async_wait_all();
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // L11^{-1} is lower triangular: only k >= c0 contributes
+  stage(0, c0);
+  int buf = 0;
+  for (int64_t k0 = c0; k0 < nc; k0 += BK) {
+    if (k0 + BK < nc) {
+      stage(buf ^ 1, k0 + BK);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncthreads();
+    const double* Ab = As[buf];
+    const double* Bb = Bs[buf];
 #pragma unroll
-    for (int kk = 0; kk < kMK; kk += 4) {
+    for (int kk = 0; kk < BK; kk += 4) {
       double fa[4], fb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) fa[a] = As[(kk + t) * kMA + wy + 8 * a + g];
+      for (int a = 0; a < 4; ++a) fa[a] = Ab[(kk + t) * kMA + wy + 8 * a + g];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) fb[b] = Bs[(wx + 8 * b + g) * kMS + kk + t];
+      for (int b = 0; b < 4; ++b) fb[b] = Bb[(wx + 8 * b + g) * SB + kk + t];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
     }
+    __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
