@@ -1535,7 +1535,6 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t G = s.groups, c = 3 * G;
   const int nb = (int)((G + kPG - 1) / kPG);
-  const unsigned H = gridDim.x - 1;
   const double h2 = s.h2;
   double* lamg = s.lam;
   unsigned* psolved = &ctl->solved;
@@ -1842,7 +1841,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
       double* Tn = slot ? sm.T0 : sm.T1;
       double* lamc = sm.lamx + slot * kPR;         // lambda_b (this solve)
       double* lamp = sm.lamx + (slot ^ 1) * kPR;   // lambda_{b-1}
-      const int64_t rb = 3 * (int64_t)b * kPG, rb1 = 3 * (int64_t)b1 * kPG, rbm = 3 * (int64_t)bm * kPG;
+      const int64_t rb = 3 * (int64_t)b * kPG, rb1 = 3 * (int64_t)b1 * kPG;
       const int si = tid - (64 + kRowOwners);  // phase-B diagonal-shift thread, one row (kPR <= 128)
       if (warp == 0) {
         // ---- sequential block solve ----

@@ -26,8 +26,6 @@ constexpr int kGemvRows = 32;   // rows per dense panel task
 constexpr int kGemvJ = 256;     // staged pivot rows of the RHS per pass
 constexpr int kBwdRows = 4;     // pivot rows per backward task (warp per row)
 constexpr int kMT = 64;         // DMMA panel tile (rows, cols)
-constexpr int kMK = 32;         // DMMA k-chunk
-constexpr int kMS = kMK + 4;    // smem stride (== 4 mod 16)
 constexpr int kMA = kMT + 4;    // k-major stride of tiles staged from column-major sources
 
 // RHS block of supernode s: R_s = rhs + roff[s], f_s x w_s column-major;
