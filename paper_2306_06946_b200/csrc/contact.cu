@@ -368,7 +368,7 @@ __global__ void csr_spmv_kernel(int64_t rows, const int64_t* __restrict__ rp, co
 // fixed summation order.  Used for the mapping compliance of contact DoFs:
 // U_o = S_o (E^T A^-1 E) S_o^T with E the unit columns of the DoFs S_o touches.
 constexpr int kEll = 4;
-__global__ void __launch_bounds__(256) sandwich_kernel(int64_t m, int64_t k, const int32_t* __restrict__ ecol,
+__global__ void __launch_bounds__(1024) sandwich_kernel(int64_t m, int64_t k, const int32_t* __restrict__ ecol,
                                                        const double* __restrict__ eval, const double* __restrict__ C,
                                                        int64_t ldc, double* __restrict__ U, int64_t ldu) {
   extern __shared__ double tsm[];
@@ -431,7 +431,7 @@ int cnb_sandwich(int64_t m, int64_t k, const int32_t* ell_col, const double* ell
     return CNB_E_VALIDATION;
   }
   CNB_CUDA(cudaFuncSetAttribute(sandwich_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  sandwich_kernel<<<(unsigned)m, 256, smem, (cudaStream_t)stream>>>(m, k, ell_col, ell_val, C, ldc, U, ldu);
+  sandwich_kernel<<<(unsigned)m, 1024, smem, (cudaStream_t)stream>>>(m, k, ell_col, ell_val, C, ldc, U, ldu);
   CNB_LAUNCH_CHECK("sandwich_kernel");
   return CNB_OK;
 }
