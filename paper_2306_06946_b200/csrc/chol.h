@@ -18,8 +18,9 @@
 namespace cnb {
 
 constexpr int kPanel = 32;   // pivot panel width of the dense front factorisation
-constexpr int kBlkPanels = 8;  // panels per trailing-update block: the trailing matrix is
-                               // updated once per kBlkPanels * kPanel = 128 columns (K = 128)
+constexpr int kBlkPanels = 16;  // panels per trailing-update block: the trailing matrix is
+                               // updated once per kBlkPanels * kPanel = 512 columns (K <= 512,
+                               // i.e. once per supernode piece: pieces are <= 512 wide)
 constexpr int kTile = 64;    // SYRK / GEMM output tile
 constexpr int kEaCols = 8;   // parent columns per extend-add task (small: more CTAs in flight)
 constexpr int kInvCols = 8;  // columns of L11^{-1} per inversion task
