@@ -49,6 +49,7 @@ __device__ __forceinline__ double panel_entry(const double* __restrict__ P, cons
 // of block kb is inverted already (D_kb, kept by potrf_kernel), so each block
 // step is y = D_kb v (a small product, no sequential row loop) followed by the
 // update of the rows below with the panel columns of L.
+static_assert(32 * kInvCols == 256, "trinv_kernel: one warp per column of the block (256 threads)");
 __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                     const double* __restrict__ front, const double* __restrict__ kkinv,
                                                     double* __restrict__ linv) {
