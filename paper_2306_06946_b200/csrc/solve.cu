@@ -612,8 +612,11 @@ __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const do
                                                    const int32_t* __restrict__ tile_sn, int64_t ncols,
                                                    const int64_t* __restrict__ sorted_cols, double* __restrict__ U,
                                                    int64_t ldu, int rank, int world) {
-  __shared__ double Ya[kGT * kGS];
-  __shared__ double Yb[kGT * kGS];
+  // (supernode, 16-deep k chunk) sequence of the tile, cp.async double buffer:
+  // chunk q+1 is staged while chunk q is multiplied (41 KB static shared memory)
+  constexpr int BK = 16, SB = BK + 4;
+  __shared__ double Ya[2][kGT * SB];
+  __shared__ double Yb[2][kGT * SB];
   // multi-GPU: this rank owns tiles t = rank, rank + world, ... (round robin)
   const int64_t t = (int64_t)blockIdx.x * world + rank;
   int64_t A = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -629,52 +632,74 @@ __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const do
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int32_t e = tile_ptr[t]; e < tile_ptr[t + 1]; ++e) {
+  const int32_t e0 = tile_ptr[t], e1 = tile_ptr[t + 1];
+  auto stage = [&](int buf, int32_t e, int64_t k0) {
     const int64_t s = tile_sn[e];
     const int64_t nc = d_nc(S, s);
     const int64_t lo = R.lo[s], w = R.w[s];
     const double* Ys = Y + yoff[s];
     const int64_t ldy = nc + (nc & 1);  // Y columns 16-byte aligned (panel_mma_kernel)
-    for (int64_t k0 = 0; k0 < nc; k0 += kGK) {
-      __syncthreads();
-      // 16-byte copies of k pairs; a pair straddling nc takes its valid element
-      // alone and a zero (the padding entry of Y is never written)
-      for (int idx = threadIdx.x; idx < (kGK / 2) * kGT; idx += blockDim.x) {
-        const int kk = 2 * (idx % (kGK / 2)), cc = idx / (kGK / 2);
-        const int64_t k = k0 + kk;
-        const int64_t la = ra0 + cc - lo, lb = rb0 + cc - lo;
-        const bool ia = la >= 0 && la < w, ib = lb >= 0 && lb < w;
-        double* da = &Ya[cc * kGS + kk];
-        double* db = &Yb[cc * kGS + kk];
-        if (k + 1 < nc) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(da)),
-                       "l"(ia ? Ys + la * ldy + k : Ys), "r"(ia ? 16 : 0)
-                       : "memory");
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(db)),
-                       "l"(ib ? Ys + lb * ldy + k : Ys), "r"(ib ? 16 : 0)
-                       : "memory");
-        } else {
-          cp_async8(da, Ys + la * ldy + k, ia && k < nc);
-          cp_async8(db, Ys + lb * ldy + k, ib && k < nc);
-          da[1] = 0.0;
-          db[1] = 0.0;
-        }
-      }
-      cp_async_wait_all();
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < kGK; kk += 4) {
-        double fa[4], fb[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) fa[a] = Ya[(wy + 8 * a + g) * kGS + kk + tq];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) fb[b] = Yb[(wx + 8 * b + g) * kGS + kk + tq];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+    // 16-byte copies of k pairs; a pair straddling nc takes its valid element
+    // alone and a zero (the padding entry of Y is never written)
+    for (int idx = threadIdx.x; idx < (BK / 2) * kGT; idx += blockDim.x) {
+      const int kk = 2 * (idx % (BK / 2)), cc = idx / (BK / 2);
+      const int64_t k = k0 + kk;
+      const int64_t la = ra0 + cc - lo, lb = rb0 + cc - lo;
+      const bool ia = la >= 0 && la < w, ib = lb >= 0 && lb < w;
+      double* da = &Ya[buf][cc * SB + kk];
+      double* db = &Yb[buf][cc * SB + kk];
+      if (k + 1 < nc) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(da)),
+                     "l"(ia ? Ys + la * ldy + k : Ys), "r"(ia ? 16 : 0)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(db)),
+                     "l"(ib ? Ys + lb * ldy + k : Ys), "r"(ib ? 16 : 0)
+                     : "memory");
+      } else {
+        cp_async8(da, Ys + la * ldy + k, ia && k < nc);
+        cp_async8(db, Ys + lb * ldy + k, ib && k < nc);
+        da[1] = 0.0;
+        db[1] = 0.0;
       }
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int32_t e = e0;
+  int64_t k0 = 0;
+  if (e < e1) stage(0, e, 0);
+  int buf = 0;
+  while (e < e1) {
+    int32_t en = e;
+    int64_t kn = k0 + BK;
+    if (kn >= d_nc(S, tile_sn[e])) {
+      ++en;
+      kn = 0;
+    }
+    if (en < e1) {
+      stage(buf ^ 1, en, kn);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* Pa = Ya[buf];
+    const double* Pb = Yb[buf];
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) fa[a] = Pa[(wy + 8 * a + g) * SB + kk + tq];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) fb[b] = Pb[(wx + 8 * b + g) * SB + kk + tq];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+    }
+    __syncthreads();
+    e = en;
+    k0 = kn;
+    buf ^= 1;
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
