@@ -299,9 +299,13 @@ int cnb_fe_gather(int64_t nblocks, const int64_t* cptr, const int64_t* contrib, 
                   double* f, void* stream);
 /* A = (1 + h alpha) M + (h beta + h^2) K with fixed rows/cols -> identity and
  * b = h (f_ext - f_el - alpha M v - beta K v) - h^2 K v, b[fixed] = 0
- * (SoftBody.assemble dynamics.py:183-211); non-finite b -> CNB_E_NONFINITE. */
-int cnb_fe_system(int64_t n, const int64_t* rowptr, const int64_t* col, const double* Kvals, const double* m3,
-                  const int8_t* fixed, double h, double alpha, double beta, const double* fel, const double* Kv,
+ * (SoftBody.assemble dynamics.py:183-211); non-finite b -> CNB_E_NONFINITE.
+ * (rowptr, col) is A's pattern: K's entries whose row and column are both
+ * free plus every diagonal (dynamics.py:192-200).  a_src[e] is A entry e's
+ * index in Kvals (-1 for a fixed DoF's diagonal); a_src = NULL when A and K
+ * share a pattern (no fixed DoFs).  Avals or b may be NULL. */
+int cnb_fe_system(int64_t n, const int64_t* rowptr, const int64_t* col, const int64_t* a_src, const double* Kvals,
+                  const double* m3, const int8_t* fixed, double h, double alpha, double beta, const double* fel, const double* Kv,
                   const double* v, const double* fext, double* Avals, double* b, cnb_status_t* d_status,
                   void* stream);
 

@@ -149,11 +149,20 @@ class Body:
     def internal_force(self, q, v):
         """K(q - q0) + a M v + b K v (dynamics.py:172-177)."""
         m3 = np.repeat(self.masses, 3)
-        return self.K @ (q - self.x0.ravel()) + self.alpha * (m3 * v) + self.beta * (self.K @ v)
+        K = self.stiffness_at(q)
+        return self.elastic_force(q) + self.alpha * (m3 * v) + self.beta * (K @ v)
+
+    def stiffness_at(self, q):
+        """Stiffness at configuration q (constant for the linear material)."""
+        return self.K
+
+    def elastic_force(self, q):
+        return self.K @ (q - self.x0.ravel())
 
     def system(self, q, v, h, gravity):
         """A and b of backward Euler (dynamics.py:183-211)."""
-        Kc = self.K.tocoo()
+        K = self.stiffness_at(q)
+        Kc = K.tocoo()
         m3 = np.repeat(self.masses, 3)
         fx = self.fixed_mask
         keep = ~(fx[Kc.row] | fx[Kc.col])
@@ -165,11 +174,84 @@ class Body:
         f_ext = m3 * np.tile(np.asarray(gravity, dtype=np.float64), len(self.x0))
         if self.extra_force is not None:
             f_ext = f_ext + np.tile(np.asarray(self.extra_force, dtype=np.float64), len(self.x0))
-        b = h * (f_ext - self.internal_force(q, v)) - h * h * (self.K @ v)
+        b = h * (f_ext - self.internal_force(q, v)) - h * h * (K @ v)
         b[fx] = 0.0
         if not np.all(np.isfinite(b)):
             raise OracleError("NonFiniteForce", "rhs not finite")
         return A, b
+
+
+# --------------------------------------------------------------------------
+# corotational material (north star; NOT in the reference)
+# --------------------------------------------------------------------------
+# The reference material is linear (dynamics.py:165-177): K is assembled once
+# and f_el = K (q - q0).  The corotational variant keeps the reference's
+# element blocks K_e (dynamics.py:88-93) and its backward-Euler system
+# (183-211) but, per tet, rotates them by the rotation R_e of the deformation
+# gradient F_e = sum_a x_a g_a^T:
+#     K(q)  = sum_e R_e K_e R_e^T,
+#     f_el  = sum_e R_e K_e (R_e^T x_e - x0_e),
+# and the factorisation is redone every step (the reference caches it for the
+# whole simulation, scene.py:411-415).  Parity against the reference itself
+# is defined only for the linear material, so this restatement is pinned by
+# its own properties (tests/test_oracle_corot_cpu.py): exact reduction to the
+# linear material at rest, zero force and rotated K under rigid motions,
+# symmetry, and f_el equal to the gradient of the element energy
+# 1/2 sum_e u_e^T K_e u_e, u_e = R_e^T x_e - x0_e (finite differences).
+
+def rotation_factor(F):
+    """Rotation maximising tr(R^T F) over SO(3) for a stack of 3x3 matrices:
+    R = U diag(1, 1, det(U V^T)) V^T.  For det F > 0 this is the orthogonal
+    polar factor of F (scipy.linalg.polar's u); for inverted elements the
+    reflection is removed along the smallest singular direction."""
+    U, _, Vt = np.linalg.svd(F)
+    d = np.sign(np.linalg.det(U @ Vt))
+    U = U.copy()
+    U[..., :, 2] *= d[..., None]
+    return U @ Vt
+
+
+class CorotBody(Body):
+    """Corotational soft body: the reference element blocks rotated per tet."""
+
+    refactor_each_step = True
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        self.grads, self.vols = shape_gradients(self.x0, self.tets)
+        self.Ke = element_blocks(self.x0, self.tets, self.young, self.poisson)  # (e, a, b, 3, 3)
+        dof = 3 * self.tets[:, :, None] + np.arange(3)
+        self._r = np.broadcast_to(dof[:, :, None, :, None], self.Ke.shape).ravel()
+        self._c = np.broadcast_to(dof[:, None, :, None, :], self.Ke.shape).ravel()
+
+    def rotations(self, q):
+        x = np.asarray(q, dtype=np.float64).reshape(-1, 3)
+        F = np.einsum("eai,eaj->eij", x[self.tets], self.grads)
+        return rotation_factor(F)
+
+    def element_state(self, q):
+        """(R (e,3,3), rotated blocks Kb (e,4,4,3,3), element forces fe (e,4,3), local u)."""
+        x = np.asarray(q, dtype=np.float64).reshape(-1, 3)
+        R = self.rotations(q)
+        u = np.einsum("eji,eaj->eai", R, x[self.tets]) - self.x0[self.tets]
+        fl = np.einsum("eabij,ebj->eai", self.Ke, u)
+        fe = np.einsum("eij,eaj->eai", R, fl)
+        Kb = np.einsum("eik,eabkl,ejl->eabij", R, self.Ke, R)
+        return R, Kb, fe, u
+
+    def stiffness_at(self, q):
+        _, Kb, _, _ = self.element_state(q)
+        return sp.coo_matrix((Kb.ravel(), (self._r, self._c)), shape=(self.n, self.n)).tocsr()
+
+    def elastic_force(self, q):
+        _, _, fe, _ = self.element_state(q)
+        f = np.zeros((len(self.x0), 3))
+        np.add.at(f, self.tets.ravel(), fe.reshape(-1, 3))
+        return f.ravel()
+
+    def energy(self, q):
+        _, _, _, u = self.element_state(q)
+        return 0.5 * float(np.einsum("eai,eabij,ebj->", u, self.Ke, u))
 
 
 class Factor:
@@ -645,7 +727,7 @@ class Scene:
         F, free_dv, q_free, S = {}, {}, {}, {}
         for i, b in enumerate(self.bodies):
             A, rhs = b.system(self.q[i], self.v[i], h, self.g)
-            if self.factors[i] is None:
+            if self.factors[i] is None or getattr(b, "refactor_each_step", False):
                 self.factors[i] = Factor(A)
             F[i] = self.factors[i]
             free_dv[i] = F[i].solve(rhs)

@@ -63,7 +63,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_csr_spmv": [I64, P, P, P, P, P, F64, P],
     "cnb_fe_element": [I64, P, P, P, P, P, F64, F64, I32, P, P, P, P],
     "cnb_fe_gather": [I64, P, P, P, P, P, I64, P, P, P, P, P],
-    "cnb_fe_system": [I64, P, P, P, P, P, F64, F64, F64, P, P, P, P, P, P, P, P],
+    "cnb_fe_system": [I64, P, P, P, P, P, P, F64, F64, F64, P, P, P, P, P, P, P, P],
     "cnb_chol_analyze": [I64, P, P, I32, P, I32, P],
     "cnb_chol_destroy": [P],
     "cnb_chol_info": [P, P, P],

@@ -208,36 +208,35 @@ def _skew(r):
 
 
 def attachment_triplets(attachment: Attachment, n_dofs: int, row0: int):
-    """COO triplets of one attachment's 3 x n_dofs velocity map."""
-    rows, cols, vals = [], [], []
-    if attachment.kind == AttachKind.VERTEX:
-        if not 0 <= 3 * attachment.vertex + 2 < n_dofs:
-            raise InvalidAttachmentError(f"vertex {attachment.vertex} out of range")
-        for i in range(3):
-            rows.append(row0 + i)
-            cols.append(3 * attachment.vertex + i)
-            vals.append(1.0)
-    elif attachment.kind == AttachKind.BARYCENTRIC:
-        for node, w in zip(attachment.triangle, attachment.weights):
-            if not 0 <= 3 * node + 2 < n_dofs:
-                raise InvalidAttachmentError(f"triangle node {node} out of range")
-            for i in range(3):
-                rows.append(row0 + i)
-                cols.append(3 * int(node) + i)
-                vals.append(float(w))
-    elif attachment.kind == AttachKind.RIGID_LOCAL:
+    """COO triplets (rows, cols, vals) of one attachment's 3 x n_dofs velocity map
+    (reference collision.py:430-462).
+
+    A point attached to nodes k with weights w moves with sum_k w_k v_k, so node
+    k contributes w_k I_3 at columns 3k..3k+2 (VERTEX: one node, weight 1;
+    BARYCENTRIC: the triangle's nodes).  A rigid lever r maps the 6 body DoFs
+    through [I_3, -skew(r)] (its nonzeros, row-major).  Entries come out row
+    block by row block in node order, the reference's triplet order.
+    """
+    kind = attachment.kind
+    if kind == AttachKind.RIGID_LOCAL:
         if n_dofs != 6:
             raise InvalidAttachmentError("rigid attachment on a non-rigid object")
-        blk = np.hstack([np.eye(3), -_skew(attachment.lever)])
-        for i in range(3):
-            for j in range(6):
-                if blk[i, j] != 0.0:
-                    rows.append(row0 + i)
-                    cols.append(j)
-                    vals.append(blk[i, j])
+        jac = np.concatenate([np.eye(3), -_skew(attachment.lever)], axis=1)
+        r, c = np.nonzero(jac)
+        return (row0 + r).tolist(), c.tolist(), jac[r, c].tolist()
+    if kind == AttachKind.VERTEX:
+        nodes, weights, what = np.array([int(attachment.vertex)]), np.ones(1), "vertex"
+    elif kind == AttachKind.BARYCENTRIC:
+        nodes = np.asarray(attachment.triangle, dtype=np.int64).reshape(-1)
+        weights, what = np.asarray(attachment.weights, dtype=np.float64).reshape(-1), "triangle node"
     else:
         raise InvalidAttachmentError(f"attachment kind {attachment.kind} carries no DOFs")
-    return rows, cols, vals
+    bad = (nodes < 0) | (3 * nodes + 2 >= n_dofs)
+    if bad.any():
+        raise InvalidAttachmentError(f"{what} {int(nodes[bad][0])} out of range")
+    rows = row0 + np.tile(np.arange(3), len(nodes))
+    cols = (3 * nodes[:, None] + np.arange(3)).reshape(-1)
+    return rows.tolist(), cols.tolist(), np.repeat(weights, 3).tolist()
 
 
 # --------------------------------------------------------------------------

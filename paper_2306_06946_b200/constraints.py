@@ -125,6 +125,15 @@ class SignedMapping:
     idx: np.ndarray
     side: np.ndarray
     _dev: tuple | None = None
+    _sorted: sp.csr_matrix | None = None
+
+    @property
+    def sorted_csr(self) -> sp.csr_matrix:
+        """The same matrix with ascending columns per row (device planning order);
+        ``csr`` keeps the reference's own entry order."""
+        if self._sorted is None:
+            self._sorted = self.csr.sorted_indices() if not self.csr.has_sorted_indices else self.csr
+        return self._sorted
 
     @property
     def shape(self):
@@ -180,8 +189,8 @@ def build_signed_mapping(pairs, object_id: int, n_dofs: int, fixed_mask=None) ->
             side.append(1 if sign > 0 else -1)
     S = sp.coo_matrix((vals, (rows, cols)), shape=(3 * len(plist), n_dofs)).tocsr()
     if fixed_mask is not None and np.asarray(fixed_mask).any():
+        # the reference's product keeps its (unsorted) column order per row
         S = (S @ sp.diags(np.where(fixed_mask, 0.0, 1.0))).tocsr()
-    S.sort_indices()
     return SignedMapping(S, np.asarray(idx, dtype=np.int64), np.asarray(side, dtype=np.int8))
 
 
@@ -210,8 +219,9 @@ def _signed_mapping_table(table: PairTable, object_id: int, n_dofs: int, fixed_m
     vals = np.concatenate(vals) if vals else np.zeros(0)
     S = sp.coo_matrix((vals, (rows, cols)), shape=(3 * m, n_dofs)).tocsr()
     if fixed_mask is not None and np.asarray(fixed_mask).any():
+        # same CSR as the reference before the product, so the same (unsorted)
+        # column order per row after it (constraints.py:116-119)
         S = (S @ sp.diags(np.where(fixed_mask, 0.0, 1.0))).tocsr()
-    S.sort_indices()
     return SignedMapping(S, ii.astype(np.int64), np.where(ss == 0, 1, -1).astype(np.int8))
 
 

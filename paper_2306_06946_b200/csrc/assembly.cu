@@ -21,10 +21,88 @@
 
 namespace cnb {
 
+// Rotation maximising tr(R^T F) over SO(3) for any F (Horn's quaternion
+// form): tr(R(q)^T F) = q^T N q for a unit quaternion q, with N the symmetric
+// 4x4 matrix below, so the maximiser is N's top eigenvector (cyclic Jacobi,
+// fp64).  It equals the polar factor when det F > 0 and
+// U diag(1, 1, -1) V^T (F = U S V^T) for inverted elements — the oracle's
+// rotation_factor (oracle/cn_oracle.py).
+__device__ void max_trace_rotation(const double F[9], double R[9]) {
+  // S = F^T in Horn's notation (S_ab = sum over points of a_a b_b)
+  const double Sxx = F[0], Sxy = F[3], Sxz = F[6];
+  const double Syx = F[1], Syy = F[4], Syz = F[7];
+  const double Szx = F[2], Szy = F[5], Szz = F[8];
+  double A[4][4] = {{Sxx + Syy + Szz, Syz - Szy, Szx - Sxz, Sxy - Syx},
+                    {Syz - Szy, Sxx - Syy - Szz, Sxy + Syx, Szx + Sxz},
+                    {Szx - Sxz, Sxy + Syx, -Sxx + Syy - Szz, Syz + Szy},
+                    {Sxy - Syx, Szx + Sxz, Syz + Szy, -Sxx - Syy + Szz}};
+  double V[4][4] = {{1, 0, 0, 0}, {0, 1, 0, 0}, {0, 0, 1, 0}, {0, 0, 0, 1}};
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < 3; ++p)
+      for (int q = p + 1; q < 4; ++q) off += fabs(A[p][q]);
+    if (off == 0.0) break;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = p + 1; q < 4; ++q) {
+        const double apq = A[p][q];
+        const double g = 100.0 * fabs(apq);
+        if (sweep > 3 && fabs(A[p][p]) + g == fabs(A[p][p]) && fabs(A[q][q]) + g == fabs(A[q][q])) {
+          A[p][q] = A[q][p] = 0.0;
+          continue;
+        }
+        if (apq == 0.0) continue;
+        const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
+        double t;
+        if (fabs(theta) > 1e150) {
+          t = 0.5 / theta;
+        } else {
+          t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+          if (theta < 0.0) t = -t;
+        }
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < 4; ++k) {  // columns p, q
+          const double akp = A[k][p], akq = A[k][q];
+          A[k][p] = c * akp - sn * akq;
+          A[k][q] = sn * akp + c * akq;
+        }
+        for (int k = 0; k < 4; ++k) {  // rows p, q
+          const double apk = A[p][k], aqk = A[q][k];
+          A[p][k] = c * apk - sn * aqk;
+          A[q][k] = sn * apk + c * aqk;
+        }
+        for (int k = 0; k < 4; ++k) {
+          const double vkp = V[k][p], vkq = V[k][q];
+          V[k][p] = c * vkp - sn * vkq;
+          V[k][q] = sn * vkp + c * vkq;
+        }
+      }
+  }
+  int best = 0;
+  for (int k = 1; k < 4; ++k)
+    if (A[k][k] > A[best][best]) best = k;
+  double w = V[0][best], x = V[1][best], y = V[2][best], z = V[3][best];
+  const double inv = 1.0 / sqrt(w * w + x * x + y * y + z * z);
+  w *= inv;
+  x *= inv;
+  y *= inv;
+  z *= inv;
+  R[0] = w * w + x * x - y * y - z * z;
+  R[1] = 2.0 * (x * y - w * z);
+  R[2] = 2.0 * (x * z + w * y);
+  R[3] = 2.0 * (x * y + w * z);
+  R[4] = w * w - x * x + y * y - z * z;
+  R[5] = 2.0 * (y * z - w * x);
+  R[6] = 2.0 * (x * z - w * y);
+  R[7] = 2.0 * (y * z + w * x);
+  R[8] = w * w - x * x - y * y + z * z;
+}
+
 // Orthogonal polar factor by Newton iteration R <- (R + R^{-T}) / 2 from F
-// (quadratic convergence, exact to rounding for det F > 0).  For inverted or
-// degenerate elements (det F <= 0) the closest rotation is taken by the
-// axis-angle fixed point of Mueller et al. (maximises tr(R^T F)) from I.
+// (quadratic convergence, exact to rounding for det F > 0).  Inverted or
+// degenerate elements (det F <= 1e-12) take the rotation maximising
+// tr(R^T F) instead (max_trace_rotation).
 __device__ void polar_rotation(const double F[9], double R[9]) {
   const double det = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
                      F[2] * (F[3] * F[7] - F[4] * F[6]);
@@ -53,34 +131,7 @@ __device__ void polar_rotation(const double F[9], double R[9]) {
     }
     return;
   }
-  // Mueller, Bender, Chentanez, Macklin (2016): rotation maximising tr(R^T F)
-  for (int e = 0; e < 9; ++e) R[e] = (e % 4 == 0) ? 1.0 : 0.0;
-  for (int it = 0; it < 100; ++it) {
-    double om[3] = {0, 0, 0}, dn = 0.0;
-    for (int c = 0; c < 3; ++c) {  // columns
-      const double r0 = R[c], r1 = R[3 + c], r2 = R[6 + c];
-      const double a0 = F[c], a1 = F[3 + c], a2 = F[6 + c];
-      om[0] += r1 * a2 - r2 * a1;
-      om[1] += r2 * a0 - r0 * a2;
-      om[2] += r0 * a1 - r1 * a0;
-      dn += r0 * a0 + r1 * a1 + r2 * a2;
-    }
-    const double sc = 1.0 / (fabs(dn) + 1e-9);
-    om[0] *= sc;
-    om[1] *= sc;
-    om[2] *= sc;
-    const double w = sqrt(om[0] * om[0] + om[1] * om[1] + om[2] * om[2]);
-    if (w < 1e-12) break;
-    const double ax[3] = {om[0] / w, om[1] / w, om[2] / w};
-    const double c = cos(w), s = sin(w), t = 1.0 - c;
-    const double Q[9] = {t * ax[0] * ax[0] + c,         t * ax[0] * ax[1] - s * ax[2], t * ax[0] * ax[2] + s * ax[1],
-                         t * ax[0] * ax[1] + s * ax[2], t * ax[1] * ax[1] + c,         t * ax[1] * ax[2] - s * ax[0],
-                         t * ax[0] * ax[2] - s * ax[1], t * ax[1] * ax[2] + s * ax[0], t * ax[2] * ax[2] + c};
-    double N[9];
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) N[3 * i + j] = Q[3 * i] * R[j] + Q[3 * i + 1] * R[3 + j] + Q[3 * i + 2] * R[6 + j];
-    for (int e = 0; e < 9; ++e) R[e] = N[e];
-  }
+  max_trace_rotation(F, R);
 }
 
 // One thread per tet.  grads: (tets, 4, 3) rest shape-function gradients;
@@ -185,11 +236,15 @@ __global__ void gather_forces_kernel(int64_t nnodes, const int64_t* __restrict__
 }
 
 // A = k_scale K + diag((1 + h alpha) m) with fixed rows/cols -> identity.
-// diag_idx[dof] = CSR index of the diagonal entry; fixed (per DoF, int8).
+// A has its own CSR pattern (rp, ci): the reference keeps a K entry only when
+// neither its row nor its column is fixed, plus one diagonal entry per DoF
+// (dynamics.py:190-200).  src[e] = index of A entry e in K's value array (-1:
+// a fixed DoF's diagonal); src == NULL means A shares K's pattern (no fixed
+// DoFs).  fixed: per DoF, int8.
 __global__ void system_matrix_kernel(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
-                                     const double* __restrict__ K, const double* __restrict__ m3,
-                                     const int8_t* __restrict__ fixed, double k_scale, double m_scale,
-                                     double* __restrict__ A) {
+                                     const int64_t* __restrict__ src, const double* __restrict__ K,
+                                     const double* __restrict__ m3, const int8_t* __restrict__ fixed,
+                                     double k_scale, double m_scale, double* __restrict__ A) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const bool fr = fixed[r] != 0;
@@ -199,7 +254,7 @@ __global__ void system_matrix_kernel(int64_t n, const int64_t* __restrict__ rp, 
     if (fr || fixed[c]) {
       v = (c == r) ? 1.0 : 0.0;
     } else {
-      v = k_scale * K[e];
+      v = k_scale * K[src ? src[e] : e];
       if (c == r) v += m_scale * m3[r];
     }
     A[e] = v;
@@ -252,14 +307,14 @@ int cnb_fe_gather(int64_t nblocks, const int64_t* cptr, const int64_t* contrib, 
   return CNB_OK;
 }
 
-int cnb_fe_system(int64_t n, const int64_t* rowptr, const int64_t* col, const double* Kvals, const double* m3,
-                  const int8_t* fixed, double h, double alpha, double beta, const double* fel, const double* Kv,
+int cnb_fe_system(int64_t n, const int64_t* rowptr, const int64_t* col, const int64_t* a_src, const double* Kvals,
+                  const double* m3, const int8_t* fixed, double h, double alpha, double beta, const double* fel, const double* Kv,
                   const double* v, const double* fext, double* Avals, double* b, cnb_status_t* d_status,
                   void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n <= 0) return CNB_OK;
   if (Avals) {
-    system_matrix_kernel<<<grid_for(n, 128), 128, 0, st>>>(n, rowptr, col, Kvals, m3, fixed, h * beta + h * h,
+    system_matrix_kernel<<<grid_for(n, 128), 128, 0, st>>>(n, rowptr, col, a_src, Kvals, m3, fixed, h * beta + h * h,
                                                            1.0 + h * alpha, Avals);
     CNB_LAUNCH_CHECK("system_matrix_kernel");
   }

@@ -138,6 +138,29 @@ class _FeLayout:
         self.fptr = np.zeros(nn + 1, dtype=np.int64)
         self.fptr[1:] = np.cumsum(fcnt)
 
+    def system_pattern(self, fixed_dof: np.ndarray):
+        """Pattern of A given the per-DoF fixed mask (dynamics.py:190-200).
+
+        The reference keeps a K entry only when neither its row nor its
+        column is fixed and adds one diagonal entry per DoF; structural zeros
+        of the kept 3x3 blocks stay.  Returns (rowptr, indices, src) with
+        src[e] = index of A entry e in K's values (-1: a fixed DoF's
+        diagonal), or src None when nothing is fixed (A shares K's pattern).
+        """
+        if not fixed_dof.any():
+            return self.rowptr, self.indices, None
+        n = len(self.rowptr) - 1
+        row = np.repeat(np.arange(n), np.diff(self.rowptr))
+        keep = ~(fixed_dof[row] | fixed_dof[self.indices])
+        fdof = np.flatnonzero(fixed_dof)
+        rows = np.concatenate([row[keep], fdof])
+        cols = np.concatenate([self.indices[keep], fdof])
+        src = np.concatenate([np.flatnonzero(keep), np.full(len(fdof), -1, dtype=np.int64)])
+        order = np.lexsort((cols, rows))
+        rowptr = np.zeros(n + 1, dtype=np.int64)
+        rowptr[1:] = np.cumsum(np.bincount(rows, minlength=n))
+        return rowptr, cols[order].astype(np.int64), src[order].astype(np.int64)
+
 
 class SoftBody:
     """Tetrahedral FE body (or a tetless particle cloud with explicit masses)."""
@@ -214,8 +237,15 @@ class SoftBody:
                 K=dv.zeros(lay.rowptr[-1], d), Kv=dv.empty(self.n_dofs, d), fel=dv.zeros(self.n_dofs, d),
                 R=dv.empty((max(ne, 1), 9), d),
             )
-            D["pattern"] = SparsityPattern(lay.rowptr, lay.indices, self.n_dofs, block_size=3,
+            a_rowptr, a_indices, a_src = lay.system_pattern(self.fixed_mask)
+            D["pattern"] = SparsityPattern(a_rowptr, a_indices, self.n_dofs, block_size=3,
                                            coords=self.mesh.nodes)
+            if a_src is None:
+                D["a_rowptr"], D["a_indices"], D["a_src"] = D["rowptr"], D["indices"], None
+            else:
+                D["a_rowptr"] = torch.as_tensor(a_rowptr, device=d)
+                D["a_indices"] = torch.as_tensor(a_indices, device=d)
+                D["a_src"] = torch.as_tensor(a_src, device=d)
             self._dev = D
             if self.material == "linear":
                 self._assemble_elements(D["x0"])  # K at rest, constant
@@ -286,9 +316,10 @@ class SoftBody:
         self._elastic(q)
         self._kmul(v, D["Kv"])
         b = dv.empty(self.n_dofs)
-        A_vals = dv.empty(D["lay"].rowptr[-1]) if with_matrix else None
+        A_vals = dv.empty(D["pattern"].nnz) if with_matrix else None
         st = _lib.status(b.device)
-        _lib.call("cnb_fe_system", self.n_dofs, D["rowptr"].data_ptr(), D["indices"].data_ptr(), D["K"].data_ptr(),
+        _lib.call("cnb_fe_system", self.n_dofs, D["a_rowptr"].data_ptr(), D["a_indices"].data_ptr(),
+                  D["a_src"].data_ptr() if D["a_src"] is not None else None, D["K"].data_ptr(),
                   D["m3"].data_ptr(), D["fixed"].data_ptr(), float(h), float(self.rayleigh_mass),
                   float(self.rayleigh_stiffness), D["fel"].data_ptr(), D["Kv"].data_ptr(), v.data_ptr(),
                   self._fext(gravity).data_ptr(), A_vals.data_ptr() if A_vals is not None else None, b.data_ptr(),

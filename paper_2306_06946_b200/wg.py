@@ -45,7 +45,7 @@ def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, sha
     U = dv.empty((3 * mo, 3 * mo))
     if mo:
         rows = (3 * idx[:, None] + np.arange(3)).ravel()
-        csr = S.csr
+        csr = S.sorted_csr
         colptr = np.zeros(3 * mo + 1, dtype=np.int64)
         counts = np.diff(csr.indptr)[rows]
         colptr[1:] = np.cumsum(counts)

@@ -387,6 +387,47 @@ def scene_io():
     shutil.rmtree(tmp)
 
 
+def fixed_mapping():
+    """Two stacked five-tet blocks; the lower one rests on the ground with its
+    bottom layer and part of its top face fixed, so vertex-plane and
+    barycentric rows both land on fixed DoFs.  Records the reference's pair
+    keys, the signed mappings S_o (build_signed_mapping constraints.py:101-120:
+    fixed columns zeroed and dropped) and the system-matrix patterns
+    (SoftBody.assemble dynamics.py:183-211: fixed rows/cols -> identity), then
+    a 3-step forced fast-scheme trajectory."""
+    lower = five_tet_grid((5, 3, 5), 0.01, (0.0, 0.0015, 0.0))
+    upper = five_tet_grid((4, 2, 4), 0.01, (0.005, 0.0235, 0.005))
+    ln = lower.nodes
+    bottom = np.flatnonzero(ln[:, 1] <= ln[:, 1].min() + 1e-12)
+    top = np.flatnonzero(ln[:, 1] >= ln[:, 1].max() - 1e-12)
+    fixed_top = top[(ln[top, 0] <= 0.02 + 1e-12) & (ln[top, 2] <= 0.02 + 1e-12)]
+    fixed = np.sort(np.concatenate([bottom, fixed_top]))
+    soft0 = rsc.SoftSpec(name="lower", mesh=cn.TetMesh(lower.nodes, lower.tets), young=1e4, poisson=0.4,
+                         density=1000.0, fixed_nodes=fixed)
+    soft1 = rsc.SoftSpec(name="upper", mesh=cn.TetMesh(upper.nodes, upper.tets), young=2e3, poisson=0.4,
+                         density=1000.0, velocity=(0.0, -0.1, 0.0))
+    plane = rsc.PlaneSpec(name="ground", normal=(0.0, 1.0, 0.0), offset=0.0)
+    cfg = rsc.SceneConfig(objects=[soft0, soft1, plane], h=0.01, threshold=0.004,
+                          pgs=rsol.PgsConfig(max_iterations=400, tolerance=1e-10, friction=0.4),
+                          newton=rsol.NewtonConfig(scheme="fast", max_iterations=3, penetration_tol=-1,
+                                                   rotation_tol=-1),
+                          output=rsc.OutputConfig(snapshots=False, metrics=False))
+    sim = rsc.Simulation(cfg)
+    out = {}
+    ctx, free, states, pen_before, timings, t_next = sim.prepare_step(build_wg=True)
+    for oid, S in ctx.S_by_object.items():
+        S = S.tocsr()
+        out[f"S{oid}_indptr"], out[f"S{oid}_indices"], out[f"S{oid}_data"] = S.indptr, S.indices, S.data
+    for obj in sim.dynamic_objects:
+        A, b = obj.body.assemble(obj.state, cfg.h, cfg.gravity)
+        out[f"A{obj.oid}_indptr"], out[f"A{obj.oid}_indices"] = A.csr.indptr, A.csr.indices
+        out[f"A{obj.oid}_data"], out[f"b{obj.oid}"] = A.csr.data, b
+    out.update(_run_scene(cfg, 3, {0}, tag="fixed_mapping"))
+    out.update(lower_nodes=lower.nodes, lower_tets=lower.tets, upper_nodes=upper.nodes, upper_tets=upper.tets,
+               fixed=fixed)
+    save("fixed_mapping.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kat_rebuild", "kat_pgs", "kat_frames", "kat_linalg", "scenes", "scenes_standard",
                              "scene_io", "cylinder_press"]

@@ -138,3 +138,14 @@ def test_fill_is_reasonable_against_superlu():
     # stored entries include structural zeros of relaxed supernodes; plain
     # nested dissection fills more than minimum degree at this small size
     assert S["info"][2] <= 3.0 * nnz_superlu, (S["info"][2], nnz_superlu)
+
+
+def test_reference_matrix_with_fixed_nodes(golden):
+    """The reference's own A (fixed nodes [0, 1, 2]: identity rows, the fixed
+    nodes isolated in the node graph) through the blocked geometric analysis."""
+    g = golden("kat_linalg.npz")
+    n = len(g["b"])
+    A = sp.csr_matrix((g["data"], g["indices"], g["indptr"]), shape=(n, n))
+    S, A = analyze(A, bs=3, coords=g["nodes"], leaf=4)
+    x = emulate_factor_solve(S, A, g["b"])
+    assert np.abs(x - g["x"]).max() <= 1e-12 * np.abs(g["x"]).max()
