@@ -273,14 +273,31 @@ int cnb_chol_solve(cnb_chol_t h, const double* B, int64_t ldb, double* X, int64_
  * CSC form (colptr, rowidx = DoF ids, vals).  Y = L^{-1} P S^T is formed only
  * on the elimination paths of the columns and U = Y^T Y by fp64 MMA tiles.
  * Replaces solve_multi(S^T) + S @ X of assemble_Wg constraints.py:175-178.
- * flops_out (host, may be NULL) = {forward-solve flops, Gram flops}.
- * Multi-GPU: with world > 1 the 64x64 Gram tiles are split
- * round-robin over ranks; this rank writes its tiles and zeros elsewhere, and
- * the caller sums U over ranks (NCCL all-reduce) — exact, since every entry is
- * produced by exactly one rank.  world = 1: the whole U. */
+ * flops_out (host, may be NULL) = {forward-solve flops, Gram flops}. */
 int cnb_chol_compliance(cnb_chol_t h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
-                        const double* vals, double* U, int64_t ldu, double* flops_out, int32_t rank,
-                        int32_t world, void* stream);
+                        const double* vals, double* U, int64_t ldu, double* flops_out, void* stream);
+
+/* The same U over `world` GPUs, right-hand-side columns split per rank with the
+ * factor replicated (constraints.py:155-179 -> linalg.py:98-106).
+ * Protocol, every rank, in order (the caller owns the collectives):
+ *   plan(rank, world) -> sizes[0] = doubles of every rank's compact Y (send
+ *       count), sizes[1] = doubles of every rank's Gram tile buffer, sizes[2..3]
+ *       = this rank's sorted column range; flops_out = this rank's share;
+ *   forward(ysend): forward solve of the rank's columns into ysend;
+ *   caller: all-gather ysend -> yall (world x sizes[0], rank-major);
+ *   gram(yall, tiles): every rank's Y unpacked, this rank's 64x64 Gram tiles
+ *       (tile t -> rank t mod world) into tiles (sizes[1]);
+ *   caller: all-gather tiles -> tiles_all (world x sizes[1]);
+ *   finish(tiles_all, U, ldu): every tile scattered into U (and its mirror).
+ * Every column's forward solve and every tile's Gram sum are computed exactly
+ * as by cnb_chol_compliance, so U is bit-identical for every world size.  The
+ * plan lives in the handle until the next plan call. */
+int cnb_chol_compliance_plan(cnb_chol_t h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
+                             const double* vals, int32_t rank, int32_t world, int64_t* sizes, double* flops_out,
+                             void* stream);
+int cnb_chol_compliance_forward(cnb_chol_t h, double* ysend, void* stream);
+int cnb_chol_compliance_gram(cnb_chol_t h, const double* yall, double* tiles, void* stream);
+int cnb_chol_compliance_finish(cnb_chol_t h, const double* tiles_all, double* U, int64_t ldu, void* stream);
 
 /* ---- FE assembly (contactnewton/dynamics.py) ------------------------------ */
 

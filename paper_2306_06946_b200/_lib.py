@@ -71,7 +71,11 @@ _SIGNATURES: dict[str, list] = {
     "cnb_chol_export": [P, ctypes.c_char_p, P],
     "cnb_chol_factor": [P, P, P, P],
     "cnb_chol_solve": [P, P, I64, P, I64, I64, P],
-    "cnb_chol_compliance": [P, I64, P, P, P, P, I64, P, I32, I32, P],
+    "cnb_chol_compliance": [P, I64, P, P, P, P, I64, P, P],
+    "cnb_chol_compliance_plan": [P, I64, P, P, P, I32, I32, P, P, P],
+    "cnb_chol_compliance_forward": [P, P, P],
+    "cnb_chol_compliance_gram": [P, P, P, P],
+    "cnb_chol_compliance_finish": [P, P, P, I64, P],
     "cnb_bench_dmma": [I32, P, P],
     "cnb_bench_latency": [P, P],
     "cnb_launch_count": [],

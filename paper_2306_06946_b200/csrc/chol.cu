@@ -508,6 +508,7 @@ static void chol_free(CholHandle* h) {
   h->plan8.release();
   for (GrowBuf* b : {&h->bp, &h->tbuf, &h->c_int, &h->c_rhs, &h->c_val, &h->c_y}) b->release();
   h->c_pin.release();
+  free_compliance_plan(h);
 }
 
 static std::map<std::string, std::pair<const void*, size_t>> export_table(const CholHandle* h) {
@@ -710,14 +711,36 @@ int cnb_chol_solve(cnb_chol_t hh, const double* B, int64_t ldb, double* X, int64
 }
 
 int cnb_chol_compliance(cnb_chol_t hh, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
-                        const double* vals, double* U, int64_t ldu, double* flops_out, int32_t rank, int32_t world,
-                        void* stream) {
+                        const double* vals, double* U, int64_t ldu, double* flops_out, void* stream) {
   CholHandle* h = H(hh);
   if (!h->factored) {
     set_error("chol_compliance: not factorised");
     return CNB_E_VALIDATION;
   }
-  return compliance(h, ncols, colptr, rowidx, vals, U, ldu, flops_out, rank, world, (cudaStream_t)stream);
+  return compliance(h, ncols, colptr, rowidx, vals, U, ldu, flops_out, (cudaStream_t)stream);
+}
+
+int cnb_chol_compliance_plan(cnb_chol_t hh, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
+                             const double* vals, int32_t rank, int32_t world, int64_t* sizes, double* flops_out,
+                             void* stream) {
+  CholHandle* h = H(hh);
+  if (!h->factored) {
+    set_error("chol_compliance_plan: not factorised");
+    return CNB_E_VALIDATION;
+  }
+  return compliance_split_plan(h, ncols, colptr, rowidx, vals, rank, world, sizes, flops_out, (cudaStream_t)stream);
+}
+
+int cnb_chol_compliance_forward(cnb_chol_t hh, double* ysend, void* stream) {
+  return compliance_split_forward(H(hh), ysend, (cudaStream_t)stream);
+}
+
+int cnb_chol_compliance_gram(cnb_chol_t hh, const double* yall, double* tiles, void* stream) {
+  return compliance_split_gram(H(hh), yall, tiles, (cudaStream_t)stream);
+}
+
+int cnb_chol_compliance_finish(cnb_chol_t hh, const double* tiles_all, double* U, int64_t ldu, void* stream) {
+  return compliance_split_finish(H(hh), tiles_all, U, ldu, (cudaStream_t)stream);
 }
 
 }  // extern "C"

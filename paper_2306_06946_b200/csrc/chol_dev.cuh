@@ -10,6 +10,8 @@
 
 namespace cnb {
 
+struct CompliancePlan;  // solve.cu
+
 struct DevSym {
   const int64_t* first;
   const int64_t* rows_ptr;
@@ -93,6 +95,7 @@ struct CholHandle {
   GrowBuf c_int, c_rhs, c_val, c_y;                      // compliance workspace
   PinnedBuf c_pin;                                       // pinned staging of the compliance plan
   double last_gram_flops = 0.0, last_fwd_flops = 0.0;
+  CompliancePlan* cplan = nullptr;                       // multi-GPU split protocol state
 
   DevSym sym() const {
     return DevSym{d_first,   d_rows_ptr, d_rows, d_front_off, d_child_ptr,
@@ -103,7 +106,14 @@ struct CholHandle {
 // solve.cu
 int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t k, cudaStream_t st);
 int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx, const double* vals,
-               double* U, int64_t ldu, double* flops_out, int rank, int world, cudaStream_t st);
+               double* U, int64_t ldu, double* flops_out, cudaStream_t st);
+int compliance_split_plan(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
+                          const double* vals, int rank, int world, int64_t* sizes, double* flops_out,
+                          cudaStream_t st);
+int compliance_split_forward(CholHandle* h, double* ysend, cudaStream_t st);
+int compliance_split_gram(CholHandle* h, const double* yall, double* tiles, cudaStream_t st);
+int compliance_split_finish(CholHandle* h, const double* tiles_all, double* U, int64_t ldu, cudaStream_t st);
+void free_compliance_plan(CholHandle* h);
 int trinv_level(CholHandle* h, int level, cudaStream_t st);
 
 }  // namespace cnb

@@ -611,12 +611,12 @@ __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const do
                                                    const int64_t* __restrict__ yoff, const int32_t* __restrict__ tile_ptr,
                                                    const int32_t* __restrict__ tile_sn, int64_t ncols,
                                                    const int64_t* __restrict__ sorted_cols, double* __restrict__ U,
-                                                   int64_t ldu, int rank, int world) {
+                                                   int64_t ldu, double* __restrict__ tiles, int rank, int world) {
   // (supernode, 16-deep k chunk) sequence of the tile, cp.async double buffer:
   // chunk q+1 is staged while chunk q is multiplied (41 KB static shared memory)
   constexpr int BK = 16, SB = BK + 4;
-  __shared__ double Ya[2][kGT * SB];
-  __shared__ double Yb[2][kGT * SB];
+  __shared__ __align__(16) double Ya[2][kGT * SB];  // 16-byte cp.async destinations
+  __shared__ __align__(16) double Yb[2][kGT * SB];
   // multi-GPU: this rank owns tiles t = rank, rank + world, ... (round robin)
   const int64_t t = (int64_t)blockIdx.x * world + rank;
   int64_t A = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -701,6 +701,17 @@ __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const do
     k0 = kn;
     buf ^= 1;
   }
+  if (tiles) {  // split mode: the whole 64x64 tile into this rank's slot (scattered by the caller's finish)
+    double* T = tiles + (int64_t)blockIdx.x * (kGT * kGT);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          T[(wy + 8 * a + g) * kGT + wx + 8 * b + 2 * tq + hh] = acc[a][b][hh];
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -723,17 +734,80 @@ __global__ void scatter_rhs_kernel(int64_t nnz, const int64_t* __restrict__ dst,
   if (k < nnz) rhs[dst[k]] = val[k];
 }
 
+// Multi-GPU split: each rank forward-solves a contiguous range
+// of the sorted right-hand-side columns (windows clipped to the range) into a
+// compact Y of its own; the caller all-gathers the compact Ys (NCCL); every
+// rank unpacks them into the full Y and computes the 64x64 Gram tiles it
+// owns (round robin, tile t -> rank t mod world) into a tile buffer; the
+// caller all-gathers the tile buffers and every rank scatters all tiles into
+// U.  Each column's forward solve and each tile's Gram sum run exactly as on
+// one GPU, so U is bit-identical for every world size.
+__global__ void unpack_y_kernel(int64_t nseg, const int64_t* __restrict__ seg, const double* __restrict__ src,
+                                double* __restrict__ dst) {
+  // segment q = (src offset, dst offset, length): one CTA per segment, grid-stride
+  for (int64_t q = blockIdx.x; q < nseg; q += gridDim.x) {
+    const int64_t so = seg[3 * q], d0 = seg[3 * q + 1], len = seg[3 * q + 2];
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) dst[d0 + i] = src[so + i];
+  }
+}
+
+__global__ void scatter_tiles_kernel(int64_t npairs, int world, int64_t per_rank, const double* __restrict__ tiles,
+                                     int64_t ncols, const int64_t* __restrict__ sorted_cols, double* __restrict__ U,
+                                     int64_t ldu) {
+  const int64_t t = blockIdx.x;
+  if (t >= npairs) return;
+  int64_t A = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((A + 1) * (A + 2) / 2 <= t) ++A;
+  while (A * (A + 1) / 2 > t) --A;
+  const int64_t B = t - A * (A + 1) / 2;
+  const double* T = tiles + ((t % world) * per_rank + t / world) * (int64_t)(kGT * kGT);
+  for (int e = threadIdx.x; e < kGT * kGT; e += blockDim.x) {
+    const int i = e / kGT, j = e % kGT;
+    const int64_t ra = A * kGT + i, rb = B * kGT + j;
+    if (ra >= ncols || rb >= ncols || (A == B && rb > ra)) continue;
+    const double v = T[e];
+    const int64_t ja = sorted_cols[ra], jb = sorted_cols[rb];
+    U[ja * ldu + jb] = v;
+    U[jb * ldu + ja] = v;
+  }
+}
+
 struct CompliancePlan {
-  std::vector<int64_t> sorted_cols, lo, w, roff, yoff, sc_dst;
+  int64_t ncols = 0;
+  int rank = 0, world = 1;
+  // full problem: sorted columns, windows, Y layout, Gram tiles
+  std::vector<int64_t> sorted_cols, lo, w, yoff;
+  std::vector<int32_t> tile_ptr, tile_sn;
+  int64_t npairs = 0, tiles_per_rank = 0;
+  double gram_flops = 0.0, fwd_flops = 0.0;
+  // this rank's forward solve (windows clipped to its column range)
+  std::vector<int64_t> flo, fw, froff, fyoff, sc_dst;
   std::vector<double> sc_val;
   std::vector<std::vector<int32_t>> asm_t, panel_t;  // per level, (s, r0, c0)
-  std::vector<int32_t> tile_ptr, tile_sn;
-  double gram_flops = 0.0, fwd_flops = 0.0;
+  double rank_fwd_flops = 0.0;
+  // split bookkeeping: column boundaries (sorted order), unpack segments, send size
+  std::vector<int64_t> split, seg;
+  int64_t send_doubles = 0;
+  // device offsets into h->c_int (bytes) and record lists
+  size_t o_lo = 0, o_w = 0, o_yoff = 0, o_sorted = 0, o_flo = 0, o_fw = 0, o_froff = 0, o_fyoff = 0, o_dst = 0,
+         o_seg = 0, o_tptr = 0, o_tsn = 0;
+  std::vector<std::pair<size_t, size_t>> arec, prec;
+  bool uploaded = false;
 };
 
-static int build_compliance_plan(const Symbolic& S, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
-                                 const double* vals, CompliancePlan& P) {
+void free_compliance_plan(CholHandle* h) {
+  delete h->cplan;
+  h->cplan = nullptr;
+}
+
+static inline int64_t ystride(int64_t nc) { return nc + (nc & 1); }  // Y columns 16-byte aligned
+
+static int plan_build(const Symbolic& S, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
+                      const double* vals, int rank, int world, CompliancePlan& P) {
   const int64_t ns = S.ns;
+  P.ncols = ncols;
+  P.rank = rank;
+  P.world = world;
   std::vector<int64_t> dof_sn(S.n);
   for (int64_t s = 0; s < ns; ++s)
     for (int64_t d = S.first[s]; d < S.first[s + 1]; ++d) dof_sn[d] = s;
@@ -750,16 +824,16 @@ static int build_compliance_plan(const Symbolic& S, int64_t ncols, const int64_t
   P.sorted_cols.resize(ncols);
   std::iota(P.sorted_cols.begin(), P.sorted_cols.end(), 0);
   std::stable_sort(P.sorted_cols.begin(), P.sorted_cols.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
-  std::vector<int64_t> rank(ncols);
-  for (int64_t r = 0; r < ncols; ++r) rank[P.sorted_cols[r]] = r;
+  std::vector<int64_t> pos(ncols);
+  for (int64_t r = 0; r < ncols; ++r) pos[P.sorted_cols[r]] = r;
   std::vector<int64_t> lo(ns, INT64_MAX), hi(ns, -1);
   for (int64_t j = 0; j < ncols; ++j)
     for (int64_t e = colptr[j]; e < colptr[j + 1]; ++e) {
       const int64_t s = dof_sn[S.iperm[rowidx[e]]];
-      lo[s] = std::min(lo[s], rank[j]);
-      hi[s] = std::max(hi[s], rank[j] + 1);
+      lo[s] = std::min(lo[s], pos[j]);
+      hi[s] = std::max(hi[s], pos[j] + 1);
     }
-  for (int64_t s = 0; s < ns; ++s) {
+  for (int64_t s = 0; s < ns; ++s) {  // postorder: a window contains its children's
     const int64_t p = S.parent[s];
     if (p >= 0 && hi[s] > 0) {
       lo[p] = std::min(lo[p], lo[s]);
@@ -768,41 +842,110 @@ static int build_compliance_plan(const Symbolic& S, int64_t ncols, const int64_t
   }
   P.lo.assign(ns, 0);
   P.w.assign(ns, 0);
-  P.roff.assign(ns + 1, 0);
   P.yoff.assign(ns + 1, 0);
   for (int64_t s = 0; s < ns; ++s) {
     if (hi[s] > 0) {
       P.lo[s] = lo[s];
       P.w[s] = hi[s] - lo[s];
     }
-    P.roff[s + 1] = P.roff[s] + S.f(s) * P.w[s];
-    P.yoff[s + 1] = P.yoff[s] + (S.nc(s) + (S.nc(s) & 1)) * P.w[s];  // even column stride
+    P.yoff[s + 1] = P.yoff[s] + ystride(S.nc(s)) * P.w[s];
     const double nc = (double)S.nc(s), nr = (double)S.nr(s), w = (double)P.w[s];
     P.fwd_flops += w * (nc * nc + 2.0 * nc * nr);
   }
-  for (int64_t j = 0; j < ncols; ++j)
+  // column ranges of the ranks, balanced by forward work (f_s nc_s per column of each window)
+  P.split.assign(world + 1, ncols);
+  P.split[0] = 0;
+  if (world > 1) {
+    std::vector<double> diff(ncols + 1, 0.0);
+    for (int64_t s = 0; s < ns; ++s)
+      if (P.w[s]) {
+        const double c = (double)S.f(s) * (double)S.nc(s);
+        diff[P.lo[s]] += c;
+        diff[P.lo[s] + P.w[s]] -= c;
+      }
+    std::vector<double> cum(ncols + 1, 0.0);
+    double run = 0.0;
+    for (int64_t j = 0; j < ncols; ++j) {
+      run += diff[j];
+      cum[j + 1] = cum[j] + run;
+    }
+    for (int q = 1; q < world; ++q) {
+      const double target = cum[ncols] * q / world;
+      P.split[q] = std::lower_bound(cum.begin(), cum.end(), target) - cum.begin();
+      P.split[q] = std::max(P.split[q], P.split[q - 1]);
+    }
+  }
+  // every rank's clipped windows: compact Y layout and the unpack segments
+  P.send_doubles = 1;
+  for (int q = 0; q < world; ++q) {
+    const int64_t ca = P.split[q], cb = P.split[q + 1];
+    int64_t off = 0;
+    for (int64_t s = 0; s < ns; ++s) {
+      if (!P.w[s]) continue;
+      const int64_t l = std::max(P.lo[s], ca), r = std::min(P.lo[s] + P.w[s], cb);
+      if (r <= l) continue;
+      const int64_t len = (r - l) * ystride(S.nc(s));
+      if (world > 1) P.seg.insert(P.seg.end(), {off, P.yoff[s] + (l - P.lo[s]) * ystride(S.nc(s)), len});
+      off += len;
+    }
+    P.send_doubles = std::max(P.send_doubles, off);
+  }
+  if (world > 1)  // segment sources are offsets within the rank's slot of the gathered buffer
+    for (int q = 0, k = 0; q < world; ++q) {
+      const int64_t ca = P.split[q], cb = P.split[q + 1];
+      for (int64_t s = 0; s < ns; ++s) {
+        if (!P.w[s]) continue;
+        const int64_t l = std::max(P.lo[s], ca), r = std::min(P.lo[s] + P.w[s], cb);
+        if (r <= l) continue;
+        P.seg[3 * k++] += q * P.send_doubles;
+      }
+    }
+  // this rank's forward plan
+  const int64_t ca = P.split[rank], cb = P.split[rank + 1];
+  P.flo.assign(ns, 0);
+  P.fw.assign(ns, 0);
+  P.froff.assign(ns + 1, 0);
+  P.fyoff.assign(ns + 1, 0);
+  for (int64_t s = 0; s < ns; ++s) {
+    if (P.w[s]) {
+      const int64_t l = std::max(P.lo[s], ca), r = std::min(P.lo[s] + P.w[s], cb);
+      if (r > l) {
+        P.flo[s] = l;
+        P.fw[s] = r - l;
+      }
+    }
+    P.froff[s + 1] = P.froff[s] + S.f(s) * P.fw[s];
+    P.fyoff[s + 1] = P.fyoff[s] + ystride(S.nc(s)) * P.fw[s];
+    const double nc = (double)S.nc(s), nr = (double)S.nr(s), w = (double)P.fw[s];
+    P.rank_fwd_flops += w * (nc * nc + 2.0 * nc * nr);
+  }
+  for (int64_t j = 0; j < ncols; ++j) {
+    if (pos[j] < ca || pos[j] >= cb) continue;
     for (int64_t e = colptr[j]; e < colptr[j + 1]; ++e) {
       const int64_t p = S.iperm[rowidx[e]];
       const int64_t s = dof_sn[p];
-      P.sc_dst.push_back(P.roff[s] + (rank[j] - P.lo[s]) * S.f(s) + (p - S.first[s]));
+      P.sc_dst.push_back(P.froff[s] + (pos[j] - P.flo[s]) * S.f(s) + (p - S.first[s]));
       P.sc_val.push_back(vals[e]);
     }
+  }
   P.asm_t.assign(S.n_levels, {});
   P.panel_t.assign(S.n_levels, {});
   for (int l = 0; l < S.n_levels; ++l)
     for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
       const int64_t s = S.level_sn[q];
-      if (P.w[s] == 0) continue;
+      if (P.fw[s] == 0) continue;
       if (S.child_ptr[s + 1] > S.child_ptr[s])
         for (int64_t r = 0; r < S.f(s); r += kAsmRows)
-          for (int64_t c = 0; c < P.w[s]; c += kAsmCols)
+          for (int64_t c = 0; c < P.fw[s]; c += kAsmCols)
             P.asm_t[l].insert(P.asm_t[l].end(), {(int32_t)s, (int32_t)r, (int32_t)c});
       for (int64_t r = 0; r < S.f(s); r += kMT)
-        for (int64_t c = 0; c < P.w[s]; c += kMT) P.panel_t[l].insert(P.panel_t[l].end(), {(int32_t)s, (int32_t)r, (int32_t)c});
+        for (int64_t c = 0; c < P.fw[s]; c += kMT) P.panel_t[l].insert(P.panel_t[l].end(), {(int32_t)s, (int32_t)r, (int32_t)c});
     }
+  // Gram tiles of the full problem
   const int64_t nt = (ncols + kGT - 1) / kGT;
-  const int64_t npairs = nt * (nt + 1) / 2;
-  std::vector<int32_t> count(npairs + 1, 0);
+  P.npairs = nt * (nt + 1) / 2;
+  P.tiles_per_rank = (P.npairs + world - 1) / world;
+  std::vector<int32_t> count(P.npairs + 1, 0);
   for (int64_t s = 0; s < ns; ++s) {
     if (P.w[s] == 0) continue;
     const int64_t t0 = P.lo[s] / kGT, t1 = (P.lo[s] + P.w[s] - 1) / kGT;
@@ -810,9 +953,9 @@ static int build_compliance_plan(const Symbolic& S, int64_t ncols, const int64_t
       for (int64_t b = t0; b <= a; ++b) count[a * (a + 1) / 2 + b + 1]++;
     P.gram_flops += (double)S.nc(s) * (double)P.w[s] * (double)(P.w[s] + 1);
   }
-  for (int64_t t = 0; t < npairs; ++t) count[t + 1] += count[t];
+  for (int64_t t = 0; t < P.npairs; ++t) count[t + 1] += count[t];
   P.tile_ptr = count;
-  P.tile_sn.assign(count[npairs], 0);
+  P.tile_sn.assign(count[P.npairs], 0);
   std::vector<int32_t> fill(count.begin(), count.end() - 1);
   for (int64_t s = 0; s < ns; ++s) {
     if (P.w[s] == 0) continue;
@@ -823,52 +966,50 @@ static int build_compliance_plan(const Symbolic& S, int64_t ncols, const int64_t
   return CNB_OK;
 }
 
-int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx, const double* vals,
-               double* U, int64_t ldu, double* flops_out, int rank, int world, cudaStream_t st) {
-  if (ncols <= 0) return CNB_OK;
-  if (world < 1 || rank < 0 || rank >= world) {
-    set_error("compliance: invalid rank %d / world %d", rank, world);
-    return CNB_E_VALIDATION;
-  }
+// Upload the plan (one pinned staging copy, asynchronous) and size the workspaces.
+static int plan_upload(CholHandle* h, CompliancePlan& P, cudaStream_t st) {
   const Symbolic& S = h->S;
-  CompliancePlan P;
-  int rc = build_compliance_plan(S, ncols, colptr, rowidx, vals, P);
-  if (rc) return rc;
-  if (flops_out) {
-    flops_out[0] = P.fwd_flops;
-    flops_out[1] = P.gram_flops;
-  }
   std::vector<int64_t> ints;
   auto put = [&](const std::vector<int64_t>& v) {
-    size_t o = ints.size();
+    size_t o = ints.size() * sizeof(int64_t);
     ints.insert(ints.end(), v.begin(), v.end());
     return o;
   };
-  const size_t o_lo = put(P.lo), o_w = put(P.w), o_roff = put(P.roff), o_yoff = put(P.yoff),
-               o_sorted = put(P.sorted_cols), o_dst = put(P.sc_dst);
+  P.o_lo = put(P.lo);
+  P.o_w = put(P.w);
+  P.o_yoff = put(P.yoff);
+  P.o_sorted = put(P.sorted_cols);
+  P.o_flo = put(P.flo);
+  P.o_fw = put(P.fw);
+  P.o_froff = put(P.froff);
+  P.o_fyoff = put(P.fyoff);
+  P.o_dst = put(P.sc_dst);
+  P.o_seg = put(P.seg);
   std::vector<int32_t> i32;
-  std::vector<std::pair<size_t, size_t>> arec, prec;
+  P.arec.clear();
+  P.prec.clear();
   for (int l = 0; l < S.n_levels; ++l) {
-    arec.push_back({i32.size(), P.asm_t[l].size() / 3});
+    P.arec.push_back({i32.size(), P.asm_t[l].size() / 3});
     i32.insert(i32.end(), P.asm_t[l].begin(), P.asm_t[l].end());
-    prec.push_back({i32.size(), P.panel_t[l].size() / 3});
+    P.prec.push_back({i32.size(), P.panel_t[l].size() / 3});
     i32.insert(i32.end(), P.panel_t[l].begin(), P.panel_t[l].end());
   }
-  const size_t o_tptr = i32.size();
+  const size_t t_tptr = i32.size();
   i32.insert(i32.end(), P.tile_ptr.begin(), P.tile_ptr.end());
-  const size_t o_tsn = i32.size();
+  const size_t t_tsn = i32.size();
   i32.insert(i32.end(), P.tile_sn.begin(), P.tile_sn.end());
   const size_t bytes64 = ints.size() * sizeof(int64_t);
+  const size_t off32 = (bytes64 + 15) & ~(size_t)15;
   const size_t bytes32 = i32.size() * sizeof(int32_t);
-  if ((rc = h->c_int.ensure(bytes64 + bytes32 + 16))) return rc;
-  if ((rc = h->c_rhs.ensure(std::max<int64_t>(1, P.roff[S.ns]) * sizeof(double)))) return rc;
+  for (auto& r : P.arec) r.first = off32 + r.first * sizeof(int32_t);
+  for (auto& r : P.prec) r.first = off32 + r.first * sizeof(int32_t);
+  P.o_tptr = off32 + t_tptr * sizeof(int32_t);
+  P.o_tsn = off32 + t_tsn * sizeof(int32_t);
+  int rc;
+  if ((rc = h->c_int.ensure(off32 + bytes32 + 16))) return rc;
+  if ((rc = h->c_rhs.ensure(std::max<int64_t>(1, P.froff[S.ns]) * sizeof(double)))) return rc;
   if ((rc = h->c_y.ensure(std::max<int64_t>(1, P.yoff[S.ns]) * sizeof(double)))) return rc;
   if ((rc = h->c_val.ensure(std::max<size_t>(1, P.sc_val.size()) * sizeof(double)))) return rc;
-  char* base = (char*)h->c_int.p;
-  int64_t* d64 = (int64_t*)base;
-  const size_t off32 = (bytes64 + 15) & ~(size_t)15;
-  int32_t* d32 = (int32_t*)(base + off32);
-  // stage through pinned memory: the uploads stay asynchronous (no stream sync)
   const size_t vbytes = P.sc_val.size() * sizeof(double);
   const size_t offv = (off32 + bytes32 + 15) & ~(size_t)15;
   if ((rc = h->c_pin.ensure(offv + vbytes + 16))) return rc;
@@ -876,44 +1017,140 @@ int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_
   memcpy(pin, ints.data(), bytes64);
   if (bytes32) memcpy(pin + off32, i32.data(), bytes32);
   if (vbytes) memcpy(pin + offv, P.sc_val.data(), vbytes);
-  CNB_CUDA(cudaMemcpyAsync(base, pin, off32 + bytes32, cudaMemcpyHostToDevice, st));
+  CNB_CUDA(cudaMemcpyAsync(h->c_int.p, pin, off32 + bytes32, cudaMemcpyHostToDevice, st));
   if (vbytes) CNB_CUDA(cudaMemcpyAsync(h->c_val.p, pin + offv, vbytes, cudaMemcpyHostToDevice, st));
   if ((rc = h->c_pin.mark(st))) return rc;
+  P.uploaded = true;
+  return CNB_OK;
+}
+
+template <typename T>
+static inline T* at(const GrowBuf& b, size_t off) {
+  return (T*)((char*)b.p + off);
+}
+
+// Forward solve of this rank's columns: Y (compact layout fyoff) = L^{-1} P E.
+static int plan_forward(CholHandle* h, const CompliancePlan& P, double* Y, cudaStream_t st) {
+  const Symbolic& S = h->S;
   double* rhs = (double*)h->c_rhs.p;
-  double* Y = (double*)h->c_y.p;
-  CNB_CUDA(cudaMemsetAsync(rhs, 0, std::max<int64_t>(1, P.roff[S.ns]) * sizeof(double), st));
+  CNB_CUDA(cudaMemsetAsync(rhs, 0, std::max<int64_t>(1, P.froff[S.ns]) * sizeof(double), st));
   const int64_t nnz = (int64_t)P.sc_val.size();
   if (nnz) {
-    scatter_rhs_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, d64 + o_dst, (const double*)h->c_val.p, rhs);
+    scatter_rhs_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, at<int64_t>(h->c_int, P.o_dst),
+                                                           (const double*)h->c_val.p, rhs);
     CNB_LAUNCH_CHECK("scatter_rhs_kernel");
   }
   DevSym sym = h->sym();
-  RhsView R{rhs, d64 + o_roff, d64 + o_lo, d64 + o_w};
+  RhsView R{rhs, at<int64_t>(h->c_int, P.o_froff), at<int64_t>(h->c_int, P.o_flo), at<int64_t>(h->c_int, P.o_fw)};
   for (int l = 0; l < S.n_levels; ++l) {
-    if (arec[l].second) {
-      asm_kernel<<<(unsigned)arec[l].second, kSolveThreads, 0, st>>>(sym, d32 + arec[l].first, R, 0, nullptr, S.n);
+    if (P.arec[l].second) {
+      asm_kernel<<<(unsigned)P.arec[l].second, kSolveThreads, 0, st>>>(sym, at<int32_t>(h->c_int, P.arec[l].first),
+                                                                        R, 0, nullptr, S.n);
       CNB_LAUNCH_CHECK("asm_kernel(sparse)");
     }
-    if (prec[l].second) {
-      panel_mma_kernel<<<(unsigned)prec[l].second, 128, 0, st>>>(sym, d32 + prec[l].first, R, h->d_p21, h->d_linv,
-                                                                 Y, d64 + o_yoff);
+    if (P.prec[l].second) {
+      panel_mma_kernel<<<(unsigned)P.prec[l].second, 128, 0, st>>>(sym, at<int32_t>(h->c_int, P.prec[l].first), R,
+                                                                   h->d_p21, h->d_linv, Y,
+                                                                   at<int64_t>(h->c_int, P.o_fyoff));
       CNB_LAUNCH_CHECK("panel_mma_kernel");
     }
   }
-  const int64_t nt = (ncols + kGT - 1) / kGT;
-  const int64_t npairs = nt * (nt + 1) / 2;
-  if (world > 1) {
-    // only this rank's tiles are written; the caller sums U over ranks
-    for (int64_t r = 0; r < ncols; ++r) CNB_CUDA(cudaMemsetAsync(U + r * ldu, 0, ncols * sizeof(double), st));
+  return CNB_OK;
+}
+
+// Gram tiles of this rank over the full Y: into U directly (world 1) or into
+// the rank's tile buffer (slot = t / world).
+static int plan_gram(CholHandle* h, const CompliancePlan& P, const double* Y, double* U, int64_t ldu, double* tiles,
+                     cudaStream_t st) {
+  const int64_t owned = (P.npairs - P.rank + P.world - 1) / P.world;
+  if (owned <= 0) return CNB_OK;
+  RhsView R{nullptr, nullptr, at<int64_t>(h->c_int, P.o_lo), at<int64_t>(h->c_int, P.o_w)};
+  gram_kernel<<<(unsigned)owned, 128, 0, st>>>(h->sym(), R, Y, at<int64_t>(h->c_int, P.o_yoff),
+                                               at<int32_t>(h->c_int, P.o_tptr), at<int32_t>(h->c_int, P.o_tsn),
+                                               P.ncols, at<int64_t>(h->c_int, P.o_sorted), U, ldu, tiles, P.rank,
+                                               P.world);
+  CNB_LAUNCH_CHECK("gram_kernel");
+  return CNB_OK;
+}
+
+int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx, const double* vals,
+               double* U, int64_t ldu, double* flops_out, cudaStream_t st) {
+  if (ncols <= 0) return CNB_OK;
+  CompliancePlan P;
+  int rc = plan_build(h->S, ncols, colptr, rowidx, vals, 0, 1, P);
+  if (rc) return rc;
+  if ((rc = plan_upload(h, P, st))) return rc;
+  if (flops_out) {
+    flops_out[0] = P.fwd_flops;
+    flops_out[1] = P.gram_flops;
   }
-  const int64_t owned = (npairs - rank + world - 1) / world;
-  if (owned > 0) {
-    gram_kernel<<<(unsigned)owned, 128, 0, st>>>(sym, R, Y, d64 + o_yoff, d32 + o_tptr, d32 + o_tsn, ncols,
-                                                 d64 + o_sorted, U, ldu, rank, world);
-    CNB_LAUNCH_CHECK("gram_kernel");
-  }
+  double* Y = (double*)h->c_y.p;
+  if ((rc = plan_forward(h, P, Y, st))) return rc;
+  if ((rc = plan_gram(h, P, Y, U, ldu, nullptr, st))) return rc;
   h->last_fwd_flops = P.fwd_flops;
   h->last_gram_flops = P.gram_flops;
+  return CNB_OK;
+}
+
+int compliance_split_plan(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
+                          const double* vals, int rank, int world, int64_t* sizes, double* flops_out,
+                          cudaStream_t st) {
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("compliance: invalid rank %d / world %d", rank, world);
+    return CNB_E_VALIDATION;
+  }
+  free_compliance_plan(h);
+  h->cplan = new CompliancePlan();
+  CompliancePlan& P = *h->cplan;
+  int rc = plan_build(h->S, ncols, colptr, rowidx, vals, rank, world, P);
+  if (rc) return rc;
+  if ((rc = plan_upload(h, P, st))) return rc;
+  sizes[0] = P.send_doubles;
+  sizes[1] = P.tiles_per_rank * kGT * kGT;
+  sizes[2] = P.split[rank];
+  sizes[3] = P.split[rank + 1];
+  if (flops_out) {
+    flops_out[0] = P.rank_fwd_flops;
+    flops_out[1] = P.gram_flops / world;
+  }
+  return CNB_OK;
+}
+
+int compliance_split_forward(CholHandle* h, double* ysend, cudaStream_t st) {
+  if (!h->cplan) {
+    set_error("compliance_split_forward: no plan");
+    return CNB_E_VALIDATION;
+  }
+  return plan_forward(h, *h->cplan, ysend, st);
+}
+
+int compliance_split_gram(CholHandle* h, const double* yall, double* tiles, cudaStream_t st) {
+  if (!h->cplan) {
+    set_error("compliance_split_gram: no plan");
+    return CNB_E_VALIDATION;
+  }
+  const CompliancePlan& P = *h->cplan;
+  double* Y = (double*)h->c_y.p;
+  const int64_t nseg = (int64_t)P.seg.size() / 3;
+  if (nseg) {
+    unpack_y_kernel<<<(unsigned)std::min<int64_t>(nseg, 148 * 16), 256, 0, st>>>(
+        nseg, at<int64_t>(h->c_int, P.o_seg), yall, Y);
+    CNB_LAUNCH_CHECK("unpack_y_kernel");
+  }
+  return plan_gram(h, P, Y, nullptr, 0, tiles, st);
+}
+
+int compliance_split_finish(CholHandle* h, const double* tiles_all, double* U, int64_t ldu, cudaStream_t st) {
+  if (!h->cplan) {
+    set_error("compliance_split_finish: no plan");
+    return CNB_E_VALIDATION;
+  }
+  const CompliancePlan& P = *h->cplan;
+  if (P.npairs) {
+    scatter_tiles_kernel<<<(unsigned)P.npairs, 256, 0, st>>>(P.npairs, P.world, P.tiles_per_rank, tiles_all,
+                                                             P.ncols, at<int64_t>(h->c_int, P.o_sorted), U, ldu);
+    CNB_LAUNCH_CHECK("scatter_tiles_kernel");
+  }
   return CNB_OK;
 }
 

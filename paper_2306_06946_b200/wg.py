@@ -31,10 +31,11 @@ SANDWICH_MAX_K = 29000    # row buffer of the sandwich kernel (227 KB of shared 
 
 
 def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, shard: bool = True):
-    """U_o for one object.  Under torch.distributed (world > 1) the Gram tiles are
-    split across ranks and summed with one all-reduce (parallel.py)."""
+    """U_o for one object.  Under torch.distributed (world > 1) the right-hand-side
+    columns are split across ranks (forward solve + Gram tiles) and joined by two
+    NCCL all-gathers (parallel.split_compliance); the result is bit-identical."""
     from .constraints import ObjectCompliance
-    from .parallel import reduce_shards, world_info
+    from .parallel import split_compliance, world_info
 
     rank, world = world_info(group) if shard else (0, 1)
 
@@ -64,10 +65,12 @@ def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, sha
             e_val = np.ones(k)
             dofs = np.ascontiguousarray(dofs, dtype=np.int64)
             C = dv.empty((k, k))
-            _lib.call("cnb_chol_compliance", F._h, k, e_ptr.ctypes.data, dofs.ctypes.data, e_val.ctypes.data,
-                      C.data_ptr(), k, fl, rank, world, _lib.stream())
             if world > 1:
-                reduce_shards(C, group)
+                info = split_compliance(F, k, e_ptr, dofs, e_val, C, k, group=group, rank=rank, world=world)
+                fl[0], fl[1] = info["flops"]
+            else:
+                _lib.call("cnb_chol_compliance", F._h, k, e_ptr.ctypes.data, dofs.ctypes.data, e_val.ctypes.data,
+                          C.data_ptr(), k, fl, _lib.stream())
             ell_col = np.zeros((3 * mo, ELL_WIDTH), dtype=np.int32)
             ell_val = np.zeros((3 * mo, ELL_WIDTH))
             slot = np.arange(len(rowidx)) - np.repeat(colptr[:-1], per_row)
@@ -78,11 +81,12 @@ def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, sha
             d_val = dv.upload(ell_val)
             _lib.call("cnb_sandwich", 3 * mo, k, d_col.data_ptr(), d_val.data_ptr(), C.data_ptr(), k, U.data_ptr(),
                       3 * mo, _lib.stream())
+        elif world > 1:
+            info = split_compliance(F, 3 * mo, colptr, rowidx, vals, U, 3 * mo, group=group, rank=rank, world=world)
+            fl[0], fl[1] = info["flops"]
         else:
             _lib.call("cnb_chol_compliance", F._h, 3 * mo, colptr.ctypes.data, rowidx.ctypes.data, vals.ctypes.data,
-                      U.data_ptr(), 3 * mo, fl, rank, world, _lib.stream())
-            if world > 1:
-                reduce_shards(U, group)
+                      U.data_ptr(), 3 * mo, fl, _lib.stream())
         if stats is not None:
             stats["fwd_flops"] = stats.get("fwd_flops", 0.0) + fl[0]
             stats["gram_flops"] = stats.get("gram_flops", 0.0) + fl[1]

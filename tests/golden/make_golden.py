@@ -205,6 +205,81 @@ def scenes():
         save(f"{name}.npz", **out)
 
 
+def beam_cfg0_full():
+    """BASELINE cfg0 exactly as specified: 100 steps from 2 cm above the plane,
+    jitter from default_rng(0).  Per-step pair counts, Newton iterations, PGS
+    sweeps and pen_after; q and v every 10 steps and at the end."""
+    cfg, mesh = beam_cfg0(drop=0.02)
+    sim = rsc.Simulation(cfg)
+    rng = np.random.default_rng(0)
+    obj = sim.dynamic_objects[0]
+    obj.state.q = obj.state.q + rng.uniform(-1e-4, 1e-4, obj.state.q.shape)
+    npairs, newton, sweeps, pen = [], [], [], []
+    out = {}
+    for s in range(100):
+        rep = sim.step()
+        npairs.append(rep.c_groups)
+        newton.append(rep.newton_iterations)
+        sweeps.append(rep.pgs_iterations_total)
+        pen.append(rep.pen_after)
+        if s % 10 == 9:
+            out[f"q{s}"], out[f"v{s}"] = obj.state.q.copy(), obj.state.v.copy()
+            print("beam100 step", s, "pairs", rep.c_groups, "pgs", rep.pgs_iterations_total, flush=True)
+    out.update(npairs=np.array(npairs), newton=np.array(newton), sweeps=np.array(sweeps), pen_after=np.array(pen),
+               nodes=mesh.nodes, tets=mesh.tets, normal=np.array(cfg.objects[1].normal))
+    save("beam_cfg0_100.npz", **out)
+
+
+def cfg1_parity():
+    """BASELINE cfg1 (isolated compliance-update bench) run by the reference
+    itself: n = 12 000 (40x10x10-node 5-tet grid), 500 barycentric contacts,
+    W_g = S A^-1 S^T (assemble_Wg constraints.py:155-179), then 10 frame
+    re-draws: W_k = D_k W_g D_k^T (rebuild_W_fast 182-191, naive gemm) and
+    dx_k = h A^-1 S^T D_k^T lam_k (_mechanical_correction solver.py:250-257).
+    The inputs come from workloads.cfg1_inputs (the benched workload).  Stored:
+    sampled rows of W_g and every W_k, the products W_g r and W_k r for a fixed
+    random r (every entry enters), and dx_k (3 in full, every k sampled)."""
+    import workloads as wk
+
+    inp = wk.cfg1_inputs()
+    nodes = inp["nodes"]
+    body = cn.SoftBody(cn.TetMesh(nodes, inp["tets"]), young=5e3, poisson=0.45, density=1000.0,
+                       rayleigh_mass=0.0, rayleigh_stiffness=0.0)
+    st = body.initial_state()
+    A, _ = body.assemble(st, wk.H, (0.0, -9.81, 0.0))
+    F = cn.factorize(A)
+    pairs = []
+    for i in range(wk.CFG1_CONTACTS):
+        tri = inp["tris"][inp["tri_idx"][i]]
+        w = inp["weights"][i]
+        p = w @ nodes[tri]
+        pairs.append(rcol.ProximityPair(
+            0, 1, rcol.Attachment(rcol.AttachKind.BARYCENTRIC, 0, triangle=tri.copy(), weights=w.copy()),
+            rcol.Attachment(rcol.AttachKind.WORLD, 1, world_point=p.copy()), p.copy(), p.copy(),
+            np.array([0.0, 1.0, 0.0]), 0.0, i, int(inp["tri_idx"][i])))
+    S = rcon.build_signed_mapping(pairs, 0, body.n_dofs, body.fixed_mask)
+    wg = rcon.assemble_Wg({0: S}, {0: F})
+    m = 3 * wk.CFG1_CONTACTS
+    rng = np.random.default_rng(11)
+    rows = np.sort(rng.choice(m, 32, replace=False))
+    r = rng.standard_normal(m)
+    dsel = np.sort(rng.choice(body.n_dofs, 600, replace=False))
+    out = dict(rows=rows, r=r, dsel=dsel, wg_rows=wg.wg[rows], wg_r=wg.wg @ r,
+               S_indptr=S.indptr, S_indices=S.indices, S_data=S.data)
+    for k in range(wk.CFG1_REDRAWS):
+        frames = [rcol.ContactFrame(n=f[0], t1=f[1], t2=f[2]) for f in inp["Ds"][k]]
+        D = rcon.assemble_direction(frames)
+        W = rcon.rebuild_W_fast(D, wg).W
+        out[f"W{k}_rows"], out[f"W{k}_r"] = W[rows[:8]], W @ r
+        t = D.apply_transposed(inp["lams"][k])
+        dx = wk.H * F.solve(S.T @ t)
+        out[f"dx{k}_sel"] = dx[dsel]
+        if k in (0, 4, 9):
+            out[f"dx{k}"] = dx
+        print("cfg1 redraw", k, flush=True)
+    save("cfg1_parity.npz", **out)
+
+
 def scenes_standard():
     """Reference runs of the standard (Alg. 2) and single schemes on block_on_plane."""
     from dataclasses import replace

@@ -221,3 +221,35 @@ def test_cylinder_press_cfg2_style(cn, golden):
     # fixed nodes stay at rest
     q = _h(sim.objects[0].state.q).reshape(-1, 3)
     assert np.array_equal(q[g["fixed"]], g["nodes"][g["fixed"]])
+
+
+def test_beam_cfg0_full_100_steps(cn, golden):
+    """BASELINE cfg0 exactly: 100 steps from 2 cm above the 10-degree plane
+    against the reference's own run (tests/golden/beam_cfg0_100.npz): pair
+    counts and Newton iterations every step, q and v every 10 steps."""
+    g = golden("beam_cfg0_100.npz")
+    mesh = cn.TetMesh(g["nodes"], g["tets"])
+    cfg = cn.SceneConfig(
+        objects=[cn.SoftSpec(name="beam", mesh=mesh, young=5e3, poisson=0.45, density=1000.0),
+                 cn.PlaneSpec(name="ground", normal=tuple(g["normal"]), offset=0.0)],
+        threshold=0.005, pgs=cn.PgsConfig(1000, 1e-10, 0.5),
+        newton=cn.NewtonConfig(scheme="fast", max_iterations=5, penetration_tol=-1.0, rotation_tol=-1.0),
+        output=cn.OutputConfig(snapshots=False, metrics=False))
+    sim = cn.Simulation(cfg)
+    rng = np.random.default_rng(0)
+    st = sim.objects[0].state
+    sim.objects[0].state = cn.MechanicalState(_h(st.q) + rng.uniform(-1e-4, 1e-4, st.q.shape[0]), st.v)
+    sweeps = []
+    for s in range(100):
+        rep = sim.step()
+        assert rep.c_groups == int(g["npairs"][s]), s
+        assert rep.newton_iterations == int(g["newton"][s])
+        sweeps.append(rep.pgs_iterations_total)
+        if s % 10 == 9:
+            for key, arr in (("q", sim.objects[0].state.q), ("v", sim.objects[0].state.v)):
+                ref = g[f"{key}{s}"]
+                tol = 1e-6 * np.abs(ref).max() if key == "q" else 1e-6 * max(np.abs(ref).max(), 1e-3)
+                assert np.abs(_h(arr) - ref).max() <= tol, (s, key)
+    # the PGS stopping rule sees the same iterates: sweep totals agree closely
+    ref = g["sweeps"].astype(float)
+    assert np.all(np.abs(np.array(sweeps) - ref) <= 0.02 * ref + 2)

@@ -1,17 +1,25 @@
-"""Multi-process (gloo, world_size 2, CPU) checks of the N>1 host logic: the Gram
-tile ownership partitions U exactly once, and the zero-filled per-rank shards
-summed by all-reduce reproduce the single-process U bit for bit."""
+"""Multi-process (gloo, world_size 2 and 3, CPU) checks of the N>1 host logic.
+
+parallel.run_split drives the column-split compliance protocol (plan, forward
+of the rank's columns, all-gather of the compact Y, Gram tiles t -> rank
+t mod world, all-gather of the tile buffers, scatter).  Here it runs over real
+gloo collectives with a numpy model of the kernels (per-column triangular
+solves, 64 x 64 Gram tiles), and every rank must end with exactly the
+single-process C = Y^T Y.  The same orchestration calls the CUDA kernels on
+the GPU (tests/test_gpu_parallel.py checks those against one GPU bit for bit).
+"""
 
 import os
 import socket
 
 import numpy as np
 import pytest
+import scipy.linalg as sla
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2306_06946_b200.parallel import tile_owner
+from paper_2306_06946_b200.parallel import GRAM_TILE, all_gather, run_split, tile_owner
 
 
 def _free_port():
@@ -32,29 +40,106 @@ def test_tile_ownership_partitions_every_entry_once():
                 assert counts.max() <= 1.35 * counts.mean()
 
 
-def _worker(rank, world, port, U_full, out):
+class NumpySteps:
+    """The kernels' contract in numpy: Y = L^-1 E column by column, Gram tiles."""
+
+    def __init__(self, L, E, rank, world):
+        self.L, self.E, self.rank, self.world = L, E, rank, world
+        self.n, self.k = E.shape
+        b = np.linspace(0, self.k, world + 1).astype(int)
+        self.cols = [(b[q], b[q + 1]) for q in range(world)]
+        nt = (self.k + GRAM_TILE - 1) // GRAM_TILE
+        self.npairs = nt * (nt + 1) // 2
+        self.per_rank = (self.npairs + world - 1) // world
+        self.C = None
+
+    def plan(self):
+        send = max(b - a for a, b in self.cols) * self.n
+        return max(send, 1), self.per_rank * GRAM_TILE * GRAM_TILE, (0.0, 0.0)
+
+    def forward(self, ysend):
+        a, b = self.cols[self.rank]
+        ysend.zero_()
+        for j in range(a, b):
+            y = sla.solve_triangular(self.L, self.E[:, j], lower=True)
+            ysend[(j - a) * self.n:(j - a + 1) * self.n] = torch.from_numpy(y)
+
+    def _Y(self, yall):
+        send = yall.numel() // self.world
+        Y = np.zeros((self.n, self.k))
+        for q, (a, b) in enumerate(self.cols):
+            blk = yall[q * send:q * send + (b - a) * self.n].numpy().reshape(b - a, self.n)
+            Y[:, a:b] = blk.T
+        return Y
+
+    @staticmethod
+    def _tile(t):
+        A = int((np.sqrt(8 * t + 1) - 1) // 2)
+        while (A + 1) * (A + 2) // 2 <= t:
+            A += 1
+        while A * (A + 1) // 2 > t:
+            A -= 1
+        return A, t - A * (A + 1) // 2
+
+    def gram(self, yall, tiles):
+        Y = np.zeros((self.n, self.npairs and ((self.k + GRAM_TILE - 1) // GRAM_TILE) * GRAM_TILE))
+        Y[:, :self.k] = self._Y(yall)
+        tiles.zero_()
+        for slot, t in enumerate(range(self.rank, self.npairs, self.world)):
+            A, B = self._tile(t)
+            blk = Y[:, A * GRAM_TILE:(A + 1) * GRAM_TILE].T @ Y[:, B * GRAM_TILE:(B + 1) * GRAM_TILE]
+            tiles[slot * GRAM_TILE ** 2:(slot + 1) * GRAM_TILE ** 2] = torch.from_numpy(blk.ravel())
+
+    def finish(self, tiles_all):
+        kp = ((self.k + GRAM_TILE - 1) // GRAM_TILE) * GRAM_TILE
+        C = np.zeros((kp, kp))
+        T = tiles_all.numpy()
+        for t in range(self.npairs):
+            A, B = self._tile(t)
+            off = ((t % self.world) * self.per_rank + t // self.world) * GRAM_TILE ** 2
+            blk = T[off:off + GRAM_TILE ** 2].reshape(GRAM_TILE, GRAM_TILE)
+            C[A * GRAM_TILE:(A + 1) * GRAM_TILE, B * GRAM_TILE:(B + 1) * GRAM_TILE] = blk
+            C[B * GRAM_TILE:(B + 1) * GRAM_TILE, A * GRAM_TILE:(A + 1) * GRAM_TILE] = blk.T
+        self.C = C[:self.k, :self.k]
+
+
+def _problem():
+    rng = np.random.default_rng(0)
+    n, k = 90, 150
+    M = rng.standard_normal((n, n))
+    A = M @ M.T + n * np.eye(n)
+    L = np.linalg.cholesky(A)
+    E = np.zeros((n, k))
+    E[rng.integers(0, n, k), np.arange(k)] = 1.0
+    return L, E
+
+
+def _worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    own = tile_owner(U_full.shape[0], world)
-    shard = torch.as_tensor(np.where(own == rank, U_full, 0.0))
-    dist.all_reduce(shard, op=dist.ReduceOp.SUM)
-    out[rank] = shard.numpy()
+    L, E = _problem()
+    steps = NumpySteps(L, E, rank, world)
+
+    # the production gather (parallel.all_gather: all_gather_into_tensor), over gloo
+    run_split(steps, world, all_gather(), lambda n: torch.empty(int(n), dtype=torch.float64))
+    out[rank] = steps.C
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_gloo_two_rank_shard_reduce_is_exact():
-    rng = np.random.default_rng(0)
-    Y = rng.standard_normal((40, 150))
-    U = Y.T @ Y
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_split_protocol_reproduces_one_process(world):
+    L, E = _problem()
+    single = NumpySteps(L, E, 0, 1)
+    run_split(single, 1, lambda o, i: o.copy_(i), lambda n: torch.empty(int(n), dtype=torch.float64))
+    Y = sla.solve_triangular(L, E, lower=True)
+    assert np.abs(single.C - Y.T @ Y).max() <= 1e-12 * np.abs(single.C).max()
     mgr = mp.Manager()
     out = mgr.dict()
-    port = _free_port()
-    mp.spawn(_worker, args=(world, port, U, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     for r in range(world):
-        assert np.array_equal(out[r], U)
+        assert np.array_equal(out[r], single.C)
 
 
 def test_cfg4_copy_partition_covers_every_copy_once():
