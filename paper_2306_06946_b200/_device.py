@@ -40,6 +40,38 @@ def empty(shape, dev=None, dtype=torch.float64) -> torch.Tensor:
     return torch.empty(shape, dtype=dtype, device=dev or device())
 
 
+def square(c: int, dev=None) -> torch.Tensor:
+    """(c, c) fp64 matrix whose rows are 16-byte aligned: a view of a (c, c + c % 2)
+    buffer.  Dense constraint-space operators (W) use it so the PGS kernel can
+    move tiles with tensor TMA (the global row pitch must be a multiple of 16
+    bytes); pass ``t.stride(0)`` as the leading dimension."""
+    buf = torch.empty((c, c + (c & 1)), dtype=torch.float64, device=dev or device())
+    return buf[:, :c]
+
+
+def mat64(x, dev=None) -> torch.Tensor:
+    """A dense operator as a row-major fp64 device matrix, keeping (or creating) the
+    16-byte aligned row pitch of ``square`` for square matrices."""
+    dev = dev or device()
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+    if t.device != dev or t.dtype != torch.float64:
+        t = t.to(device=dev, dtype=torch.float64)
+    if t.dim() == 2 and t.shape[0] == t.shape[1]:
+        if t.stride(1) == 1 and (t.stride(0) % 2 == 0 or t.shape[0] <= 1):
+            return t
+        out = square(t.shape[0], dev)
+        out.copy_(t)
+        return out
+    return t.contiguous()
+
+
+def ld(t: torch.Tensor) -> int:
+    """Leading dimension (row pitch, elements) of a row-major matrix view."""
+    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+        raise ValueError(f"expected a row-major matrix view, got shape {tuple(t.shape)} strides {t.stride()}")
+    return int(t.stride(0)) if t.shape[0] > 1 else int(t.shape[1])
+
+
 def zeros(shape, dev=None, dtype=torch.float64) -> torch.Tensor:
     return torch.zeros(shape, dtype=dtype, device=dev or device())
 

@@ -140,8 +140,18 @@ def check(code: int, what: str = "") -> None:
     raise cls(f"{what}: {msg}" if what else msg)
 
 
+# entry points whose workspaces are (re)allocated before any launch: on a
+# device out-of-memory they are retried once after torch's caching allocator
+# returned its unused blocks (the library's cudaMalloc competes with it)
+_OOM_RETRY = {"cnb_chol_compliance", "cnb_chol_compliance_plan", "cnb_chol_solve"}
+
+
 def call(name: str, *args) -> None:
-    check(getattr(lib(), name)(*args), name)
+    code = getattr(lib(), name)(*args)
+    if code == 100 and name in _OOM_RETRY and "out of memory" in lib().cnb_last_error().decode(errors="replace"):
+        torch.cuda.empty_cache()
+        code = getattr(lib(), name)(*args)
+    check(code, name)
 
 
 def require_cuda(device=None) -> torch.device:

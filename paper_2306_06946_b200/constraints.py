@@ -313,10 +313,10 @@ def rebuild_W_fast(D: DirectionMatrix, wg: MappingDelassus, out: torch.Tensor | 
     """W = D W_g D^T (constraints.py:182-191), bit-identical to the reference."""
     if D.c != wg.dim:
         raise DimensionMismatchError(f"direction matrix is {D.c} rows, W_g is {wg.dim}")
-    W = out if out is not None else dv.empty((D.c, D.c))
+    W = out if out is not None else dv.square(D.c)
     if D.c:
-        _lib.call("cnb_rebuild_w", D.n_groups, D.blocks.data_ptr(), wg.wg.data_ptr(), wg.wg.shape[1],
-                  W.data_ptr(), W.shape[1], _lib.stream())
+        _lib.call("cnb_rebuild_w", D.n_groups, D.blocks.data_ptr(), wg.wg.data_ptr(), dv.ld(wg.wg),
+                  W.data_ptr(), dv.ld(W), _lib.stream())
     return Delassus(W)
 
 

@@ -135,10 +135,10 @@ def regularize(W):
 
 def local_solve(alpha: int, W, delta_cur, lam, mu: float, h2: float):
     """One group's Signorini/Coulomb block solve (solver.py:124-165), on the device."""
-    W_t, d_t, l_t = dv.f64(W), dv.f64(delta_cur), dv.f64(lam)
+    W_t, d_t, l_t = dv.mat64(W), dv.f64(delta_cur), dv.f64(lam)
     out = dv.empty(3)
     st = _lib.status(out.device)
-    _lib.call("cnb_local_solve", int(alpha), W_t.shape[0] // 3, W_t.data_ptr(), W_t.shape[1], d_t.data_ptr(),
+    _lib.call("cnb_local_solve", int(alpha), W_t.shape[0] // 3, W_t.data_ptr(), dv.ld(W_t), d_t.data_ptr(),
               l_t.data_ptr(), float(mu), float(h2), out.data_ptr(), st.ptr, _lib.stream())
     st.raise_if_set("local_solve")
     return out
@@ -166,7 +166,7 @@ def pgs_device(W: torch.Tensor, delta_base: torch.Tensor, h: float, config: PgsC
         raise SingularBlockError(f"W is {tuple(W.shape)}, violation has {c} rows")
     ws = ws or PgsWorkspace(c, config.max_iterations)
     st = _lib.status(dev)
-    _lib.call("cnb_pgs", c // 3, W.data_ptr(), W.shape[1], delta_base.data_ptr(), float(h), float(config.friction),
+    _lib.call("cnb_pgs", c // 3, W.data_ptr(), dv.ld(W), delta_base.data_ptr(), float(h), float(config.friction),
               float(config.tolerance), int(config.max_iterations), ws.lam.data_ptr(), ws.delta_end.data_ptr(),
               ws.eps.data_ptr(), ws.ic.data_ptr(), None, st.ptr, _lib.stream())
     return PgsResult(ws.lam, ws.delta_end, ws.eps, ws.ic, st)
@@ -175,7 +175,7 @@ def pgs_device(W: torch.Tensor, delta_base: torch.Tensor, h: float, config: PgsC
 def pgs(W, delta_base, h: float, config: PgsConfig) -> PgsResult:
     """Sweep the groups until the relative lambda change drops below tolerance
     (solver.py:168-202).  Returns device lam and delta_end."""
-    W_t, d_t = dv.f64(W), dv.f64(delta_base)
+    W_t, d_t = dv.mat64(W), dv.f64(delta_base)
     res = pgs_device(W_t, d_t, h, config)
     res._resolve()
     return res
@@ -265,7 +265,7 @@ def newton_fast(ctx: StepContext, ncfg: NewtonConfig, pcfg: PgsConfig) -> Correc
     p_a = dv.f64(ctx.p_a0).reshape(-1, 3).clone()
     p_b = dv.f64(ctx.p_b0).reshape(-1, 3).clone()
     acc = dv.zeros(c)
-    W = dv.empty((c, c))
+    W = dv.square(c)  # 16-byte aligned rows: the pipelined PGS kernel moves W tiles by TMA
     delta = dv.empty(c)
     t = dv.empty(c)
     rot = dv.zeros(1)
@@ -354,7 +354,7 @@ def newton_standard(ctx: StepContext, ncfg: NewtonConfig, pcfg: PgsConfig, group
         e0 = timer.mark()
         Dm = DirectionMatrix(D)
         H = {oid: assemble_H(Dm, S) for oid, S in sorted(ctx.S_by_object.items())}
-        W = assemble_W_standard(H, ctx.F_by_object, group=group).W
+        W = dv.mat64(assemble_W_standard(H, ctx.F_by_object, group=group).W)  # aligned rows for PGS
         e1 = timer.mark()
         compute_violation(Dm, p_a, p_b, out=delta)
         res = pgs_device(W, delta, ctx.h, pcfg, PgsWorkspace(c, pcfg.max_iterations))

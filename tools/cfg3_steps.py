@@ -12,7 +12,9 @@ import bench  # noqa: E402
 import paper_2306_06946_b200 as cn  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 15
-sim = cn.Simulation(bench.make_cfg3_config(cn))
+shift = float(sys.argv[2]) if len(sys.argv) > 2 else 0.0
+gap = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+sim = cn.Simulation(bench.make_cfg3_config(cn, shift=shift, gap=gap))
 for s in range(steps):
     t0 = time.perf_counter()
     try:

@@ -92,11 +92,12 @@ def cfg1_inputs():
     return dict(nodes=nodes, tets=tets, tris=tris, tri_idx=tri_idx, weights=weights, Ds=Ds, lams=lams)
 
 
-def cfg3_meshes(nxz=CFG3_NXZ, ny=CFG3_NY):
-    """Lower and upper block (nodes, tets); the upper block's bottom face lies on the lower's top."""
+def cfg3_meshes(nxz=CFG3_NXZ, ny=CFG3_NY, shift=0.0, gap=0.0):
+    """Lower and upper block (nodes, tets); the upper block sits ``gap`` above the
+    lower's top face, shifted by ``shift`` in x and z."""
     lower = five_tet_grid((nxz, ny, nxz), 0.01)
     top = float(lower[0][:, 1].max())
-    upper = five_tet_grid((nxz, ny, nxz), 0.01, (0.0, top, 0.0))
+    upper = five_tet_grid((nxz, ny, nxz), 0.01, (shift, top + gap, shift))
     return lower, upper
 
 
