@@ -195,32 +195,6 @@ int cnb_detect_vertex_mesh(int64_t nv, const int64_t* vids, const double* pts_a,
 
 /* ---- projected Gauss-Seidel (contactnewton/solver.py) -------------------- */
 
-/* Workspace bytes needed by cnb_pgs for c = 3*groups rows. */
-int64_t cnb_pgs_work_bytes(int64_t groups);
-
-/* Diagnostics of the grid-scale PGS kernels (env CNB_PGS_PROFILE=1): summed
- * nanoseconds (slots 16-31: cycles) per phase since the last call, out[32]; slot meanings are
- * listed at the stamp() calls of each kernel in csrc/pgs.cu. */
-int cnb_pgs_profile(double* out);
-/* Diagnostic: summed cycles of the POTRF kernel's phases (CTA 0 of every launch)
- * since the last call: out[0] loads, [1] factor, [2] store L, [3] inverse,
- * [4] store L^{-1}, out[7] launches. */
-int cnb_potrf_profile(double* out);
-/* Diagnostic: fp64 DMMA GEMM tile-shape variants, C = A B (row-major; sizes
- * multiples of the variant's tile). */
-int cnb_bench_gemm(int32_t variant, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
-                   int64_t ldb, double* C, int64_t ldc, void* stream);
-
-/* Diagnostic: cycles per group of the PGS block solve while the other warps of
- * the CTA generate load of kind `mode` (0 idle, 1 LDS, 2 SHFL, 3 global polls,
- * 4 bulk copies into shared memory, 5 fp64 FMA). out[0] = cycles / group. */
-int cnb_bench_contention(int32_t mode, int32_t reps, double* out, void* stream);
-
-/* Cycles per group of the sequential warp block solve of the PGS kernels on a
- * resident synthetic tile (diagnostic microbenchmark; variant selects the
- * update / projection form), out[0] cycles per group, out[1] checksum. */
-int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stream);
-
 /* PGS with Signorini + isotropic Coulomb disk in the reference's canonical
  * group order.  Replaces pgs solver.py:168-202, local_solve 124-165 and
  * regularize 99-121.
@@ -229,8 +203,8 @@ int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stre
  * Singular blocks set d_status to CNB_E_SINGULAR_BLOCK (index = group). */
 int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_base,
             double h, double mu, double tol, int32_t max_iter, double* lam,
-            double* delta_end, double* eps_hist, int32_t* iters_conv, void* work,
-            cnb_status_t* d_status, void* stream);
+            double* delta_end, double* eps_hist, int32_t* iters_conv, cnb_status_t* d_status,
+            void* stream);
 
 /* One group's local solve (solver.py:124-165) as a device call, for API
  * parity with local_solve; out (3). */
@@ -333,18 +307,6 @@ int cnb_fe_system(int64_t n, const int64_t* rowptr, const int64_t* col, const in
  * stiffness products of SoftBody.assemble dynamics.py:202-208. */
 int cnb_csr_spmv(int64_t rows, const int64_t* rowptr, const int64_t* col, const double* val,
                  const double* x, double* y, double alpha, void* stream);
-
-/* ---- tooling --------------------------------------------------------------- */
-
-/* Number of kernels this library has launched in the process so far. */
-long long cnb_launch_count(void);
-
-/* Cycles per dependent op (out: host, 6): DFMA, DADD, fp64 div, fp64 sqrt,
- * 64-bit shuffle, FFMA. */
-int cnb_bench_latency(double* out /* 9 doubles */, void* stream);
-
-/* fp64 MMA (DMMA) throughput of the whole GPU in TFLOP/s (out: host). */
-int cnb_bench_dmma(int32_t iters, double* out, void* stream);
 
 /* ---- dense products (contactnewton/linalg.py) ---------------------------- */
 

@@ -1,0 +1,44 @@
+/* Diagnostics and measurement hooks of libcnb200.so (not part of the drop-in
+ * boundary in cn_b200.h): used by bench.py and tools/ to count launches, read
+ * phase profiles of the PGS / factor kernels and measure the fp64 tensor-core
+ * peak the rooflines are quoted against.  Same conventions as cn_b200.h. */
+#ifndef CN_B200_DIAG_H
+#define CN_B200_DIAG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Number of kernels this library has launched in the process so far. */
+long long cnb_launch_count(void);
+
+/* Phase profile of the pipelined PGS kernel (env CNB_PGS_PROFILE=1): summed SM
+ * cycles per slot since the last call, out[32]; slot meanings are listed at the
+ * stamp() calls in csrc/pgs.cu.  CNB_E_VALIDATION when profiling is off. */
+int cnb_pgs_profile(double* out);
+
+/* Summed cycles of the POTRF kernel's phases (CTA 0 of every launch) since the
+ * last call: out[0] loads, [1] factor, [2] store L, [3] inverse, [4] store
+ * L^{-1}, out[7] launches. */
+int cnb_potrf_profile(double* out);
+
+/* fp64 DMMA GEMM tile-shape variants, C = A B (row-major; sizes multiples of
+ * the variant's tile). */
+int cnb_bench_gemm(int32_t variant, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                   int64_t ldb, double* C, int64_t ldc, void* stream);
+
+/* Cycles per dependent op (out: host, 6): DFMA, DADD, fp64 div, fp64 sqrt,
+ * 64-bit shuffle, FFMA. */
+int cnb_bench_latency(double* out /* 9 doubles */, void* stream);
+
+/* fp64 MMA (DMMA) throughput of the whole GPU in TFLOP/s (out: host): the
+ * tensor roofline denominator (not in MEASURED_PEAKS.json). */
+int cnb_bench_dmma(int32_t iters, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CN_B200_DIAG_H */

@@ -51,13 +51,10 @@ _SIGNATURES: dict[str, list] = {
     "cnb_signed_gaps": [I64, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "cnb_detect_work_bytes": [I64, I64],
     "cnb_detect_vertex_mesh": [I64, P, P, I64, P, P, F64, P, P, P, P],
-    "cnb_pgs_work_bytes": [I64],
     "cnb_pgs_profile": [P],
     "cnb_potrf_profile": [P],
     "cnb_bench_gemm": [I32, I64, I64, I64, P, I64, P, I64, P, I64, P],
-    "cnb_bench_block_solve": [I32, I32, P, P],
-    "cnb_bench_contention": [I32, I32, P, P],
-    "cnb_pgs": [I64, P, I64, P, F64, F64, F64, I32, P, P, P, P, P, P, P],
+    "cnb_pgs": [I64, P, I64, P, F64, F64, F64, I32, P, P, P, P, P, P],
     "cnb_local_solve": [I64, I64, P, I64, P, P, F64, F64, P, P, P],
     "cnb_gemm_naive": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, P],
     "cnb_csr_spmv": [I64, P, P, P, P, P, F64, P],
@@ -83,7 +80,6 @@ _SIGNATURES: dict[str, list] = {
 _RESTYPES = {
     "cnb_launch_count": ctypes.c_longlong,
     "cnb_last_error": ctypes.c_char_p,
-    "cnb_pgs_work_bytes": I64,
     "cnb_detect_work_bytes": I64,
     "cnb_chol_export_bytes": I64,
 }

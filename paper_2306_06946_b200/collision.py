@@ -518,39 +518,6 @@ def signed_gaps(pairs, views: dict):
 # detection (once per step, before the hot path)
 # --------------------------------------------------------------------------
 
-def closest_points_on_triangles(tris: np.ndarray, p: np.ndarray):
-    """Ericson closest point of p on every triangle; first true region wins
-    (collision.py:138-184)."""
-    a, b, c = tris[:, 0], tris[:, 1], tris[:, 2]
-    ab, ac = b - a, c - a
-    ap, bp, cp = p - a, p - b, p - c
-    d1 = np.einsum("ij,ij->i", ab, ap)
-    d2 = np.einsum("ij,ij->i", ac, ap)
-    d3 = np.einsum("ij,ij->i", ab, bp)
-    d4 = np.einsum("ij,ij->i", ac, bp)
-    d5 = np.einsum("ij,ij->i", ab, cp)
-    d6 = np.einsum("ij,ij->i", ac, cp)
-    va = d3 * d6 - d5 * d4
-    vb = d5 * d2 - d1 * d6
-    vc = d1 * d4 - d3 * d2
-    with np.errstate(divide="ignore", invalid="ignore"):
-        v_ab = np.where(d1 != d3, d1 / (d1 - d3), 0.0)
-        w_ac = np.where(d2 != d6, d2 / (d2 - d6), 0.0)
-        den_bc = (d4 - d3) + (d5 - d6)
-        w_bc = np.where(den_bc != 0, (d4 - d3) / den_bc, 0.0)
-        den = va + vb + vc
-        v_in = np.where(den != 0, vb / den, 1.0 / 3.0)
-        w_in = np.where(den != 0, vc / den, 1.0 / 3.0)
-    zero = 0.0 * d1
-    conds = [(d1 <= 0) & (d2 <= 0), (d3 >= 0) & (d4 <= d3), (vc <= 0) & (d1 >= 0) & (d3 <= 0),
-             (d6 >= 0) & (d5 <= d6), (vb <= 0) & (d2 >= 0) & (d6 <= 0),
-             (va <= 0) & (d4 - d3 >= 0) & (d5 - d6 >= 0)]
-    v = np.select(conds, [zero, 1.0 + zero, v_ab, zero, zero, 1.0 - w_bc], default=v_in)
-    w = np.select(conds, [zero, zero, zero, 1.0 + zero, w_ac, w_bc], default=w_in)
-    u = 1.0 - v - w
-    return a + v[:, None] * ab + w[:, None] * ac, np.column_stack([u, v, w])
-
-
 def triangle_normals(tris: np.ndarray) -> np.ndarray:
     n = np.cross(tris[:, 1] - tris[:, 0], tris[:, 2] - tris[:, 0])
     ln = np.linalg.norm(n, axis=1, keepdims=True)

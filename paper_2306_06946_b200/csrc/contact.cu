@@ -413,7 +413,7 @@ using namespace cnb;
 
 extern "C" {
 
-int cnb_abi_version(void) { return 1; }
+int cnb_abi_version(void) { return 2; }
 
 int cnb_sandwich(int64_t m, int64_t k, const int32_t* ell_col, const double* ell_val, const double* C, int64_t ldc,
                  double* U, int64_t ldu, void* stream) {

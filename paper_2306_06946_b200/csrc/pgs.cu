@@ -159,47 +159,6 @@ __device__ __forceinline__ void group_const(const double Wd[9], double h2, Group
   k.b1 = fma(k.it10, k.htn0, k.it11 * k.htn1);
 }
 
-// local_solve with the precomputed constants: same branches and projection
-// as solver.py:124-165; divisions by loop-invariant quantities become
-// multiplications by reciprocals (last-ulp differences only).
-__device__ __forceinline__ int local_solve_fast(const double d[3], const double l[3], const GroupConst& k,
-                                                double mu, double out[3]) {
-  if (k.bad & 1) return CNB_E_SINGULAR_BLOCK;
-  const double ln_old = l[0];
-  const double x = fma(-d[0], k.ihw, ln_old);
-  const double ln = x > 0.0 ? x : 0.0;
-  if (ln == 0.0) {
-    out[0] = out[1] = out[2] = 0.0;
-    return 0;
-  }
-  if (mu == 0.0) {
-    out[0] = ln;
-    out[1] = out[2] = 0.0;
-    return 0;
-  }
-  if (k.bad & 2) return CNB_E_SINGULAR_BLOCK;
-  const double dln = ln - ln_old;
-  const double dt0 = fma(k.htn0, dln, d[1]);
-  const double dt1 = fma(k.htn1, dln, d[2]);
-  double lt0 = l[1] - fma(k.it00, dt0, k.it01 * dt1);
-  double lt1 = l[2] - fma(k.it10, dt0, k.it11 * dt1);
-  const double radius = mu * ln;
-  const double n2 = fma(lt0, lt0, lt1 * lt1);
-  if (n2 > radius * radius) {
-    const double sc = radius * rsqrt(n2);
-    lt0 *= sc;
-    lt1 *= sc;
-  }
-  out[0] = ln;
-  out[1] = lt0;
-  out[2] = lt1;
-  return 0;
-}
-
-// Branch-free local_solve_fast: every lane evaluates its own group with the
-// same instruction stream (no divergence in the sequential chain); the
-// caller keeps only the result of the lane whose turn it is.  Same values as
-// local_solve_fast (the unprojected branch multiplies by exactly 1.0).
 // fp64 1/sqrt(x) for x > 0 without the library's special-case branch: the
 // hardware approximation (rsqrt.approx.f64) refined by two Newton steps.
 __device__ __forceinline__ double rsqrt_nr(double x) {
@@ -210,6 +169,12 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
+// Branch-free local_solve (solver.py:124-165) with the precomputed constants
+// (divisions by loop-invariant quantities become multiplications by
+// reciprocals): every lane evaluates its own group with the same instruction
+// stream (no divergence in the sequential chain); the caller keeps only the
+// result of the lane whose turn it is (the unprojected branch multiplies by
+// exactly 1.0).
 template <int V = 0>
 __device__ __forceinline__ int local_solve_sel(const double d[3], const double l[3], const GroupConst& k,
                                                double mu, double out[3]) {
@@ -290,153 +255,6 @@ __device__ __forceinline__ void block_solve(const double* __restrict__ Wt, int n
   }
 }
 
-// Latency-shortened local_solve for the sequential chain (same branches and
-// projection as solver.py:124-165, reassociated):
-//   dln = max(-d_n/(h^2 W_nn), -l_n)              (= max(0, l_n - d_n/(h^2 W_nn)) - l_n)
-//   lt  = [l_t - T^-1 d_t] - T^-1 h^2 W_tn dln   (the bracket is independent of dln)
-//   projection scale from rsqrt.approx + one Newton step (relative error ~1e-13)
-// and the lambda change is returned pre-scaled by h^2, so the delta update
-// after the broadcast is three fused multiply-adds.  About 15 dependent fp64
-// operations per group instead of ~25.  dh = h^2 (new - old); h2l = h^2 l.
-__device__ __forceinline__ int local_solve_v2(const double d[3], const double l[3], const double h2l[3],
-                                              const GroupConst& k, double mu, double h2, double out[3],
-                                              double dh[3]) {
-  const double m = d[0] * k.ihw;
-  const double x = fma(-d[0], k.ihw, l[0]);
-  const double ln = x > 0.0 ? x : 0.0;        // Python max(0.0, x) (NaN -> 0.0)
-  const double dln = m < l[0] ? -m : -l[0];   // ln - l_n, one compare-select
-  const double a0 = fma(-k.it00, d[1], fma(-k.it01, d[2], l[1]));
-  const double a1 = fma(-k.it10, d[1], fma(-k.it11, d[2], l[2]));
-  const double lt0 = fma(-k.b0, dln, a0);
-  const double lt1 = fma(-k.b1, dln, a1);
-  const double radius = mu * ln;
-  const double n2 = fma(lt0, lt0, lt1 * lt1);
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(n2));
-  const double e = fma(-0.5 * n2, y * y, 1.5);
-  const double sc = n2 > radius * radius ? (radius * y) * e : 1.0;
-  const bool zero = !(x > 0.0) || mu == 0.0;
-  out[0] = ln;
-  out[1] = zero ? 0.0 : lt0 * sc;
-  out[2] = zero ? 0.0 : lt1 * sc;
-  dh[0] = h2 * dln;
-  dh[1] = zero ? -h2l[1] : fma(h2 * lt0, sc, -h2l[1]);
-  dh[2] = zero ? -h2l[2] : fma(h2 * lt1, sc, -h2l[2]);
-  return ((k.bad & 1) || (!zero && (k.bad & 2))) ? 1 : 0;
-}
-
-// block_solve with local_solve_v2, branch-free: the lambda change is
-// broadcast as soon as it exists and the owning lane's commit is a select.
-// Wt: the block's regularised diagonal tile (unscaled W, row stride ld).
-__device__ __forceinline__ void block_solve_v2(const double* __restrict__ Wt, int ld, int ng, int lane,
-                                               double dl_[3], double lm[3], const GroupConst& kc, double mu,
-                                               double h2, double& dsq, int& err) {
-  const double* wrow = Wt + 3 * lane * ld;
-  double h2l[3] = {h2 * lm[0], h2 * lm[1], h2 * lm[2]};
-#pragma unroll 2
-  for (int g = 0; g < ng; ++g) {
-    double w[9];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) w[3 * a + c] = wrow[a * ld + 3 * g + c];
-    double nw[3], dh[3];
-    const int e = local_solve_v2(dl_, lm, h2l, kc, mu, h2, nw, dh);
-    const double d0 = __shfl_sync(0xffffffffu, dh[0], g);
-    const double d1 = __shfl_sync(0xffffffffu, dh[1], g);
-    const double d2 = __shfl_sync(0xffffffffu, dh[2], g);
-    const bool me = lane == g;
-    const double q0 = nw[0] - lm[0], q1 = nw[1] - lm[1], q2 = nw[2] - lm[2];
-    const double sq = fma(q0, q0, fma(q1, q1, q2 * q2));
-    dsq += me ? sq : 0.0;
-    err |= me ? e : 0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      lm[a] = me ? nw[a] : lm[a];
-      h2l[a] = me ? h2 * nw[a] : h2l[a];
-    }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) dl_[a] = fma(w[3 * a + 2], d2, fma(w[3 * a + 1], d1, fma(w[3 * a], d0, dl_[a])));
-  }
-}
-
-// local_solve_v2 with the critical path shortened further (~150 cycles per
-// group on sm_100a instead of ~230): the normal branch is decided by comparing
-// the fresh delta_n against l_n h^2 W_nn (no multiply before the compare), the
-// projected and unprojected tangential changes are both formed and one
-// predicate-ready select picks the result, and the Newton step of the
-// reciprocal square root is folded into the final fused multiply-add.
-// Returns the h^2-scaled changes dh (broadcast first) and the new lambda.
-__device__ __forceinline__ int local_solve_v3(const double d[3], const double l[3], const double h2l[3],
-                                              double lhw, const GroupConst& k, double mu, double h2,
-                                              double out[3], double dh[3]) {
-  const bool open = d[0] < lhw;                 // d_n / (h^2 W_nn) < l_n  <=>  x > 0
-  const double m = d[0] * k.ihw;
-  const double dln = open ? -m : -l[0];         // max(0, l_n - m) - l_n
-  const double x = fma(-d[0], k.ihw, l[0]);
-  const double ln = x > 0.0 ? x : 0.0;          // Python max(0.0, x) (NaN -> 0.0)
-  const double a0 = fma(-k.it00, d[1], fma(-k.it01, d[2], l[1]));
-  const double a1 = fma(-k.it10, d[1], fma(-k.it11, d[2], l[2]));
-  const double lt0 = fma(-k.b0, dln, a0);
-  const double lt1 = fma(-k.b1, dln, a1);
-  const double radius = mu * ln;
-  const double n2 = fma(lt0, lt0, lt1 * lt1);
-  const bool proj = n2 > radius * radius;
-  const bool zero = !(x > 0.0) || mu == 0.0;
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(n2));
-  const double e = fma(-0.5 * n2, y * y, 1.5);  // Newton factor: rsqrt(n2) = y e
-  const double ry = radius * y;
-  const double hl0 = h2 * lt0, hl1 = h2 * lt1;
-  const double p0 = fma(hl0 * ry, e, -h2l[1]), p1 = fma(hl1 * ry, e, -h2l[2]);  // projected
-  const double u0 = hl0 - h2l[1], u1 = hl1 - h2l[2];                          // inside the cone
-  dh[0] = h2 * dln;
-  dh[1] = zero ? -h2l[1] : (proj ? p0 : u0);
-  dh[2] = zero ? -h2l[2] : (proj ? p1 : u1);
-  const double sc = proj ? ry * e : 1.0;
-  out[0] = ln;
-  out[1] = zero ? 0.0 : lt0 * sc;
-  out[2] = zero ? 0.0 : lt1 * sc;
-  return ((k.bad & 1) || (!zero && (k.bad & 2))) ? 1 : 0;
-}
-
-__device__ __forceinline__ void block_solve_v3(const double* __restrict__ Wt, int ld, int ng, int lane,
-                                               double dl_[3], double lm[3], const GroupConst& kc, double mu,
-                                               double h2, double& dsq, int& err) {
-  const double* wrow = Wt + 3 * lane * ld;
-  double h2l[3] = {h2 * lm[0], h2 * lm[1], h2 * lm[2]};
-  double lhw = lm[0] * kc.hwnn;
-#pragma unroll 2
-  for (int g = 0; g < ng; ++g) {
-    double w[9];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) w[3 * a + c] = wrow[a * ld + 3 * g + c];
-    double nw[3], dh[3];
-    const int e = local_solve_v3(dl_, lm, h2l, lhw, kc, mu, h2, nw, dh);
-    const double d0 = __shfl_sync(0xffffffffu, dh[0], g);
-    const double d1 = __shfl_sync(0xffffffffu, dh[1], g);
-    const double d2 = __shfl_sync(0xffffffffu, dh[2], g);
-    const bool me = lane == g;
-    const double q0 = nw[0] - lm[0], q1 = nw[1] - lm[1], q2 = nw[2] - lm[2];
-    const double sq = fma(q0, q0, fma(q1, q1, q2 * q2));
-    dsq += me ? sq : 0.0;
-    err |= me ? e : 0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      lm[a] = me ? nw[a] : lm[a];
-      h2l[a] = me ? h2 * nw[a] : h2l[a];
-    }
-    lhw = me ? nw[0] * kc.hwnn : lhw;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) dl_[a] = fma(w[3 * a + 2], d2, fma(w[3 * a + 1], d1, fma(w[3 * a], d0, dl_[a])));
-  }
-}
-
-// Lane-strided partial dot product  sum_{j in [lo,hi), j = lo+lane mod 32} w[j] x[j]
-// with four independent accumulators and the loads of four iterations issued
-// before their FMAs (in-order issue would otherwise stall on every load).
 template <bool CG>
 __device__ __forceinline__ double lane_dot(const double* __restrict__ w, const double* __restrict__ x, int64_t lo,
                                            int64_t hi, int lane) {
@@ -749,20 +567,6 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 // spin until *p >= target (or stop / watchdog); returns false on timeout
-__device__ bool wait_geq(volatile unsigned* p, unsigned target, volatile unsigned* stop, GridCtl* ctl) {
-  const unsigned long long t0 = global_ns();
-  while (*p < target) {
-    if (stop && *stop) return true;
-    if (global_ns() - t0 > 20000000000ull) {  // 20 s
-      atomicExch(&ctl->timeout, 1u);
-      atomicExch(&ctl->stop, 1u);
-      return false;
-    }
-    __nanosleep(64);
-  }
-  return true;
-}
-
 // Regularisation shift (solver.py:99-121) and the per-group constants of the
 // regularised diagonal blocks, once per PGS call; lambda <- 0.
 constexpr int kKC = 10;  // doubles per packed GroupConst
@@ -844,354 +648,7 @@ __global__ void __launch_bounds__(kPrepThreads) pgs_prep2_kernel(PgsScene s, dou
   }
 }
 
-constexpr int kGridThreads = 512;
 constexpr int kHelpPre = 32;  // W values per lane a helper warp holds in registers (32 x 32 columns)
-
-// Shared memory of the solver CTA (helpers reuse the space for lambda):
-//   T0, T1 : diagonal tiles (double-buffered), Wx: cross tile W[b rows, bp cols]
-//            (all kBR x kLDT; T[(t+1)&1] also stages the helpers' partials)
-//   dcur   : delta of the block being solved
-//   lamx   : lambda of the block solved in the previous step
-//   lamn[2], kcn[2]: next block's lambda / group constants (prefetched)
-struct GridSmem {
-  double *T0, *T1, *Wx, *dcur, *lamx, *lamn, *kcn, *red;
-  int* flags;
-};
-
-__host__ __device__ inline size_t grid_smem_bytes() {
-  return sizeof(double) * (size_t)(3 * kBR * kLDT + 2 * kBR + 2 * kBR + 2 * kKC * kBG + 32) + 4 * sizeof(int);
-}
-
-__device__ __forceinline__ GridSmem grid_carve(char* base) {
-  GridSmem g;
-  double* p = (double*)base;
-  g.T0 = p;
-  p += kBR * kLDT;
-  g.T1 = p;
-  p += kBR * kLDT;
-  g.Wx = p;
-  p += kBR * kLDT;
-  g.dcur = p;
-  p += kBR;
-  g.lamx = p;
-  p += kBR;
-  g.lamn = p;
-  p += 2 * kBR;
-  g.kcn = p;
-  p += 2 * kKC * kBG;
-  g.red = p;
-  p += 32;
-  g.flags = (int*)p;
-  return g;
-}
-
-__global__ void __launch_bounds__(kGridThreads) pgs_grid_kernel(PgsScene s, const double* __restrict__ dshift,
-                                                                const double* __restrict__ kconst, double* partial,
-                                                                GridCtl* ctl, int nch, int lam_in_smem,
-                                                                unsigned long long* prof) {
-  // prof (optional, CNB_PGS_PROFILE=1): summed ns per phase, see cnb_pgs_profile
-  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp = 0;
-  auto stamp = [&](int k) {
-    if (prof && threadIdx.x == 0) {
-      const unsigned long long now = global_ns();
-      if (k >= 0) pf[k] += now - tp;
-      tp = now;
-    }
-  };
-  extern __shared__ __align__(16) char smem_raw[];
-  GridSmem sm = grid_carve(smem_raw);
-  double* lams = (double*)smem_raw;  // helpers: resident copy of lambda
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = blockDim.x >> 5;
-  const int64_t G = s.groups, c = 3 * G;
-  const int nb = (int)((G + kBG - 1) / kBG);
-  const unsigned H = gridDim.x - 1;
-  const bool solver = blockIdx.x == 0;
-  const double h2 = s.h2;
-  const int64_t csz = (c + nch - 1) / nch;
-  double* lamg = s.lam;
-  volatile unsigned* vsolved = &ctl->solved;
-  volatile unsigned* vstop = &ctl->stop;
-  double dl_[3] = {0, 0, 0}, lm[3] = {0, 0, 0};
-  double dsq = 0.0;
-  int iterations = 0;
-  bool converged = false;
-  if (tid == 0) sm.flags[0] = sm.flags[1] = 0;
-  auto rows_of = [&](int blk) { return 3 * (int)min((int64_t)kBG, G - (int64_t)blk * kBG); };
-  // prefetch (cp.async) of block `blk`'s diagonal tile into T, its lambda and
-  // group constants into slot `slot`, and W[blk rows, cols of block `xb`] into
-  // Wx; threads [t0, t0 + nt) participate.
-  auto prefetch = [&](int blk, int xb, double* T, int slot, int t0, int nt) {
-    const int64_t rb0 = 3 * (int64_t)blk * kBG, xb0 = 3 * (int64_t)xb * kBG;
-    const int rws = rows_of(blk), xcols = rows_of(xb);
-    const int tw = (tid - t0) >> 5, ntw = nt >> 5;
-    for (int i = tw; i < rws; i += ntw) {
-      const double* src = s.W + (rb0 + i) * s.ldw;
-      for (int j = lane; j < rws; j += 32) cp_async8(&T[i * kLDT + j], src + rb0 + j, true);
-      if (xb >= 0)
-        for (int j = lane; j < xcols; j += 32) cp_async8(&sm.Wx[i * kLDT + j], src + xb0 + j, true);
-    }
-    copy_cg(&sm.lamn[slot * kBR], lamg + rb0, rws, tid - t0, nt);  // rewritten every sweep: bypass L1
-    for (int e = tid - t0; e < kKC * rws / 3; e += nt)
-      cp_async8(&sm.kcn[slot * kKC * kBG + e], kconst + kKC * (rb0 / 3) + e, true);
-  };
-  __syncthreads();
-  stamp(-1);
-  if (solver) prefetch(0, -1, sm.T0, 0, 0, blockDim.x);
-  for (unsigned t = 0;; ++t) {
-    const int b = (int)(t % nb);
-    const int sweep = (int)(t / nb);
-    const int bp = (b == 0) ? nb - 1 : b - 1;  // block solved at step t-1
-    const int bn = (b + 1 == nb) ? 0 : b + 1;
-    const int64_t g0 = (int64_t)b * kBG;
-    const int ng = (int)min((int64_t)kBG, G - g0);
-    const int rows = 3 * ng;
-    const int64_t r0 = 3 * g0;
-    if (solver) {
-      const int slot = (nb == 1) ? 0 : (int)(t & 1);
-      double* Tc = slot ? sm.T1 : sm.T0;  // this block's diagonal tile
-      double* Tn = slot ? sm.T0 : sm.T1;  // next block's tile / partial staging
-      if (t > 0 && tid == 0) {
-        stamp(3);  // epilogue of step t-1 -> here
-        // per-slot counters: a cumulative count could be reached by helpers
-        // running a step ahead while a slow one has not finished step t-1
-        wait_geq(&ctl->ready4[(t - 1) & 3], H * ((t - 1) / 4 + 1), nullptr, ctl);
-      }
-      stamp(0);  // wait for helpers
-      __syncthreads();
-      // delta_base of the block and (t > 0, nb > 1) the helpers' partials
-      for (int i = tid; i < rows; i += blockDim.x) cp_async8(&sm.dcur[i], s.delta_base + r0 + i, true);
-      const double* part = partial + (size_t)((t - 1) & 1) * kBR * nch;
-      if (t > 0 && nb > 1) copy_cg(Tn, part, rows * nch, tid, blockDim.x);  // written by other SMs
-      cp_async_wait_all();
-      __syncthreads();
-      if (t == 0 || nb > 1)  // regularisation shift (solver.py:119-120) on the fresh tile
-        for (int i = tid; i < rows; i += blockDim.x) Tc[i * kLDT + i] = add(Tc[i * kLDT + i], dshift[(r0 + i) / 3]);
-      if (nb == 1) __syncthreads();
-      if (t > 0) {
-        // ---- delta of block b = delta_base + h^2 (partials + W[b, bp] lam_bp), thread per row
-        const int xcols = rows_of(bp);
-        const double* X = (nb > 1) ? sm.Wx : Tc;  // nb == 1: the block itself (regularised)
-        for (int i = tid; i < rows; i += blockDim.x) {
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-          const double* xr = X + i * kLDT;
-          int j = 0;
-          for (; j + 4 <= xcols; j += 4) {
-            a0 = fma(xr[j], sm.lamx[j], a0);
-            a1 = fma(xr[j + 1], sm.lamx[j + 1], a1);
-            a2 = fma(xr[j + 2], sm.lamx[j + 2], a2);
-            a3 = fma(xr[j + 3], sm.lamx[j + 3], a3);
-          }
-          for (; j < xcols; ++j) a0 = fma(xr[j], sm.lamx[j], a0);
-          double acc = (a0 + a1) + (a2 + a3);
-          if (nb > 1)
-            for (int ch = 0; ch < nch; ++ch) acc += Tn[i * nch + ch];
-          sm.dcur[i] = add(sm.dcur[i], mul(h2, acc));
-        }
-      }
-      __syncthreads();
-      stamp(1);  // delta of block b
-      if (warp != 0 && nb > 1) {
-        // ---- warps 1..15: prefetch the next block while warp 0 solves
-        prefetch(bn, b, Tn, slot ^ 1, 32, blockDim.x - 32);
-      }
-      if (warp == 0) {
-        const bool mine = lane < ng;
-        GroupConst kc{};
-        if (mine) {
-          const double* kk = sm.kcn + slot * kKC * kBG + kKC * lane;  // record layout: load_group_const
-          kc.ihw = kk[0];
-          kc.it00 = kk[1];
-          kc.it01 = kk[2];
-          kc.it10 = kk[3];
-          kc.it11 = kk[4];
-          kc.bad = (int)kk[7];
-          kc.htn0 = kk[8];
-          kc.htn1 = kk[9];
-          for (int a = 0; a < 3; ++a) {  // nb == 1: the block's own lambda from the previous step
-            lm[a] = (nb == 1 && t > 0) ? sm.lamx[3 * lane + a] : sm.lamn[slot * kBR + 3 * lane + a];
-            dl_[a] = sm.dcur[3 * lane + a];
-          }
-        } else {
-          kc.ihw = 1.0;
-          lm[0] = lm[1] = lm[2] = dl_[0] = dl_[1] = dl_[2] = 0.0;
-        }
-        int err = 0;
-        block_solve<false>(Tc, ng, lane, dl_, lm, kc, s.mu, h2, dsq, err);
-        stamp(7);  // the sequential loop itself (+ kc / lambda loads)
-        const unsigned bad = __ballot_sync(0xffffffffu, mine && err);
-        if (bad) {
-          const int g = __ffs(bad) - 1;  // first failing group in Gauss-Seidel order
-          if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(g0 + g), 1.0 / kc.ihw);
-          if (lane == 0) sm.flags[0] = 1;
-        } else if (mine) {
-          for (int a = 0; a < 3; ++a) {
-            __stcg(lamg + 3 * (g0 + lane) + a, lm[a]);
-            sm.lamx[3 * lane + a] = lm[a];
-          }
-        }
-        __syncwarp();
-        // early hand-off: helpers may start on this block's lambda before the
-        // rest of the CTA reaches the barrier (a stop decided below is seen by
-        // them at their next wait)
-        if (lane == 0 && !bad) {
-          __threadfence();
-          atomicExch((unsigned*)vsolved, t + 1);
-        }
-      }
-      __syncthreads();
-      stamp(2);  // group solves (+ next-block prefetch)
-      bool stop = sm.flags[0] != 0;
-      if (!stop && b + 1 == nb) {
-        // ---- end of sweep: epsilon (solver.py:194-199)
-        iterations = sweep + 1;
-        if (warp == 0) {
-          const double v = warp_sum(dsq);
-          if (lane == 0) sm.red[0] = v;
-        }
-        double nl = 0.0;
-        for (int64_t i = tid; i < c; i += blockDim.x) {
-          const double l = __ldcg(lamg + i);
-          nl += l * l;
-        }
-        nl = warp_sum(nl);
-        if (lane == 0) sm.red[1 + warp] = nl;
-        __syncthreads();
-        if (tid == 0) {
-          double den2 = 0.0;
-          for (int w = 0; w < nwarps; ++w) den2 += sm.red[1 + w];
-          const double num = sqrt(sm.red[0]), den = sqrt(den2);
-          const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
-          s.eps_hist[sweep] = eps;
-          sm.flags[1] = (eps <= s.tol) ? 1 : 0;
-        }
-        __syncthreads();
-        dsq = 0.0;
-        converged = sm.flags[1] != 0;
-        stop = converged || (sweep + 1 >= s.max_iter);
-      }
-      if (ctl->timeout) stop = true;
-      if (stop) {
-        if (tid == 0) {
-          __threadfence();
-          atomicExch((unsigned*)vstop, 1u);
-        }
-        break;
-      }
-    } else {
-      // ---- helper: partials for the rows of block bn over all columns except
-      // block b, with lambda as of the end of step t-1.  The W slice of this
-      // step is loaded into registers before waiting for the solver.
-      const int64_t gn0 = (int64_t)bn * kBG;
-      const int rows_n = 3 * (int)min((int64_t)kBG, G - gn0);
-      const int64_t cb0 = r0, cb1 = r0 + rows;  // block b columns excluded
-      const unsigned hw = (blockIdx.x - 1) * nwarps + warp;
-      const bool has_item = nb > 1 && hw < (unsigned)(rows_n * nch);
-      const int i = has_item ? (int)(hw / nch) : 0, ch = has_item ? (int)(hw % nch) : 0;
-      const int64_t r = 3 * gn0 + i;
-      const int64_t c0 = (int64_t)ch * csz, c1 = min(c, c0 + csz);
-      const double* wr = s.W + r * s.ldw;
-      double wv[kHelpPre];
-#pragma unroll
-      for (int u = 0; u < kHelpPre; ++u) {
-        const int64_t j = c0 + lane + 32 * u;
-        const bool ok = has_item && j < c1 && (j < cb0 || j >= cb1);
-        wv[u] = ok ? wr[j] : 0.0;
-      }
-      if (blockIdx.x == 1) stamp(6);  // helper: ready -> next wait start
-      if (tid == 0) wait_geq(vsolved, t, vstop, ctl);
-      if (blockIdx.x == 1) stamp(4);  // helper: wait for the solver
-      __syncthreads();
-      if (*vstop) break;
-      if (lam_in_smem) {
-        // helpers keep lambda in shared memory: only the block solved at step t-1 changed
-        if (t == 0) {
-          for (int64_t j = tid; j < c; j += blockDim.x) lams[j] = 0.0;
-        } else {
-          const int64_t pb0 = 3 * (int64_t)bp * kBG;
-          const int pcols = rows_of(bp);
-          for (int j = tid; j < pcols; j += blockDim.x) lams[pb0 + j] = __ldcg(lamg + pb0 + j);
-        }
-        __syncthreads();
-      }
-      if (has_item) {
-        double a[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int u = 0; u < kHelpPre; ++u) {
-          const int64_t j = min(c0 + lane + 32 * u, c - 1);
-          a[u & 3] = fma(wv[u], lam_in_smem ? lams[j] : __ldcg(lamg + j), a[u & 3]);
-        }
-        for (int64_t j0 = c0 + 32 * kHelpPre; j0 < c1; j0 += 32 * kHelpPre) {  // slices wider than the registers
-#pragma unroll 8
-          for (int u = 0; u < kHelpPre; ++u) {
-            const int64_t j = j0 + lane + 32 * u;
-            if (j < c1 && (j < cb0 || j >= cb1))
-              a[u & 3] = fma(wr[j], lam_in_smem ? lams[j] : __ldcg(lamg + j), a[u & 3]);
-          }
-        }
-        double acc = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
-        if (lane == 0) {
-          if (r >= c0 && r < c1) acc = fma(dshift[r / 3], lam_in_smem ? lams[r] : __ldcg(lamg + r), acc);
-          __stcg(partial + (size_t)(t & 1) * kBR * nch + (size_t)i * nch + ch, acc);
-        }
-      }
-      __syncthreads();
-      if (blockIdx.x == 1) stamp(5);  // helper: lambda refresh + partials
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd(&ctl->ready4[t & 3], 1u);
-      }
-    }
-  }
-  // ---- everyone: wait for the final lambda, then delta_end = delta_base + h^2 W_reg lam
-  cp_async_wait_all();  // drain prefetches issued for a block that was never solved
-  if (tid == 0) wait_geq(vstop, 1u, nullptr, ctl);
-  __syncthreads();
-  __threadfence();
-  const unsigned gw = blockIdx.x * nwarps + warp, ngw = gridDim.x * nwarps;
-  for (int64_t r = gw; r < c; r += ngw) {
-    const double* wr = s.W + r * s.ldw;
-    double acc = lane_dot<true>(wr, lamg, 0, c, lane);
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      acc = fma(dshift[r / 3], __ldcg(lamg + r), acc);
-      s.delta_end[r] = add(s.delta_base[r], mul(h2, acc));
-    }
-  }
-  if (prof && tid == 0 && blockIdx.x <= 1)
-    for (int k = 0; k < 8; ++k) atomicAdd(prof + k, pf[k]);
-  if (solver && tid == 0) {
-    s.iters_conv[0] = iterations;
-    s.iters_conv[1] = converged ? 1 : 0;
-    if (ctl->timeout) raise_status(s.status, CNB_E_INTERNAL, 0, 0.0);
-  }
-}
-
-// ============================================================================
-// Pipelined grid PGS (lookahead 2)
-// ============================================================================
-// Same iterate as pgs_cta / pgs_grid_kernel, restructured so that the solver
-// warp's sequential block solve is the only thing on the critical path.
-// Blocks of kPG = 26 groups (kPR = 78 rows); step t solves block b = t mod nb.
-//
-//   helpers (CTAs 1..H), step t: once lambda of block b-1 is published, the
-//     lazy row products of block b+2 over every column except blocks b and
-//     b+1 (whose lambda is not final yet).  They have two block solves of
-//     slack, so the inter-SM hand-off latency is hidden.  They also pull the
-//     excluded column blocks of their rows into L2 for the solver's TMA.
-//   solver CTA, step t:
-//     warp 0    : sequential block solve of b (lane = group, block_solve_v4);
-//     warp 1    : publishes lambda_{b-1} (release store), ||lambda||^2 of the sweep;
-//     warp 2    : 2-D tensor TMA of T(b+1), W[b+1, b] and, once X2 is done,
-//                 X = W[b+2, b] for the next step: one instruction per tile, no
-//                 load instructions on the solver's SM;
-//     warp 3    : lambda(b+1), group constants of b+1;
-//     warps 5-7, 9-11, 13-15: X2 = W[b+1, b-1] lambda_{b-1} from the X tile and
-//                 the helpers' partials of block b+1 (step t-1), fixed order.
-//     Warps 4, 8, 12 share the solver's SM sub-partition and stay idle.
-//     then all  : delta(b+1) = delta_base + h^2 (partials + X2 + W[b+1, b] lambda_b)
-//                 (one 78 x 78 GEMV from shared memory), two barriers.
-// Every sum is taken in a fixed order: the result is bitwise repeatable.
 constexpr int kPipeThreads = 512;
 constexpr int kPG = 26;             // groups per block
 constexpr int kPR = 3 * kPG;        // rows per block
@@ -1246,48 +703,6 @@ __device__ __forceinline__ PipeSmem pipe_carve(char* base) {
   p += kPR;
   g.dsh = p;
   p += kPG;
-  g.red = p;
-  p += 8;
-  g.bar = (unsigned long long*)p;
-  p += 2;
-  g.flags = (int*)p;
-  return g;
-}
-
-// Shared-memory layout of the solver CTA with the fused next-block update
-// (pgs_pipe_kernel<true>): double-buffered diagonal tiles T and next-block tiles
-// Wn = W[b+1, b], lambda (new, old) / group constants / delta(b) per step parity.
-struct Pipe5Smem {
-  double *T[2], *Wn[2], *lamx, *lamn, *kcn, *sv, *dpre, *red;
-  unsigned long long* bar;  // [slot]: T(b) and W[b+1, b] of that step parity
-  int* flags;
-};
-
-__host__ __device__ inline size_t pipe5_smem_bytes() {
-  return 128 + sizeof(double) * (size_t)(4 * kTileD + 6 * kPR + 2 * kKCP * kPG + 4 * kPG + 8) + 16 + 8 * sizeof(int);
-}
-
-__device__ __forceinline__ Pipe5Smem pipe5_carve(char* base) {
-  Pipe5Smem g;
-  double* p = (double*)base;
-  g.T[0] = p;
-  p += kTileD;
-  g.T[1] = p;
-  p += kTileD;
-  g.Wn[0] = p;
-  p += kTileD;
-  g.Wn[1] = p;
-  p += kTileD;
-  g.lamx = p;
-  p += 2 * kPR;
-  g.lamn = p;
-  p += 2 * kPR;
-  g.kcn = p;
-  p += 2 * kKCP * kPG;
-  g.sv = p;
-  p += 4 * kPG;
-  g.dpre = p;
-  p += 2 * kPR;
   g.red = p;
   p += 8;
   g.bar = (unsigned long long*)p;
@@ -1381,72 +796,6 @@ __device__ __forceinline__ void block_solve_v4(const double* __restrict__ Wt, in
   }
 }
 
-// block_solve_v4 that also accumulates, for the NEXT block, dn += h^2 W[next, this]
-// (lambda change) group by group from the broadcast changes: Wn holds the rows of
-// the next block (lane l <-> its group l) over the columns of this block, stride
-// ld.  The extra loads / FMAs are independent of the sequential chain.  Lanes
-// past the tile's groups (> lmax) read row lmax instead (their results are unused).
-template <bool FRIC>
-__device__ __forceinline__ void block_solve_v5(const double* __restrict__ Wt, const double* __restrict__ Wn, int ld,
-                                               int ng, int lane, double dl_[3], double dn[3], const double lm[3],
-                                               const GroupConst& kc, double mu, double h2, double* __restrict__ sv,
-                                               int lmax) {
-  const int lr = min(lane, lmax);
-  const double* wrow = Wt + 3 * lr * ld;
-  const double* nrow = Wn + 3 * lr * ld;
-  const double h2l1 = h2 * lm[1], h2l2 = h2 * lm[2];
-  const double nl0 = -lm[0], lhw = lm[0] * kc.hwnn, nihw = -kc.ihw;
-#pragma unroll 2
-  for (int g = 0; g < ng; ++g) {
-    double w[9], wn[9];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        w[3 * a + c] = wrow[a * ld + 3 * g + c];
-        wn[3 * a + c] = nrow[a * ld + 3 * g + c];
-      }
-    const double d0 = dl_[0], d1 = dl_[1], d2 = dl_[2];
-    const bool open = d0 < lhw;
-    const double x = fma(nihw, d0, lm[0]);
-    const double dln = open ? d0 * nihw : nl0;
-    double dh0 = h2 * dln, dh1, dh2;
-    if (FRIC) {
-      const double a0 = fma(-kc.it00, d1, fma(-kc.it01, d2, lm[1]));
-      const double a1 = fma(-kc.it10, d1, fma(-kc.it11, d2, lm[2]));
-      const double lt0 = fma(-kc.b0, dln, a0), lt1 = fma(-kc.b1, dln, a1);
-      const double radius = mu * x;
-      const double n2 = fma(lt0, lt0, lt1 * lt1);
-      const bool proj = n2 > radius * radius;
-      double y;
-      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(n2));
-      const double e = fma(-0.5 * n2, y * y, 1.5);
-      const double ry = radius * y;
-      const double hl0 = h2 * lt0, hl1 = h2 * lt1;
-      const double p0 = fma(hl0 * ry, e, -h2l1), p1 = fma(hl1 * ry, e, -h2l2);
-      const double u0 = hl0 - h2l1, u1 = hl1 - h2l2;
-      dh1 = open ? (proj ? p0 : u0) : -h2l1;
-      dh2 = open ? (proj ? p1 : u1) : -h2l2;
-    } else {
-      dh1 = -h2l1;
-      dh2 = -h2l2;
-    }
-    const double s0 = __shfl_sync(0xffffffffu, dh0, g);
-    const double s1 = __shfl_sync(0xffffffffu, dh1, g);
-    const double s2 = __shfl_sync(0xffffffffu, dh2, g);
-    asm volatile(
-        "{\n .reg .pred p;\n setp.eq.s32 p, %0, %1;\n"
-        " @p st.shared.v2.f64 [%2], {%3, %4};\n @p st.shared.v2.f64 [%2+16], {%5, %6};\n}\n" ::"r"(lane),
-        "r"(g), "r"(smem_u32(sv + 4 * g)), "d"(x), "d"(dh1), "d"(dh2), "d"(open ? 1.0 : 0.0)
-        : "memory");
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      dl_[a] = fma(w[3 * a + 2], s2, fma(w[3 * a + 1], s1, fma(w[3 * a], s0, dl_[a])));
-      dn[a] = fma(wn[3 * a + 2], s2, fma(wn[3 * a + 1], s1, fma(wn[3 * a], s0, dn[a])));
-    }
-  }
-}
-
 // lambda of the lane's group from its block_solve_v4 record; dsq += |change|^2;
 // returns the error flag (W_nn <= 0, or a singular tangential block when used)
 __device__ __forceinline__ int block_commit(const double* sv, int lane, double lm[3], const GroupConst& kc,
@@ -1520,7 +869,6 @@ __device__ __forceinline__ double ll_load(const double* slot, unsigned tag, Grid
   return __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
 }
 
-template <bool V5>
 __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, const double* __restrict__ dshift,
                                                                 const double* __restrict__ kconst, double* partial,
                                                                 GridCtl* ctl, int nch, int lam_in_smem, int tma,
@@ -1555,244 +903,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
     }
   };
 
-  if (blockIdx.x == 0 && V5) {
-    // ---- solver CTA with the next-block update folded into the block solve ----
-    // Step t solves block b with block_solve_v5, which also accumulates, lane l
-    // for group l of block b+1, dn = h^2 W[b+1, b] (lambda_b change).  Everything
-    // else delta(b+1) needs is formed off the critical path during the solve:
-    //   X2 warps: dpre(b+1) = delta_base + h^2 (helper partials + W[b+1, b-1]
-    //             lambda_{b-1} (global / L2) + W[b+1, b] lambda_b(old) (tile Wn));
-    //   warp 2:   tensor TMA of T(b+1) and Wn = W[b+2, b+1] for the next step, then
-    //             the regularisation shift of T(b+1)'s diagonal;
-    //   warp 3:   lambda(b+1) and the group constants of b+1;
-    //   warp 1:   publisher (as in the v4 path).
-    // The solver then starts block b+1 from dpre(b+1) + dn right after one
-    // barrier at which the other warps have long arrived: no phase B.
-    Pipe5Smem sm = pipe5_carve(smem_raw);
-    const int xi = x2_index(warp);
-    const int K5 = kKCP * kPG;
-    if (tid == 0) {
-      sm.flags[0] = sm.flags[1] = 0;
-      mbar_init(sm.bar, 1);
-      mbar_init(sm.bar + 1, 1);
-    }
-    for (int i = tid; i < kPR; i += blockDim.x) {
-      sm.lamx[i] = sm.lamx[kPR + i] = 0.0;
-      sm.lamn[i] = sm.lamn[kPR + i] = 0.0;  // lambda starts at zero
-      sm.dpre[i] = i < rows_of(0) ? s.delta_base[i] : 0.0;
-      sm.dpre[kPR + i] = 0.0;
-    }
-    for (int e = tid; e < kKCP * rows_of(0) / 3; e += blockDim.x)
-      sm.kcn[e] = kconst[kKC * (e / kKCP) + (e % kKCP)];
-    __syncthreads();
-    if (tid == 64) {  // T(0) and Wn = W[1, 0] for step 0
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(sm.bar, 2u * kPR * kPS * 8);
-      tma_load_2d(sm.T[0], &tmap, 0, 0, sm.bar);
-      tma_load_2d(sm.Wn[0], &tmap, 0, kPR, sm.bar);
-    }
-    if (warp == 2) {
-      mbar_wait(sm.bar, 0);
-      for (int i = lane; i < rows_of(0); i += 32) sm.T[0][i * kPS + i] = add(sm.T[0][i * kPS + i], dshift[i / 3]);
-    }
-    double dsq = 0.0;
-    const double ih2 = 1.0 / h2;
-    double dn[3] = {0.0, 0.0, 0.0};
-    volatile unsigned* vcnt = (volatile unsigned*)(sm.flags + 4);  // [0] lambda in smem, [1] published (steps)
-    if (tid == 0) {
-      sm.flags[2] = 0;
-      vcnt[0] = vcnt[1] = 0;
-    }
-    __syncthreads();
-    stamp(-1);
-    int iterations = 0;
-    bool converged = false;
-    if (warp != 1) {
-    for (unsigned t = 0;; ++t) {
-      const int b = (int)(t % nb), sweep = (int)(t / nb);
-      const int b1 = wrap(b + 1), b2 = wrap(b + 2), bm = (b == 0) ? nb - 1 : b - 1;
-      const int rows = rows_of(b), rows1 = rows_of(b1), rowsm = rows_of(bm);
-      const int slot = (int)(t & 1);
-      double* Tc = sm.T[slot];
-      double* Tn = sm.T[slot ^ 1];
-      const double* Wc = sm.Wn[slot];
-      double* lamc = sm.lamx + slot * kPR;           // lambda_b (this solve)
-      const double* lamp = sm.lamx + (slot ^ 1) * kPR;  // lambda_{b-1}
-      const double* lamo = sm.lamn + slot * kPR;      // lambda_b before this solve
-      const int64_t rb = 3 * (int64_t)b * kPG, rb1 = 3 * (int64_t)b1 * kPG, rb2 = 3 * (int64_t)b2 * kPG;
-      const int64_t rbm = 3 * (int64_t)bm * kPG;
-      if (warp == 0) {
-        // ---- sequential block solve ----
-        const int ng = rows / 3;
-        const bool mine = lane < ng;
-        GroupConst kc;
-        load_group_const(kc, sm.kcn + slot * K5 + kKCP * lane, mine, kKCP);
-        double lm[3], dl[3];
-        mbar_wait(sm.bar + slot, (t >> 1) & 1u);  // T(b), W[b+1, b] (landed during the previous step)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          lm[a] = mine ? lamo[3 * lane + a] : 0.0;
-          dl[a] = mine ? add(sm.dpre[slot * kPR + 3 * lane + a], dn[a]) : 0.0;
-          dn[a] = 0.0;
-        }
-        stamp(13);
-        if (s.mu != 0.0)
-          block_solve_v5<true>(Tc, Wc, kPS, ng, lane, dl, dn, lm, kc, s.mu, h2, sm.sv, kPG - 1);
-        else
-          block_solve_v5<false>(Tc, Wc, kPS, ng, lane, dl, dn, lm, kc, s.mu, h2, sm.sv, kPG - 1);
-        __syncwarp();
-        stamp(14);
-        const int err = mine ? block_commit(sm.sv, lane, lm, kc, s.mu, ih2, dsq) : 0;
-        const unsigned bad = __ballot_sync(0xffffffffu, err);
-        if (bad) {
-          const int g = __ffs(bad) - 1;  // first failing group in Gauss-Seidel order
-          if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(rb / 3 + g), 1.0 / kc.ihw);
-          if (lane == 0) sm.flags[0] = 1;
-        }
-        if (t >= 2)  // the publisher has read this slot's previous lambda (step t-2)
-          while (vcnt[1] + 1 < t) {
-          }
-        if (mine)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) lamc[3 * lane + a] = lm[a];
-        __syncwarp();
-        __threadfence_block();
-        if (lane == 0) vcnt[0] = t + 1;  // lambda_b in shared memory: the publisher takes it
-        if (b == nb - 1) {  // end of sweep: ||dlam||^2 and ||lambda||^2 (publisher: blocks 0..nb-2)
-          const double l2 = mine ? (lm[0] * lm[0] + lm[1] * lm[1]) + lm[2] * lm[2] : 0.0;
-          const double sl = warp_sum(l2), sd = warp_sum(dsq);
-          dsq = 0.0;
-          if (lane == 0 && !sm.flags[0]) {
-            while (vcnt[1] < t) {  // the publisher's sum of blocks 0..nb-2 (step t-1) is in red[2]
-            }
-            const double num = sqrt(sd), den = sqrt(sl + sm.red[2]);
-            const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
-            s.eps_hist[sweep] = eps;
-            sm.flags[1] = (eps <= s.tol) ? 1 : ((sweep + 1 >= s.max_iter) ? 2 : 0);
-          }
-        }
-        stamp(2);
-      } else if (warp == 2) {
-        // T(b+1) and Wn = W[b+2, b+1] for the next step, then T(b+1)'s diagonal shift
-        const int ns = slot ^ 1;
-        if (lane == 0) {
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(sm.bar + ns, 2u * kPR * kPS * 8);
-          tma_load_2d(Tn, &tmap, (int)rb1, (int)rb1, sm.bar + ns);
-          tma_load_2d(sm.Wn[ns], &tmap, (int)rb1, (int)rb2, sm.bar + ns);
-        }
-        mbar_wait(sm.bar + ns, ((t + 1) >> 1) & 1u);
-        for (int i = lane; i < rows1; i += 32) Tn[i * kPS + i] = add(Tn[i * kPS + i], dshift[(rb1 + i) / 3]);
-        stamp(10);
-      } else if (warp == 3) {
-        // lambda(b+1) (published in the previous sweep) and the group constants of b+1
-        double* lnx = sm.lamn + (slot ^ 1) * kPR;
-        double* kcx = sm.kcn + (slot ^ 1) * K5;
-        for (int e = lane; e < kKCP * rows1 / 3; e += 32) {
-          const int g = e / kKCP, k = e - g * kKCP;
-          cp_async8(&kcx[e], kconst + kKC * (rb1 / 3 + g) + k, true);
-        }
-        for (int j = lane; j < kPR; j += 32) lnx[j] = j < rows1 ? __ldcg(lamg + rb1 + j) : 0.0;
-        cp_async_wait_all();
-      } else if (xi >= 0) {
-        // dpre(b+1) = delta_base + h^2 ((partials + X2) + W[b+1, b] lambda_b(old)), fixed order;
-        // lanes 3k..3k+2 share row xi + kXW k, a third of the columns each
-        double x2v = 0.0, wov = 0.0;
-        {
-          const int k = lane / 3, part = lane - 3 * k;
-          const int i = xi + kXW * k;
-          if (lane < 3 * kXRows && i < rows1) {
-            const double* wr = s.W + (rb1 + i) * s.ldw + rbm;
-            const int j0 = part * (kPR / 3), j1m = min(j0 + kPR / 3, rowsm), j1 = min(j0 + kPR / 3, rows);
-            double a0 = 0.0, a1 = 0.0;
-            int j = j0;
-            for (; j + 1 < j1m; j += 2) {
-              a0 = fma(__ldg(wr + j), lamp[j], a0);
-              a1 = fma(__ldg(wr + j + 1), lamp[j + 1], a1);
-            }
-            if (j < j1m) a0 = fma(__ldg(wr + j), lamp[j], a0);
-            x2v = a0 + a1;
-            mbar_wait(sm.bar + slot, (t >> 1) & 1u);  // Wn = W[b+1, b]
-            const double* xr = Wc + i * kPS;
-            double c0 = 0.0, c1 = 0.0;
-            for (j = j0; j + 1 < j1; j += 2) {
-              c0 = fma(xr[j], lamo[j], c0);
-              c1 = fma(xr[j + 1], lamo[j + 1], c1);
-            }
-            if (j < j1) c0 = fma(xr[j], lamo[j], c0);
-            wov = c0 + c1;
-          }
-          x2v = (x2v + __shfl_down_sync(0xffffffffu, x2v, 1)) + __shfl_down_sync(0xffffffffu, x2v, 2);
-          wov = (wov + __shfl_down_sync(0xffffffffu, wov, 1)) + __shfl_down_sync(0xffffffffu, wov, 2);
-        }
-        if (xi == 0) stamp(6);
-        // partials of block b+1 (helpers, step t-1), fixed order; lane k <-> row xi + kXW k
-        const double* part = partial + 2 * (size_t)((t + kPartBufs - 1) % kPartBufs) * pstride;
-        double pvl = 0.0;
-        {
-          const int i = xi + kXW * lane;
-          if (t > 0 && lane < kXRows && i < rows1) {
-            const int nseg = ((i + 1) * nch - 1) / kHelpWarps - (i * nch) / kHelpWarps + 1;
-            for (int sg = 0; sg < nseg; ++sg) pvl += ll_load(part + 2 * ((size_t)i * kSeg + sg), tag0 + t - 1, ctl);
-          }
-        }
-        const double pk = __shfl_sync(0xffffffffu, pvl, lane / 3);  // lane 3k picks up row k's sum
-        {
-          const int k = lane / 3, i = xi + kXW * k;
-          if (lane == 3 * k && k < kXRows && i < rows1)
-            sm.dpre[(slot ^ 1) * kPR + i] = add(s.delta_base[rb1 + i], mul(h2, (pk + x2v) + wov));
-        }
-        if (xi == 0) stamp(7);
-      }
-      asm volatile("bar.sync 5, %0;" ::"n"(kPipeThreads - 32) : "memory");  // end of step (all but the publisher)
-      if (warp == 0 || warp == 5) stamp(0); else stamp(-1);
-      if (b == nb - 1) {
-        iterations = sweep + 1;
-        converged = sm.flags[1] == 1;
-      }
-      if (sm.flags[0] || sm.flags[1]) {
-        if (tid == 0) sm.flags[2] = 1;  // the publisher stops after this step
-        break;
-      }
-    }
-    } else {
-      // ---- warp 1: publisher (see the v4 path) ----
-      double sumsq = 0.0;
-      for (unsigned t = 0;; ++t) {
-        if (lane == 0) {
-          while (vcnt[0] < t + 1 && !*(volatile int*)&sm.flags[2]) __nanosleep(20);
-          if (*(volatile unsigned*)&ctl->timeout) sm.flags[0] = 1;  // watchdog fired elsewhere
-        }
-        const unsigned go = __shfl_sync(0xffffffffu, vcnt[0] >= t + 1 ? 1u : 0u, 0);
-        if (!go) break;
-        __threadfence_block();
-        const int b = (int)(t % nb), rows = rows_of(b);
-        const int64_t rb = 3 * (int64_t)b * kPG;
-        const double* lamc = sm.lamx + (t & 1) * kPR;
-        double v = 0.0;
-        for (int j = lane; j < rows; j += 32) {
-          const double l = lamc[j];
-          __stcg(lamg + rb + j, l);
-          v = fma(l, l, v);
-        }
-        __syncwarp();
-        if (lane == 0) st_release_gpu(psolved, t + 1);
-        if (b == 0) sumsq = 0.0;
-        if (b < nb - 1) sumsq += warp_sum(v);
-        if (b == nb - 2 && lane == 0) sm.red[2] = sumsq;
-        __syncwarp();
-        __threadfence_block();
-        if (lane == 0) vcnt[1] = t + 1;
-      }
-    }
-    // everyone (publisher included): last lambda block is in global memory; release the grid
-    __syncthreads();
-    if (tid == 0) {
-      st_release_gpu(pstop, 1u);
-      s.iters_conv[0] = iterations;
-      s.iters_conv[1] = converged ? 1 : 0;
-    }
-  } else if (blockIdx.x == 0) {
+  if (blockIdx.x == 0) {
     PipeSmem sm = pipe_carve(smem_raw);
     const int xi = x2_index(warp);
     if (tid == 0) {
@@ -2631,167 +1742,6 @@ __global__ void __launch_bounds__(kCopyThreads, 2) pgs_copy_kernel(const PgsScen
       if (pf[k]) atomicAdd(prof + 8 + k, pf[k]);
 }
 
-template <int V>
-__global__ void __launch_bounds__(32) bench_block_solve_kernel(int reps, double* out) {
-  extern __shared__ __align__(16) char bsm[];
-  double* T = (double*)bsm;
-  const int lane = threadIdx.x;
-  for (int i = 0; i < kBR; ++i)
-    for (int j = lane; j < kBR; j += 32) {
-      const double v = (i == j) ? 4.0 : 0.05 * sin(0.37 * i + 0.91 * j + 0.13 * i * j) / (1.0 + fabs(i - j));
-      T[i * kLDT + j] = v;
-    }
-  __syncwarp();
-  for (int i = 0; i < kBR; ++i)  // symmetrise
-    for (int j = lane; j < i; j += 32) T[j * kLDT + i] = T[i * kLDT + j];
-  __syncwarp();
-  const double h2 = 1e-4;
-  double Wd[9];
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) Wd[3 * a + b] = T[(3 * lane + a) * kLDT + 3 * lane + b];
-  GroupConst kc;
-  group_const(Wd, h2, kc);
-  if (V & 1) {
-    for (int i = 0; i < kBR; ++i)
-      for (int j = lane; j < kBR; j += 32) T[i * kLDT + j] *= h2;
-    __syncwarp();
-  }
-  double dl_[3], lm[3] = {0.0, 0.0, 0.0}, dsq = 0.0;
-  int err = 0;
-  long long t0 = clock64();
-  for (int r = 0; r < reps; ++r) {
-    dl_[0] = -1e-4 * (1.0 + 0.01 * lane);
-    dl_[1] = ((V & 4) ? 3e-4 : 3e-5) * sin(1.0 * lane);  // V bit 2: tangential loads outside the cone
-    dl_[2] = ((V & 4) ? 3e-4 : 3e-5) * cos(1.0 * lane);
-    if (V & 128) {
-      double dn[3] = {0.0, 0.0, 0.0};
-      block_solve_v5<true>(T, T + 3, kPR, kPG, lane, dl_, dn, lm, kc, 0.4, h2, T + kBR * kLDT, kPG - 1);
-      __syncwarp();
-      err |= block_commit(T + kBR * kLDT, lane, lm, kc, 0.4, 1.0 / h2, dsq);
-      dsq += dn[0] + dn[1] + dn[2];
-    } else if (V & 64) {
-      block_solve_v4<true>(T, kPR, kPG, lane, dl_, lm, kc, 0.4, h2, T + kBR * kLDT);
-      __syncwarp();
-      err |= block_commit(T + kBR * kLDT, lane, lm, kc, 0.4, 1.0 / h2, dsq);
-    } else if (V & 32) {
-      block_solve_v4<true>(T, kLDT, kBG, lane, dl_, lm, kc, 0.4, h2, T + kBR * kLDT);
-      __syncwarp();
-      err |= block_commit(T + kBR * kLDT, lane, lm, kc, 0.4, 1.0 / h2, dsq);
-    } else if (V & 16)
-      block_solve_v3(T, kLDT, kBG, lane, dl_, lm, kc, 0.4, h2, dsq, err);
-    else if (V & 8)
-      block_solve_v2(T, kLDT, kBG, lane, dl_, lm, kc, 0.4, h2, dsq, err);
-    else
-      block_solve<false, (V & 3)>(T, kBG, lane, dl_, lm, kc, 0.4, h2, dsq, err);
-  }
-  long long t1 = clock64();
-  const double s = warp_sum(lm[0] + lm[1] + lm[2] + dsq);
-  if (lane == 0) {
-    out[0] = (double)(t1 - t0) / ((double)reps * ((V & 192) ? kPG : kBG));
-    out[1] = s;
-  }
-}
-
-// Contention experiment (diagnostic): warp 0 runs block_solve_v4 on a
-// 26-group tile (stride 78) while the other warps (except 4, 8, 12, as in
-// pgs_pipe_kernel) generate one kind of load: 0 idle, 1 shared-memory loads,
-// 2 shuffles, 3 global polling loads, 4 bulk copies into shared memory,
-// 5 fp64 FMA chains.  out[0] = solver cycles per group.
-template <int MODE>
-__global__ void __launch_bounds__(512) bench_contention_kernel(int reps, const double* gsrc, double* out) {
-  extern __shared__ __align__(128) double csm[];
-  double* T = csm;                     // 78 x 78 tile
-  double* sv = csm + kPR * kPR;        // 4 * 26 records
-  double* buf = sv + 4 * kPG;          // noise buffer (48 KB)
-  unsigned long long* bar = (unsigned long long*)(buf + 6144);
-  volatile int* done = (volatile int*)(bar + 1);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int e = tid; e < kPR * kPR; e += blockDim.x) {
-    const int i = e / kPR, j = e % kPR;
-    T[e] = (i == j) ? 4.0 : 0.05 * sin(0.37 * i + 0.91 * j + 0.13 * i * j) / (1.0 + fabs((double)(i - j)));
-  }
-  for (int e = tid; e < 6144; e += blockDim.x) buf[e] = 1.0 + 1e-3 * e;
-  if (tid == 0) {
-    *done = 0;
-    mbar_init(bar, 1);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const double h2 = 1e-4;
-    double Wd[9];
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) Wd[3 * a + b] = T[(3 * lane + a) * kPR + 3 * lane + b];
-    GroupConst kc;
-    group_const(Wd, h2, kc);
-    double lm[3] = {0.0, 0.0, 0.0}, dl_[3], dsq = 0.0;
-    int err = 0;
-    const long long t0 = clock64();
-    for (int r = 0; r < reps; ++r) {
-      dl_[0] = -1e-4 * (1.0 + 0.01 * lane);
-      dl_[1] = 3e-4 * sin(1.0 * lane);
-      dl_[2] = 3e-4 * cos(1.0 * lane);
-      block_solve_v4<true>(T, kPR, kPG, lane, dl_, lm, kc, 0.4, h2, sv);
-      __syncwarp();
-      err |= block_commit(sv, lane, lm, kc, 0.4, 1.0 / h2, dsq);
-    }
-    const long long t1 = clock64();
-    const double sres = warp_sum(lm[0] + lm[1] + lm[2] + dsq);
-    if (lane == 0) {
-      out[0] = (double)(t1 - t0) / ((double)reps * kPG);
-      out[1] = sres + err;
-      *done = 1;
-    }
-  } else if ((warp & 3) != 0) {
-    double acc = 0.0;
-    unsigned phase = 0;
-    while (!*done) {
-      if (MODE == 1) {
-        for (int k = 0; k < 64; ++k) acc += T[((warp * 7 + k) % kPR) * kPR + lane + (k & 1) * 32];
-      } else if (MODE == 2) {
-        for (int k = 0; k < 16; ++k) acc = warp_sum(acc + k);
-      } else if (MODE == 3) {
-        unsigned v;
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gsrc) : "memory");
-        acc += v;
-        __nanosleep(64);
-      } else if (MODE == 4) {
-        if (warp == 2 && lane == 0) {
-          mbar_arrive_expect_tx(bar, 3 * 16384);
-          for (int q = 0; q < 3; ++q) bulk_g2s(buf + q * 2048, gsrc + q * 2048, 16384, bar);
-          while (!mbar_try_wait(bar, phase)) {
-          }
-          phase ^= 1;
-        }
-      } else if (MODE == 5) {
-        for (int k = 0; k < 64; ++k) acc = fma(acc, 0.999999, 1e-9);
-      } else {
-        __nanosleep(200);
-      }
-    }
-    if (acc == 12345.678) out[1] = acc;
-  }
-}
-
-static int launch_contention(int mode, int reps, const double* g, double* d, cudaStream_t st) {
-  const int sm = (int)(sizeof(double) * (kPR * kPR + 4 * kPG + 6144) + 64);
-#define CNB_CONT(M)                                                                                      \
-  CNB_CUDA(cudaFuncSetAttribute(bench_contention_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
-  bench_contention_kernel<M><<<1, 512, sm, st>>>(reps, g, d);
-  switch (mode) {
-    case 0: CNB_CONT(0) break;
-    case 1: CNB_CONT(1) break;
-    case 2: CNB_CONT(2) break;
-    case 3: CNB_CONT(3) break;
-    case 4: CNB_CONT(4) break;
-    default: CNB_CONT(5) break;
-  }
-#undef CNB_CONT
-  CNB_LAUNCH_CHECK("bench_contention_kernel");
-  return CNB_OK;
-}
-
-// CNB_PGS_PROFILE=1: per-phase nanosecond sums of the grid kernel (device
-// buffer, read back with cnb_pgs_profile)
 static unsigned long long* pgs_profile_buffer() {
   static unsigned long long* buf = nullptr;
   static int on = -1;
@@ -2806,43 +1756,36 @@ static unsigned long long* pgs_profile_buffer() {
   return buf;
 }
 
-// CNB_PGS_KERNEL=grid selects the one-step-lookahead kernel (pgs_grid_kernel);
-// the default is the pipelined lookahead-2 kernel (pgs_pipe_kernel), which
-// needs at least four blocks.
-static bool use_pipe_kernel(const PgsScene& s) {
-  const char* e = getenv("CNB_PGS_KERNEL");
-  if (e && e[0] == 'g') return false;
-  // 16-byte row pairs (helpers) and TMA rows need an even pitch and an aligned base
-  return (s.groups + kPG - 1) / kPG >= 4 && (s.ldw & 1) == 0 && ((uintptr_t)s.W & 15) == 0;
-}
-
-static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
+// Grid-scale PGS: the pipelined lookahead-2 kernel (pgs_pipe_kernel), one CTA
+// per SM.  Its tiles move by tensor TMA and 16-byte row pairs, so W must have a
+// 16-byte aligned base and an even row pitch; other layouts are first copied
+// into an aligned scratch matrix (the Python layer always allocates aligned W).
+static int launch_pgs_grid(PgsScene s, cudaStream_t st) {
   int dev = 0, sms = 0;
   CNB_CUDA(cudaGetDevice(&dev));
   CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const bool pipe = use_pipe_kernel(s);
-  // tensor TMA needs a 16-byte aligned base and row pitch (even ldw)
-  int tma = (((uintptr_t)s.W & 15) == 0 && (s.ldw & 1) == 0) ? 1 : 0;
+  if ((s.ldw & 1) || ((uintptr_t)s.W & 15)) {
+    static GrowBuf aligned;
+    const int64_t c = 3 * s.groups, ld = c + (c & 1);
+    int rc = aligned.ensure((size_t)c * ld * sizeof(double));
+    if (rc) return rc;
+    CNB_CUDA(cudaMemcpy2DAsync(aligned.p, ld * sizeof(double), s.W, s.ldw * sizeof(double), c * sizeof(double), c,
+                               cudaMemcpyDeviceToDevice, st));
+    s.W = (const double*)aligned.p;
+    s.ldw = ld;
+  }
+  int tma = 1;
   int dbg = 0;
-  bool want_v5 = false;
   {
     const char* e = getenv("CNB_PGS_TMA");
-    if (e && e[0] == '0') tma = 0;
+    if (e && e[0] == '0') tma = 0;  // cp.async staging of the tiles instead of tensor TMA
     const char* d = getenv("CNB_PGS_DEBUG");
     if (d) dbg = atoi(d) & ~1;
-    // CNB_PGS_PIPE=v5: experimental solver CTA with the next-block update folded into
-    // the block solve (no delta phase).  Measured slower at cfg3 (8.3 vs 5.3 us per
-    // block step): the overlapped tile fetches and X2 loads contend with the solve
-    // and the next tiles land late, so the default stays the v4 solver CTA.
-    const char* v = getenv("CNB_PGS_PIPE");
-    want_v5 = v && !strcmp(v, "v5");
   }
-  const bool v5 = pipe && tma && !dbg && want_v5;
-  const void* kfn = pipe ? (v5 ? (const void*)pgs_pipe_kernel<true> : (const void*)pgs_pipe_kernel<false>)
-                         : (const void*)pgs_grid_kernel;
-  const int nthreads = pipe ? kPipeThreads : kGridThreads;
-  const size_t tiles = pipe ? (v5 ? pipe5_smem_bytes() : pipe_smem_bytes()) : grid_smem_bytes();
-  const size_t lam_bytes = sizeof(double) * (size_t)(3 * s.groups) + (pipe ? 128 : 0);  // + alignment slack
+  const void* kfn = (const void*)pgs_pipe_kernel;
+  const int nthreads = kPipeThreads;
+  const size_t tiles = pipe_smem_bytes();
+  const size_t lam_bytes = sizeof(double) * (size_t)(3 * s.groups) + 128;  // + alignment slack
   const int lam_in_smem = lam_bytes <= pgs_max_smem() ? 1 : 0;
   const size_t smem = std::max(tiles, lam_in_smem ? lam_bytes : (size_t)0);
   if (smem > pgs_max_smem()) {
@@ -2861,8 +1804,7 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   // one (row, column-slice) item per helper warp; the partials of a block are
   // staged in a kBR x kLDT tile by the solver
   // pipe: a row spans at most kSeg helper CTAs, so nch <= (kSeg - 1) * kHelpWarps
-  const int nch = std::max(1, std::min(((grid - 1) * nwarps) / (pipe ? kPR : kBR),
-                                       pipe ? (kSeg - 1) * kHelpWarps : kLDT));
+  const int nch = std::max(1, std::min(((grid - 1) * nwarps) / kPR, (kSeg - 1) * kHelpWarps));
   const size_t bytes =
       64 + sizeof(double) * ((size_t)s.groups * (1 + kKC) + 1 + kPartBufs * (size_t)kBR * std::max(nch, kSeg));
   static void* ws_p = nullptr;
@@ -2895,7 +1837,7 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   unsigned long long* prof = pgs_profile_buffer();
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
-  if (pipe && tma) {
+  if (tma) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
       cudaDriverEntryPointQueryResult q;
@@ -2913,8 +1855,6 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       tma = 0;  // fall back to cp.async staging
   }
-  void* args_grid[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
-                       (void*)&nchv, (void*)&lis, (void*)&prof};
   int tma_arg = tma | dbg;
   // record tags: unique across launches (a record left by an earlier call never matches)
   static unsigned tag_base = 1;
@@ -2924,8 +1864,8 @@ static int launch_pgs_grid(const PgsScene& s, cudaStream_t st) {
   tag_base += (unsigned)steps;
   void* args_pipe[] = {(void*)&sc, (void*)&dshift, (void*)&kconst, (void*)&partial, (void*)&ctl,
                        (void*)&nchv, (void*)&lis, (void*)&tma_arg, (void*)&prof, (void*)&tag0, (void*)&tmap};
-  CNB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthreads), pipe ? args_pipe : args_grid, smem, st));
-  CNB_LAUNCH_CHECK(pipe ? (v5 ? "pgs_pipe_kernel<v5>" : "pgs_pipe_kernel") : "pgs_grid_kernel");
+  CNB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthreads), args_pipe, smem, st));
+  CNB_LAUNCH_CHECK("pgs_pipe_kernel");
   return CNB_OK;
 }
 
@@ -2942,67 +1882,6 @@ static int pgs_grid_override() {
 using namespace cnb;
 
 extern "C" {
-
-int64_t cnb_pgs_work_bytes(int64_t groups) { (void)groups; return 0; }
-
-// Cycles per group of the warp block solve (diagnostic): variant v of block_solve on a
-// resident synthetic tile, reps repetitions.  out[0] = cycles / group.
-int cnb_bench_block_solve(int32_t variant, int32_t reps, double* out, void* stream) {
-  double* d = nullptr;
-  CNB_CUDA(cudaMalloc(&d, 2 * sizeof(double)));
-  cudaStream_t st = (cudaStream_t)stream;
-  const int sm = (int)(sizeof(double) * (kBR * kLDT + 4 * kBG));
-#define CNB_BBS(V)                                                                                  \
-  CNB_CUDA(cudaFuncSetAttribute(bench_block_solve_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
-  bench_block_solve_kernel<V><<<1, 32, sm, st>>>(reps, d);
-  switch (variant) {
-    case 0: CNB_BBS(0) break;
-    case 1: CNB_BBS(1) break;
-    case 2: CNB_BBS(2) break;
-    case 3: CNB_BBS(3) break;
-    case 4: CNB_BBS(4) break;
-    case 5: CNB_BBS(5) break;
-    case 6: CNB_BBS(6) break;
-    case 7: CNB_BBS(7) break;
-    case 8: CNB_BBS(8) break;
-    case 9: CNB_BBS(12) break;
-    case 10: CNB_BBS(16) break;
-    case 11: CNB_BBS(20) break;
-    case 12: CNB_BBS(32) break;
-    case 13: CNB_BBS(36) break;
-    case 14: CNB_BBS(132) break;
-    default: CNB_BBS(100) break;
-  }
-#undef CNB_BBS
-  CNB_LAUNCH_CHECK("bench_block_solve_kernel");
-  double h[2];
-  CNB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
-  CNB_CUDA(cudaStreamSynchronize(st));
-  cudaFree(d);
-  out[0] = h[0];
-  out[1] = h[1];
-  return CNB_OK;
-}
-
-// Solver-warp cycles per group under one kind of concurrent load in the same
-// CTA (diagnostic, see bench_contention_kernel).  out[0] = cycles / group.
-int cnb_bench_contention(int32_t mode, int32_t reps, double* out, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  double *d = nullptr, *g = nullptr;
-  CNB_CUDA(cudaMalloc(&d, 2 * sizeof(double)));
-  CNB_CUDA(cudaMalloc(&g, 8192 * sizeof(double)));
-  CNB_CUDA(cudaMemsetAsync(g, 0, 8192 * sizeof(double), st));
-  int rc = launch_contention(mode, reps, g, d, st);
-  if (rc) return rc;
-  double h[2];
-  CNB_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
-  CNB_CUDA(cudaStreamSynchronize(st));
-  cudaFree(d);
-  cudaFree(g);
-  out[0] = h[0];
-  out[1] = h[1];
-  return CNB_OK;
-}
 
 // Phase sums (ns) of the grid PGS kernel since the last call (CNB_PGS_PROFILE=1):
 // out[0] solver wait, [1] delta, [2] solves, [3] epilogue, [4] helper wait,
@@ -3023,8 +1902,7 @@ int cnb_pgs_profile(double* out) {
 
 int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_base, double h, double mu,
             double tol, int32_t max_iter, double* lam, double* delta_end, double* eps_hist,
-            int32_t* iters_conv, void* work, cnb_status_t* d_status, void* stream) {
-  (void)work;
+            int32_t* iters_conv, cnb_status_t* d_status, void* stream) {
   if (groups < 0 || max_iter < 1) {
     set_error("pgs: invalid arguments (groups=%lld, max_iter=%d)", (long long)groups, max_iter);
     return CNB_E_VALIDATION;
@@ -3048,7 +1926,8 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
   // large scenes: the grid-scale kernel (helpers on every SM); small ones stay
   // on one CTA with lambda in shared memory
   const int ov = pgs_grid_override();
-  const bool grid = smem > pgs_max_smem() || (ov < 0 ? groups > 512 : ov == 1);
+  // the pipelined kernel needs at least four blocks of kPG groups
+  const bool grid = groups >= 4 * kPG && (smem > pgs_max_smem() || (ov < 0 ? groups > 512 : ov == 1));
   if (grid) return launch_pgs_grid(s, (cudaStream_t)stream);
   CNB_CUDA(cudaFuncSetAttribute(pgs_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   pgs_single_kernel<<<1, kPgsThreads, smem, (cudaStream_t)stream>>>(s);

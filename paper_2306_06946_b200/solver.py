@@ -168,7 +168,7 @@ def pgs_device(W: torch.Tensor, delta_base: torch.Tensor, h: float, config: PgsC
     st = _lib.status(dev)
     _lib.call("cnb_pgs", c // 3, W.data_ptr(), dv.ld(W), delta_base.data_ptr(), float(h), float(config.friction),
               float(config.tolerance), int(config.max_iterations), ws.lam.data_ptr(), ws.delta_end.data_ptr(),
-              ws.eps.data_ptr(), ws.ic.data_ptr(), None, st.ptr, _lib.stream())
+              ws.eps.data_ptr(), ws.ic.data_ptr(), st.ptr, _lib.stream())
     return PgsResult(ws.lam, ws.delta_end, ws.eps, ws.ic, st)
 
 

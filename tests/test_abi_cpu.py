@@ -8,13 +8,19 @@ import re
 
 from paper_2306_06946_b200 import _lib
 
-HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "cn_b200.h")
+INCLUDE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+HEADER = os.path.join(INCLUDE, "cn_b200.h")
 
 
 def declared_symbols():
-    text = open(HEADER).read()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(cnb_[a-z0-9_]+)\s*\(", text)))
+    """Every cnb_* function declared by include/*.h (the boundary cn_b200.h and the
+    diagnostics header cn_b200_diag.h)."""
+    names = set()
+    for f in sorted(os.listdir(INCLUDE)):
+        if f.endswith(".h"):
+            text = re.sub(r"/\*.*?\*/", "", open(os.path.join(INCLUDE, f)).read(), flags=re.S)
+            names.update(re.findall(r"\b(cnb_[a-z0-9_]+)\s*\(", text))
+    return sorted(names)
 
 
 def test_library_exports_every_declared_symbol():
@@ -41,8 +47,8 @@ def test_status_codes_map_to_reference_exceptions():
 
 
 def test_host_only_entry_points_run_without_gpu():
-    assert _lib.lib().cnb_abi_version() == 1
+    assert _lib.lib().cnb_abi_version() == 2
     assert isinstance(_lib.lib().cnb_launch_count(), int)
     # argument validation happens before any device work
-    rc = _lib.lib().cnb_pgs(4, None, 12, None, 0.01, 0.5, 1e-6, 0, None, None, None, None, None, None, None)
+    rc = _lib.lib().cnb_pgs(4, None, 12, None, 0.01, 0.5, 1e-6, 0, None, None, None, None, None, None)
     assert rc == 6  # CNB_E_VALIDATION: max_iter < 1
