@@ -593,16 +593,17 @@ def run_gpu_cfg3(args, rank, world):
     groups = [r.c_groups for r in reps]
     sweeps = [r.pgs_iterations_total for r in reps]
     pgs_s = sum(r.t_pgs for r in reps)
-    passes = sum(s + r.newton_iterations for s, r in zip(sweeps, reps))
+    # one pass over W per sweep; delta_end needs none (formed from the proximity update)
+    passes = sum(sweeps)
     bytes_pass = [8.0 * (3 * g) ** 2 for g in groups]
-    alg = sum(b * (s + r.newton_iterations) for b, s, r in zip(bytes_pass, sweeps, reps))
+    alg = sum(b * s for b, s in zip(bytes_pass, sweeps))
     ach = alg / pgs_s / 1e9
     roof = {"kernel": "pgs_pipe_kernel (exact-order projected Gauss-Seidel, dense W, lookahead-2 pipeline)",
             "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": pgs_ncu_traffic_per_sweep(),
             "traffic_unit": "bytes per W pass (ncu --set full dram read+write)", "peak_source": src,
             "algorithmic_bytes_per_pass": bytes_pass[-1],
-            "passes": "every sweep plus the delta_end pass of every Newton iteration",
+            "passes": "one W pass per sweep (delta_end is formed from the proximity update, no pass)",
             "passes_per_step_mean": round(passes / len(reps), 2),
             "ms_per_pass": round(pgs_s * 1e3 / max(passes, 1), 4)}
     dmma = dmma_peak_tflops(torch, _lib)

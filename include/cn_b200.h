@@ -198,13 +198,16 @@ int cnb_detect_vertex_mesh(int64_t nv, const int64_t* vids, const double* pts_a,
 /* PGS with Signorini + isotropic Coulomb disk in the reference's canonical
  * group order.  Replaces pgs solver.py:168-202, local_solve 124-165 and
  * regularize 99-121.
- *   lam (c), delta_end (c): outputs; eps_hist (max_iter): per-sweep epsilon;
- *   iters_conv (2 int32): sweeps performed, converged flag.
+ *   lam (c): output; delta_end (c, may be NULL): delta_base + h^2 W_reg lam
+ *   (solver.py:201; NULL skips that extra pass over W); eps_hist (max_iter):
+ *   per-sweep epsilon; iters_conv (2 int32): sweeps performed, converged flag;
+ *   shift_out (groups, may be NULL): the regularisation shift added to each
+ *   group's diagonal block (0 where none).
  * Singular blocks set d_status to CNB_E_SINGULAR_BLOCK (index = group). */
 int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_base,
             double h, double mu, double tol, int32_t max_iter, double* lam,
-            double* delta_end, double* eps_hist, int32_t* iters_conv, cnb_status_t* d_status,
-            void* stream);
+            double* delta_end, double* eps_hist, int32_t* iters_conv, double* shift_out,
+            cnb_status_t* d_status, void* stream);
 
 /* One group's local solve (solver.py:124-165) as a device call, for API
  * parity with local_solve; out (3). */

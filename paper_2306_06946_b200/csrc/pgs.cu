@@ -50,6 +50,7 @@ struct PgsScene {
   double* eps_hist;
   int* iters_conv;
   DevStatus* status;
+  double* shift_out;  // per-group regularisation shift (may be null)
 };
 
 // eigenvalues of a symmetric 3x3 by cyclic Jacobi (converges to rounding)
@@ -337,6 +338,7 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
     double mn = fmin(e[0], fmin(e[1], e[2]));
     double scale = fmax(fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2]))), 1e-300);
     sm.dshift[g] = (mn <= 1e-12 * scale) ? shift : 0.0;
+    if (s.shift_out) s.shift_out[g] = sm.dshift[g];
   }
   for (int64_t i = tid; i < c; i += blockDim.x) sm.lam[i] = 0.0;
   __syncthreads();
@@ -465,8 +467,8 @@ __device__ void pgs_cta(const PgsScene& s, PgsSmem sm) {
     if (sm.flags[0] || converged) break;
   }
   __syncthreads();
-  // ---- delta_end = delta_base + h^2 W_reg lam (solver.py:201) ----
-  for (int64_t r = warp; r < c; r += nwarps) {
+  // ---- delta_end = delta_base + h^2 W_reg lam (solver.py:201); skipped when not wanted ----
+  for (int64_t r = warp; s.delta_end && r < c; r += nwarps) {
     const double* wr = s.W + r * s.ldw;
     double acc = lane_dot<false>(wr, sm.lam, 0, c, lane);
     acc = warp_sum(acc);
@@ -1395,7 +1397,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
   if (tid == 0) wait_acq(pstop, 1u, nullptr, ctl);
   __syncthreads();
   const unsigned gw = blockIdx.x * (kPipeThreads / 32) + warp, ngw = gridDim.x * (kPipeThreads / 32);
-  for (int64_t r = gw; r < c; r += ngw) {
+  for (int64_t r = gw; s.delta_end && r < c; r += ngw) {
     const double* wr = s.W + r * s.ldw;
     double acc = lane_dot<true>(wr, lamg, 0, c, lane);
     acc = warp_sum(acc);
@@ -1866,6 +1868,8 @@ static int launch_pgs_grid(PgsScene s, cudaStream_t st) {
                        (void*)&nchv, (void*)&lis, (void*)&tma_arg, (void*)&prof, (void*)&tag0, (void*)&tmap};
   CNB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(nthreads), args_pipe, smem, st));
   CNB_LAUNCH_CHECK("pgs_pipe_kernel");
+  if (s.shift_out)
+    CNB_CUDA(cudaMemcpyAsync(s.shift_out, dshift, s.groups * sizeof(double), cudaMemcpyDeviceToDevice, st));
   return CNB_OK;
 }
 
@@ -1902,7 +1906,7 @@ int cnb_pgs_profile(double* out) {
 
 int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_base, double h, double mu,
             double tol, int32_t max_iter, double* lam, double* delta_end, double* eps_hist,
-            int32_t* iters_conv, cnb_status_t* d_status, void* stream) {
+            int32_t* iters_conv, double* shift_out, cnb_status_t* d_status, void* stream) {
   if (groups < 0 || max_iter < 1) {
     set_error("pgs: invalid arguments (groups=%lld, max_iter=%d)", (long long)groups, max_iter);
     return CNB_E_VALIDATION;
@@ -1922,6 +1926,7 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
   s.eps_hist = eps_hist;
   s.iters_conv = iters_conv;
   s.status = (DevStatus*)d_status;
+  s.shift_out = shift_out;
   const size_t smem = pgs_smem_bytes(groups);
   // large scenes: the grid-scale kernel (helpers on every SM); small ones stay
   // on one CTA with lambda in shared memory
@@ -1985,6 +1990,7 @@ int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off,
     sc.eps_hist = eps_hist + (int64_t)i * max_iter;
     sc.iters_conv = iters_conv + 2 * i;
     sc.status = (DevStatus*)d_status;
+    sc.shift_out = nullptr;
   }
   // per-copy pipelined kernel unless CNB_PGS_BATCHED=cta asks for the plain single-CTA iterate
   static const bool plain = [] {

@@ -153,11 +153,14 @@ class PgsWorkspace:
         self.delta_end = dv.empty(c)
         self.eps = dv.empty(max(1, max_iter))
         self.ic = dv.zeros(2, dtype=torch.int32)
+        self.shift = dv.empty(max(1, c // 3))
 
 
 def pgs_device(W: torch.Tensor, delta_base: torch.Tensor, h: float, config: PgsConfig,
-               ws: PgsWorkspace | None = None) -> PgsResult:
-    """Asynchronous PGS: launches and returns device results (no host sync)."""
+               ws: PgsWorkspace | None = None, delta_end: bool = True) -> PgsResult:
+    """Asynchronous PGS: launches and returns device results (no host sync).
+    ``delta_end=False`` skips the final pass over W (the caller forms delta_end
+    another way) and records the regularisation shifts in ``ws.shift``."""
     c = int(delta_base.shape[0])
     dev = delta_base.device
     if c == 0:
@@ -167,8 +170,9 @@ def pgs_device(W: torch.Tensor, delta_base: torch.Tensor, h: float, config: PgsC
     ws = ws or PgsWorkspace(c, config.max_iterations)
     st = _lib.status(dev)
     _lib.call("cnb_pgs", c // 3, W.data_ptr(), dv.ld(W), delta_base.data_ptr(), float(h), float(config.friction),
-              float(config.tolerance), int(config.max_iterations), ws.lam.data_ptr(), ws.delta_end.data_ptr(),
-              ws.eps.data_ptr(), ws.ic.data_ptr(), st.ptr, _lib.stream())
+              float(config.tolerance), int(config.max_iterations), ws.lam.data_ptr(),
+              ws.delta_end.data_ptr() if delta_end else None, ws.eps.data_ptr(), ws.ic.data_ptr(),
+              None if delta_end else ws.shift.data_ptr(), st.ptr, _lib.stream())
     return PgsResult(ws.lam, ws.delta_end, ws.eps, ws.ic, st)
 
 
@@ -288,10 +292,15 @@ def newton_fast(ctx: StepContext, ncfg: NewtonConfig, pcfg: PgsConfig) -> Correc
         compute_violation(Dm, p_a, p_b, out=delta)
         # every iteration keeps its own lambda (lam_history holds references)
         ws_k = ws if k == 0 else PgsWorkspace(c, pcfg.max_iterations)
-        res = pgs_device(W, delta, ctx.h, pcfg, ws_k)
+        res = pgs_device(W, delta, ctx.h, pcfg, ws_k, delta_end=False)
         e2 = timer.mark()
         _lib.call("cnb_apply_dt", m, D.data_ptr(), res.lam.data_ptr(), t.data_ptr(), acc.data_ptr(), _lib.stream())
         prox_update_inplace(p_a, p_b, ctx.wg, t, ctx.h)
+        # delta_end = delta_base + h^2 W_reg lam (solver.py:201) without a pass over W:
+        # the proximity update moved p_a - p_b by h^2 W_g D^T lam, so D (p_a - p_b)
+        # is delta_base + h^2 W lam; the regularisation adds h^2 shift_g lam_g
+        compute_violation(Dm, p_a, p_b, out=ws_k.delta_end)
+        ws_k.delta_end.view(-1, 3).addcmul_(ws_k.shift[:m, None], res.lam.view(-1, 3), value=ctx.h * ctx.h)
         e3 = timer.mark()
         pen = _penetration_device(res.delta_end)
         lam_history.append(res.lam)

@@ -50,5 +50,5 @@ def test_host_only_entry_points_run_without_gpu():
     assert _lib.lib().cnb_abi_version() == 2
     assert isinstance(_lib.lib().cnb_launch_count(), int)
     # argument validation happens before any device work
-    rc = _lib.lib().cnb_pgs(4, None, 12, None, 0.01, 0.5, 1e-6, 0, None, None, None, None, None, None)
+    rc = _lib.lib().cnb_pgs(4, None, 12, None, 0.01, 0.5, 1e-6, 0, None, None, None, None, None, None, None)
     assert rc == 6  # CNB_E_VALIDATION: max_iter < 1
