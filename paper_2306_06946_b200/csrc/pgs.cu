@@ -571,8 +571,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // spin until *p >= target (or stop / watchdog); returns false on timeout
 // Regularisation shift (solver.py:99-121) and the per-group constants of the
 // regularised diagonal blocks, once per PGS call; lambda <- 0.
-constexpr int kKC = 10;  // doubles per packed GroupConst
-constexpr int kKCP = 8;  // leading doubles of the record the pipelined kernel stages
+constexpr int kKC = 11;  // doubles per packed GroupConst
+constexpr int kKCP = 9;  // leading doubles of the record the pipelined kernel stages
 // Regularisation (solver.py:99-121) and the per-group constants of the grid
 // kernels, grid-wide in two passes (a single CTA is latency-bound on the strided
 // diagonal loads): pass 1, one thread per group,
@@ -644,8 +644,9 @@ __global__ void __launch_bounds__(kPrepThreads) pgs_prep2_kernel(PgsScene s, dou
     o[5] = kc.b0;
     o[6] = kc.b1;
     o[7] = (double)kc.bad;
-    o[8] = kc.htn0;
-    o[9] = kc.htn1;
+    o[8] = kc.hwnn;
+    o[9] = kc.htn0;
+    o[10] = kc.htn1;
     for (int a = 0; a < 3; ++a) s.lam[3 * g + a] = 0.0;
   }
 }
@@ -669,13 +670,13 @@ __device__ __forceinline__ int x2_index(int warp) {  // warps 5,6,7,9,10,11,13,1
 }
 
 struct PipeSmem {
-  double *T0, *T1, *Wx, *X, *dcur, *lamx, *lamn, *kcn, *sv, *dbs, *dsh, *red;
-  unsigned long long* bar;  // [0] T + Wx, [1] X
+  double *T0, *T1, *Wt, *X, *dcur, *lamx, *lamn, *kcn, *sv, *dbs, *dsh, *red;
+  unsigned long long* bar;  // [0] T + Wt, [1] X
   int* flags;
 };
 
 __host__ __device__ inline size_t pipe_smem_bytes() {
-  return 128 + sizeof(double) * (size_t)(4 * kTileD + kPR + 2 * kPR + kPR + kKCP * kPG + 4 * kPG + kPR + kPG + 8) +
+  return 128 + sizeof(double) * (size_t)(4 * kTileD + kPR + 2 * kPR + 2 * kPR + kKCP * kPG + 4 * kPG + kPR + kPG + 8) +
          16 + 8 * sizeof(int);
 }
 
@@ -687,7 +688,7 @@ __device__ __forceinline__ PipeSmem pipe_carve(char* base) {
   p += kTileD;
   g.T1 = p;
   p += kTileD;
-  g.Wx = p;
+  g.Wt = p;
   p += kTileD;
   g.X = p;
   p += kTileD;
@@ -695,8 +696,8 @@ __device__ __forceinline__ PipeSmem pipe_carve(char* base) {
   p += kPR;
   g.lamx = p;
   p += 2 * kPR;
-  g.lamn = p;
-  p += kPR;
+  g.lamn = p;  // old lambda of the block being solved / of the next one, by step parity
+  p += 2 * kPR;
   g.kcn = p;
   p += kKCP * kPG;
   g.sv = p;
@@ -714,7 +715,7 @@ __device__ __forceinline__ PipeSmem pipe_carve(char* base) {
 }
 
 // group constants of one group from a packed record (global or shared):
-// [ihw, it00, it01, it10, it11, b0, b1, bad, htn0, htn1]; the pipelined
+// [ihw, it00, it01, it10, it11, b0, b1, bad, hwnn, htn0, htn1]; the pipelined
 // kernel stages only the first kKCP (what block_solve_v4 reads)
 __device__ __forceinline__ void load_group_const(GroupConst& k, const double* kk, bool valid, int stride = kKC) {
   if (valid) {
@@ -726,9 +727,9 @@ __device__ __forceinline__ void load_group_const(GroupConst& k, const double* kk
     k.b0 = kk[5];
     k.b1 = kk[6];
     k.bad = (int)kk[7];
-    k.htn0 = stride > 8 ? kk[8] : 0.0;
-    k.htn1 = stride > 9 ? kk[9] : 0.0;
-    k.hwnn = 1.0 / k.ihw;
+    k.hwnn = kk[8];
+    k.htn0 = stride > 9 ? kk[9] : 0.0;
+    k.htn1 = stride > 10 ? kk[10] : 0.0;
   } else {
     k.ihw = k.hwnn = 1.0;
     k.htn0 = k.htn1 = k.it00 = k.it01 = k.it10 = k.it11 = k.b0 = k.b1 = 0.0;
@@ -745,10 +746,14 @@ __device__ __forceinline__ void load_group_const(GroupConst& k, const double* kk
 // lambda is read by the chain only at its own step).  Same branches as
 // local_solve (solver.py:124-165): normal clamp at zero, frictionless,
 // tangential stick solve, projection onto the cone.
-template <bool FRIC>
+// CHUNKS: after the groups ending at e1 and e2 and after the last group the
+// warp arrives at named barriers 7, 8 and 9 (with the phase-B warp, 64
+// threads): the records of those groups are final, and the phase-B warp folds
+// them into the next block's delta while the chain continues.
+template <bool FRIC, bool CHUNKS = false>
 __device__ __forceinline__ void block_solve_v4(const double* __restrict__ Wt, int ld, int ng, int lane,
                                                double dl_[3], const double lm[3], const GroupConst& kc, double mu,
-                                               double h2, double* __restrict__ sv) {
+                                               double h2, double* __restrict__ sv, int e1 = 0, int e2 = 0) {
   const double* wrow = Wt + 3 * lane * ld;
   const double h2l1 = h2 * lm[1], h2l2 = h2 * lm[2];
   const double nl0 = -lm[0], lhw = lm[0] * kc.hwnn, nihw = -kc.ihw;
@@ -795,7 +800,12 @@ __device__ __forceinline__ void block_solve_v4(const double* __restrict__ Wt, in
         : "memory");
 #pragma unroll
     for (int a = 0; a < 3; ++a) dl_[a] = fma(w[3 * a + 2], s2, fma(w[3 * a + 1], s1, fma(w[3 * a], s0, dl_[a])));
+    if (CHUNKS) {
+      if (g == e1 - 1) asm volatile("bar.arrive 7, 64;" ::: "memory");
+      if (g == e2 - 1) asm volatile("bar.arrive 8, 64;" ::: "memory");
+    }
   }
+  if (CHUNKS) asm volatile("bar.arrive 9, 64;" ::: "memory");
 }
 
 // lambda of the lane's group from its block_solve_v4 record; dsq += |change|^2;
@@ -906,8 +916,22 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
   };
 
   if (blockIdx.x == 0) {
+    // ---- solver CTA.  Step t solves block b; meanwhile, for block b+1:
+    //   warp 2: tensor TMA of T(b+1) and Wt = W[b, b+1] (the transpose of
+    //           W[b+1, b] by symmetry: its rows are W[b+1, b]'s columns), then
+    //           X = W[b+2, b] for the next step's X2, then the regularisation
+    //           shift of T(b+1)'s diagonal;
+    //   warp 3: lambda(b+1) (previous sweep), group constants, delta_base and
+    //           shifts of b+1; then phase B: W[b+1, b] (lambda_b new) folded in
+    //           chunk by chunk as the solver releases its groups (named
+    //           barriers 7-9), so only the last chunk follows the chain;
+    //   X2 warps: W[b+1, b-1] lambda_{b-1} and the helpers' row partials;
+    //   warp 1: publisher of each solved block's lambda.
+    // One CTA barrier per step (B2); the other hand-offs are named barriers
+    // between the warps involved.
     PipeSmem sm = pipe_carve(smem_raw);
     const int xi = x2_index(warp);
+    constexpr int kC1 = 9, kC2 = 18;  // phase-B chunk ends (groups)
     if (tid == 0) {
       sm.flags[0] = sm.flags[1] = 0;
       mbar_init(sm.bar, 1);
@@ -922,7 +946,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
     }
     for (int i = tid; i < kPR; i += blockDim.x) {
       sm.dcur[i] = i < rows_of(0) ? s.delta_base[i] : 0.0;
-      sm.lamn[i] = 0.0;  // lambda starts at zero (prep zeroed the global copy)
+      sm.lamn[i] = sm.lamn[kPR + i] = 0.0;  // lambda starts at zero (prep zeroed the global copy)
       sm.lamx[i] = sm.lamx[kPR + i] = 0.0;
     }
     __syncthreads();
@@ -932,9 +956,6 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
     double dsq = 0.0;
     const double ih2 = 1.0 / h2;
     if (warp == 0) load_group_const(kc, kconst + kKC * lane, lane < rows_of(0) / 3);
-    const bool rowner = tid >= 64 && tid < 64 + kRowOwners;
-    // phase-B GEMV (warps 2..11): 8 rows x 4 column phases per warp; a quarter-warp
-    // reads 8 rows of 16-byte pairs, distinct banks for the 78-double row pitch
     volatile unsigned* vcnt = (volatile unsigned*)(sm.flags + 4);  // [0] lambda in smem, [1] published (steps)
     if (tid == 0) {
       sm.flags[2] = 0;
@@ -954,24 +975,26 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
       double* Tn = slot ? sm.T0 : sm.T1;
       double* lamc = sm.lamx + slot * kPR;         // lambda_b (this solve)
       double* lamp = sm.lamx + (slot ^ 1) * kPR;   // lambda_{b-1}
+      const double* lold = sm.lamn + slot * kPR;   // lambda_b before this solve
+      double* lnext = sm.lamn + (slot ^ 1) * kPR;  // lambda_{b+1} before its solve
       const int64_t rb = 3 * (int64_t)b * kPG, rb1 = 3 * (int64_t)b1 * kPG;
-      const int si = tid - (64 + kRowOwners);  // phase-B diagonal-shift thread, one row (kPR <= 128)
+      const int ng = rows / 3;
+      const int e1 = min(ng, kC1), e2 = min(ng, kC2);
       if (warp == 0) {
         // ---- sequential block solve ----
-        const int ng = rows / 3;
         const bool mine = lane < ng;
         double lm[3], dl[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          lm[a] = mine ? sm.lamn[3 * lane + a] : 0.0;
+          lm[a] = mine ? lold[3 * lane + a] : 0.0;
           dl[a] = mine ? sm.dcur[3 * lane + a] : 0.0;
         }
-        if (!(dbg & 2)) asm volatile("bar.arrive 2, %0;" ::"n"(64 + 32 * kXW));  // dcur, lamn consumed
+        asm volatile("bar.arrive 2, %0;" ::"n"(32 + 32 * kXW));  // dcur consumed
         stamp(13);
         if (s.mu != 0.0)
-          block_solve_v4<true>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv);
+          block_solve_v4<true, true>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv, e1, e2);
         else
-          block_solve_v4<false>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv);
+          block_solve_v4<false, true>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv, e1, e2);
         __syncwarp();
         stamp(14);
         const int err = mine ? block_commit(sm.sv, lane, lm, kc, s.mu, ih2, dsq) : 0;
@@ -981,7 +1004,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           if (lane == g) raise_status(s.status, CNB_E_SINGULAR_BLOCK, (int)(rb / 3 + g), 1.0 / kc.ihw);
           if (lane == 0) sm.flags[0] = 1;
         }
-        if (t >= 2 && !(dbg & 2))  // the publisher has read this slot's previous lambda (step t-2)
+        if (t >= 2)  // the publisher has read this slot's previous lambda (step t-2)
           while (vcnt[1] + 1 < t) {
           }
         if (mine)
@@ -1000,25 +1023,39 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           dsq = 0.0;
         }
         stamp(2);
-      } else if (dbg & 2) {
-        // timing experiment: aux warps idle (wrong results)
+        // next block's group constants (warp 3 staged them: barrier 10)
+        asm volatile("bar.sync 10, 64;" ::: "memory");
+        load_group_const(kc, sm.kcn + kKCP * lane, lane < rows1 / 3, kKCP);
+        if (b == nb - 1 && lane == 0 && !sm.flags[0]) {
+          while (vcnt[1] < t) {  // the publisher's sum of blocks 0..nb-2 (step t-1) is in red[2]
+          }
+          const double num = sqrt(sm.red[0]), den = sqrt(sm.red[1] + sm.red[2]);
+          const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
+          s.eps_hist[sweep] = eps;
+          sm.flags[1] = (eps <= s.tol) ? 1 : ((sweep + 1 >= s.max_iter) ? 2 : 0);
+        }
+        stamp(0);
       } else if (warp == 2) {
-        // T(b+1) and W[b+1, b]: one tensor-TMA box each (out-of-range rows and
+        // T(b+1) and Wt = W[b, b+1]: one tensor-TMA box each (out-of-range rows and
         // columns of a ragged last block arrive as zeros)
         if (tma) {
           if (lane == 0) {
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(sm.bar, 2u * kPR * kPS * 8);
             tma_load_2d(Tn, &tmap, (int)rb1, (int)rb1, sm.bar);
-            tma_load_2d(sm.Wx, &tmap, (int)rb, (int)rb1, sm.bar);
+            tma_load_2d(sm.Wt, &tmap, (int)rb1, (int)rb, sm.bar);
           }
         } else {
           for (int i = 0; i < rows1; ++i) {
             const double* src = s.W + (rb1 + i) * s.ldw;
             for (int j = lane; j < rows1; j += 32) cp_async8(&Tn[i * kPS + j], src + rb1 + j, true);
-            for (int j = lane; j < rows; j += 32) cp_async8(&sm.Wx[i * kPS + j], src + rb + j, true);
+          }
+          for (int i = 0; i < rows; ++i) {
+            const double* src = s.W + (rb + i) * s.ldw;
+            for (int j = lane; j < rows1; j += 32) cp_async8(&sm.Wt[i * kPS + j], src + rb1 + j, true);
           }
           cp_async_wait_all();
+          __syncwarp();
         }
         stamp(10);
         // X = W[b+2, b] for the next step's X2, once this step's X2 has read the tile
@@ -1038,6 +1075,10 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           cp_async_wait_all();
         }
         stamp(12);
+        // regularisation shift of T(b+1)'s diagonal (shifts staged by warp 3: barrier 11)
+        if (tma) mbar_wait(sm.bar, t & 1);
+        asm volatile("bar.sync 11, 64;" ::: "memory");
+        for (int i = lane; i < rows1; i += 32) Tn[i * kPS + i] = add(Tn[i * kPS + i], sm.dsh[i / 3]);
       } else if (warp == 3) {
         double lv[3];
 #pragma unroll
@@ -1049,16 +1090,55 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           const int g = e / kKCP, k = e - g * kKCP;
           cp_async8(&sm.kcn[e], kconst + kKC * (rb1 / 3 + g) + k, true);
         }
-        // delta_base and the regularisation shifts of block b+1 for phase B
+        // delta_base and the regularisation shifts of block b+1
         for (int j = lane; j < rows1; j += 32) cp_async8(&sm.dbs[j], s.delta_base + rb1 + j, true);
         if (lane < rows1 / 3) cp_async8(&sm.dsh[lane], dshift + rb1 / 3 + lane, true);
-        asm volatile("bar.sync 2, %0;" ::"n"(64 + 32 * kXW));  // warp 0 has read lamn
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
           const int j = lane + 32 * u;
-          if (j < kPR) sm.lamn[j] = lv[u];
+          if (j < kPR) lnext[j] = lv[u];
         }
         cp_async_wait_all();
+        __syncwarp();
+        asm volatile("bar.arrive 10, 64;" ::: "memory");  // constants of b+1 -> warp 0
+        asm volatile("bar.arrive 11, 64;" ::: "memory");  // shifts of b+1 -> warp 2
+        // ---- phase B: v = W[b+1, b] lambda_b, lane <-> rows lane, lane+32, lane+64 of
+        // block b+1; lambda_b of a group from the solver's record (block_commit's
+        // arithmetic), the column of W[b+1, b] from row 3g+a of Wt (contiguous)
+        if (tma) mbar_wait(sm.bar, t & 1);
+        double v[3] = {0.0, 0.0, 0.0};
+        const bool fr = s.mu != 0.0;
+        auto fold = [&](int gs, int ge) {
+          for (int g = gs; g < ge; ++g) {
+            const double2 ra = *reinterpret_cast<const double2*>(sm.sv + 4 * g);      // x, dh1
+            const double2 rc = *reinterpret_cast<const double2*>(sm.sv + 4 * g + 2);  // dh2, open
+            const bool open = rc.y != 0.0, fric = open && fr;
+            const double n0 = open ? fmax(ra.x, 0.0) : 0.0;
+            const double n1 = fric ? fma(ra.y, ih2, lold[3 * g + 1]) : 0.0;
+            const double n2 = fric ? fma(rc.x, ih2, lold[3 * g + 2]) : 0.0;
+            const double* w0 = sm.Wt + (3 * g) * kPS;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+              const int r = lane + 32 * u;
+              if (r < kPR)
+                v[u] = fma(w0[2 * kPS + r], n2, fma(w0[kPS + r], n1, fma(w0[r], n0, v[u])));
+            }
+          }
+        };
+        asm volatile("bar.sync 7, 64;" ::: "memory");
+        fold(0, e1);
+        asm volatile("bar.sync 8, 64;" ::: "memory");
+        fold(e1, e2);
+        asm volatile("bar.sync 9, 64;" ::: "memory");
+        fold(e2, ng);
+        stamp(9);
+        // the X2 warps' part of delta(b+1) is in dcur (barrier 12)
+        asm volatile("bar.sync 12, %0;" ::"n"(32 + 32 * kXW) : "memory");
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int r = lane + 32 * u;
+          if (r < rows1) sm.dcur[r] = add(sm.dbs[r], mul(h2, sm.dcur[r] + v[u]));
+        }
       } else if (xi >= 0) {
         // X2 = W[b+1, b-1] lambda_{b-1} from the X tile (fetched last step)
         if (tma && t > 0) mbar_wait(sm.bar + 1, (t - 1) & 1);
@@ -1096,65 +1176,15 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
             for (int sg = 0; sg < nseg; ++sg) pvl += ll_load(part + 2 * ((size_t)i * kSeg + sg), tag0 + t - 1, ctl);
           }
         }
-        asm volatile("bar.sync 2, %0;" ::"n"(64 + 32 * kXW));  // warp 0 has read dcur
+        asm volatile("bar.sync 2, %0;" ::"n"(32 + 32 * kXW));  // warp 0 has read dcur
         const double pk = __shfl_sync(0xffffffffu, pvl, lane / 3);  // lane 3k picks up row k's sum
         {
           const int k = lane / 3, i = xi + kXW * k;
           if (lane == 3 * k && k < kXRows && i < rows1) sm.dcur[i] = x2v + pk;  // partial sums of block b+1
         }
+        __syncwarp();
+        asm volatile("bar.arrive 12, %0;" ::"n"(32 + 32 * kXW) : "memory");  // -> warp 3 (phase B)
         if (xi == 0) stamp(7);
-      }
-      asm volatile("bar.sync 5, %0;" ::"n"(kPipeThreads - 32) : "memory");  // B1 (all but the publisher)
-      if (warp == 0 || warp == 5) stamp(0); else stamp(-1);
-      // ---- phase B: delta(b+1), shift of T(b+1)'s diagonal, sweep-end epsilon ----
-      if (rowner) {
-        if (tid == 64) stamp(-1);
-        if (tma) mbar_wait(sm.bar, t & 1);
-        if (tid == 64) stamp(15);  // phase B: wait for T(b+1) / W[b+1, b]
-        // W[b+1, b] lambda_b: warp rw (0..9) takes rows rw + 10 k (k < 8), lanes the
-        // column pairs 2 lane and 2 lane + 64: lambda_b is loaded once per lane and
-        // every W row is one contiguous 512-byte read (shared-memory bandwidth is
-        // the limit of this GEMV); one 8-row warp reduction
-        const int rw = warp - 2;
-        const int j0 = 2 * lane, j1 = 2 * lane + 64;
-        double2 l0, l1;
-        l0.x = j0 < rows ? lamc[j0] : 0.0;
-        l0.y = j0 + 1 < rows ? lamc[j0 + 1] : 0.0;
-        l1.x = j1 < rows ? lamc[j1] : 0.0;
-        l1.y = j1 + 1 < rows ? lamc[j1 + 1] : 0.0;
-        double acc8[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int r = rw + 10 * k;
-          double a = 0.0;
-          if (r < rows1) {
-            const double* xr = sm.Wx + r * kPS;
-            const double2 x0 = *reinterpret_cast<const double2*>(xr + j0);
-            a = fma(x0.y, l0.y, x0.x * l0.x);
-            if (j1 < rows) {
-              const double2 x1 = *reinterpret_cast<const double2*>(xr + j1);
-              a = fma(x1.y, l1.y, fma(x1.x, l1.x, a));
-            }
-          }
-          acc8[k] = a;
-        }
-        const double v = warp_sum8(acc8, lane);
-        const int r = rw + 10 * (4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1));
-        if ((lane & 3) == 0 && r < rows1) sm.dcur[r] = add(sm.dbs[r], mul(h2, sm.dcur[r] + v));
-        if (tid == 64) stamp(9);  // phase B GEMV
-      } else if (tid >= 64 + kRowOwners) {
-        if (tma) mbar_wait(sm.bar, t & 1);
-        if (si < rows1) Tn[si * kPS + si] = add(Tn[si * kPS + si], sm.dsh[si / 3]);
-      } else {  // warp 0
-        load_group_const(kc, sm.kcn + kKCP * lane, lane < rows1 / 3, kKCP);
-        if (b == nb - 1 && lane == 0 && !sm.flags[0]) {
-          while (vcnt[1] < t) {  // the publisher's sum of blocks 0..nb-2 (step t-1) is in red[2]
-          }
-          const double num = sqrt(sm.red[0]), den = sqrt(sm.red[1] + sm.red[2]);
-          const double eps = (num == 0.0) ? 0.0 : (den == 0.0 ? INFINITY : num / den);
-          s.eps_hist[sweep] = eps;
-          sm.flags[1] = (eps <= s.tol) ? 1 : ((sweep + 1 >= s.max_iter) ? 2 : 0);
-        }
       }
       asm volatile("bar.sync 6, %0;" ::"n"(kPipeThreads - 32) : "memory");  // B2 (all but the publisher)
       if (warp == 0 || warp == 5) stamp(1); else stamp(-1);
@@ -1550,6 +1580,7 @@ __global__ void __launch_bounds__(kCopyThreads, 2) pgs_copy_kernel(const PgsScen
     o[5] = kc.b0;
     o[6] = kc.b1;
     o[7] = (double)kc.bad;
+    o[8] = kc.hwnn;
   }
   for (int64_t i = tid; i < c; i += blockDim.x) lam[i] = 0.0;
   {
@@ -1820,7 +1851,7 @@ static int launch_pgs_grid(PgsScene s, cudaStream_t st) {
   GridCtl* ctl = (GridCtl*)ws_p;
   double* dshift = (double*)((char*)ws_p + 64);
   double* kconst = dshift + s.groups;
-  double* partial = kconst + kKC * s.groups + (s.groups & 1);  // 16-byte aligned (copy_cg)
+  double* partial = kconst + kKC * s.groups + (((1 + kKC) * s.groups) & 1);  // 16-byte aligned (copy_cg)
   {
     // regularisation shifts + group constants, grid-wide (two passes)
     const int nparts = (int)((s.groups + kPrepThreads - 1) / kPrepThreads);
