@@ -209,6 +209,20 @@ int cnb_pgs(int64_t groups, const double* W, int64_t ldw, const double* delta_ba
             double* delta_end, double* eps_hist, int32_t* iters_conv, double* shift_out,
             cnb_status_t* d_status, void* stream);
 
+/* Graph-coloured PGS (north star option; NOT the reference's iterate): the
+ * groups are visited colour by colour (colour_ptr[ncolours + 1] offsets into
+ * colour_groups[groups], host arrays, built so that no two groups sharing a
+ * DoF share a colour), all groups of a colour updated at once from the lambda
+ * at the colour's start, one CTA per group streaming its rows of W.  Same
+ * local solve, regularisation, stopping rule and outputs as cnb_pgs; W and lam
+ * need 16-byte aligned rows (even ldw).  omega in (0, 1]: under-relaxation of
+ * each group's change (a dense W makes plain Jacobi inside a colour diverge).
+ * Validated on the converged lambda. */
+int cnb_pgs_coloured(int64_t groups, const double* W, int64_t ldw, const double* delta_base, double h, double mu,
+                     double tol, int32_t max_iter, const int64_t* colour_ptr, const int64_t* colour_groups,
+                     int32_t ncolours, double omega, double* lam, double* delta_end, double* eps_hist,
+                     int32_t* iters_conv, double* shift_out, cnb_status_t* d_status, void* stream);
+
 /* One group's local solve (solver.py:124-165) as a device call, for API
  * parity with local_solve; out (3). */
 int cnb_local_solve(int64_t alpha, int64_t groups, const double* W, int64_t ldw,

@@ -55,6 +55,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_potrf_profile": [P],
     "cnb_bench_gemm": [I32, I64, I64, I64, P, I64, P, I64, P, I64, P],
     "cnb_pgs": [I64, P, I64, P, F64, F64, F64, I32, P, P, P, P, P, P, P],
+    "cnb_pgs_coloured": [I64, P, I64, P, F64, F64, F64, I32, P, P, I32, F64, P, P, P, P, P, P, P],
     "cnb_local_solve": [I64, I64, P, I64, P, P, F64, F64, P, P, P],
     "cnb_gemm_naive": [I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, P],
     "cnb_csr_spmv": [I64, P, P, P, P, P, F64, P],

@@ -31,16 +31,28 @@ from .constraints import (
     prox_update_inplace,
     rebuild_W_fast,
 )
-from .errors import SingularBlockError, ValidationError
+from .errors import DimensionMismatchError, SingularBlockError, ValidationError
 
 SCHEMES = ("single", "standard", "fast")
 
 
+ORDERINGS = ("exact", "coloured")
+
+
 @dataclass
 class PgsConfig:
+    """PGS budget and friction (solver.py:52-64).  ``ordering`` (not in the
+    reference) selects the group order: "exact" — the reference's canonical
+    Gauss-Seidel order (default, parity-pinned); "coloured" — groups coloured
+    so that no two groups sharing a DoF share a colour, each colour updated at
+    once (the north star's graph-coloured variant; a different iterate, checked
+    on the converged lambda only)."""
+
     max_iterations: int = 30
     tolerance: float = 1e-6
     friction: float = 0.5
+    ordering: str = "exact"
+    relaxation: float = 1.0  # coloured ordering only: under-relaxation of each group's change
 
     def __post_init__(self):
         if self.max_iterations < 1:
@@ -49,6 +61,10 @@ class PgsConfig:
             raise ValidationError("pgs.tolerance must be positive")
         if self.friction < 0:
             raise ValidationError("friction coefficient must be >= 0")
+        if self.ordering not in ORDERINGS:
+            raise ValidationError(f"unknown pgs ordering {self.ordering!r}, pick from {ORDERINGS}")
+        if not 0.0 < self.relaxation <= 1.0:
+            raise ValidationError("pgs.relaxation must be in (0, 1]")
 
 
 @dataclass
@@ -156,11 +172,41 @@ class PgsWorkspace:
         self.shift = dv.empty(max(1, c // 3))
 
 
+def colour_groups(S_by_object: dict, groups: int):
+    """Greedy colouring of the contact groups in canonical order: two groups that
+    share a DoF column of any object's S (the sparsified coupling graph of W)
+    get different colours.  Returns (colour_ptr, groups by colour), int64; the
+    groups of a colour stay in canonical order."""
+    keys = [[] for _ in range(groups)]
+    for oid, S in sorted(S_by_object.items()):
+        csr = S.sorted_csr if hasattr(S, "sorted_csr") else S.tocsr()
+        rows = np.repeat(np.arange(csr.shape[0]), np.diff(csr.indptr))
+        for i, k in zip(rows // 3, csr.indices // 3):  # (group, node of this object)
+            keys[i].append((oid, int(k)))
+    colour = np.empty(groups, dtype=np.int64)
+    used: dict = {}
+    for i in range(groups):
+        taken = set()
+        for k in set(keys[i]):
+            taken |= used.get(k, set())
+        col = 0
+        while col in taken:
+            col += 1
+        colour[i] = col
+        for k in set(keys[i]):
+            used.setdefault(k, set()).add(col)
+    order = np.lexsort((np.arange(groups), colour)).astype(np.int64)
+    ptr = np.zeros(int(colour.max(initial=-1)) + 2, dtype=np.int64)
+    ptr[1:] = np.cumsum(np.bincount(colour, minlength=len(ptr) - 1))
+    return ptr, order
+
+
 def pgs_device(W: torch.Tensor, delta_base: torch.Tensor, h: float, config: PgsConfig,
-               ws: PgsWorkspace | None = None, delta_end: bool = True) -> PgsResult:
+               ws: PgsWorkspace | None = None, delta_end: bool = True, colours=None) -> PgsResult:
     """Asynchronous PGS: launches and returns device results (no host sync).
     ``delta_end=False`` skips the final pass over W (the caller forms delta_end
-    another way) and records the regularisation shifts in ``ws.shift``."""
+    another way) and records the regularisation shifts in ``ws.shift``.
+    ``config.ordering == "coloured"`` needs ``colours`` = colour_groups(...)."""
     c = int(delta_base.shape[0])
     dev = delta_base.device
     if c == 0:
@@ -169,18 +215,28 @@ def pgs_device(W: torch.Tensor, delta_base: torch.Tensor, h: float, config: PgsC
         raise SingularBlockError(f"W is {tuple(W.shape)}, violation has {c} rows")
     ws = ws or PgsWorkspace(c, config.max_iterations)
     st = _lib.status(dev)
-    _lib.call("cnb_pgs", c // 3, W.data_ptr(), dv.ld(W), delta_base.data_ptr(), float(h), float(config.friction),
-              float(config.tolerance), int(config.max_iterations), ws.lam.data_ptr(),
-              ws.delta_end.data_ptr() if delta_end else None, ws.eps.data_ptr(), ws.ic.data_ptr(),
-              None if delta_end else ws.shift.data_ptr(), st.ptr, _lib.stream())
+    common = (ws.lam.data_ptr(), ws.delta_end.data_ptr() if delta_end else None, ws.eps.data_ptr(),
+              ws.ic.data_ptr(), None if delta_end else ws.shift.data_ptr(), st.ptr, _lib.stream())
+    if config.ordering == "coloured":
+        if colours is None:
+            raise ValidationError("coloured PGS needs the group colouring (solver.colour_groups)")
+        ptr, grp = (np.ascontiguousarray(x, dtype=np.int64) for x in colours)
+        if len(grp) != c // 3:
+            raise DimensionMismatchError(f"colouring covers {len(grp)} groups, W has {c // 3}")
+        _lib.call("cnb_pgs_coloured", c // 3, W.data_ptr(), dv.ld(W), delta_base.data_ptr(), float(h),
+                  float(config.friction), float(config.tolerance), int(config.max_iterations), ptr.ctypes.data,
+                  grp.ctypes.data, len(ptr) - 1, float(config.relaxation), *common)
+    else:
+        _lib.call("cnb_pgs", c // 3, W.data_ptr(), dv.ld(W), delta_base.data_ptr(), float(h),
+                  float(config.friction), float(config.tolerance), int(config.max_iterations), *common)
     return PgsResult(ws.lam, ws.delta_end, ws.eps, ws.ic, st)
 
 
-def pgs(W, delta_base, h: float, config: PgsConfig) -> PgsResult:
+def pgs(W, delta_base, h: float, config: PgsConfig, colours=None) -> PgsResult:
     """Sweep the groups until the relative lambda change drops below tolerance
     (solver.py:168-202).  Returns device lam and delta_end."""
     W_t, d_t = dv.mat64(W), dv.f64(delta_base)
-    res = pgs_device(W_t, d_t, h, config)
+    res = pgs_device(W_t, d_t, h, config, colours=colours)
     res._resolve()
     return res
 
@@ -200,6 +256,12 @@ class StepContext:
     refresh: Callable | None = None
     wg: MappingDelassus | None = None
     table: PairTable | None = None
+    colours: tuple | None = None  # coloured PGS: (colour_ptr, groups), built on first use
+
+    def colouring(self):
+        if self.colours is None:
+            self.colours = colour_groups(self.S_by_object, len(self.pairs))
+        return self.colours
 
 
 @dataclass
@@ -292,7 +354,8 @@ def newton_fast(ctx: StepContext, ncfg: NewtonConfig, pcfg: PgsConfig) -> Correc
         compute_violation(Dm, p_a, p_b, out=delta)
         # every iteration keeps its own lambda (lam_history holds references)
         ws_k = ws if k == 0 else PgsWorkspace(c, pcfg.max_iterations)
-        res = pgs_device(W, delta, ctx.h, pcfg, ws_k, delta_end=False)
+        res = pgs_device(W, delta, ctx.h, pcfg, ws_k, delta_end=False,
+                         colours=ctx.colouring() if pcfg.ordering == "coloured" else None)
         e2 = timer.mark()
         _lib.call("cnb_apply_dt", m, D.data_ptr(), res.lam.data_ptr(), t.data_ptr(), acc.data_ptr(), _lib.stream())
         prox_update_inplace(p_a, p_b, ctx.wg, t, ctx.h)
@@ -366,7 +429,8 @@ def newton_standard(ctx: StepContext, ncfg: NewtonConfig, pcfg: PgsConfig, group
         W = dv.mat64(assemble_W_standard(H, ctx.F_by_object, group=group).W)  # aligned rows for PGS
         e1 = timer.mark()
         compute_violation(Dm, p_a, p_b, out=delta)
-        res = pgs_device(W, delta, ctx.h, pcfg, PgsWorkspace(c, pcfg.max_iterations))
+        res = pgs_device(W, delta, ctx.h, pcfg, PgsWorkspace(c, pcfg.max_iterations),
+                         colours=ctx.colouring() if pcfg.ordering == "coloured" else None)
         e2 = timer.mark()
         t = dv.empty(c)
         _lib.call("cnb_apply_dt", m, D.data_ptr(), res.lam.data_ptr(), t.data_ptr(), acc.data_ptr(), _lib.stream())
