@@ -135,3 +135,65 @@ def placement(nodes, normals, clearance):
         lift = (clearance - float((nodes @ nrm).min())) / nrm[1]
         out[i] = nodes + np.array([0.0, lift, 0.0])
     return out
+
+
+# ----------------------------------------------------------------------------
+# cfg2: soft ellipsoid pressed by a rotating rigid cylinder
+# ----------------------------------------------------------------------------
+
+CFG2_SEMI = (0.10, 0.06, 0.05)
+CFG2_SPACING = 0.0035        # jittered lattice spacing: ~30 000 nodes (90 000 DoF)
+CFG2_CYL_RADIUS = 0.01
+CFG2_INDENT = 0.003          # cylinder's initial indentation into the top (builder's choice)
+
+
+def ellipsoid_mesh(semi=CFG2_SEMI, spacing=CFG2_SPACING, seed=0):
+    """Seeded jittered lattice inside an ellipsoid, Delaunay tets (scipy), tets with
+    the centroid outside or a volume below 1e-3 spacing^3 dropped, orientation
+    made positive, unused points removed."""
+    from scipy.spatial import Delaunay
+
+    rng = np.random.default_rng(seed)
+    a = np.asarray(semi, dtype=np.float64)
+    axes = [np.arange(-ai, ai + 1e-12, spacing) for ai in a]
+    P = np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1).reshape(-1, 3)
+    P = P + rng.uniform(-0.25 * spacing, 0.25 * spacing, P.shape)
+    P = P[((P / a) ** 2).sum(axis=1) <= 1.0]
+    T = Delaunay(P).simplices.astype(np.int64)
+    T = T[((P[T].mean(axis=1) / a) ** 2).sum(axis=1) <= 1.0]
+    v = np.einsum("ij,ij->i", np.cross(P[T[:, 1]] - P[T[:, 0]], P[T[:, 2]] - P[T[:, 0]]), P[T[:, 3]] - P[T[:, 0]]) / 6
+    T[v < 0] = T[v < 0][:, [0, 2, 1, 3]]
+    T = T[np.abs(v) >= 1e-3 * spacing ** 3]
+    used = np.unique(T)
+    remap = -np.ones(len(P), dtype=np.int64)
+    remap[used] = np.arange(len(used))
+    return P[used], remap[T]
+
+
+def cylinder_surface(radius=CFG2_CYL_RADIUS, length=0.12, n_theta=48, n_z=40):
+    """Open cylinder side surface along z through the origin, outward wound."""
+    th = np.linspace(0.0, 2 * np.pi, n_theta, endpoint=False)
+    zs = np.linspace(-0.5 * length, 0.5 * length, n_z + 1)
+    pts = np.array([[radius * np.cos(t), radius * np.sin(t), z] for z in zs for t in th])
+    tris = []
+    for k in range(n_z):
+        for j in range(n_theta):
+            a, b = k * n_theta + j, k * n_theta + (j + 1) % n_theta
+            c, d = a + n_theta, b + n_theta
+            tris += [[a, b, d], [a, d, c]]
+    tris = np.array(tris, dtype=np.int64)
+    n0 = np.cross(pts[tris[:, 1]] - pts[tris[:, 0]], pts[tris[:, 2]] - pts[tris[:, 0]])
+    out = pts[tris].mean(axis=1) * np.array([1.0, 1.0, 0.0])
+    flip = np.einsum("ij,ij->i", n0, out) < 0
+    tris[flip] = tris[flip][:, ::-1]
+    return pts, tris
+
+
+def cfg2_arrays():
+    """nodes, tets, fixed (bottom 5 % by y), cylinder points (placed) and triangles,
+    cylinder centre."""
+    nodes, tets = ellipsoid_mesh()
+    fixed = np.sort(np.argsort(nodes[:, 1], kind="stable")[: max(1, len(nodes) // 20)])
+    pts, tris = cylinder_surface()
+    center = np.array([0.0, float(nodes[:, 1].max()) + CFG2_CYL_RADIUS - CFG2_INDENT, 0.0])
+    return nodes, tets, fixed, pts + center, tris, center
