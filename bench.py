@@ -62,7 +62,7 @@ CFG3_SHIFT, CFG3_GAP = 0.005, 0.001  # upper block half a cell off the lower gri
 # its PGS extrapolation takes them from here (the GPU arm's own cpu_baseline
 # passes the values it just measured)
 CFG3_GROUPS = 7500
-CFG3_SWEEPS_PER_ITER = 30.0
+CFG3_SWEEPS_PER_ITER = 16.1  # profiles/r02_bench_cfg3.json: 161 sweeps over 10 iterations at the timed step
 CFG4_COPIES = workloads.CFG4_COPIES
 CFG4_PREROLL = 12
 METRIC_CFG3 = ("ms per full time step (cfg3 450k-DoF two-body scene); also ms per Newton constraint-update "
