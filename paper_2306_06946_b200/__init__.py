@@ -26,6 +26,7 @@ from .collision import (
     PairTable,
     PlaneGeometry,
     Pose,
+    SphereGeometry,
     ProximityPair,
     build_frames,
     detect,
@@ -66,6 +67,7 @@ from .solver import (
 from .dynamics import (
     FreeMotion,
     MechanicalState,
+    RigidBody,
     SoftBody,
     compute_free_motion,
     integrate_correction,
@@ -77,6 +79,7 @@ from .scene import (
     MotionSpec,
     OutputConfig,
     PlaneSpec,
+    RigidSphereSpec,
     SceneConfig,
     Simulation,
     Snapshot,

@@ -122,6 +122,18 @@ class PlaneGeometry:
         self.normal = n / nn
 
 
+@dataclass
+class SphereGeometry:
+    """A rigid sphere for detection (collision.py:127-132): centre, radius and the
+    body pose its contact points are expressed in."""
+
+    object_id: int
+    center: np.ndarray
+    radius: float
+    pose: Pose
+    dynamic: bool = True
+
+
 # --------------------------------------------------------------------------
 # frames as device blocks
 # --------------------------------------------------------------------------
@@ -249,7 +261,7 @@ class PairSoA:
     ``PairTable.from_soa`` uploads them without building Python objects."""
 
     FIELDS = ("kind", "obj", "node", "w", "local", "world", "lnormal", "has_ln", "ref", "pa", "pb", "signed",
-              "keys")
+              "keys", "lever")
 
     def __init__(self, m: int = 0):
         self.kind = np.full((m, 2), 4, dtype=np.int8)
@@ -265,6 +277,7 @@ class PairSoA:
         self.pb = np.zeros((m, 3))
         self.signed = np.zeros(m)
         self.keys = np.zeros((m, 4), dtype=np.int64)
+        self.lever = np.zeros((m, 3))  # RIGID_LOCAL side A: contact point minus the body centre
 
     def __len__(self) -> int:
         return len(self.keys)
@@ -296,6 +309,9 @@ class PairSoA:
             return Attachment(AttachKind.VERTEX, oid, vertex=int(self.node[i, s, 0]))
         if kind == 1:
             return Attachment(AttachKind.BARYCENTRIC, oid, triangle=self.node[i, s].copy(), weights=self.w[i, s].copy())
+        if kind == 2:
+            return Attachment(AttachKind.RIGID_LOCAL, oid, local_point=self.local[i, s].copy(),
+                              lever=self.lever[i].copy())
         if kind == 3:
             ln = self.lnormal[i].copy() if (s == 1 and self.has_ln[i]) else None
             return Attachment(AttachKind.LOCAL, oid, local_point=self.local[i, s].copy(), local_normal=ln)
@@ -680,6 +696,31 @@ def _aabbs(meshes):
     return out
 
 
+def _sphere_vs_plane(sph: SphereGeometry, plane: PlaneGeometry, threshold: float) -> PairSoA:
+    """One pair when the sphere is within ``threshold`` of the plane
+    (collision.py:290-316): side A the sphere's surface point along -n (a
+    body-frame RIGID_LOCAL attachment with its lever), side B its foot on the
+    plane (WORLD)."""
+    n = plane.normal
+    center = np.asarray(sph.center, dtype=np.float64)
+    center_dist = float(n @ center - plane.offset)
+    signed = center_dist - sph.radius
+    r = PairSoA(1 if signed <= threshold else 0)
+    if not len(r):
+        return r
+    surface = center - sph.radius * n
+    foot = center - center_dist * n
+    r.kind[0] = (2, 4)
+    r.obj[0] = (sph.object_id, plane.object_id)
+    r.local[0, 0] = sph.pose.inverse_apply(surface)
+    r.lever[0] = surface - center
+    r.world[0, 1] = foot
+    r.pa[0], r.pb[0], r.ref[0] = surface, foot, n
+    r.signed[0] = signed
+    r.keys[0] = (sph.object_id, plane.object_id, 0, -1)
+    return r
+
+
 def detect_soa(geometries, threshold: float) -> PairSoA:
     """Pairs with signed distance <= threshold in canonical order (collision.py:320-345),
     as arrays."""
@@ -703,6 +744,10 @@ def detect_soa(geometries, threshold: float) -> PairSoA:
         for plane in planes:
             if ga.dynamic:
                 parts.append(_vertex_vs_plane(ga, plane, threshold))
+    for sph in (g for g in geometries if isinstance(g, SphereGeometry)):
+        for plane in planes:
+            if sph.dynamic:
+                parts.append(_sphere_vs_plane(sph, plane, threshold))
     return PairSoA.concat(parts).sort()
 
 

@@ -11,7 +11,8 @@ factorised once per simulation).  ``material="corotational"`` (north star;
 SURVEY.md §9 #1) rotates every element's stiffness by the polar factor of its
 deformation gradient, so A changes every step and is refactorised.  Both
 assemble with csrc/assembly.cu (one thread per tet, deterministic gathers).
-Rigid bodies are out of scope (no BASELINE configuration uses them).
+``RigidBody`` (dynamics.py:214-249) is the 6-DoF sphere: its generalized mass
+(m I, R I_body R^T) is a 6 x 6 system factorised on the device every step.
 """
 
 from __future__ import annotations
@@ -332,6 +333,49 @@ class SoftBody:
             _lib.status(dv.device()).raise_if_set("assemble")
         except _lib.errors.NonFiniteForceError:
             raise NonFiniteForceError("assembled right-hand side is not finite") from None
+
+
+@dataclass
+class RigidBody:
+    """Six-DoF rigid body with a sphere as collision geometry (dynamics.py:214-249).
+    DoFs: velocity (3) and angular velocity (3) in world axes."""
+
+    mass: float
+    inertia: np.ndarray  # (3, 3) body frame, kg m^2
+    radius: float = 0.1
+
+    def __post_init__(self):
+        if self.mass <= 0:
+            raise ValidationError(f"rigid mass must be positive, got {self.mass}")
+        self.inertia = np.asarray(self.inertia, dtype=np.float64).reshape(3, 3)
+        eig = np.linalg.eigvalsh(0.5 * (self.inertia + self.inertia.T))
+        if eig.min() <= 0:
+            raise ValidationError("rigid inertia must be symmetric positive definite")
+
+    @property
+    def n_dofs(self) -> int:
+        return 6
+
+    @property
+    def fixed_mask(self) -> np.ndarray:
+        return np.zeros(6, dtype=bool)
+
+    def assemble(self, rotation, h: float, gravity):
+        """Generalized mass diag(m I, R I R^T) and the gravity impulse (no internal forces)."""
+        if h <= 0:
+            raise ValidationError(f"time step must be positive, got {h}")
+        R = np.asarray(rotation, dtype=np.float64).reshape(3, 3)
+        A = np.zeros((6, 6))
+        A[:3, :3] = self.mass * np.eye(3)
+        A[3:, 3:] = R @ self.inertia @ R.T
+        b = np.zeros(6)
+        b[:3] = h * self.mass * np.asarray(gravity, dtype=np.float64)
+        if not np.all(np.isfinite(b)):
+            raise NonFiniteForceError("assembled right-hand side is not finite")
+        return SparseSym(sp.csr_matrix(A), check=False), dv.f64(b)
+
+    def check_finite(self) -> None:
+        """The right-hand side was checked on the host by ``assemble``."""
 
 
 def compute_free_motion(A: SparseSym, b, state: MechanicalState, h: float,

@@ -503,6 +503,51 @@ def fixed_mapping():
     save("fixed_mapping.npz", **out)
 
 
+def rigid_spheres():
+    """Rigid spheres (dynamics.py:214-249, RIGID_LOCAL rows collision.py:448-457,
+    sphere-plane pairs collision.py:290-316) on a tilted plane with friction,
+    one spinning, beside a soft box that lands on the plane: 14 forced fast-scheme steps.  Per step the
+    pair keys, Newton iterations, q / v of every dynamic object and the
+    spheres' rotations."""
+    ang = np.deg2rad(15.0)
+    normal = (float(np.sin(ang)), float(np.cos(ang)), 0.0)
+    box = cn.box_mesh((0.04, 0.04, 0.04), (2, 2, 2), (0.1, 0.045, 0.0))
+    objs = [rsc.SoftSpec(name="box", mesh=box, young=2e4, poisson=0.3, density=800.0),
+            rsc.RigidSphereSpec(name="ball", mass=0.3, radius=0.02, position=(0.0, 0.0215, 0.0),
+                                velocity=(0.2, -0.3, 0.0, 0.0, 0.0, 4.0),
+                                inertia=np.diag([1e-4, 1.2e-4, 0.8e-4])),
+            rsc.RigidSphereSpec(name="marble", mass=0.05, radius=0.01, position=(-0.06, 0.012, 0.03),
+                                velocity=(0.0, 0.0, 0.0, 0.0, 0.0, 0.0),
+                                inertia=(0.4 * 0.05 * 0.01 ** 2) * np.eye(3)),
+            rsc.PlaneSpec(name="ground", normal=normal, offset=0.0)]
+    cfg = rsc.SceneConfig(objects=objs, h=0.01, threshold=0.006,
+                          pgs=rsol.PgsConfig(max_iterations=500, tolerance=1e-11, friction=0.4),
+                          newton=rsol.NewtonConfig(scheme="fast", max_iterations=3, penetration_tol=-1,
+                                                   rotation_tol=-1),
+                          output=rsc.OutputConfig(snapshots=False, metrics=False))
+    sim = rsc.Simulation(cfg)
+    out = {}
+    for st in range(14):
+        ctx, free, states, pen_before, timings, t_next = sim.prepare_step(build_wg=True)
+        res = rsol.newton_fast(ctx, cfg.newton, cfg.pgs)
+        out[f"s{st}_keys"] = np.array([(p.object_a, p.object_b, p.vertex_id, p.element_id) for p in ctx.pairs],
+                                      dtype=np.int64).reshape(-1, 4)
+        if ctx.pairs:
+            out[f"s{st}_lamhist"] = np.stack(res.lam_history)
+        rep = sim.step()
+        out[f"s{st}_npairs"] = rep.c_groups
+        out[f"s{st}_newton"] = rep.newton_iterations
+        for obj in sim.dynamic_objects:
+            out[f"s{st}_q{obj.oid}"] = obj.state.q.copy()
+            out[f"s{st}_v{obj.oid}"] = obj.state.v.copy()
+            if obj.kind == "rigid":
+                out[f"s{st}_R{obj.oid}"] = obj.rotation.copy()
+        print("rigid_spheres step", st, "pairs", rep.c_groups, "newton", rep.newton_iterations,
+              "pgs", rep.pgs_iterations_total, flush=True)
+    out.update(box_nodes=box.nodes, box_tets=box.tets, normal=np.array(normal))
+    save("rigid_spheres.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kat_rebuild", "kat_pgs", "kat_frames", "kat_linalg", "scenes", "scenes_standard",
                              "scene_io", "cylinder_press"]

@@ -37,3 +37,17 @@ def test_out_of_range_and_dofless_kinds():
         attachment_triplets(Attachment(AttachKind.RIGID_LOCAL, 0, lever=np.zeros(3)), 30, 0)
     with pytest.raises(InvalidAttachmentError):
         attachment_triplets(Attachment(AttachKind.WORLD, 0, world_point=np.zeros(3)), 30, 0)
+
+
+def test_rigid_mapping_rows():
+    """S for a sphere-plane pair (collision.py:290-316, rows collision.py:448-457):
+    [I, -skew(lever)], the plane side carrying no DoFs."""
+    import paper_2306_06946_b200 as cn
+
+    sph = cn.SphereGeometry(0, np.array([0.0, 0.05, 0.0]), 0.05, cn.Pose(np.eye(3), np.array([0.0, 0.05, 0.0])))
+    pairs = cn.detect([sph, cn.PlaneGeometry(1, np.array((0.0, 1.0, 0.0)), 0.0)], 0.01)
+    assert len(pairs) == 1 and pairs[0].attach_a.kind == cn.AttachKind.RIGID_LOCAL
+    S = cn.build_signed_mapping(pairs, 0, 6).csr.toarray()
+    lever = np.array([0.0, -0.05, 0.0])
+    skew = np.array([[0.0, -lever[2], lever[1]], [lever[2], 0.0, -lever[0]], [-lever[1], lever[0], 0.0]])
+    assert np.array_equal(S, np.hstack([np.eye(3), -skew]))

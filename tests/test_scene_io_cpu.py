@@ -75,3 +75,27 @@ def test_metrics_schema(sc):
     with open(os.path.join(GOLDEN, "scene_io_metrics.csv")) as fh:
         header = next(csv.reader(fh))
     assert tuple(header) == tuple(sc.StepReport.CSV_FIELDS)
+
+
+def test_rigid_sphere_entry(tmp_path):
+    """rigid_sphere scene entries (reference scene.py:268-290): default solid-sphere
+    inertia, 3- or 6-component velocities, validation."""
+    import numpy as np
+    import pytest
+
+    from paper_2306_06946_b200.errors import ValidationError
+    from paper_2306_06946_b200.scene import RigidSphereSpec, load_scene
+
+    path = tmp_path / "r.scn"
+    path.write_text("objects:\n  - {name: b, type: rigid_sphere, mass: 2.0, radius: 0.1, position: [0, 1, 0],"
+                    " velocity: [1, 0, 0]}\n  - {name: c, type: rigid_sphere, mass: 1.0, radius: 0.2,"
+                    " inertia: [1, 2, 3], velocity: [0, 0, 0, 0, 0, 5]}\n  - {name: g, type: plane}\n")
+    cfg = load_scene(path)
+    b, c = cfg.objects[0], cfg.objects[1]
+    assert isinstance(b, RigidSphereSpec) and b.mass == 2.0 and b.position == (0.0, 1.0, 0.0)
+    assert np.allclose(b.inertia, 0.4 * 2.0 * 0.01 * np.eye(3), rtol=1e-15, atol=0)
+    assert b.velocity == (1.0, 0.0, 0.0, 0.0, 0.0, 0.0)
+    assert np.array_equal(c.inertia, np.diag([1.0, 2.0, 3.0])) and c.velocity[5] == 5.0
+    path.write_text("objects:\n  - {name: b, type: rigid_sphere, mass: 1, radius: 1, velocity: [1, 2]}\n")
+    with pytest.raises(ValidationError):
+        load_scene(path)
