@@ -309,6 +309,12 @@ def assemble_Wg(S_by_object: dict, F_by_object: dict, group=None) -> MappingDela
     return MappingDelassus(_sum_compliance([per[o] for o in ids], dim), per)
 
 
+def sum_compliance(per: dict, dim: int) -> MappingDelassus:
+    """W_g from per-object parts already formed (object_compliance), summed in
+    ascending object id like assemble_Wg."""
+    return MappingDelassus(_sum_compliance([per[o] for o in sorted(per)], dim), per)
+
+
 def rebuild_W_fast(D: DirectionMatrix, wg: MappingDelassus, out: torch.Tensor | None = None) -> Delassus:
     """W = D W_g D^T (constraints.py:182-191), bit-identical to the reference."""
     if D.c != wg.dim:
