@@ -19,9 +19,9 @@ long long cnb_launch_count(void);
  * stamp() calls in csrc/pgs.cu.  CNB_E_VALIDATION when profiling is off. */
 int cnb_pgs_profile(double* out);
 
-/* Summed cycles of the POTRF kernel's phases (CTA 0 of every launch) since the
- * last call: out[0] loads, [1] factor, [2] store L, [3] inverse, [4] store
- * L^{-1}, out[7] launches. */
+/* Summed cycles of the 32 x 32 POTRF phases (every call, standalone or fused
+ * into the SYRK; warp 0, the inverse runs beside it on warp 1) since the last
+ * call: out[0] loads, [1] elimination loop, out[7] calls. */
 int cnb_potrf_profile(double* out);
 
 /* fp64 DMMA GEMM tile-shape variants, C = A B (row-major; sizes multiples of
@@ -29,9 +29,10 @@ int cnb_potrf_profile(double* out);
 int cnb_bench_gemm(int32_t variant, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                    int64_t ldb, double* C, int64_t ldc, void* stream);
 
-/* Cycles per dependent op (out: host, 6): DFMA, DADD, fp64 div, fp64 sqrt,
- * 64-bit shuffle, FFMA. */
-int cnb_bench_latency(double* out /* 9 doubles */, void* stream);
+/* out (host, 12): cycles per dependent op -- DFMA, DADD, fp64 div, fp64 sqrt,
+ * 64-bit shuffle, FFMA, select, MUFU.RSQ64H, DMUL -- then one warp's issue
+ * cost: cycles per DFMA, per broadcast LDS.64, per POTRF bulk step. */
+int cnb_bench_latency(double* out /* 12 doubles */, void* stream);
 
 /* fp64 MMA (DMMA) throughput of the whole GPU in TFLOP/s (out: host): the
  * tensor roofline denominator (not in MEASURED_PEAKS.json). */

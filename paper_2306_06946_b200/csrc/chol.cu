@@ -82,121 +82,167 @@ __global__ void __launch_bounds__(256, 6) extend_add_kernel(DevSym S, const int3
   }
 }
 
-// POTRF of the kw x kw diagonal block of panel k0 and the inverse of the
-// resulting L_kk (kept in kkinv slot kk_off[s] + panel, 32 x 32 row-major, for
-// the TRSM and the inversion of L11 (solve.cu trinv_kernel); the TRSM
-// then is a plain DMMA product).  One CTA per front, one thread per block
-// entry (32 x 32 = 1024 threads): every elimination step is a single
-// parallel update between barriers, and the code stays a compact loop
-// (a fully unrolled register version thrashes the instruction cache).
-// Rows / columns >= kw are padded with the identity.
-// diagnostic: cycle sums of potrf phases (CTA 0 of every launch), cnb_potrf_profile
+// diagnostic: cycle sums of potrf phases (loads, factor + inverse) and calls, cnb_potrf_profile
 __device__ unsigned long long g_potrf_prof[8];
 
-// POTRF of panel k0's diagonal block of front s by one warp (lane = threadIdx.x
-// & 31), right-looking: at step j every lane i > j scales its l_ij and updates
-// its own row a[i][j+1..i] with the broadcast column j.  The update loops are
-// unrolled by 8 with predication so a lane keeps eight independent shared loads /
-// FMAs in flight (a single warp has nothing else to hide latency with).  1/sqrt
-// comes from rsqrt.approx + two Newton steps: the libm sqrt and the IEEE
-// division are long subroutines on the sequential chain.  Then Y = L^{-1} by the
-// same scheme, lane c owning column c (in place: Y starts as the identity).
-// a, y: kPanel x (kPanel + 1) shared scratch, rd: kPanel.
-__device__ void potrf_panel(const DevSym& S, int64_t s, int k0, double* __restrict__ front,
-                            double* __restrict__ kkinv, DevStatus* st, double (*a)[kPanel + 1],
-                            double (*y)[kPanel + 1], double* rd, bool stamp) {
+// POTRF of the kw x kw diagonal block of panel k0 and the inverse of the
+// resulting L_kk (kept in kkinv slot kk_off[s] + panel, 32 x 32 row-major, for
+// the TRSM and the inversion of L11 (solve.cu trinv_kernel); the TRSM then is a
+// plain DMMA product).  Two warps (threads 0..63 of the CTA); rows / columns
+// >= kw are padded with the identity.
+//
+// Warp 0 factors.  Lane i keeps row i in registers as a shift register: before
+// elimination step j, a[q] holds column j + q, so every step touches the same
+// compile-time register names (a runtime-indexed register array would spill to
+// local memory, and unrolling the 32 steps thrashes the instruction cache).
+// Step j: lane i scales its l_ij, column j of L goes to shared memory, and
+// a[q] <- a[q + 1] - l_ij l_(j+1+q),j for the columns that still exist (the
+// steps run in four phases of decreasing width).  Only the next pivot is on
+// the sequential chain, and lane j + 1 forms it from its own l_(j+1),j:
+// broadcast, rsqrt, scale -- placed between the bulk multiply-adds in program
+// order so that in-order issue overlaps them.  Columns are read as 16-byte
+// pairs (row j of the scratch is offset so that element j + 1 is aligned).
+// L goes back to the front after the loop: a global store inside it would make
+// every step's release (a CTA memory barrier) wait for the store's completion.
+// Warp 1 forms Y = L^{-1} (lane c owns column c, shift register u = rows j + q)
+// from the published columns, one step behind (a shared-memory flag per step).
+// Fused multiply-adds in the order of the step-by-step definition.
+// cols: kPanel rows of 2 kPanel doubles (column j of L, rows >= 32 zero), then
+// kPanel reciprocal pivots, then the step flag.
+constexpr int kPotrfSmem = (2 * kPanel * kPanel + kPanel + 2) * (int)sizeof(double);
+__device__ __forceinline__ double* potrf_col(double* cols, int j) { return cols + j * (2 * kPanel) + ((j + 1) & 1); }
+
+// one elimination step with QN live columns after the pivot: returns the next
+// pivot's inverse square root through (d, inv)
+template <int QN>
+__device__ __forceinline__ void potrf_step(double (&a)[kPanel], int j, int i, int kw, double* cols, double* rd,
+                                           unsigned flag_s, double& d, double& inv, int& bad, double& bad_d) {
+  double* col = potrf_col(cols, j);
+  const bool fail = bad < 0 && j < kw && !(d > 0.0);
+  bad = fail ? j : bad;
+  bad_d = fail ? d : bad_d;
+  const double lij = (i == j ? d : a[0]) * inv;  // rows above j: never read
+  col[i] = lij;
+  if (i == 0) rd[j] = inv;
+  __syncwarp();
+  if (i == 0) asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(flag_s), "r"(j + 1) : "memory");
+  d = __shfl_sync(0xffffffffu, fma(-lij, lij, a[1]), (j + 1) & 31);
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double hd = -0.5 * d;
+  const double2* c2 = reinterpret_cast<const double2*>(col + j + 1);
+#pragma unroll
+  for (int q0 = 0; q0 < QN; q0 += 8) {
+    double lk[8];
+#pragma unroll
+    for (int v = 0; v < 8; v += 2)
+      if (q0 + v < QN) {
+        const double2 t = c2[(q0 + v) / 2];
+        lk[v] = t.x;
+        lk[v + 1] = t.y;
+      }
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      if (q0 + v < QN) a[q0 + v] = fma(-lij, lk[v], a[q0 + v + 1]);
+    if (q0 == 0 || q0 == (QN > 16 ? 16 : 8)) r = r * fma(hd, r * r, 1.5);
+  }
+  if (QN <= 8) r = r * fma(hd, r * r, 1.5);  // (one bulk chunk only)
+  inv = d > 0.0 ? r : __longlong_as_double(0x7ff8000000000000LL);
+}
+
+template <int QN>
+__device__ __forceinline__ void inverse_step(double (&u)[kPanel], int j, int i, const double* cols, const double* rd,
+                                             unsigned flag_s, double* Y) {
+  for (;;) {  // acquire: the column's stores are visible once its flag is
+    int v;
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(flag_s) : "memory");
+    if (v > j) break;
+  }
+  const double* col = potrf_col(const_cast<double*>(cols), j);
+  const double yj = u[0] * rd[j];  // (L^{-1})[j][i]
+  Y[j * kPanel + i] = yj;
+  const double2* c2 = reinterpret_cast<const double2*>(col + j + 1);
+#pragma unroll
+  for (int q0 = 0; q0 < QN; q0 += 8) {
+    double lk[8];
+#pragma unroll
+    for (int v = 0; v < 8; v += 2)
+      if (q0 + v < QN) {
+        const double2 t = c2[(q0 + v) / 2];
+        lk[v] = t.x;
+        lk[v + 1] = t.y;
+      }
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      if (q0 + v < QN) u[q0 + v] = fma(-lk[v], yj, u[q0 + v + 1]);
+  }
+}
+
+__device__ __noinline__ void potrf_panel(const DevSym& S, int64_t s, int k0, double* __restrict__ front,
+                                         double* __restrict__ kkinv, DevStatus* st, double* __restrict__ cols) {
   const int64_t nc = d_nc(S, s), ldf = d_ldf(S, s);
   const int kw = (int)min((int64_t)kPanel, nc - k0);
-  double* F = front + S.front_off[s];
-  const int i = threadIdx.x & 31;
-  long long ts[6];
+  double* rd = cols + 2 * kPanel * kPanel;
+  const unsigned flag_s = smem_u32(rd + kPanel);
+  const int i = threadIdx.x & 31, w = (threadIdx.x >> 5) & 1;
+  for (int e = threadIdx.x & 63; e < 2 * kPanel * kPanel; e += 64) cols[e] = 0.0;
+  if (threadIdx.x == 0) *reinterpret_cast<int*>(rd + kPanel) = 0;
+  asm volatile("bar.sync 1, 64;" ::: "memory");
+  if (w == 1) {  // ---- inverse ----
+    double* Y = kkinv + (S.kk_off[s] + k0 / kPanel) * (kPanel * kPanel);
+    double u[kPanel];
+#pragma unroll
+    for (int l = 0; l < kPanel; ++l) u[l] = l == i ? 1.0 : 0.0;
+    int j = 0;
+    for (; j < 8; ++j) inverse_step<31>(u, j, i, cols, rd, flag_s, Y);
+    for (; j < 16; ++j) inverse_step<23>(u, j, i, cols, rd, flag_s, Y);
+    for (; j < 24; ++j) inverse_step<15>(u, j, i, cols, rd, flag_s, Y);
+    for (; j < 32; ++j) inverse_step<7>(u, j, i, cols, rd, flag_s, Y);
+    return;
+  }
+  // ---- factor ----
+  double* F = front + S.front_off[s] + (int64_t)k0 * ldf + k0;
+  long long ts[3];
   ts[0] = clock64();
-#pragma unroll 8
-  for (int l = 0; l < kPanel; ++l)  // lane i loads row i, column by column: coalesced over rows
-    a[i][l] = (i < kw && l < kw && l <= i) ? F[(int64_t)(k0 + l) * ldf + k0 + i] : (l == i ? 1.0 : 0.0);
-  __syncwarp();
+  double a[kPanel];
+#pragma unroll
+  for (int l = 0; l < kPanel; ++l)
+    a[l] = (i < kw && l < kw && l <= i) ? F[(int64_t)l * ldf + i] : (l == i ? 1.0 : 0.0);
   ts[1] = clock64();
-  for (int j = 0; j < kPanel; ++j) {
-    const double d = a[j][j];
-    const double aij = a[i][j];
-    if (j < kw && !(d > 0.0) && i == 0) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + j), d);
-    double inv;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(d));
-    inv = inv * fma(-0.5 * d, inv * inv, 1.5);
-    inv = inv * fma(-0.5 * d, inv * inv, 1.5);
-    if (!(d > 0.0)) inv = __longlong_as_double(0x7ff8000000000000LL);
-    const double lij = aij * inv;
-    __syncwarp();
-    if (i == j) {
-      a[j][j] = d * inv;
-      rd[j] = inv;
-    }
-    if (i > j) a[i][j] = lij;
-    __syncwarp();
-    for (int k0u = j + 1; k0u < kPanel; k0u += 8) {
-      double lk[8], ai[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = min(k0u + u, kPanel - 1);
-        lk[u] = a[k][j];
-        ai[u] = a[i][k];
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = k0u + u;
-        if (k < kPanel && k <= i) a[i][k] = fma(-lij, lk[u], ai[u]);
-      }
-    }
-    __syncwarp();
-  }
+  double d = __shfl_sync(0xffffffffu, a[0], 0);
+  double inv;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(d));
+  inv = inv * fma(-0.5 * d, inv * inv, 1.5);
+  inv = inv * fma(-0.5 * d, inv * inv, 1.5);
+  inv = d > 0.0 ? inv : __longlong_as_double(0x7ff8000000000000LL);
+  int bad = -1;
+  double bad_d = 0.0;
+  int j = 0;
+  for (; j < 8; ++j) potrf_step<31>(a, j, i, kw, cols, rd, flag_s, d, inv, bad, bad_d);
+  for (; j < 16; ++j) potrf_step<23>(a, j, i, kw, cols, rd, flag_s, d, inv, bad, bad_d);
+  for (; j < 24; ++j) potrf_step<15>(a, j, i, kw, cols, rd, flag_s, d, inv, bad, bad_d);
+  for (; j < 32; ++j) potrf_step<7>(a, j, i, kw, cols, rd, flag_s, d, inv, bad, bad_d);
   ts[2] = clock64();
-#pragma unroll 8
+  // L back into the front (a store inside the loop would make every step's
+  // release fence wait for it): lane i writes row i, column by column
+#pragma unroll 1
   for (int l = 0; l < kw; ++l)
-    if (i < kw && l <= i) F[(int64_t)(k0 + l) * ldf + k0 + i] = a[i][l];
-  ts[3] = clock64();
-  // Y = L^{-1}: lane c owns column c; step r: y[r][c] *= 1/L[r][r] (= rd[r]), then
-  // rows below subtract L[q][r] y[r][c]
-  const int c = i;
-#pragma unroll 8
-  for (int r = 0; r < kPanel; ++r) y[r][c] = (r == c) ? 1.0 : 0.0;
-  __syncwarp();
-  for (int r = 0; r < kPanel; ++r) {
-    const double yr = y[r][c] * rd[r];
-    y[r][c] = yr;
-    for (int q0 = r + 1; q0 < kPanel; q0 += 8) {
-      double lq[8], yq[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int q = min(q0 + u, kPanel - 1);
-        lq[u] = a[q][r];
-        yq[u] = y[q][c];
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (q0 + u < kPanel) y[q0 + u][c] = fma(-lq[u], yr, yq[u]);
-    }
-  }
-  __syncwarp();
-  ts[4] = clock64();
-  double* Y = kkinv + (S.kk_off[s] + k0 / kPanel) * (kPanel * kPanel);  // kept for the TRSM and L11^{-1}
-#pragma unroll 8
-  for (int r = 0; r < kPanel; ++r) Y[r * kPanel + c] = y[r][c];
-  ts[5] = clock64();
-  if (stamp && i == 0) {
-    for (int k = 0; k < 5; ++k) atomicAdd(&g_potrf_prof[k], (unsigned long long)(ts[k + 1] - ts[k]));
+    if (i >= l && i < kw) F[(int64_t)l * ldf + i] = potrf_col(cols, l)[i];
+  if (bad >= 0 && i == 0) raise_status(st, CNB_E_NOT_SPD, (int)(S.first[s] + k0 + bad), bad_d);
+  if (i == 0) {
+    atomicAdd(&g_potrf_prof[0], (unsigned long long)(ts[1] - ts[0]));
+    atomicAdd(&g_potrf_prof[1], (unsigned long long)(ts[2] - ts[1]));
     atomicAdd(&g_potrf_prof[7], 1ull);
   }
 }
 
 // POTRF of every front's first panel (later panels are factored at the end of the
 // SYRK update that last touches them, see syrk_kernel)
-__global__ void __launch_bounds__(32) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
+__global__ void __launch_bounds__(64) potrf_kernel(DevSym S, const int32_t* __restrict__ tasks, int k0,
                                                    double* __restrict__ front, double* __restrict__ kkinv,
                                                    DevStatus* st) {
-  __shared__ double a[kPanel][kPanel + 1];
-  __shared__ double y[kPanel][kPanel + 1];
-  __shared__ double rd[kPanel];
-  potrf_panel(S, tasks[blockIdx.x], k0, front, kkinv, st, a, y, rd, blockIdx.x == 0);
+  __shared__ __align__(16) double cols[kPotrfSmem / sizeof(double)];
+  potrf_panel(S, tasks[blockIdx.x], k0, front, kkinv, st, cols);
 }
 
 // TRSM of the rows below the diagonal block: X = B L_kk^{-T} as a DMMA product
@@ -268,7 +314,8 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
 // are conflict-free with a row stride == 4 mod 16 doubles.
 constexpr int kSK = kTile + 4;  // smem stride of one k column of a staged tile
 constexpr size_t kSyrkSmem = 2 * 2 * kPanel * kSK * sizeof(double);
-__global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode,
+static_assert(kPotrfSmem <= kSyrkSmem, "the fused POTRF reuses the SYRK staging buffers");
+__global__ void __launch_bounds__(128, 3) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode,
                                                    double* __restrict__ front, double* __restrict__ kkinv,
                                                    DevStatus* st) {
   extern __shared__ __align__(16) double syrk_sm[];
@@ -384,11 +431,7 @@ __global__ void __launch_bounds__(128) syrk_kernel(DevSym S, const int32_t* __re
   // it receives) factors it right away: no separate POTRF launch for panels > 0
   if (ti == 0 && tj == 0 && t0 < nc) {
     __syncthreads();  // the tile's stores are visible to the CTA
-    if (warp == 0) {
-      double (*a)[kPanel + 1] = reinterpret_cast<double (*)[kPanel + 1]>(syrk_sm);
-      double (*y)[kPanel + 1] = reinterpret_cast<double (*)[kPanel + 1]>(syrk_sm + kPanel * (kPanel + 1));
-      potrf_panel(S, s, (int)t0, front, kkinv, st, a, y, syrk_sm + 2 * kPanel * (kPanel + 1), false);
-    }
+    if (warp < 2) potrf_panel(S, s, (int)t0, front, kkinv, st, syrk_sm);
   }
 }
 
@@ -552,7 +595,7 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
     for (size_t p = 0; p < h->potrf[l].size(); ++p) {
       const int k0 = (int)(p * kPanel);
       if (p == 0 && h->potrf[l][p].count) {  // later panels: fused into the preceding SYRK
-        potrf_kernel<<<(unsigned)h->potrf[l][p].count, 32, 0, st>>>(sym, h->potrf[l][p].ptr, k0, h->d_front,
+        potrf_kernel<<<(unsigned)h->potrf[l][p].count, 64, 0, st>>>(sym, h->potrf[l][p].ptr, k0, h->d_front,
                                                                        h->d_kkinv, d_status);
         CNB_LAUNCH_CHECK("potrf_kernel");
       }

@@ -65,6 +65,61 @@ __global__ void latency_kernel(int n, double seed, double* out, long long* cyc) 
   }
 }
 
+// Single-warp issue throughput (cycles per warp instruction / per bulk step):
+// out[0] DFMA, 8 independent chains; out[1] LDS.64 of one broadcast address;
+// out[2] the 32x32 POTRF's bulk step (31 broadcast LDS.64 + 31 DFMA, shift
+// register, as chol.cu potrf_panel).
+__global__ void throughput_kernel(int n, double seed, double* out, long long* cyc) {
+  __shared__ double sm[128];
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < 128; e += 32) sm[e] = 1.0 + 1e-9 * e;
+  __syncwarp();
+  double c[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c[k] = seed + k;
+  long long t0 = clock64();
+  for (int it = 0; it < n; ++it) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = fma(c[k], 1.0000001, 1e-9);
+  }
+  long long t1 = clock64();
+  double acc = 0.0;
+  volatile int off = 0;
+  const int o = off;
+  for (int it = 0; it < n; ++it) {
+    double v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = sm[(o + it + k) & 127];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc += v[k] * 0.0;  // cheap consumer (DADD chain, 1 per load)
+  }
+  long long t2 = clock64();
+  double a[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) a[k] = seed + k + lane;
+  for (int it = 0; it < n; ++it) {
+    const double lij = a[0] * 1e-3;
+    const double* col = sm + (it & 63);
+#pragma unroll
+    for (int q = 0; q < 31; ++q) a[q] = fma(-lij, col[q + 1], a[q + 1]);
+    a[31] = 1.0;
+  }
+  long long t3 = clock64();
+  double s = acc;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += c[k];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) s += a[k];
+  if (lane == 0) {
+    cyc[0] = t1 - t0;
+    cyc[1] = t2 - t1;
+    cyc[2] = t3 - t2;
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
 // GEMM tile-shape experiments (C = A B, row-major, fp64 DMMA): BM x BN CTA tile,
 // WM x WN warp tiles, BK-deep k chunks double-buffered with cp.async (8- or
 // 16-byte copies), A staged [m][k], B staged [k][n] (both conflict-free
@@ -191,20 +246,26 @@ using namespace cnb;
 
 extern "C" {
 
-// out (host, 9 doubles): cycles per dependent op, see latency_kernel.
+// out (host, 12 doubles): [0..8] cycles per dependent op, see latency_kernel;
+// [9..11] single-warp issue throughput, see throughput_kernel.
 int cnb_bench_latency(double* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   double* d = nullptr;
   long long* c = nullptr;
   CNB_CUDA(cudaMalloc(&d, sizeof(double)));
-  CNB_CUDA(cudaMalloc(&c, 9 * sizeof(long long)));
+  CNB_CUDA(cudaMalloc(&c, 12 * sizeof(long long)));
   const int n = 4096;
   latency_kernel<<<1, 32, 0, st>>>(n, 1.5, d, c);
   CNB_LAUNCH_CHECK("latency_kernel");
-  long long h[9];
+  throughput_kernel<<<1, 32, 0, st>>>(n, 1.5, d, c + 9);
+  CNB_LAUNCH_CHECK("throughput_kernel");
+  long long h[12];
   CNB_CUDA(cudaMemcpyAsync(h, c, sizeof(h), cudaMemcpyDeviceToHost, st));
   CNB_CUDA(cudaStreamSynchronize(st));
   for (int k = 0; k < 9; ++k) out[k] = (double)h[k] / n;
+  out[9] = (double)h[9] / (n * 32.0);
+  out[10] = (double)h[10] / (n * 32.0);
+  out[11] = (double)h[11] / n;
   cudaFree(d);
   cudaFree(c);
   return CNB_OK;

@@ -47,7 +47,7 @@ def main():
     _lib.call("cnb_potrf_profile", pp)
     n = max(pp[7], 1)
     print(json.dumps({"potrf_cycles_per_launch": {k: round(pp[i] / n) for i, k in enumerate(
-        ["loads", "factor", "store_L", "inverse", "store_Y"])}, "launches": pp[7]}), flush=True)
+        ["loads", "elimination_loop"])}, "launches": pp[7]}), flush=True)
     ms = min(times)
     print(json.dumps({"dofs": body.n_dofs, "supernodes": F.n_supernodes, "levels": F.n_levels, "nnz_L": F.nnz_L,
                       "gflop": round(F.flops / 1e9, 1), "ms": round(ms, 3),
