@@ -1012,8 +1012,9 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
 #pragma unroll
           for (int a = 0; a < 3; ++a) lamc[3 * lane + a] = lm[a];
         __syncwarp();
-        __threadfence_block();
-        if (lane == 0) vcnt[0] = t + 1;  // lambda_b in shared memory: the publisher takes it
+        if (lane == 0)  // lambda_b in shared memory: the publisher takes it (release: no full fence)
+          asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32((const void*)&vcnt[0])), "r"(t + 1)
+                       : "memory");
         if (b == nb - 1) {  // end of sweep: ||dlam||^2 and this block's ||lambda||^2
           const double l2 = mine ? (lm[0] * lm[0] + lm[1] * lm[1]) + lm[2] * lm[2] : 0.0;
           const double sl = warp_sum(l2), sd = warp_sum(dsq);
@@ -1210,9 +1211,10 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
           while (vcnt[0] < t + 1 && !*(volatile int*)&sm.flags[2]) __nanosleep(20);
           if (*(volatile unsigned*)&ctl->timeout) sm.flags[0] = 1;  // watchdog fired elsewhere
         }
-        const unsigned go = __shfl_sync(0xffffffffu, vcnt[0] >= t + 1 ? 1u : 0u, 0);
+        unsigned seen;
+        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(seen) : "r"(smem_u32((const void*)&vcnt[0])) : "memory");
+        const unsigned go = __shfl_sync(0xffffffffu, seen >= t + 1 ? 1u : 0u, 0);
         if (!go) break;
-        __threadfence_block();
         const int b = (int)(t % nb), rows = rows_of(b);
         const int64_t rb = 3 * (int64_t)b * kPG;
         const double* lamc = sm.lamx + (t & 1) * kPR;
@@ -1229,8 +1231,9 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         if (b < nb - 1) sumsq += warp_sum(v);
         if (b == nb - 2 && lane == 0) sm.red[2] = sumsq;
         __syncwarp();
-        __threadfence_block();
-        if (lane == 0) vcnt[1] = t + 1;
+        if (lane == 0)
+          asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32((const void*)&vcnt[1])), "r"(t + 1)
+                       : "memory");
       }
     }
     // everyone (publisher included): last lambda block is in global memory; release the grid
