@@ -453,12 +453,9 @@ static int chol_upload(CholHandle* h) {
   UP(d_map_dst, map_dst)
   UP(d_perm, perm)
 #undef UP
-  h->linv_off.assign(S.ns + 1, 0);
-  for (int64_t s = 0; s < S.ns; ++s) h->linv_off[s + 1] = h->linv_off[s] + S.nc(s) * S.nc(s);
-  if ((rc = upload_vec(&h->d_linv_off, h->linv_off)) != CNB_OK) return rc;
-  h->p21_off.assign(S.ns + 1, 0);
-  for (int64_t s = 0; s < S.ns; ++s) h->p21_off[s + 1] = h->p21_off[s] + S.nr(s) * S.nc(s);
-  if ((rc = upload_vec(&h->d_p21_off, h->p21_off)) != CNB_OK) return rc;
+  h->m_off.assign(S.ns + 1, 0);
+  for (int64_t s = 0; s < S.ns; ++s) h->m_off[s + 1] = h->m_off[s] + S.ldf(s) * S.nc(s);
+  if ((rc = upload_vec(&h->d_m_off, h->m_off)) != CNB_OK) return rc;
   std::vector<int32_t> all;
   struct Rec {
     int64_t off, count;
@@ -525,8 +522,9 @@ static int chol_upload(CholHandle* h) {
     for (auto& r : so_rec[l]) h->syrk_out[l].push_back(mk(r));
   }
   CNB_CUDA(cudaMalloc((void**)&h->d_front, std::max<int64_t>(1, S.front_off[S.ns]) * sizeof(double)));
-  CNB_CUDA(cudaMalloc((void**)&h->d_linv, std::max<int64_t>(1, h->linv_off[S.ns]) * sizeof(double)));
-  CNB_CUDA(cudaMalloc((void**)&h->d_p21, std::max<int64_t>(1, h->p21_off[S.ns]) * sizeof(double)));
+  // the padding row of an odd-f panel is read by the 16-byte tile copies: keep it finite
+  CNB_CUDA(cudaMalloc((void**)&h->d_m, std::max<int64_t>(1, h->m_off[S.ns]) * sizeof(double)));
+  CNB_CUDA(cudaMemset(h->d_m, 0, std::max<int64_t>(1, h->m_off[S.ns]) * sizeof(double)));
   h->kk_off.assign(S.ns + 1, 0);
   for (int64_t s = 0; s < S.ns; ++s) h->kk_off[s + 1] = h->kk_off[s] + (S.nc(s) + kPanel - 1) / kPanel;
   if ((rc = upload_vec(&h->d_kk_off, h->kk_off)) != CNB_OK) return rc;
@@ -540,7 +538,7 @@ static int chol_upload(CholHandle* h) {
 static void chol_free(CholHandle* h) {
   void* ptrs[] = {h->d_first, h->d_rows_ptr, h->d_rows, h->d_front_off, h->d_child_ptr, h->d_child,
                   h->d_rel_ptr, h->d_rel, h->d_map_src, h->d_map_dst, h->d_perm, h->d_front, h->d_tasks,
-                  h->d_linv, h->d_linv_off, h->d_p21, h->d_p21_off, h->d_kkinv, h->d_vals, h->d_kk_off};
+                  h->d_m, h->d_m_off, h->d_kkinv, h->d_vals, h->d_kk_off};
   if (h->factor_exec) cudaGraphExecDestroy(h->factor_exec);
   h->factor_exec = nullptr;
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);

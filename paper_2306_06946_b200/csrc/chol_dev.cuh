@@ -21,14 +21,14 @@ struct DevSym {
   const int64_t* child;
   const int64_t* rel_ptr;
   const int32_t* rel;
-  const int64_t* linv_off;  // offsets of the inverted diagonal blocks L11^{-1}
-  const int64_t* p21_off;   // offsets of P21 = L21 L11^{-1} (nr x nc, column-major)
+  const int64_t* m_off;     // solve panels M_s = [L11^{-1}; P21] (f x nc, column-major, ld d_ldf)
   const int64_t* kk_off;    // first 32x32 diagonal-block inverse of each supernode (kkinv slots)
 };
 
 __device__ __forceinline__ int64_t d_nc(const DevSym& S, int64_t s) { return S.first[s + 1] - S.first[s]; }
 __device__ __forceinline__ int64_t d_nr(const DevSym& S, int64_t s) { return S.rows_ptr[s + 1] - S.rows_ptr[s]; }
-// column stride of front s (f rounded up to even: 16-byte aligned columns), Symbolic::ldf
+// column stride of front s (f rounded up to even: 16-byte aligned columns), Symbolic::ldf;
+// also the stride of the solve panel M_s and of the right-hand-side blocks R_s
 __device__ __forceinline__ int64_t d_ldf(const DevSym& S, int64_t s) {
   const int64_t f = d_nc(S, s) + d_nr(S, s);
   return f + (f & 1);
@@ -71,13 +71,11 @@ struct CholHandle {
   bool factored = false;
   int64_t *d_first = nullptr, *d_rows_ptr = nullptr, *d_rows = nullptr, *d_front_off = nullptr;
   int64_t *d_child_ptr = nullptr, *d_child = nullptr, *d_rel_ptr = nullptr, *d_perm = nullptr;
-  int64_t* d_linv_off = nullptr;
-  int64_t* d_p21_off = nullptr;
+  int64_t* d_m_off = nullptr;
   int32_t* d_rel = nullptr;
   int64_t *d_map_src = nullptr, *d_map_dst = nullptr;
   double* d_front = nullptr;
-  double* d_linv = nullptr;
-  double* d_p21 = nullptr;
+  double* d_m = nullptr;       // solve panels M_s = [L11^{-1}; P21 = L21 L11^{-1}], see DevSym::m_off
   double* d_kkinv = nullptr;  // inverse of every 32x32 panel diagonal block (slot kk_off[s] + panel)
   int64_t* d_kk_off = nullptr;
   std::vector<int64_t> kk_off;
@@ -86,7 +84,7 @@ struct CholHandle {
   cudaStream_t cap_stream = nullptr;
   void* factor_status = nullptr;
   long long factor_nodes = 0;
-  std::vector<int64_t> linv_off, p21_off;
+  std::vector<int64_t> m_off;
   int32_t* d_tasks = nullptr;
   std::vector<DevTasks> ea, trinv, p21;                  // per level
   std::vector<std::vector<DevTasks>> potrf, trsm, syrk, syrk_out;  // per level, per panel
@@ -99,7 +97,7 @@ struct CholHandle {
 
   DevSym sym() const {
     return DevSym{d_first,   d_rows_ptr, d_rows, d_front_off, d_child_ptr,
-                  d_child,   d_rel_ptr,  d_rel,  d_linv_off,  d_p21_off, d_kk_off};
+                  d_child,   d_rel_ptr,  d_rel,  d_m_off,     d_kk_off};
   }
 };
 

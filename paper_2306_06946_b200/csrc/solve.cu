@@ -5,10 +5,13 @@
 // (constraints.py:175-178).
 //
 // At factorisation time every diagonal block L11 of a supernode is inverted
-// (trinv_kernel).  A forward solve step of supernode s is then one
-// matrix product over its front panel M_s = [L11^{-1}; L21] (f_s x nc_s):
+// (trinv_kernel) and P21 = L21 L11^{-1} formed (p21_kernel).  A forward solve
+// step of supernode s is then one matrix product over its solve panel
+// M_s = [L11^{-1}; P21] (f_s x nc_s, column-major, even column stride ldf_s):
 //     [y_s ; u_s] = M_s r_s,   y_s -> solution rows,  R_parent -= u_s (extend-add)
-// and a backward step is two GEMVs,  x_s = L11^{-T} (y_s - L21^T x_rows).
+// and a backward step is two GEMVs,  x_s = L11^{-T} y_s - P21^T x_rows.
+// Right-hand-side blocks R_s use the same even stride, so every tile column of
+// M_s and R_s starts 16-byte aligned (16-byte asynchronous copies).
 // No serial triangle chains remain on the solve path: single right-hand
 // sides are coalesced GEMVs (bandwidth-bound), the compliance's many
 // right-hand sides are fp64 tensor-core GEMMs (mma.sync m8n8k4 f64 = DMMA).
@@ -28,21 +31,14 @@ constexpr int kBwdRows = 4;     // pivot rows per backward task (warp per row)
 constexpr int kMT = 64;         // DMMA panel tile (rows, cols)
 constexpr int kMA = kMT + 4;    // k-major stride of tiles staged from column-major sources
 
-// RHS block of supernode s: R_s = rhs + roff[s], f_s x w_s column-major;
-// global columns [lo_s, lo_s + w_s).
+// RHS block of supernode s: R_s = rhs + roff[s], f_s x w_s column-major with
+// column stride ldf_s (d_ldf); global columns [lo_s, lo_s + w_s).
 struct RhsView {
   double* rhs;
   const int64_t* roff;
   const int64_t* lo;
   const int64_t* w;
 };
-
-__device__ __forceinline__ double panel_entry(const double* __restrict__ P, const double* __restrict__ Li,
-                                              int64_t nc, int64_t nr, int64_t i, int64_t j) {
-  // M_s[i][j]: rows < nc from L11^{-1} (lower), rows >= nc from P21 = L21 L11^{-1}
-  if (i < nc) return j <= i ? Li[j * nc + i] : 0.0;
-  return P[j * nr + (i - nc)];
-}
 
 // ---- L11^{-1}, kInvCols columns per task -----------------------------------------
 // Block forward substitution L11 X = I over 32-row blocks: the diagonal block
@@ -52,18 +48,18 @@ __device__ __forceinline__ double panel_entry(const double* __restrict__ P, cons
 static_assert(32 * kInvCols == 256, "trinv_kernel: one warp per column of the block (256 threads)");
 __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                     const double* __restrict__ front, const double* __restrict__ kkinv,
-                                                    double* __restrict__ linv) {
+                                                    double* __restrict__ panel) {
   __shared__ double sD[32][33];
   __shared__ double v[32][kInvCols];
   __shared__ double y[32][kInvCols];
   const int64_t s = tasks[2 * blockIdx.x], j0 = tasks[2 * blockIdx.x + 1];
   const int64_t nc = d_nc(S, s), ldf = d_ldf(S, s);
   const double* F = front + S.front_off[s];
-  double* X = linv + S.linv_off[s];
+  double* X = panel + S.m_off[s];  // rows [0, nc) of M_s (stride ldf)
   const int ncols = (int)min((int64_t)kInvCols, nc - j0);
   for (int64_t e = threadIdx.x; e < nc * ncols; e += blockDim.x) {
     const int64_t i = e % nc, c = e / nc;
-    X[(j0 + c) * nc + i] = (i == j0 + c) ? 1.0 : 0.0;
+    X[(j0 + c) * ldf + i] = (i == j0 + c) ? 1.0 : 0.0;
   }
   __syncthreads();
   const int r = threadIdx.x & 31, cc = threadIdx.x >> 5;  // (row, column) of the 32 x kInvCols block
@@ -74,7 +70,7 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
       const int a = e >> 5, b = e & 31;
       sD[a][b] = (a < bw && b <= a) ? D[e] : 0.0;
     }
-    if (cc < kInvCols) v[r][cc] = (r < bw && cc < ncols) ? X[(j0 + cc) * nc + kb + r] : 0.0;
+    if (cc < kInvCols) v[r][cc] = (r < bw && cc < ncols) ? X[(j0 + cc) * ldf + kb + r] : 0.0;
     __syncthreads();
     if (cc < kInvCols) {
       double a0 = 0.0, a1 = 0.0;
@@ -85,7 +81,7 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
       if ((r & 1) == 0) a0 = fma(sD[r][r], v[r][cc], a0);
       const double yv = a0 + a1;
       y[r][cc] = r < bw ? yv : 0.0;
-      if (r < bw && cc < ncols) X[(j0 + cc) * nc + kb + r] = yv;
+      if (r < bw && cc < ncols) X[(j0 + cc) * ldf + kb + r] = yv;
     }
     __syncthreads();
     for (int64_t i = kb + bw + threadIdx.x; i < nc; i += blockDim.x) {
@@ -97,7 +93,7 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
 #pragma unroll
         for (int c = 0; c < kInvCols; ++c) acc[c] = fma(l, y[j][c], acc[c]);
       }
-      for (int c = 0; c < ncols; ++c) X[(j0 + c) * nc + i] -= acc[c];
+      for (int c = 0; c < ncols; ++c) X[(j0 + c) * ldf + i] -= acc[c];
     }
     __syncthreads();
   }
@@ -108,7 +104,7 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
 __global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
                                                             int dense, const double* __restrict__ Bp, int64_t n) {
   const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
-  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s);
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldr = d_ldf(S, s);
   const int64_t r1 = min(f, r0 + kAsmRows);
   const int64_t ws = R.w[s], los = R.lo[s];
   const int64_t c1 = min(ws, c0 + kAsmCols);
@@ -117,14 +113,14 @@ __global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int3
   if (dense) {
     for (int64_t c = c0; c < c1; ++c)
       for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
-        Rs[c * f + i] = i < nc ? Bp[(los + c) * n + first + i] : 0.0;
+        Rs[c * ldr + i] = i < nc ? Bp[(los + c) * n + first + i] : 0.0;
     __syncthreads();
   }
   for (int64_t ci = S.child_ptr[s]; ci < S.child_ptr[s + 1]; ++ci) {
     const int64_t ch = S.child[ci];
     const int64_t wc = R.w[ch];
     if (wc == 0) continue;
-    const int64_t ncc = d_nc(S, ch), nrc = d_nr(S, ch), fc = ncc + nrc;
+    const int64_t ncc = d_nc(S, ch), nrc = d_nr(S, ch), ldc = d_ldf(S, ch);
     const int32_t* rel = S.rel + S.rel_ptr[ch];
     int64_t a = 0, b = nrc;
     while (a < b) {
@@ -157,8 +153,8 @@ __global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int3
         if (e < tot) {
           const int cq = e / nk, kq = e - cq * nk;
           const int64_t c = cc0 + cq, k = k0 + kq;
-          u[q] = Rc[(c - off) * fc + ncc + k];
-          d[q] = Rs + c * f + rel[k];
+          u[q] = Rc[(c - off) * ldc + ncc + k];
+          d[q] = Rs + c * ldr + rel[k];
         }
       }
 #pragma unroll
@@ -177,17 +173,16 @@ __global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int3
 // through shared memory.  y -> Bp pivot rows, u subtracted from R_s.
 template <int NC>
 __global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
-                                                         const double* __restrict__ p21,
-                                                         const double* __restrict__ linv, double* Bp, int64_t n) {
+                                                         const double* __restrict__ panel, double* Bp,
+                                                         int64_t n) {
   __shared__ double rt[kGemvJ][NC];
   __shared__ double red[8][32][NC];
   const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1];
-  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldm = d_ldf(S, s);
   const int64_t ws = R.w[s], los = R.lo[s];
   const int ncols = (int)min((int64_t)NC, ws);
   double* Rs = R.rhs + R.roff[s];
-  const double* Li = linv + S.linv_off[s];
-  const double* P = p21 + S.p21_off[s];
+  const double* M = panel + S.m_off[s];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t i = r0 + lane;
   double acc[NC];
@@ -198,7 +193,7 @@ __global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t
     __syncthreads();
     for (int e = threadIdx.x; e < jn * NC; e += blockDim.x) {
       const int j = e % jn, c = e / jn;
-      cp_async8(&rt[j][c], Rs + c * f + jb + j, c < ncols);
+      cp_async8(&rt[j][c], Rs + c * ldm + jb + j, c < ncols);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -206,15 +201,15 @@ __global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t
       if (i < nc) {
         const int jend = (int)min((int64_t)jn, i - jb + 1);
         for (int j = grp; j < jend; j += 8) {
-          const double m = Li[(jb + j) * nc + i];
+          const double m = M[(jb + j) * ldm + i];
 #pragma unroll
           for (int c = 0; c < NC; ++c) acc[c] = fma(m, rt[j][c], acc[c]);
         }
       } else {
-        const double* pc = P + jb * nr + (i - nc);
+        const double* pc = M + jb * ldm + i;
 #pragma unroll 4
         for (int j = grp; j < jn; j += 8) {
-          const double m = pc[(int64_t)j * nr];
+          const double m = pc[(int64_t)j * ldm];
 #pragma unroll
           for (int c = 0; c < NC; ++c) acc[c] = fma(m, rt[j][c], acc[c]);
         }
@@ -235,29 +230,31 @@ __global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t
       if (i < nc)
         Bp[(los + c) * n + first + i] = v;
       else
-        Rs[c * f + i] -= v;
+        Rs[c * ldm + i] -= v;
     }
   }
 }
 
 // ---- sparse-mode forward panel product on DMMA tiles --------------------------
 // task = (s, r0, c0): 64 x 64 tile of M_s (f x nc) x R_s[0:nc, c0:c0+64];
-// rows < nc -> Y_s (nc x w, ld nc), rows >= nc: R_s -= .
+// rows < nc -> Y_s (nc x w, ld nc + (nc & 1)), rows >= nc: R_s -= .
+// Both operands are staged with 16-byte copies (M_s and R_s columns are 16-byte
+// aligned): a copy that straddles the end of a column reads the padding row of
+// M_s (zero) or, for R_s, row nc -- whose product is with a zero-filled column
+// of the A tile.
 __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
-                                                        const double* __restrict__ p21,
-                                                        const double* __restrict__ linv, double* __restrict__ Y,
+                                                        const double* __restrict__ panel, double* __restrict__ Y,
                                                         const int64_t* __restrict__ yoff) {
   // k chunks of 16, double-buffered (cp.async of chunk k+1 overlaps the MMAs of k);
   // 38 KB of static shared memory keeps four CTAs per SM
   constexpr int BK = 16, SB = BK + 4;
-  __shared__ double As[2][BK * kMA];  // [k][row]
-  __shared__ double Bs[2][kMT * SB];  // [col][k]
+  __shared__ __align__(16) double As[2][BK * kMA];  // [k][row]
+  __shared__ __align__(16) double Bs[2][kMT * SB];  // [col][k]
   const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
-  const int64_t nc = d_nc(S, s), nr = d_nr(S, s), f = nc + nr;
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldm = d_ldf(S, s);
   const int64_t ws = R.w[s];
   double* Rs = R.rhs + R.roff[s];
-  const double* P = p21 + S.p21_off[s];
-  const double* Li = linv + S.linv_off[s];
+  const double* M = panel + S.m_off[s];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wy = (warp >> 1) * 32, wx = (warp & 1) * 32;
@@ -266,19 +263,24 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  // rows of this tile that lie in L11^{-1} only need k <= row
+  // rows of this tile that lie in L11^{-1} only need k <= row (its upper triangle is zero)
   const int64_t kend = (r0 + kMT <= nc) ? min(nc, r0 + kMT) : nc;
   auto stage = [&](int buf, int64_t k0) {
-    for (int e = threadIdx.x; e < kMT * BK; e += blockDim.x) {
-      const int rr = e % kMT, kk = e / kMT;
+    for (int e = threadIdx.x; e < kMT * BK / 2; e += blockDim.x) {
+      const int rr = 2 * (e % (kMT / 2)), kk = e / (kMT / 2);
       const int64_t i = r0 + rr, j = k0 + kk;
-      const bool in = i < f && j < nc && (i >= nc || j <= i);
-      cp_async8(&As[buf][kk * kMA + rr], i < nc ? Li + j * nc + i : P + j * nr + (i - nc), in);
+      const bool in = i < f && j < nc;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(&As[buf][kk * kMA + rr])),
+                   "l"(in ? M + j * ldm + i : M), "r"(in ? 16 : 0)
+                   : "memory");
     }
-    for (int e = threadIdx.x; e < kMT * BK; e += blockDim.x) {
-      const int kk = e % BK, cc = e / BK;
+    for (int e = threadIdx.x; e < kMT * BK / 2; e += blockDim.x) {
+      const int kk = 2 * (e % (BK / 2)), cc = e / (BK / 2);
       const int64_t j = k0 + kk, c = c0 + cc;
-      cp_async8(&Bs[buf][cc * SB + kk], Rs + c * f + j, j < nc && c < ws);
+      const bool in = j < nc && c < ws;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(&Bs[buf][cc * SB + kk])),
+                   "l"(in ? Rs + c * ldm + j : Rs), "r"(in ? 16 : 0)
+                   : "memory");
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -322,17 +324,17 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
         if (i < nc)
           Ys[c * (nc + (nc & 1)) + i] = acc[a][b][hh];
         else
-          Rs[c * f + i] -= acc[a][b][hh];
+          Rs[c * ldm + i] -= acc[a][b][hh];
       }
 }
 
 // ---- dense backward: x_s = L11^{-T} y_s - P21^T x_rows (warp per pivot row) -----
-// P21 = L21 L11^{-1} overwrote L21 at factorisation time.  y comes from Bp
-// (forward result), ancestors' x from X; the supernode's x is written to X.
+// Column i of M_s holds L11^{-1}[:, i] (rows < nc) and P21[:, i] (rows >= nc).
+// y comes from Bp (forward result), ancestors' x from X; the supernode's x is
+// written to X.
 template <int NC>
 __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                            const double* __restrict__ p21,
-                                                            const double* __restrict__ linv,
+                                                            const double* __restrict__ panel,
                                                             const double* __restrict__ Bp, double* __restrict__ X,
                                                             int64_t n, int64_t k) {
   const int64_t s = tasks[3 * blockIdx.x];
@@ -341,8 +343,8 @@ __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int3
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s);
   if (i >= nc) return;
   const int ncols = (int)min((int64_t)NC, k);
-  const double* pcol = p21 + S.p21_off[s] + i * nr;  // P21[:, i]
-  const double* lcol = linv + S.linv_off[s] + i * nc;       // L11^{-1}[:, i] = row i of L11^{-T}
+  const double* lcol = panel + S.m_off[s] + i * d_ldf(S, s);  // L11^{-1}[:, i] = row i of L11^{-T}
+  const double* pcol = lcol + nc;                             // P21[:, i]
   const int64_t* rows = S.rows + S.rows_ptr[s];
   const int64_t first = S.first[s];
   // four independent partial sums per column (lane-strided chunks of 128): the
@@ -397,12 +399,11 @@ __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int3
   }
 }
 
-// ---- factor epilogue: P21 = L21 L11^{-1} (DMMA, nr x nc, column-major ld nr) -----
+// ---- factor epilogue: P21 = L21 L11^{-1} (DMMA) into rows [nc, f) of M_s ---------
 // task = (s, 64-row block q0 of L21, 64-column block c0); L11^{-1} is lower
 // triangular, so only k >= c0 contributes.
 __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                  const double* __restrict__ front, const double* __restrict__ linv,
-                                                  double* __restrict__ p21) {
+                                                  const double* __restrict__ front, double* __restrict__ panel) {
   // k chunks of 16, cp.async double buffer (as panel_mma_kernel)
   constexpr int BK = 16, SB = BK + 4;
   __shared__ double As[2][BK * kMA];  // [k][row]
@@ -410,8 +411,8 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
   const int64_t s = tasks[3 * blockIdx.x], q0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s), ldf = d_ldf(S, s);
   const double* F = front + S.front_off[s];
-  const double* Li = linv + S.linv_off[s];
-  double* P = p21 + S.p21_off[s];
+  const double* Li = panel + S.m_off[s];  // L11^{-1}: rows [0, nc) of M_s, stride ldf
+  double* P = panel + S.m_off[s] + nc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wy = (warp >> 1) * 32, wx = (warp & 1) * 32;
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
     for (int e = threadIdx.x; e < kMT * BK; e += blockDim.x) {
       const int kk = e % BK, cc = e / BK;
       const int64_t k = k0 + kk, c = c0 + cc;
-      cp_async8(&Bs[buf][cc * SB + kk], Li + c * nc + k, k < nc && c < nc && k >= c);
+      cp_async8(&Bs[buf][cc * SB + kk], Li + c * ldf + k, k < nc && c < nc && k >= c);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(128) p21_kernel(DevSym S, const int32_t* __res
       for (int hh = 0; hh < 2; ++hh) {
         const int64_t q = q0 + wy + 8 * a + g;
         const int64_t c = c0 + wx + 8 * b + 2 * t + hh;
-        if (q < nr && c < nc) P[c * nr + q] = acc[a][b][hh];
+        if (q < nr && c < nc) P[c * ldf + q] = acc[a][b][hh];
       }
 }
 
@@ -490,11 +491,11 @@ __global__ void permute_kernel(int64_t n, int64_t k, const int64_t* __restrict__
 int trinv_level(CholHandle* h, int level, cudaStream_t st) {
   const DevTasks& T = h->trinv[level];
   if (!T.count) return CNB_OK;
-  trinv_kernel<<<(unsigned)T.count, 256, 0, st>>>(h->sym(), T.ptr, h->d_front, h->d_kkinv, h->d_linv);
+  trinv_kernel<<<(unsigned)T.count, 256, 0, st>>>(h->sym(), T.ptr, h->d_front, h->d_kkinv, h->d_m);
   CNB_LAUNCH_CHECK("trinv_kernel");
   const DevTasks& P = h->p21[level];
   if (P.count) {
-    p21_kernel<<<(unsigned)P.count, 128, 0, st>>>(h->sym(), P.ptr, h->d_front, h->d_linv, h->d_p21);
+    p21_kernel<<<(unsigned)P.count, 128, 0, st>>>(h->sym(), P.ptr, h->d_front, h->d_m);
     CNB_LAUNCH_CHECK("p21_kernel");
   }
   return CNB_OK;
@@ -537,7 +538,7 @@ static int build_plan(CholHandle* h, SolvePlan& P, int64_t width) {
     P.bwd_t.push_back({P.d_tasks + rb[l].first, rb[l].second});
   }
   std::vector<int64_t> roff(S.ns + 1, 0), lo(S.ns, 0), w(S.ns, width);
-  for (int64_t s = 0; s < S.ns; ++s) roff[s + 1] = roff[s] + S.f(s) * width;
+  for (int64_t s = 0; s < S.ns; ++s) roff[s + 1] = roff[s] + S.ldf(s) * width;
   if ((rc = upload_vec(&P.d_roff, roff))) return rc;
   if ((rc = upload_vec(&P.d_lo, lo))) return rc;
   if ((rc = upload_vec(&P.d_w, w))) return rc;
@@ -557,13 +558,12 @@ static int solve_chunk(CholHandle* h, SolvePlan& P, int64_t kk, cudaStream_t st)
   for (int l = 0; l < S.n_levels; ++l) {
     asm_kernel<<<(unsigned)P.asm_t[l].count, kSolveThreads, 0, st>>>(sym, P.asm_t[l].ptr, R, 1, Bp, n);
     CNB_LAUNCH_CHECK("asm_kernel");
-    panel_gemv_kernel<NC><<<(unsigned)P.panel_t[l].count, 256, 0, st>>>(sym, P.panel_t[l].ptr, R, h->d_p21,
-                                                                         h->d_linv, Bp, n);
+    panel_gemv_kernel<NC><<<(unsigned)P.panel_t[l].count, 256, 0, st>>>(sym, P.panel_t[l].ptr, R, h->d_m, Bp, n);
     CNB_LAUNCH_CHECK("panel_gemv_kernel");
   }
   for (int l = S.n_levels - 1; l >= 0; --l) {
-    bwd_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_p21, h->d_linv,
-                                                                        Bp, T, n, kk);
+    bwd_kernel<NC><<<(unsigned)P.bwd_t[l].count, 32 * kBwdRows, 0, st>>>(sym, P.bwd_t[l].ptr, h->d_m, Bp, T, n,
+                                                                        kk);
     CNB_LAUNCH_CHECK("bwd_kernel");
   }
   return CNB_OK;
@@ -914,7 +914,7 @@ static int plan_build(const Symbolic& S, int64_t ncols, const int64_t* colptr, c
         P.fw[s] = r - l;
       }
     }
-    P.froff[s + 1] = P.froff[s] + S.f(s) * P.fw[s];
+    P.froff[s + 1] = P.froff[s] + S.ldf(s) * P.fw[s];
     P.fyoff[s + 1] = P.fyoff[s] + ystride(S.nc(s)) * P.fw[s];
     const double nc = (double)S.nc(s), nr = (double)S.nr(s), w = (double)P.fw[s];
     P.rank_fwd_flops += w * (nc * nc + 2.0 * nc * nr);
@@ -924,7 +924,7 @@ static int plan_build(const Symbolic& S, int64_t ncols, const int64_t* colptr, c
     for (int64_t e = colptr[j]; e < colptr[j + 1]; ++e) {
       const int64_t p = S.iperm[rowidx[e]];
       const int64_t s = dof_sn[p];
-      P.sc_dst.push_back(P.froff[s] + (pos[j] - P.flo[s]) * S.f(s) + (p - S.first[s]));
+      P.sc_dst.push_back(P.froff[s] + (pos[j] - P.flo[s]) * S.ldf(s) + (p - S.first[s]));
       P.sc_val.push_back(vals[e]);
     }
   }
@@ -1050,8 +1050,7 @@ static int plan_forward(CholHandle* h, const CompliancePlan& P, double* Y, cudaS
     }
     if (P.prec[l].second) {
       panel_mma_kernel<<<(unsigned)P.prec[l].second, 128, 0, st>>>(sym, at<int32_t>(h->c_int, P.prec[l].first), R,
-                                                                   h->d_p21, h->d_linv, Y,
-                                                                   at<int64_t>(h->c_int, P.o_fyoff));
+                                                                   h->d_m, Y, at<int64_t>(h->c_int, P.o_fyoff));
       CNB_LAUNCH_CHECK("panel_mma_kernel");
     }
   }
