@@ -24,6 +24,11 @@ int cnb_pgs_profile(double* out);
  * call: out[0] loads, [1] elimination loop, out[7] calls. */
 int cnb_potrf_profile(double* out);
 
+/* Global-timer stamps (ns, out: host, 64) of the last cooperative single-RHS
+ * solve's phase ends: start, permute, then per forward level assemble and
+ * panel product, per backward level, in order. */
+int cnb_solve_profile(double* out);
+
 /* fp64 DMMA GEMM tile-shape variants, C = A B (row-major; sizes multiples of
  * the variant's tile). */
 int cnb_bench_gemm(int32_t variant, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,

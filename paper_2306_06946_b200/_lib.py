@@ -53,6 +53,7 @@ _SIGNATURES: dict[str, list] = {
     "cnb_detect_vertex_mesh": [I64, P, P, I64, P, P, F64, P, P, P, P],
     "cnb_pgs_profile": [P],
     "cnb_potrf_profile": [P],
+    "cnb_solve_profile": [P],
     "cnb_bench_gemm": [I32, I64, I64, I64, P, I64, P, I64, P, I64, P],
     "cnb_pgs": [I64, P, I64, P, F64, F64, F64, I32, P, P, P, P, P, P, P],
     "cnb_pgs_coloured": [I64, P, I64, P, F64, F64, F64, I32, P, P, I32, F64, P, P, P, P, P, P, P],

@@ -624,6 +624,9 @@ using namespace cnb;
 
 extern "C" {
 
+// diagnostic: phase end times (ns) of the last cooperative single-RHS solve
+int cnb_solve_profile(double* out) { return solve_profile(out); }
+
 // diagnostic: summed cycles of the potrf phases since the last call (loads,
 // factor, store L, inverse, store Y) and the launch count in out[7]
 int cnb_potrf_profile(double* out) {

@@ -55,12 +55,19 @@ struct SolvePlan {
   std::vector<DevTasks> asm_t, panel_t, bwd_t;  // per level
   int64_t *d_roff = nullptr, *d_lo = nullptr, *d_w = nullptr;
   double* d_rhs = nullptr;
+  void* d_lv = nullptr;  // width 1: per-level task table of the cooperative solve (solve.cu SolveLevel)
+  int32_t *d_cptr = nullptr, *d_csrc = nullptr;  // its assembly gathers (solve.cu gemv1_task)
+  int coop_grid = 0;
   void release() {
-    for (void* p : {(void*)d_tasks, (void*)d_roff, (void*)d_lo, (void*)d_w, (void*)d_rhs})
+    for (void* p : {(void*)d_tasks, (void*)d_roff, (void*)d_lo, (void*)d_w, (void*)d_rhs, d_lv, (void*)d_cptr,
+                    (void*)d_csrc})
       if (p) cudaFree(p);
+    d_cptr = d_csrc = nullptr;
     d_tasks = nullptr;
     d_roff = d_lo = d_w = nullptr;
     d_rhs = nullptr;
+    d_lv = nullptr;
+    coop_grid = 0;
     width = -1;
   }
 };
@@ -102,6 +109,7 @@ struct CholHandle {
 };
 
 // solve.cu
+int solve_profile(double* out);
 int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t k, cudaStream_t st);
 int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx, const double* vals,
                double* U, int64_t ldu, double* flops_out, cudaStream_t st);

@@ -662,7 +662,6 @@ constexpr int kTileD = kTileBytes / 8;
 constexpr int kXW = 9;              // X2 warps
 constexpr int kXRows = (kPR + kXW - 1) / kXW;
 constexpr int kPartBufs = 3;
-constexpr int kRowOwners = (4 * kPR + 31) / 32 * 32;  // phase-B GEMV threads (4 per row), whole warps (2..11)
 constexpr int kHelpWarps = kPipeThreads / 32;         // warps per helper CTA
 constexpr int kSeg = 4;                                // partial slots per row (helper CTAs a row can span)
 

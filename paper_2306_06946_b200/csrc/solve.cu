@@ -15,6 +15,8 @@
 // No serial triangle chains remain on the solve path: single right-hand
 // sides are coalesced GEMVs (bandwidth-bound), the compliance's many
 // right-hand sides are fp64 tensor-core GEMMs (mma.sync m8n8k4 f64 = DMMA).
+#include <cooperative_groups.h>
+
 #include <cstring>
 #include <numeric>
 
@@ -100,10 +102,10 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
 }
 
 // ---- assemble front RHS blocks: init (dense) + extend-add children -----------
-// task = (s, row chunk r0, column chunk c0)
-__global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
-                                                            int dense, const double* __restrict__ Bp, int64_t n) {
-  const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
+// task = (s, row chunk r0, column chunk c0); any block size
+__device__ __forceinline__ void asm_task(const DevSym& S, const int32_t* __restrict__ task, const RhsView& R,
+                                         int dense, const double* __restrict__ Bp, int64_t n) {
+  const int64_t s = task[0], r0 = task[1], c0 = task[2];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldr = d_ldf(S, s);
   const int64_t r1 = min(f, r0 + kAsmRows);
   const int64_t ws = R.w[s], los = R.lo[s];
@@ -167,17 +169,20 @@ __global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int3
   }
 }
 
+__global__ void __launch_bounds__(kSolveThreads) asm_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
+                                                            int dense, const double* __restrict__ Bp, int64_t n) {
+  asm_task(S, tasks + 3 * blockIdx.x, R, dense, Bp, n);
+}
+
 // ---- dense forward panel product (GEMV, NC <= 8 columns) ----------------------
 // task = (s, row tile r0 of 32 rows): 8 warps split the pivot index j, lanes
 // take consecutive rows (coalesced column reads of M_s), partial sums reduced
 // through shared memory.  y -> Bp pivot rows, u subtracted from R_s.
 template <int NC>
-__global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
-                                                         const double* __restrict__ panel, double* Bp,
-                                                         int64_t n) {
-  __shared__ double rt[kGemvJ][NC];
-  __shared__ double red[8][32][NC];
-  const int64_t s = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1];
+__device__ __forceinline__ void gemv_task(const DevSym& S, const int32_t* __restrict__ task, const RhsView& R,
+                                          const double* __restrict__ panel, double* Bp, int64_t n,
+                                          double (*rt)[NC], double (*red)[32][NC]) {
+  const int64_t s = task[0], r0 = task[1];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldm = d_ldf(S, s);
   const int64_t ws = R.w[s], los = R.lo[s];
   const int ncols = (int)min((int64_t)NC, ws);
@@ -198,21 +203,19 @@ __global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t
     cp_async_wait_all();
     __syncthreads();
     if (i < f) {
-      if (i < nc) {
-        const int jend = (int)min((int64_t)jn, i - jb + 1);
-        for (int j = grp; j < jend; j += 8) {
-          const double m = M[(jb + j) * ldm + i];
+      // every row runs over all jn pivots (the upper triangle of L11^{-1} in M_s is
+      // zero): eight loads in flight per thread before their multiply-adds, the
+      // chain per thread stays j = grp, grp + 8, ... in order
+      const double* pc = M + jb * ldm + i;
+      for (int j0 = grp; j0 < jn; j0 += 64) {
+        double mv[8];
 #pragma unroll
-          for (int c = 0; c < NC; ++c) acc[c] = fma(m, rt[j][c], acc[c]);
-        }
-      } else {
-        const double* pc = M + jb * ldm + i;
-#pragma unroll 4
-        for (int j = grp; j < jn; j += 8) {
-          const double m = pc[(int64_t)j * ldm];
+        for (int u = 0; u < 8; ++u) mv[u] = j0 + 8 * u < jn ? pc[(int64_t)(j0 + 8 * u) * ldm] : 0.0;
 #pragma unroll
-          for (int c = 0; c < NC; ++c) acc[c] = fma(m, rt[j][c], acc[c]);
-        }
+        for (int u = 0; u < 8; ++u)
+          if (j0 + 8 * u < jn)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[c] = fma(mv[u], rt[j0 + 8 * u][c], acc[c]);
       }
     }
   }
@@ -233,6 +236,15 @@ __global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t
         Rs[c * ldm + i] -= v;
     }
   }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) panel_gemv_kernel(DevSym S, const int32_t* __restrict__ tasks, RhsView R,
+                                                         const double* __restrict__ panel, double* Bp,
+                                                         int64_t n) {
+  __shared__ double rt[kGemvJ][NC];
+  __shared__ double red[8][32][NC];
+  gemv_task<NC>(S, tasks + 3 * blockIdx.x, R, panel, Bp, n, rt, red);
 }
 
 // ---- sparse-mode forward panel product on DMMA tiles --------------------------
@@ -332,14 +344,11 @@ __global__ void __launch_bounds__(128) panel_mma_kernel(DevSym S, const int32_t*
 // Column i of M_s holds L11^{-1}[:, i] (rows < nc) and P21[:, i] (rows >= nc).
 // y comes from Bp (forward result), ancestors' x from X; the supernode's x is
 // written to X.
+// y of pivot row j, column c at yb[c * ldy + j]
 template <int NC>
-__global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                            const double* __restrict__ panel,
-                                                            const double* __restrict__ Bp, double* __restrict__ X,
-                                                            int64_t n, int64_t k) {
-  const int64_t s = tasks[3 * blockIdx.x];
-  const int64_t i = tasks[3 * blockIdx.x + 1] + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void bwd_row(const DevSym& S, int64_t s, int64_t i, int lane,
+                                        const double* __restrict__ panel, const double* __restrict__ yb,
+                                        int64_t ldy, double* __restrict__ X, int64_t n, int64_t k) {
   const int64_t nc = d_nc(S, s), nr = d_nr(S, s);
   if (i >= nc) return;
   const int ncols = (int)min((int64_t)NC, k);
@@ -347,56 +356,168 @@ __global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int3
   const double* pcol = lcol + nc;                             // P21[:, i]
   const int64_t* rows = S.rows + S.rows_ptr[s];
   const int64_t first = S.first[s];
-  // four independent partial sums per column (lane-strided chunks of 128): the
-  // gathers X[rows[q]] of a chunk are all in flight together
-  double acc[4][NC];
+  // eight independent partial sums per column (lane-strided chunks of 256): the
+  // loads and gathers X[rows[q]] of a chunk are all in flight together
+  constexpr int U = 8;
+  double acc[U][NC];
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < U; ++u)
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[u][c] = 0.0;
-  int64_t j = i + lane;
-  for (; j + 96 < nc; j += 128) {
+  for (int64_t j0 = i + lane; j0 < nc; j0 += 32 * U) {
+    double l[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double l = lcol[j + 32 * u];
+    for (int u = 0; u < U; ++u) l[u] = j0 + 32 * u < nc ? lcol[j0 + 32 * u] : 0.0;
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
-        if (c < ncols) acc[u][c] = fma(l, Bp[c * n + first + j + 32 * u], acc[u][c]);
-    }
-  }
-  for (; j < nc; j += 32) {
-    const double l = lcol[j];
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < ncols) acc[0][c] = fma(l, Bp[c * n + first + j], acc[0][c]);
-  }
-  int64_t q = lane;
-  for (; q + 96 < nr; q += 128) {
-    double pq[4];
-    int64_t rq[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      pq[u] = pcol[q + 32 * u];
-      rq[u] = rows[q + 32 * u];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int c = 0; c < NC; ++c)
-        if (c < ncols) acc[u][c] = fma(-pq[u], X[c * n + rq[u]], acc[u][c]);
+        if (c < ncols && j0 + 32 * u < nc) acc[u][c] = fma(l[u], yb[c * ldy + j0 + 32 * u], acc[u][c]);
   }
-  for (; q < nr; q += 32) {
-    const double pv = pcol[q];
-    const int64_t rv = rows[q];
+  for (int64_t q0 = lane; q0 < nr; q0 += 32 * U) {
+    double pq[U];
+    int64_t rq[U];
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (c < ncols) acc[0][c] = fma(-pv, X[c * n + rv], acc[0][c]);
+    for (int u = 0; u < U; ++u) {
+      const bool in = q0 + 32 * u < nr;
+      pq[u] = in ? pcol[q0 + 32 * u] : 0.0;
+      rq[u] = in ? rows[q0 + 32 * u] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c < ncols && rq[u] >= 0) acc[u][c] = fma(-pq[u], X[c * n + rq[u]], acc[u][c]);
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    const double v = warp_sum((acc[0][c] + acc[1][c]) + (acc[2][c] + acc[3][c]));
+    const double v = warp_sum(((acc[0][c] + acc[1][c]) + (acc[2][c] + acc[3][c])) +
+                              ((acc[4][c] + acc[5][c]) + (acc[6][c] + acc[7][c])));
     if (lane == 0 && c < ncols) X[c * n + first + i] = v;
   }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(32 * kBwdRows) bwd_kernel(DevSym S, const int32_t* __restrict__ tasks,
+                                                            const double* __restrict__ panel,
+                                                            const double* __restrict__ Bp, double* __restrict__ X,
+                                                            int64_t n, int64_t k) {
+  const int64_t s = tasks[3 * blockIdx.x];
+  bwd_row<NC>(S, s, tasks[3 * blockIdx.x + 1] + (threadIdx.x >> 5), threadIdx.x & 31, panel, Bp + S.first[s], n, X,
+              n, k);
+}
+
+// ---- single right-hand side: the whole solve in one cooperative kernel ------
+// Permute, forward levels (assemble, panel GEMV), backward levels, permute back,
+// with a grid barrier between dependent phases: the same tasks and arithmetic
+// as the per-level launches (bitwise the same result), without a launch per
+// level and phase (a 12k-DoF solve is ~25 dependent launches otherwise).
+// single RHS: the panel GEMV of gemv_task<1> with the front's assembly folded
+// in -- pivot rows are gathered while they are staged, update rows right
+// before their product is subtracted (same sums in the same order as the
+// separate assembly: start value, then the children's rows in order)
+__device__ __forceinline__ double gather_row(int32_t r, double v, const int32_t* __restrict__ cptr,
+                                             const int32_t* __restrict__ csrc, const double* rhs) {
+  for (int32_t q = cptr[r]; q < cptr[r + 1]; ++q) v = v + rhs[csrc[q]];
+  return v;
+}
+__device__ __forceinline__ void gemv1_task(const DevSym& S, const int32_t* __restrict__ task, const RhsView& R,
+                                           const double* __restrict__ panel, double* Bp,
+                                           const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
+                                           double (*rt)[1], double (*red)[32][1]) {
+  const int64_t s = task[0], r0 = task[1];
+  const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldm = d_ldf(S, s);
+  const int32_t rb = (int32_t)R.roff[s];
+  const double* M = panel + S.m_off[s];
+  const int64_t first = S.first[s];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t i = r0 + lane;
+  double acc = 0.0;
+  for (int64_t jb = 0; jb < nc; jb += kGemvJ) {
+    const int jn = (int)min((int64_t)kGemvJ, nc - jb);
+    __syncthreads();
+    for (int j = threadIdx.x; j < jn; j += blockDim.x)
+      rt[j][0] = gather_row(rb + (int32_t)(jb + j), Bp[first + jb + j], cptr, csrc, R.rhs);
+    __syncthreads();
+    if (i < f) {
+      const double* pc = M + jb * ldm + i;
+      for (int j0 = grp; j0 < jn; j0 += 64) {
+        double mv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mv[u] = j0 + 8 * u < jn ? pc[(int64_t)(j0 + 8 * u) * ldm] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + 8 * u < jn) acc = fma(mv[u], rt[j0 + 8 * u][0], acc);
+      }
+    }
+  }
+  red[grp][lane][0] = acc;
+  __syncthreads();
+  if (grp == 0 && i < f) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += red[q][lane][0];
+    // y into the front's own RHS rows (the front's other tasks may still be
+    // staging its pivot rows from Bp), updates into the rows below
+    R.rhs[rb + i] = i < nc ? v : gather_row(rb + (int32_t)i, 0.0, cptr, csrc, R.rhs) - v;
+  }
+}
+
+__device__ unsigned long long g_solve_prof[64];
+__device__ __forceinline__ unsigned long long solve_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct SolveLevel {
+  const int32_t* gemv_t;
+  const int32_t* bwd_t;
+  int32_t n_gemv, n_bwd;
+};
+
+// The assembly is a gather folded into the panel GEMV (gemv1_task): RHS
+// position r sums its children's update rows (cptr / csrc, children in order:
+// the extend-add's arithmetic, no searches).
+__global__ void __launch_bounds__(256) solve1_kernel(DevSym S, RhsView R, const double* __restrict__ panel,
+                                                     const SolveLevel* __restrict__ lv, int nlev,
+                                                     const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
+                                                     const int64_t* __restrict__ perm, const double* __restrict__ B,
+                                                     double* __restrict__ X, double* Bp, double* T, int64_t n) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double rt[kGemvJ][1];
+  __shared__ double red[8][32][1];
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  int ph = 0;
+  auto mark = [&]() {  // diagnostic: phase end times of CTA 0 (cnb_solve_profile)
+    if (gt == 0 && ph < 64) g_solve_prof[ph] = solve_ns();
+    ++ph;
+  };
+  mark();
+  for (int64_t p = gt; p < n; p += gs) Bp[p] = B[perm[p]];
+  grid.sync();
+  mark();
+  for (int l = 0; l < nlev; ++l) {
+    const SolveLevel L = lv[l];
+    for (int q = blockIdx.x; q < L.n_gemv; q += gridDim.x) {
+      gemv1_task(S, L.gemv_t + 3 * q, R, panel, Bp, cptr, csrc, rt, red);
+      __syncthreads();  // rt / red reused by the next task
+    }
+    grid.sync();
+    mark();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int l = nlev - 1; l >= 0; --l) {
+    const SolveLevel L = lv[l];
+    for (int q = blockIdx.x * 8 + warp; q < L.n_bwd * kBwdRows; q += gridDim.x * 8) {
+      const int32_t* t = L.bwd_t + 3 * (q / kBwdRows);
+      bwd_row<1>(S, t[0], t[1] + q % kBwdRows, lane, panel, R.rhs + R.roff[t[0]], 0, T, n, 1);
+    }
+    grid.sync();
+    mark();
+  }
+  for (int64_t p = gt; p < n; p += gs) X[perm[p]] = T[p];
 }
 
 // ---- factor epilogue: P21 = L21 L11^{-1} (DMMA) into rows [nc, f) of M_s ---------
@@ -543,6 +664,36 @@ static int build_plan(CholHandle* h, SolvePlan& P, int64_t width) {
   if ((rc = upload_vec(&P.d_lo, lo))) return rc;
   if ((rc = upload_vec(&P.d_w, w))) return rc;
   CNB_CUDA(cudaMalloc((void**)&P.d_rhs, std::max<int64_t>(1, roff[S.ns]) * sizeof(double)));
+  if (width == 1) {  // per-level tables of the cooperative single-RHS kernel
+    // gather lists of the assembly: RHS position roff[s] + rel_c[k] <- roff[c] + nc_c + k
+    std::vector<int32_t> cnt(roff[S.ns] + 1, 0);
+    for (int64_t s = 0; s < S.ns; ++s)
+      for (int64_t ci = S.child_ptr[s]; ci < S.child_ptr[s + 1]; ++ci) {
+        const int64_t c = S.child[ci];
+        for (int64_t k = 0; k < S.nr(c); ++k) ++cnt[roff[s] + S.rel[S.rel_ptr[c] + k] + 1];
+      }
+    std::vector<int32_t> cptr(roff[S.ns] + 1, 0);
+    for (int64_t r = 0; r < roff[S.ns]; ++r) cptr[r + 1] = cptr[r] + cnt[r + 1];
+    std::vector<int32_t> csrc(std::max<int32_t>(1, cptr[roff[S.ns]])), fill(cptr.begin(), cptr.end() - 1);
+    for (int64_t s = 0; s < S.ns; ++s)  // children ascending, rows ascending: the extend-add order
+      for (int64_t ci = S.child_ptr[s]; ci < S.child_ptr[s + 1]; ++ci) {
+        const int64_t c = S.child[ci];
+        for (int64_t k = 0; k < S.nr(c); ++k)
+          csrc[fill[roff[s] + S.rel[S.rel_ptr[c] + k]]++] = (int32_t)(roff[c] + S.nc(c) + k);
+      }
+    if ((rc = upload_vec(&P.d_cptr, cptr))) return rc;
+    if ((rc = upload_vec(&P.d_csrc, csrc))) return rc;
+    std::vector<SolveLevel> lv(S.n_levels);
+    for (int l = 0; l < S.n_levels; ++l)
+      lv[l] = SolveLevel{P.panel_t[l].ptr, P.bwd_t[l].ptr, (int32_t)P.panel_t[l].count, (int32_t)P.bwd_t[l].count};
+    CNB_CUDA(cudaMalloc(&P.d_lv, std::max<size_t>(1, lv.size()) * sizeof(SolveLevel)));
+    if (!lv.empty()) CNB_CUDA(cudaMemcpy(P.d_lv, lv.data(), lv.size() * sizeof(SolveLevel), cudaMemcpyHostToDevice));
+    int dev = 0, sms = 0, occ = 0;
+    CNB_CUDA(cudaGetDevice(&dev));
+    CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, solve1_kernel, 256, 0));
+    P.coop_grid = sms * std::min(occ, 2);
+  }
   P.width = width;
   return CNB_OK;
 }
@@ -569,6 +720,13 @@ static int solve_chunk(CholHandle* h, SolvePlan& P, int64_t kk, cudaStream_t st)
   return CNB_OK;
 }
 
+int solve_profile(double* out) {
+  unsigned long long h[64];
+  CNB_CUDA(cudaMemcpyFromSymbol(h, g_solve_prof, sizeof(h)));
+  for (int k = 0; k < 64; ++k) out[k] = (double)h[k];
+  return CNB_OK;
+}
+
 int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t k, cudaStream_t st) {
   if (k <= 0) return CNB_OK;
   const int64_t n = h->S.n;
@@ -579,6 +737,23 @@ int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t 
   if ((rc = h->bp.ensure(n * width * sizeof(double)))) return rc;
   if ((rc = h->tbuf.ensure(n * width * sizeof(double)))) return rc;
   double* Bp = (double*)h->bp.p;
+  if (width == 1 && P.coop_grid > 0) {
+    DevSym sym = h->sym();
+    RhsView R{P.d_rhs, P.d_roff, P.d_lo, P.d_w};
+    const SolveLevel* lv = (const SolveLevel*)P.d_lv;
+    int nlev = h->S.n_levels;
+    int64_t nn = n;
+    double* T = (double*)h->tbuf.p;
+    const double* panel = h->d_m;
+    const int64_t* perm = h->d_perm;
+    const int32_t* cptr = P.d_cptr;
+    const int32_t* csrc = P.d_csrc;
+    void* args[] = {(void*)&sym, (void*)&R,    (void*)&panel, (void*)&lv, (void*)&nlev, (void*)&cptr,
+                    (void*)&csrc, (void*)&perm, (void*)&B,     (void*)&X,  (void*)&Bp,   (void*)&T, (void*)&nn};
+    CNB_CUDA(cudaLaunchCooperativeKernel((const void*)solve1_kernel, dim3(P.coop_grid), dim3(256), args, 0, st));
+    CNB_LAUNCH_CHECK("solve1_kernel");
+    return CNB_OK;
+  }
   for (int64_t c0 = 0; c0 < k; c0 += width) {
     const int64_t kk = std::min(width, k - c0);
     if (kk < width) CNB_CUDA(cudaMemsetAsync(Bp, 0, n * width * sizeof(double), st));
@@ -604,8 +779,6 @@ int solve_dense(CholHandle* h, const double* B, int64_t ldb, double* X, int64_t 
 // 64x64 output tile, Y_s^T Y_s of exactly the supernodes whose window covers
 // it, in a fixed order (deterministic), on DMMA.
 constexpr int kGT = 64;
-constexpr int kGK = 32;
-constexpr int kGS = kGK + 4;  // [column][k] staging stride (== 4 mod 16: conflict-free fragments)
 
 __global__ void __launch_bounds__(128) gram_kernel(DevSym S, RhsView R, const double* __restrict__ Y,
                                                    const int64_t* __restrict__ yoff, const int32_t* __restrict__ tile_ptr,
