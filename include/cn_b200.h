@@ -255,7 +255,10 @@ int cnb_chol_factor(cnb_chol_t h, const double* vals, cnb_status_t* d_status, vo
 
 /* X = A^{-1} B for k right-hand sides stored as k contiguous length-n
  * vectors (leading dimensions ldb/ldx); X may alias B.  Replaces
- * Factorization.solve / solve_multi linalg.py:89-106. */
+ * Factorization.solve / solve_multi linalg.py:89-106.  k == 1 runs as one
+ * cooperative (grid-barrier) kernel: do not overlap two such solves, or one
+ * and cnb_pgs, on different streams (their grids could wait on each other's
+ * co-residency); order them with events. */
 int cnb_chol_solve(cnb_chol_t h, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t k,
                    void* stream);
 
