@@ -29,6 +29,7 @@ constexpr int kAsmRows = 128;   // rows per assemble task
 constexpr int kAsmCols = 64;    // columns per assemble task (sparse mode)
 constexpr int kGemvRows = 32;   // rows per dense panel task
 constexpr int kGemvJ = 256;     // staged pivot rows of the RHS per pass
+constexpr int kGemvU = 16;      // panel loads in flight per thread
 constexpr int kBwdRows = 4;     // pivot rows per backward task (warp per row)
 constexpr int kMT = 64;         // DMMA panel tile (rows, cols)
 constexpr int kMA = kMT + 4;    // k-major stride of tiles staged from column-major sources
@@ -204,15 +205,15 @@ __device__ __forceinline__ void gemv_task(const DevSym& S, const int32_t* __rest
     __syncthreads();
     if (i < f) {
       // every row runs over all jn pivots (the upper triangle of L11^{-1} in M_s is
-      // zero): eight loads in flight per thread before their multiply-adds, the
+      // zero): kGemvU loads in flight per thread before their multiply-adds, the
       // chain per thread stays j = grp, grp + 8, ... in order
       const double* pc = M + jb * ldm + i;
-      for (int j0 = grp; j0 < jn; j0 += 64) {
-        double mv[8];
+      for (int j0 = grp; j0 < jn; j0 += 8 * kGemvU) {
+        double mv[kGemvU];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) mv[u] = j0 + 8 * u < jn ? pc[(int64_t)(j0 + 8 * u) * ldm] : 0.0;
+        for (int u = 0; u < kGemvU; ++u) mv[u] = j0 + 8 * u < jn ? pc[(int64_t)(j0 + 8 * u) * ldm] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < kGemvU; ++u)
           if (j0 + 8 * u < jn)
 #pragma unroll
             for (int c = 0; c < NC; ++c) acc[c] = fma(mv[u], rt[j0 + 8 * u][c], acc[c]);
@@ -424,7 +425,9 @@ __device__ __forceinline__ double gather_row(int32_t r, double v, const int32_t*
 __device__ __forceinline__ void gemv1_task(const DevSym& S, const int32_t* __restrict__ task, const RhsView& R,
                                            const double* __restrict__ panel, double* Bp,
                                            const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
-                                           double (*rt)[1], double (*red)[32][1]) {
+                                           double* rt, double* ug, double (*red)[32][1]) {
+  // one pass of gathers for the whole task (pivot rows into rt, this task's
+  // update rows into ug) with the first panel loads already in flight
   const int64_t s = task[0], r0 = task[1];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldm = d_ldf(S, s);
   const int32_t rb = (int32_t)R.roff[s];
@@ -432,23 +435,24 @@ __device__ __forceinline__ void gemv1_task(const DevSym& S, const int32_t* __res
   const int64_t first = S.first[s];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t i = r0 + lane;
+  const double* pc = M + i;
+  double mv[kGemvU];
+#pragma unroll
+  for (int u = 0; u < kGemvU; ++u) mv[u] = (i < f && grp + 8 * u < nc) ? pc[(int64_t)(grp + 8 * u) * ldm] : 0.0;
+  for (int j = threadIdx.x; j < nc; j += blockDim.x)
+    rt[j] = gather_row(rb + (int32_t)j, Bp[first + j], cptr, csrc, R.rhs);
+  if (threadIdx.x < 32 && i >= nc && i < f) ug[lane] = gather_row(rb + (int32_t)i, 0.0, cptr, csrc, R.rhs);
+  __syncthreads();
   double acc = 0.0;
-  for (int64_t jb = 0; jb < nc; jb += kGemvJ) {
-    const int jn = (int)min((int64_t)kGemvJ, nc - jb);
-    __syncthreads();
-    for (int j = threadIdx.x; j < jn; j += blockDim.x)
-      rt[j][0] = gather_row(rb + (int32_t)(jb + j), Bp[first + jb + j], cptr, csrc, R.rhs);
-    __syncthreads();
-    if (i < f) {
-      const double* pc = M + jb * ldm + i;
-      for (int j0 = grp; j0 < jn; j0 += 64) {
-        double mv[8];
+  if (i < f) {
+    for (int j0 = grp;;) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) mv[u] = j0 + 8 * u < jn ? pc[(int64_t)(j0 + 8 * u) * ldm] : 0.0;
+      for (int u = 0; u < kGemvU; ++u)
+        if (j0 + 8 * u < nc) acc = fma(mv[u], rt[j0 + 8 * u], acc);
+      j0 += 8 * kGemvU;
+      if (j0 >= nc) break;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (j0 + 8 * u < jn) acc = fma(mv[u], rt[j0 + 8 * u][0], acc);
-      }
+      for (int u = 0; u < kGemvU; ++u) mv[u] = j0 + 8 * u < nc ? pc[(int64_t)(j0 + 8 * u) * ldm] : 0.0;
     }
   }
   red[grp][lane][0] = acc;
@@ -459,7 +463,7 @@ __device__ __forceinline__ void gemv1_task(const DevSym& S, const int32_t* __res
     for (int q = 0; q < 8; ++q) v += red[q][lane][0];
     // y into the front's own RHS rows (the front's other tasks may still be
     // staging its pivot rows from Bp), updates into the rows below
-    R.rhs[rb + i] = i < nc ? v : gather_row(rb + (int32_t)i, 0.0, cptr, csrc, R.rhs) - v;
+    R.rhs[rb + i] = i < nc ? v : ug[lane] - v;
   }
 }
 
@@ -486,7 +490,8 @@ __global__ void __launch_bounds__(256) solve1_kernel(DevSym S, RhsView R, const 
                                                      double* __restrict__ X, double* Bp, double* T, int64_t n) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ double rt[kGemvJ][1];
+  __shared__ double rt[kMaxSnCols];
+  __shared__ double ug[32];
   __shared__ double red[8][32][1];
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
   int ph = 0;
@@ -501,7 +506,7 @@ __global__ void __launch_bounds__(256) solve1_kernel(DevSym S, RhsView R, const 
   for (int l = 0; l < nlev; ++l) {
     const SolveLevel L = lv[l];
     for (int q = blockIdx.x; q < L.n_gemv; q += gridDim.x) {
-      gemv1_task(S, L.gemv_t + 3 * q, R, panel, Bp, cptr, csrc, rt, red);
+      gemv1_task(S, L.gemv_t + 3 * q, R, panel, Bp, cptr, csrc, rt, ug, red);
       __syncthreads();  // rt / red reused by the next task
     }
     grid.sync();
