@@ -530,20 +530,23 @@ def roofline_cfg1(wl, torch, _lib, phases):
 # ----------------------------------------------------------------------------
 
 def pgs_ncu_traffic_per_sweep():
-    """dram__bytes_read + dram__bytes_write of one pgs_pipe_kernel launch from the
-    committed ncu --set full capture, per W pass (30 sweeps + the delta_end pass
-    at G = 7500, the cfg3 size)."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_pgs_pipe_kernel.txt")
+    """dram__bytes_read + dram__bytes_write of the largest pgs_pipe_kernel launch of a
+    cfg3 step from the committed ncu --set full capture (profiles/
+    r02_ncu_dmma_and_pgs_kernels.txt), per W pass: that launch ran the 30-sweep cap
+    (7 301 groups) and forms delta_end without a pass, so 30 passes."""
+    path = os.path.join(ROOT, "profiles", "r02_ncu_dmma_and_pgs_kernels.txt")
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     try:
-        vals = {}
+        vals, inside = {}, False
         for line in open(path):
-            if " = " in line and "[" in line:
-                k, rest = line.split(" [", 1)
-                unit, v = rest.split("] = ")
-                scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, None)
-                if scale:
-                    vals[k] = float(v) * scale
-        return round((vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) / 31.0, 0)
+            if line.startswith("== "):
+                inside = line.startswith("== pgs_pipe_kernel")
+            elif inside and " = " in line:
+                k, rest = line.strip().split(" = ", 1)
+                parts = rest.split()
+                if len(parts) >= 2 and parts[1] in scale:
+                    vals[k] = float(parts[0]) * scale[parts[1]]
+        return round((vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) / 30.0, 0)
     except (OSError, KeyError, ValueError):
         return None
 

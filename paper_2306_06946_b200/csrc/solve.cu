@@ -483,7 +483,7 @@ struct SolveLevel {
 // The assembly is a gather folded into the panel GEMV (gemv1_task): RHS
 // position r sums its children's update rows (cptr / csrc, children in order:
 // the extend-add's arithmetic, no searches).
-__global__ void __launch_bounds__(256) solve1_kernel(DevSym S, RhsView R, const double* __restrict__ panel,
+__global__ void __launch_bounds__(256, 3) solve1_kernel(DevSym S, RhsView R, const double* __restrict__ panel,
                                                      const SolveLevel* __restrict__ lv, int nlev,
                                                      const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
                                                      const int64_t* __restrict__ perm, const double* __restrict__ B,
@@ -697,7 +697,7 @@ static int build_plan(CholHandle* h, SolvePlan& P, int64_t width) {
     CNB_CUDA(cudaGetDevice(&dev));
     CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, solve1_kernel, 256, 0));
-    P.coop_grid = sms * std::min(occ, 2);
+    P.coop_grid = sms * std::min(occ, 3);
   }
   P.width = width;
   return CNB_OK;

@@ -10,7 +10,9 @@ import bench  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 which = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
-wl = bench.Cfg3Workload() if which == "cfg3" else bench.GpuWorkload(bench.make_inputs())
+import workloads  # noqa: E402
+
+wl = bench.Cfg3Workload() if which == "cfg3" else bench.GpuWorkload(workloads.cfg1_inputs())
 for _ in range(steps):
     wl.step()
 torch.cuda.synchronize()
