@@ -697,7 +697,9 @@ static int build_plan(CholHandle* h, SolvePlan& P, int64_t width) {
     CNB_CUDA(cudaGetDevice(&dev));
     CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, solve1_kernel, 256, 0));
-    P.coop_grid = sms * std::min(occ, 3);
+    // more resident CTAs help the latency-bound bottom levels of a large tree;
+    // a small one pays more for its grid barriers than it gains
+    P.coop_grid = sms * std::min(occ, S.ns > 1000 ? 3 : 2);
   }
   P.width = width;
   return CNB_OK;
