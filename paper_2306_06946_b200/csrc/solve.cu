@@ -96,7 +96,9 @@ __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __r
 #pragma unroll
         for (int c = 0; c < kInvCols; ++c) acc[c] = fma(l, y[j][c], acc[c]);
       }
-      for (int c = 0; c < ncols; ++c) X[(j0 + c) * ldf + i] -= acc[c];
+#pragma unroll
+      for (int c = 0; c < kInvCols; ++c)  // compile-time index: acc stays in registers
+        if (c < ncols) X[(j0 + c) * ldf + i] -= acc[c];
     }
     __syncthreads();
   }
