@@ -22,6 +22,17 @@
 
 #include "chol_dev.cuh"
 
+// SYRK tile kernel: k depth of a staged chunk (16: a short prologue and two
+// double-buffered chunks even for the rank-32 in-block updates; measured 62.6 ->
+// 60.4 ms per cfg3 factor against 32) and the CTAs per SM it is compiled for
+// (3: the fused POTRF's registers stay unspilled)
+#ifndef SYRK_BK
+#define SYRK_BK 16
+#endif
+#ifndef SYRK_MINB
+#define SYRK_MINB 3
+#endif
+
 namespace cnb {
 
 __global__ void scatter_kernel(int64_t nmap, const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
 }
 
 // SYRK update on a 64x64 tile with DMMA, K staged through shared memory in
-// 32-column chunks (cp.async double buffer):
+// kSyrkBK-deep chunks (cp.async double buffer):
 //   C[rows ti, cols tj] -= P[rows ti, :] * P[rows tj, :]^T,  P = L columns [k0, k0 + kw).
 // mode 0 (in-block): P = panel p (kw <= 32), target columns [t0, block end) of
 //   every row below -- only the block's remaining pivot columns;
@@ -313,14 +324,15 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
 // copies of consecutive rows land in consecutive banks, and the fragment loads
 // are conflict-free with a row stride == 4 mod 16 doubles.
 constexpr int kSK = kTile + 4;  // smem stride of one k column of a staged tile
-constexpr size_t kSyrkSmem = 2 * 2 * kPanel * kSK * sizeof(double);
+constexpr int kSyrkBK = SYRK_BK;  // k depth of one staged chunk
+constexpr size_t kSyrkSmem = 2 * 2 * kSyrkBK * kSK * sizeof(double);
 static_assert(kPotrfSmem <= kSyrkSmem, "the fused POTRF reuses the SYRK staging buffers");
-__global__ void __launch_bounds__(128, 3) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode,
+__global__ void __launch_bounds__(128, SYRK_MINB) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode,
                                                    double* __restrict__ front, double* __restrict__ kkinv,
                                                    DevStatus* st) {
   extern __shared__ __align__(16) double syrk_sm[];
-  double* Pi = syrk_sm;                  // [2][kPanel * kSK]
-  double* Pj = syrk_sm + 2 * kPanel * kSK;
+  double* Pi = syrk_sm;                  // [2][kSyrkBK * kSK]
+  double* Pj = syrk_sm + 2 * kSyrkBK * kSK;
   const int64_t s = tasks[3 * blockIdx.x];
   const int ti = tasks[3 * blockIdx.x + 1], tj = tasks[3 * blockIdx.x + 2];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldf = d_ldf(S, s);
@@ -348,9 +360,9 @@ __global__ void __launch_bounds__(128, 3) syrk_kernel(DevSym S, const int32_t* _
   constexpr int kPairs = kTile / 2 + 1;  // 33 pairs cover 64 rows at either parity
   static_assert(2 * kPairs <= kSK, "staged tile stride too small");
   auto stage = [&](int buf, int64_t kk0) {
-    double* A = Pi + buf * kPanel * kSK;
-    double* B = Pj + buf * kPanel * kSK;
-    for (int e = threadIdx.x; e < kPanel * kPairs; e += blockDim.x) {
+    double* A = Pi + buf * kSyrkBK * kSK;
+    double* B = Pj + buf * kSyrkBK * kSK;
+    for (int e = threadIdx.x; e < kSyrkBK * kPairs; e += blockDim.x) {
       const int kc = e / kPairs, rr = 2 * (e - kc * kPairs);
       const bool kin = kk0 + kc < kw;
       const int64_t ri = r0 - sa + rr, rj = c0 - sb + rr;
@@ -374,19 +386,19 @@ __global__ void __launch_bounds__(128, 3) syrk_kernel(DevSym S, const int32_t* _
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  const int nchunk = (int)((kw + kPanel - 1) / kPanel);
+  const int nchunk = (int)((kw + kSyrkBK - 1) / kSyrkBK);
   stage(0, 0);
   for (int ck = 0; ck < nchunk; ++ck) {
     if (ck + 1 < nchunk) {
-      stage((ck + 1) & 1, (int64_t)(ck + 1) * kPanel);
+      stage((ck + 1) & 1, (int64_t)(ck + 1) * kSyrkBK);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
-    const double* A = Pi + (ck & 1) * kPanel * kSK;
-    const double* B = Pj + (ck & 1) * kPanel * kSK;
-    const int kc = (int)min((int64_t)kPanel, kw - (int64_t)ck * kPanel);
+    const double* A = Pi + (ck & 1) * kSyrkBK * kSK;
+    const double* B = Pj + (ck & 1) * kSyrkBK * kSK;
+    const int kc = (int)min((int64_t)kSyrkBK, kw - (int64_t)ck * kSyrkBK);
     if (!skip)
       for (int kk = 0; kk < kc; kk += 4) {
         double fa[4], fb[4];
