@@ -51,8 +51,8 @@ def object_compliance(S, F, dim: int, stats: dict | None = None, group=None, sha
         counts = np.diff(csr.indptr)[rows]
         colptr[1:] = np.cumsum(counts)
         starts = csr.indptr[rows]
-        sel = np.concatenate([np.arange(s, s + c) for s, c in zip(starts, counts)]) if counts.sum() else \
-            np.zeros(0, dtype=np.int64)
+        # the CSR entries of those rows, row by row (vectorised ranges)
+        sel = np.repeat(starts - colptr[:-1], counts) + np.arange(colptr[-1], dtype=np.int64)
         rowidx = np.ascontiguousarray(csr.indices[sel], dtype=np.int64)
         vals = np.ascontiguousarray(csr.data[sel], dtype=np.float64)
         fl = (ctypes.c_double * 2)()
