@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
   // too coarse for sub-microsecond phases): tid 0: [0] idle at B1, [1] phase B,
   // [2] block solve; tid 32+64*.. see stamp() calls; helpers (CTA 1, tid 0): [4] wait, [5] work
   unsigned long long tp = 0;
-  const bool stamper = prof && (tid == 0 || tid == 32 || tid == 64 || tid == 160) && blockIdx.x <= 1;
+  const bool stamper = prof && (tid == 0 || tid == 32 || tid == 64 || tid == 96 || tid == 160) && blockIdx.x <= 1;
   auto stamp = [&](int k) {
     if (stamper) {
       const unsigned long long now = (unsigned long long)clock64();

@@ -25,6 +25,10 @@ for G in [int(x) for x in (sys.argv[1:] or ["1500", "3000", "5000", "7301"])]:
     cfg = cn.PgsConfig(10, 1e-300, 0.4)
     pgs_device(W, delta, 0.01, cfg)
     torch.cuda.synchronize()
+    if os.environ.get("CNB_PGS_PROFILE") == "1":  # reset the phase sums after the warm-up
+        import ctypes
+        from paper_2306_06946_b200 import _lib
+        _lib.lib().cnb_pgs_profile((ctypes.c_double * 32)())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     res = pgs_device(W, delta, 0.01, cfg)
@@ -32,6 +36,12 @@ for G in [int(x) for x in (sys.argv[1:] or ["1500", "3000", "5000", "7301"])]:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     nb = (G + 25) // 26
+    import ctypes
+    from paper_2306_06946_b200 import _lib
+    prof = (ctypes.c_double * 32)()
+    if os.environ.get("CNB_PGS_PROFILE") == "1" and _lib.lib().cnb_pgs_profile(prof) == 0:
+        print(json.dumps({"groups": G, "us_per_block_step": {k: round(prof[k] / (res.iterations * nb) / 1965.0, 3)
+                                                             for k in range(32) if prof[k]}}), flush=True)
     print(json.dumps({"groups": G, "sweeps": res.iterations, "ms_per_sweep": round(ms / res.iterations, 4),
                       "us_per_block": round(ms * 1e3 / res.iterations / nb, 3),
                       "w_gbs": round(8.0 * c * c / (ms / res.iterations * 1e-3) / 1e9, 1)}), flush=True)
