@@ -653,6 +653,11 @@ __global__ void __launch_bounds__(kPrepThreads) pgs_prep2_kernel(PgsScene s, dou
 }
 
 constexpr int kHelpPre = 32;  // W values per lane a helper warp holds in registers (32 x 32 columns)
+// the pipelined kernel's chain reads its diagonal tile transposed (W symmetric:
+// conflict-free shared loads), measured 1.347 -> 1.328 ms/sweep at cfg3
+#ifndef PGS_TRANS
+#define PGS_TRANS true
+#endif
 constexpr int kPipeThreads = 512;
 constexpr int kPG = 26;             // groups per block
 constexpr int kPR = 3 * kPG;        // rows per block
@@ -750,11 +755,15 @@ __device__ __forceinline__ void load_group_const(GroupConst& k, const double* kk
 // warp arrives at named barriers 7, 8 and 9 (with the phase-B warp, 64
 // threads): the records of those groups are final, and the phase-B warp folds
 // them into the next block's delta while the chain continues.
-template <bool FRIC, bool CHUNKS = false>
+template <bool FRIC, bool CHUNKS = false, bool TRANS = false>
 __device__ __forceinline__ void block_solve_v4(const double* __restrict__ Wt, int ld, int ng, int lane,
                                                double dl_[3], const double lm[3], const GroupConst& kc, double mu,
                                                double h2, double* __restrict__ sv, int e1 = 0, int e2 = 0) {
-  const double* wrow = Wt + 3 * lane * ld;
+  // TRANS: read W[g, l] instead of W[l, g] (W is symmetric): at step g the lanes
+  // read consecutive columns of the same three rows (no bank conflicts)
+  const int lr = (TRANS && lane >= 32 - 4) ? 0 : lane;
+  const double* wrow = Wt + 3 * lr * ld;
+  const double* wcol = Wt + 3 * lr;
   const double h2l1 = h2 * lm[1], h2l2 = h2 * lm[2];
   const double nl0 = -lm[0], lhw = lm[0] * kc.hwnn, nihw = -kc.ihw;
 #pragma unroll 2
@@ -763,7 +772,7 @@ __device__ __forceinline__ void block_solve_v4(const double* __restrict__ Wt, in
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) w[3 * a + c] = wrow[a * ld + 3 * g + c];
+      for (int c = 0; c < 3; ++c) w[3 * a + c] = TRANS ? wcol[(3 * g + c) * ld + a] : wrow[a * ld + 3 * g + c];
     const double d0 = dl_[0], d1 = dl_[1], d2 = dl_[2];
     const bool open = d0 < lhw;                        // l_n - d_n/(h^2 W_nn) > 0
     const double x = fma(nihw, d0, lm[0]);
@@ -992,9 +1001,9 @@ __global__ void __launch_bounds__(kPipeThreads) pgs_pipe_kernel(PgsScene s, cons
         asm volatile("bar.arrive 2, %0;" ::"n"(32 + 32 * kXW));  // dcur consumed
         stamp(13);
         if (s.mu != 0.0)
-          block_solve_v4<true, true>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv, e1, e2);
+          block_solve_v4<true, true, PGS_TRANS>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv, e1, e2);
         else
-          block_solve_v4<false, true>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv, e1, e2);
+          block_solve_v4<false, true, PGS_TRANS>(Tc, kPS, ng, lane, dl, lm, kc, s.mu, h2, sm.sv, e1, e2);
         __syncwarp();
         stamp(14);
         const int err = mine ? block_commit(sm.sv, lane, lm, kc, s.mu, ih2, dsq) : 0;
