@@ -41,34 +41,26 @@ __global__ void scatter_kernel(int64_t nmap, const int64_t* __restrict__ src, co
   if (k < nmap) front[dst[k]] = vals[src[k]];
 }
 
-// extend-add: task = (parent p, parent col range [lo, hi)).  For every child
-// c of p (ascending) and every child update column k whose parent column
-// rel[k] lies in [lo, hi): F_p[rel[i], rel[k]] += U_c[i, k], i >= k.
+// extend-add: task = (parent p, parent col range [lo, hi), offset of the
+// children's row ranges).  For every child c of p (ascending) and every child
+// update column k whose parent column rel[k] lies in [lo, hi) -- the range
+// [k0, k1) comes precomputed with the symbolic analysis (no binary searches
+// on the dependent-load chain) -- F_p[rel[i], rel[k]] += U_c[i, k], i >= k.
 // Rows are processed in batches of kEaBatch per thread: all loads of a batch
 // are issued before its stores (the parent and child fronts live in one
 // buffer, so the compiler could not reorder them otherwise).
 constexpr int kEaBatch = 4;
 __global__ void __launch_bounds__(256, 6) extend_add_kernel(DevSym S, const int32_t* __restrict__ tasks,
-                                                         double* __restrict__ front) {
-  const int32_t p = tasks[3 * blockIdx.x], lo = tasks[3 * blockIdx.x + 1], hi = tasks[3 * blockIdx.x + 2];
+                                                         const int32_t* __restrict__ rng, double* __restrict__ front) {
+  const int32_t p = tasks[4 * blockIdx.x];
+  const int32_t* kr = rng + 2 * tasks[4 * blockIdx.x + 3];
   const int64_t ldp = d_ldf(S, p);
   double* Fp = front + S.front_off[p];
   for (int64_t ci = S.child_ptr[p]; ci < S.child_ptr[p + 1]; ++ci) {
     const int64_t c = S.child[ci];
     const int64_t ncc = d_nc(S, c), nrc = d_nr(S, c), ldc = d_ldf(S, c);
     const int32_t* __restrict__ rel = S.rel + S.rel_ptr[c];
-    int64_t a = 0, b = nrc;
-    while (a < b) {
-      int64_t m = (a + b) >> 1;
-      if (rel[m] < lo) a = m + 1; else b = m;
-    }
-    const int64_t k0 = a;
-    b = nrc;
-    while (a < b) {
-      int64_t m = (a + b) >> 1;
-      if (rel[m] < hi) a = m + 1; else b = m;
-    }
-    const int64_t k1 = a;
+    const int64_t k0 = kr[2 * (ci - S.child_ptr[p])], k1 = kr[2 * (ci - S.child_ptr[p]) + 1];
     const double* Fc = front + S.front_off[c];
     for (int64_t k = k0; k < k1; ++k) {
       const double* __restrict__ uc = Fc + (ncc + k) * ldc + ncc;
@@ -468,6 +460,7 @@ static int chol_upload(CholHandle* h) {
   h->m_off.assign(S.ns + 1, 0);
   for (int64_t s = 0; s < S.ns; ++s) h->m_off[s + 1] = h->m_off[s] + S.ldf(s) * S.nc(s);
   if ((rc = upload_vec(&h->d_m_off, h->m_off)) != CNB_OK) return rc;
+  if ((rc = upload_vec(&h->d_ea_rng, S.ea_rng)) != CNB_OK) return rc;
   std::vector<int32_t> all;
   struct Rec {
     int64_t off, count;
@@ -476,7 +469,7 @@ static int chol_upload(CholHandle* h) {
   std::vector<std::vector<Rec>> po_rec, tr_rec, sy_rec, so_rec;
   for (int l = 0; l < S.n_levels; ++l) {
     const LevelTasks& T = S.tasks[l];
-    ea_rec.push_back({(int64_t)all.size(), (int64_t)T.ea.size() / 3});
+    ea_rec.push_back({(int64_t)all.size(), (int64_t)T.ea.size() / 4});
     all.insert(all.end(), T.ea.begin(), T.ea.end());
     po_rec.emplace_back();
     tr_rec.emplace_back();
@@ -550,7 +543,7 @@ static int chol_upload(CholHandle* h) {
 static void chol_free(CholHandle* h) {
   void* ptrs[] = {h->d_first, h->d_rows_ptr, h->d_rows, h->d_front_off, h->d_child_ptr, h->d_child,
                   h->d_rel_ptr, h->d_rel, h->d_map_src, h->d_map_dst, h->d_perm, h->d_front, h->d_tasks,
-                  h->d_m, h->d_m_off, h->d_kkinv, h->d_vals, h->d_kk_off};
+                  h->d_m, h->d_m_off, h->d_kkinv, h->d_vals, h->d_kk_off, h->d_ea_rng};
   if (h->factor_exec) cudaGraphExecDestroy(h->factor_exec);
   h->factor_exec = nullptr;
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
@@ -599,7 +592,7 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
   }
   for (int l = 0; l < S.n_levels; ++l) {
     if (h->ea[l].count) {
-      extend_add_kernel<<<(unsigned)h->ea[l].count, 256, 0, st>>>(sym, h->ea[l].ptr, h->d_front);
+      extend_add_kernel<<<(unsigned)h->ea[l].count, 256, 0, st>>>(sym, h->ea[l].ptr, h->d_ea_rng, h->d_front);
       CNB_LAUNCH_CHECK("extend_add_kernel");
     }
     for (size_t p = 0; p < h->potrf[l].size(); ++p) {

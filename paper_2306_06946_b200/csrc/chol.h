@@ -27,7 +27,8 @@ constexpr int kInvCols = 8;  // columns of L11^{-1} per inversion task
 constexpr int kMaxSnCols = 512;  // widest supernode (wider ones are split into chains)
 
 struct LevelTasks {
-  // extend-add: (parent supernode, parent col lo, parent col hi)
+  // extend-add: (parent supernode, parent col lo, parent col hi, offset into
+  // Symbolic::ea_rng of the children's row ranges for that column range)
   std::vector<int32_t> ea;
   // per panel step p: potrf fronts, trsm (front, row chunk), syrk (front, ti, tj):
   // syrk[p] = in-block update of the block's remaining pivot columns by panel p,
@@ -36,6 +37,7 @@ struct LevelTasks {
 };
 
 struct Symbolic {
+  std::vector<int32_t> ea_rng;  // per extend-add task, per child: [k0, k1) of its rows mapping into [lo, hi)
   int64_t n = 0;   // DoFs
   int bs = 1;      // DoFs per graph node
   std::vector<int64_t> perm, iperm;        // DoF level: perm[new] = old

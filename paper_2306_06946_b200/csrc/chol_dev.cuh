@@ -80,6 +80,7 @@ struct CholHandle {
   int64_t *d_child_ptr = nullptr, *d_child = nullptr, *d_rel_ptr = nullptr, *d_perm = nullptr;
   int64_t* d_m_off = nullptr;
   int32_t* d_rel = nullptr;
+  int32_t* d_ea_rng = nullptr;  // extend-add children's row ranges (Symbolic::ea_rng)
   int64_t *d_map_src = nullptr, *d_map_dst = nullptr;
   double* d_front = nullptr;
   double* d_m = nullptr;       // solve panels M_s = [L11^{-1}; P21 = L21 L11^{-1}], see DevSym::m_off

@@ -517,6 +517,7 @@ int analyze(Symbolic& S, int64_t n, const int64_t* rowptr, const int64_t* col, i
     }
   // per-level task lists
   S.tasks.assign(S.n_levels, LevelTasks());
+  S.ea_rng.clear();
   for (int l = 0; l < S.n_levels; ++l) {
     LevelTasks& T = S.tasks[l];
     int64_t max_panels = 0;
@@ -524,9 +525,18 @@ int analyze(Symbolic& S, int64_t n, const int64_t* rowptr, const int64_t* col, i
       const int64_t s = S.level_sn[q];
       if (S.child_ptr[s + 1] > S.child_ptr[s])
         for (int64_t lo = 0; lo < S.f(s); lo += kEaCols) {
+          const int64_t hi = std::min<int64_t>(S.f(s), lo + kEaCols);
           T.ea.push_back((int32_t)s);
           T.ea.push_back((int32_t)lo);
-          T.ea.push_back((int32_t)std::min<int64_t>(S.f(s), lo + kEaCols));
+          T.ea.push_back((int32_t)hi);
+          T.ea.push_back((int32_t)(S.ea_rng.size() / 2));
+          for (int64_t ci = S.child_ptr[s]; ci < S.child_ptr[s + 1]; ++ci) {  // rel is ascending per child
+            const int64_t c = S.child[ci];
+            const int32_t* r0 = S.rel.data() + S.rel_ptr[c];
+            const int32_t* r1 = S.rel.data() + S.rel_ptr[c + 1];
+            S.ea_rng.push_back((int32_t)(std::lower_bound(r0, r1, (int32_t)lo) - r0));
+            S.ea_rng.push_back((int32_t)(std::lower_bound(r0, r1, (int32_t)hi) - r0));
+          }
         }
       max_panels = std::max(max_panels, (S.nc(s) + kPanel - 1) / kPanel);
     }
