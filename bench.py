@@ -37,6 +37,8 @@ if fewer GPUs are visible).
 from __future__ import annotations
 
 import argparse
+import contextlib
+import gc
 import json
 import os
 import statistics
@@ -319,6 +321,18 @@ def flush_l2(torch, buf):
     buf.add_(1.0)  # 512 MiB read+write > 126 MB L2
 
 
+@contextlib.contextmanager
+def _no_gc():
+    """Timed regions run with Python's cyclic collector paused (collected just
+    before): a collection pause inside one step is host jitter, not the path."""
+    gc.collect()
+    gc.disable()
+    try:
+        yield
+    finally:
+        gc.enable()
+
+
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled every 100 ms during the timed region."""
 
@@ -434,7 +448,7 @@ def run_gpu_cfg1(args, rank, world):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     phases = []
-    with ClockSampler() as clk:
+    with ClockSampler() as clk, _no_gc():
         torch.cuda.synchronize()
         launches0 = _lib.lib().cnb_launch_count()
         for i in range(args.steps):
@@ -449,10 +463,11 @@ def run_gpu_cfg1(args, rank, world):
     for _ in range(max(1, args.warmup // 2)):
         wl.step_e2e()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        wl.step_e2e()
-        torch.cuda.current_stream().synchronize()
+    with _no_gc():
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            wl.step_e2e()
+            torch.cuda.current_stream().synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     roof = roofline_cfg1(wl, torch, _lib, phases)
     total_ms, e2e_ms = _max_over_ranks(torch, world, total_ms, e2e_ms)
@@ -565,7 +580,7 @@ def run_gpu_cfg3(args, rank, world):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     reps = []
-    with ClockSampler() as clk:
+    with ClockSampler() as clk, _no_gc():
         torch.cuda.synchronize()
         launches0 = _lib.lib().cnb_launch_count()
         for i in range(args.steps):
@@ -580,9 +595,10 @@ def run_gpu_cfg3(args, rank, world):
     total_ms = sum(step_ms)
     # e2e: the same step through pinned host buffers
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        wl.step_e2e()
+    with _no_gc():
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            wl.step_e2e()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     total_ms, e2e_ms = _max_over_ranks(torch, world, total_ms, e2e_ms)
     ms_step = total_ms / args.steps
@@ -788,7 +804,7 @@ def run_gpu_cfg4(args, rank, world):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     pairs = []
     prof = _PgsBatchTimer(torch)
-    with ClockSampler() as clk:
+    with ClockSampler() as clk, _no_gc():
         torch.cuda.synchronize()
         launches0 = _lib.lib().cnb_launch_count()
         for i in range(args.steps):
@@ -804,9 +820,10 @@ def run_gpu_cfg4(args, rank, world):
         torch.distributed.barrier()
     total_ms = sum(s_.elapsed_time(e_) for s_, e_ in zip(starts, ends))
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        wl.step_e2e()
+    with _no_gc():
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            wl.step_e2e()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     total_ms, e2e_ms = _max_over_ranks(torch, world, total_ms, e2e_ms)
     ms_step = total_ms / args.steps
