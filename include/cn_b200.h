@@ -98,7 +98,8 @@ int cnb_batch_scatter_acc(int64_t m, const int32_t* pscene, const int32_t* pcand
 /* PGS of independent scenes, one CTA each (solver.py:168-202 per scene);
  * g_off / w_off / mu are HOST arrays (nscenes + 1 / nscenes / nscenes); order
  * (HOST, optional) is the launch order, a permutation of the scenes (heaviest
- * expected solve first); results are per scene whatever the order. */
+ * expected solve first); results are per scene whatever the order.
+ * delta_end may be NULL: the final pass over each scene's W is skipped. */
 int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off, const double* mu, const double* W,
                     const double* delta_base, double h, double tol, int32_t max_iter, double* lam, double* delta_end,
                     double* eps_hist, int32_t* iters_conv, const int32_t* order, cnb_status_t* d_status,

@@ -120,10 +120,21 @@ class BatchedPlaneScenes:
         self.time = 0.0
         self.step_index = 0
         self._prev_sweeps = None
+        self._bufs = {}
         self._status = _lib.status(d)
         self.last = {}
 
     # -- helpers -------------------------------------------------------------------
+    def _resident(self, name: str, size: int) -> torch.Tensor:
+        """A view of a grow-only resident buffer (the per-copy W_g / W blocks: the
+        contact count drifts by a few pairs between steps; reallocating hundreds of
+        MB then would stall the step)."""
+        buf = self._bufs.get(name)
+        if buf is None or buf.numel() < size:
+            buf = dv.empty(max(int(size * 1.25), 1))
+            self._bufs[name] = buf
+        return buf[:size]
+
     def _solve(self, B: torch.Tensor) -> torch.Tensor:
         """X (ns, n) with A x_s = b_s for every copy: one DMMA GEMM with the inverse."""
         X = torch.empty_like(B)
@@ -200,12 +211,12 @@ class BatchedPlaneScenes:
                       q_free.data_ptr(), n, pa.data_ptr(), st)
             pb = P["pb"]  # world points on the planes
             nblk = int(P["boff_h"][-1])
-            Wg, W = dv.empty(P["wsize"]), dv.empty(P["wsize"])
+            Wg, W = self._resident("Wg", P["wsize"]), self._resident("W", P["wsize"])
             _lib.call("cnb_batch_wg_gather", ns, nblk, P["boff"].data_ptr(), P["poff"].data_ptr(),
                       P["woff"].data_ptr(), P["cand"].data_ptr(), self.vids.data_ptr(), self.Ainv.data_ptr(), n,
                       Wg.data_ptr(), st)
             delta, t = dv.empty(3 * m), dv.empty(3 * m)
-            lam, dend = dv.empty(3 * m), dv.empty(3 * m)
+            lam = dv.empty(3 * m)  # (delta_end is not needed: the proximity update follows)
             eps = dv.empty((ns, self.pgs_max))
             ics = []
             rot = dv.zeros(1)
@@ -226,7 +237,7 @@ class BatchedPlaneScenes:
                 ic = torch.zeros((ns, 2), dtype=torch.int32, device=dv.device())
                 ics.append(ic)
                 _lib.call("cnb_pgs_batched", ns, g_off.ctypes.data, w_off.ctypes.data, mus.ctypes.data, W.data_ptr(),
-                          delta.data_ptr(), h, self.pgs_tol, self.pgs_max, lam.data_ptr(), dend.data_ptr(),
+                          delta.data_ptr(), h, self.pgs_tol, self.pgs_max, lam.data_ptr(), None,
                           eps.data_ptr(), ic.data_ptr(), order.ctypes.data, self._status.ptr, st)
                 _lib.call("cnb_apply_dt", m, Dk.data_ptr(), lam.data_ptr(), t.data_ptr(), acc.data_ptr(), st)
                 _lib.call("cnb_batch_prox", ns, m, P["poff"].data_ptr(), P["woff"].data_ptr(), Wg.data_ptr(),

@@ -1768,8 +1768,8 @@ __global__ void __launch_bounds__(kCopyThreads, 2) pgs_copy_kernel(const PgsScen
     if (flags[0] || converged) break;
   }
   __syncthreads();
-  // ---- delta_end = delta_base + h^2 W_reg lam (solver.py:201) ----
-  for (int64_t r = warp; r < c; r += kCopyThreads / 32) {
+  // ---- delta_end = delta_base + h^2 W_reg lam (solver.py:201); skipped when not wanted ----
+  for (int64_t r = warp; s.delta_end && r < c; r += kCopyThreads / 32) {
     double acc = lane_dot<false>(W + r * ld, lam, 0, c, lane);
     acc = warp_sum(acc);
     if (lane == 0) {
@@ -2220,7 +2220,7 @@ int cnb_pgs_batched(int32_t nscenes, const int64_t* g_off, const int64_t* w_off,
     sc.tol = tol;
     sc.max_iter = max_iter;
     sc.lam = lam + 3 * g_off[i];
-    sc.delta_end = delta_end + 3 * g_off[i];
+    sc.delta_end = delta_end ? delta_end + 3 * g_off[i] : nullptr;
     sc.eps_hist = eps_hist + (int64_t)i * max_iter;
     sc.iters_conv = iters_conv + 2 * i;
     sc.status = (DevStatus*)d_status;
