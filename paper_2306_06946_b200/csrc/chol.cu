@@ -319,9 +319,16 @@ constexpr int kSK = kTile + 4;  // smem stride of one k column of a staged tile
 constexpr int kSyrkBK = SYRK_BK;  // k depth of one staged chunk
 constexpr size_t kSyrkSmem = 2 * 2 * kSyrkBK * kSK * sizeof(double);
 static_assert(kPotrfSmem <= kSyrkSmem, "the fused POTRF reuses the SYRK staging buffers");
-__global__ void __launch_bounds__(128, SYRK_MINB) syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode,
-                                                   double* __restrict__ front, double* __restrict__ kkinv,
-                                                   DevStatus* st) {
+// TRAIL: the trailing (mode 1) launches, which never factor a panel: without
+// the fused POTRF's registers they fit SYRK_TRAIL_MINB CTAs per SM
+#ifndef SYRK_TRAIL_MINB
+#define SYRK_TRAIL_MINB 4
+#endif
+constexpr unsigned kTrailMinTiles = 4 * 148;  // trailing launches of at least this many tiles take TRAIL
+template <bool TRAIL>
+__global__ void __launch_bounds__(128, TRAIL ? SYRK_TRAIL_MINB : SYRK_MINB)
+    syrk_kernel(DevSym S, const int32_t* __restrict__ tasks, int p, int mode, double* __restrict__ front,
+                double* __restrict__ kkinv, DevStatus* st) {
   extern __shared__ __align__(16) double syrk_sm[];
   double* Pi = syrk_sm;                  // [2][kSyrkBK * kSK]
   double* Pj = syrk_sm + 2 * kSyrkBK * kSK;
@@ -409,31 +416,38 @@ __global__ void __launch_bounds__(128, SYRK_MINB) syrk_kernel(DevSym S, const in
   // C load before the first store (F aliases itself, so
   // the compiler would otherwise serialise load -> subtract -> store)
   if (!skip) {
-    double cv[4][4][2];
+    // (TRAIL: in two halves of 16 values, so the accumulators plus the loaded C fit
+    // the 128 registers of SYRK_TRAIL_MINB = 4 CTAs per SM)
+    constexpr int kHalves = TRAIL ? 2 : 1;
   #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int hv = 0; hv < kHalves; ++hv) {
+      double cv[4 / kHalves][4][2];
   #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int aa = 0; aa < 4 / kHalves; ++aa)
   #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t r = r0 + wy + 8 * a + g;
-          const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-          cv[a][b][h] = (r < f && c < cend && r >= c) ? F[c * ldf + r] : 0.0;
-        }
+        for (int b = 0; b < 4; ++b)
   #pragma unroll
-    for (int a = 0; a < 4; ++a)
+          for (int h = 0; h < 2; ++h) {
+            const int64_t r = r0 + wy + 8 * (hv * (4 / kHalves) + aa) + g;
+            const int64_t c = c0 + wx + 8 * b + 2 * t + h;
+            cv[aa][b][h] = (r < f && c < cend && r >= c) ? F[c * ldf + r] : 0.0;
+          }
   #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int aa = 0; aa < 4 / kHalves; ++aa)
   #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t r = r0 + wy + 8 * a + g;
-          const int64_t c = c0 + wx + 8 * b + 2 * t + h;
-          if (r < f && c < cend && r >= c) F[c * ldf + r] = cv[a][b][h] - acc[a][b][h];
-        }
+        for (int b = 0; b < 4; ++b)
+  #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int a = hv * (4 / kHalves) + aa;
+            const int64_t r = r0 + wy + 8 * a + g;
+            const int64_t c = c0 + wx + 8 * b + 2 * t + h;
+            if (r < f && c < cend && r >= c) F[c * ldf + r] = cv[aa][b][h] - acc[a][b][h];
+          }
+    }
   }
   // the tile holding the next panel's diagonal block (this update is the last one
   // it receives) factors it right away: no separate POTRF launch for panels > 0
-  if (ti == 0 && tj == 0 && t0 < nc) {
+  if (!TRAIL && ti == 0 && tj == 0 && t0 < nc) {
     __syncthreads();  // the tile's stores are visible to the CTA
     if (warp < 2) potrf_panel(S, s, (int)t0, front, kkinv, st, syrk_sm);
   }
@@ -535,7 +549,8 @@ static int chol_upload(CholHandle* h) {
   if ((rc = upload_vec(&h->d_kk_off, h->kk_off)) != CNB_OK) return rc;
   CNB_CUDA(cudaMalloc((void**)&h->d_kkinv, std::max<int64_t>(1, h->kk_off[S.ns]) * kPanel * kPanel * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_vals, std::max<int64_t>(1, S.csr_nnz) * sizeof(double)));
-  CNB_CUDA(cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem));
+  CNB_CUDA(cudaFuncSetAttribute(syrk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem));
+  CNB_CUDA(cudaFuncSetAttribute(syrk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem));
   h->uploaded = true;
   return CNB_OK;
 }
@@ -608,13 +623,17 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
         CNB_LAUNCH_CHECK("trsm_kernel");
       }
       if (h->syrk[l][p].count) {
-        syrk_kernel<<<(unsigned)h->syrk[l][p].count, 128, kSyrkSmem, st>>>(sym, h->syrk[l][p].ptr, (int)p, 0,
+        syrk_kernel<false><<<(unsigned)h->syrk[l][p].count, 128, kSyrkSmem, st>>>(sym, h->syrk[l][p].ptr, (int)p, 0,
                                                                            h->d_front, h->d_kkinv, d_status);
         CNB_LAUNCH_CHECK("syrk_kernel");
       }
       if (h->syrk_out[l][p].count) {
-        syrk_kernel<<<(unsigned)h->syrk_out[l][p].count, 128, kSyrkSmem, st>>>(sym, h->syrk_out[l][p].ptr, (int)p,
-                                                                               1, h->d_front, h->d_kkinv, d_status);
+        // (mode 1 factors no panel: t0 = block end = nc, pieces are <= 512 wide);
+        // large launches take the 4-CTA-per-SM variant, small (latency-bound) ones
+        // keep the plain epilogue
+        const unsigned n1 = (unsigned)h->syrk_out[l][p].count;
+        auto k1 = n1 >= kTrailMinTiles ? syrk_kernel<true> : syrk_kernel<false>;
+        k1<<<n1, 128, kSyrkSmem, st>>>(sym, h->syrk_out[l][p].ptr, (int)p, 1, h->d_front, h->d_kkinv, d_status);
         CNB_LAUNCH_CHECK("syrk_kernel");
       }
     }
