@@ -308,9 +308,10 @@ __global__ void __launch_bounds__(128) trsm_kernel(DevSym S, const int32_t* __re
 //   C[rows ti, cols tj] -= P[rows ti, :] * P[rows tj, :]^T,  P = L columns [k0, k0 + kw).
 // mode 0 (in-block): P = panel p (kw <= 32), target columns [t0, block end) of
 //   every row below -- only the block's remaining pivot columns;
-// mode 1 (trailing): P = the whole block of panel p (kw <= 128 columns), target
-//   [block end, f).  The trailing matrix is read and written once per 128
-//   columns, with K = 128 per pass (16 flop per byte of C).
+// mode 1 (trailing): P = the whole block of panel p (kw <= kBlkPanels * kPanel
+//   = 512 columns: the whole supernode piece), target [block end, f).  The
+//   trailing matrix is read and written once per piece, with K <= 512 (up to
+//   64 flop per byte of C).
 // 4 warps, each a 32x32 quadrant = 4x4 fragments of 8x8.  The staged panels
 // are k-major ([k][row], as in the column-major front), so the asynchronous
 // copies of consecutive rows land in consecutive banks, and the fragment loads
