@@ -57,12 +57,13 @@ struct SolvePlan {
   double* d_rhs = nullptr;
   void* d_lv = nullptr;  // width 1: per-level task table of the cooperative solve (solve.cu SolveLevel)
   int32_t *d_cptr = nullptr, *d_csrc = nullptr;  // its assembly gathers (solve.cu gemv1_task)
+  int32_t* d_g1 = nullptr;                         // its panel tasks (kG1Rows rows each)
   int coop_grid = 0;
   void release() {
     for (void* p : {(void*)d_tasks, (void*)d_roff, (void*)d_lo, (void*)d_w, (void*)d_rhs, d_lv, (void*)d_cptr,
-                    (void*)d_csrc})
+                    (void*)d_csrc, (void*)d_g1})
       if (p) cudaFree(p);
-    d_cptr = d_csrc = nullptr;
+    d_cptr = d_csrc = d_g1 = nullptr;
     d_tasks = nullptr;
     d_roff = d_lo = d_w = nullptr;
     d_rhs = nullptr;

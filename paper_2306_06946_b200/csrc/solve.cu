@@ -28,6 +28,8 @@ constexpr int kSolveThreads = 128;
 constexpr int kAsmRows = 128;   // rows per assemble task
 constexpr int kAsmCols = 64;    // columns per assemble task (sparse mode)
 constexpr int kGemvRows = 32;   // rows per dense panel task
+constexpr int kG1Rows = 16;     // rows per panel task of the cooperative single-RHS solve on levels with few
+                                // tasks (kGemvRows on the others)
 constexpr int kGemvJ = 256;     // staged pivot rows of the RHS per pass
 constexpr int kGemvU = 16;      // panel loads in flight per thread
 constexpr int kBwdRows = 4;     // pivot rows per backward task (warp per row)
@@ -424,48 +426,56 @@ __device__ __forceinline__ double gather_row(int32_t r, double v, const int32_t*
   for (int32_t q = cptr[r]; q < cptr[r + 1]; ++q) v = v + rhs[csrc[q]];
   return v;
 }
+template <int ROWS>
 __device__ __forceinline__ void gemv1_task(const DevSym& S, const int32_t* __restrict__ task, const RhsView& R,
                                            const double* __restrict__ panel, double* Bp,
                                            const int32_t* __restrict__ cptr, const int32_t* __restrict__ csrc,
-                                           double* rt, double* ug, double (*red)[32][1]) {
+                                           double* rt, double* ug, double* red_) {
+  constexpr int kG1Grp = 256 / ROWS;  // column groups
+  double(*red)[ROWS] = reinterpret_cast<double(*)[ROWS]>(red_);
   // one pass of gathers for the whole task (pivot rows into rt, this task's
-  // update rows into ug) with the first panel loads already in flight
+  // update rows into ug) with the first panel loads already in flight.  A task
+  // is ROWS rows x all nc columns, split over 256 / ROWS column groups.  Levels
+  // with few tasks (the top levels' few large fronts) take ROWS = 16 (a
+  // half-warp reads 128 contiguous bytes of a panel column): twice the tasks and
+  // half the dependent load batches per thread.
   const int64_t s = task[0], r0 = task[1];
   const int64_t nc = d_nc(S, s), f = nc + d_nr(S, s), ldm = d_ldf(S, s);
   const int32_t rb = (int32_t)R.roff[s];
   const double* M = panel + S.m_off[s];
   const int64_t first = S.first[s];
-  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int64_t i = r0 + lane;
+  const int lr = threadIdx.x % ROWS, grp = threadIdx.x / ROWS;
+  const int64_t i = r0 + lr;
   const double* pc = M + i;
   double mv[kGemvU];
 #pragma unroll
-  for (int u = 0; u < kGemvU; ++u) mv[u] = (i < f && grp + 8 * u < nc) ? pc[(int64_t)(grp + 8 * u) * ldm] : 0.0;
+  for (int u = 0; u < kGemvU; ++u)
+    mv[u] = (i < f && grp + kG1Grp * u < nc) ? pc[(int64_t)(grp + kG1Grp * u) * ldm] : 0.0;
   for (int j = threadIdx.x; j < nc; j += blockDim.x)
     rt[j] = gather_row(rb + (int32_t)j, Bp[first + j], cptr, csrc, R.rhs);
-  if (threadIdx.x < 32 && i >= nc && i < f) ug[lane] = gather_row(rb + (int32_t)i, 0.0, cptr, csrc, R.rhs);
+  if (threadIdx.x < ROWS && i >= nc && i < f) ug[lr] = gather_row(rb + (int32_t)i, 0.0, cptr, csrc, R.rhs);
   __syncthreads();
   double acc = 0.0;
   if (i < f) {
     for (int j0 = grp;;) {
 #pragma unroll
       for (int u = 0; u < kGemvU; ++u)
-        if (j0 + 8 * u < nc) acc = fma(mv[u], rt[j0 + 8 * u], acc);
-      j0 += 8 * kGemvU;
+        if (j0 + kG1Grp * u < nc) acc = fma(mv[u], rt[j0 + kG1Grp * u], acc);
+      j0 += kG1Grp * kGemvU;
       if (j0 >= nc) break;
 #pragma unroll
-      for (int u = 0; u < kGemvU; ++u) mv[u] = j0 + 8 * u < nc ? pc[(int64_t)(j0 + 8 * u) * ldm] : 0.0;
+      for (int u = 0; u < kGemvU; ++u) mv[u] = j0 + kG1Grp * u < nc ? pc[(int64_t)(j0 + kG1Grp * u) * ldm] : 0.0;
     }
   }
-  red[grp][lane][0] = acc;
+  red[grp][lr] = acc;
   __syncthreads();
   if (grp == 0 && i < f) {
     double v = 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v += red[q][lane][0];
+    for (int q = 0; q < kG1Grp; ++q) v += red[q][lr];
     // y into the front's own RHS rows (the front's other tasks may still be
     // staging its pivot rows from Bp), updates into the rows below
-    R.rhs[rb + i] = i < nc ? v : ug[lane] - v;
+    R.rhs[rb + i] = i < nc ? v : ug[lr] - v;
   }
 }
 
@@ -477,9 +487,9 @@ __device__ __forceinline__ unsigned long long solve_ns() {
 }
 
 struct SolveLevel {
-  const int32_t* gemv_t;
+  const int32_t* gemv_t;  // panel tasks of `rows` rows
   const int32_t* bwd_t;
-  int32_t n_gemv, n_bwd;
+  int32_t n_gemv, n_bwd, rows;
 };
 
 // The assembly is a gather folded into the panel GEMV (gemv1_task): RHS
@@ -493,8 +503,8 @@ __global__ void __launch_bounds__(256, 3) solve1_kernel(DevSym S, RhsView R, con
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double rt[kMaxSnCols];
-  __shared__ double ug[32];
-  __shared__ double red[8][32][1];
+  __shared__ double ug[kGemvRows];
+  __shared__ double red[256];
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
   int ph = 0;
   auto mark = [&]() {  // diagnostic: phase end times of CTA 0 (cnb_solve_profile)
@@ -508,7 +518,10 @@ __global__ void __launch_bounds__(256, 3) solve1_kernel(DevSym S, RhsView R, con
   for (int l = 0; l < nlev; ++l) {
     const SolveLevel L = lv[l];
     for (int q = blockIdx.x; q < L.n_gemv; q += gridDim.x) {
-      gemv1_task(S, L.gemv_t + 3 * q, R, panel, Bp, cptr, csrc, rt, ug, red);
+      if (L.rows == kG1Rows)
+        gemv1_task<kG1Rows>(S, L.gemv_t + 3 * q, R, panel, Bp, cptr, csrc, rt, ug, red);
+      else
+        gemv1_task<kGemvRows>(S, L.gemv_t + 3 * q, R, panel, Bp, cptr, csrc, rt, ug, red);
       __syncthreads();  // rt / red reused by the next task
     }
     grid.sync();
@@ -690,11 +703,6 @@ static int build_plan(CholHandle* h, SolvePlan& P, int64_t width) {
       }
     if ((rc = upload_vec(&P.d_cptr, cptr))) return rc;
     if ((rc = upload_vec(&P.d_csrc, csrc))) return rc;
-    std::vector<SolveLevel> lv(S.n_levels);
-    for (int l = 0; l < S.n_levels; ++l)
-      lv[l] = SolveLevel{P.panel_t[l].ptr, P.bwd_t[l].ptr, (int32_t)P.panel_t[l].count, (int32_t)P.bwd_t[l].count};
-    CNB_CUDA(cudaMalloc(&P.d_lv, std::max<size_t>(1, lv.size()) * sizeof(SolveLevel)));
-    if (!lv.empty()) CNB_CUDA(cudaMemcpy(P.d_lv, lv.data(), lv.size() * sizeof(SolveLevel), cudaMemcpyHostToDevice));
     int dev = 0, sms = 0, occ = 0;
     CNB_CUDA(cudaGetDevice(&dev));
     CNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -702,6 +710,28 @@ static int build_plan(CholHandle* h, SolvePlan& P, int64_t width) {
     // more resident CTAs help the latency-bound bottom levels of a large tree;
     // a small one pays more for its grid barriers than it gains
     P.coop_grid = sms * std::min(occ, S.ns > 1000 ? 3 : 2);
+    // panel tasks: kG1Rows rows on levels whose kGemvRows tasks would leave more
+    // than half of the grid idle
+    std::vector<int32_t> g1;
+    std::vector<SolveLevel> lv(S.n_levels);
+    std::vector<int64_t> g1off(S.n_levels);
+    for (int l = 0; l < S.n_levels; ++l) {
+      const int64_t off = (int64_t)g1.size();
+      int64_t n32 = 0;
+      for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) n32 += (S.f(S.level_sn[q]) + kGemvRows - 1) / kGemvRows;
+      const int rows = 2 * n32 < P.coop_grid ? kG1Rows : kGemvRows;
+      for (int64_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
+        const int64_t s = S.level_sn[q];
+        for (int64_t r = 0; r < S.f(s); r += rows) g1.insert(g1.end(), {(int32_t)s, (int32_t)r, 0});
+      }
+      g1off[l] = off;
+      lv[l] = SolveLevel{nullptr, P.bwd_t[l].ptr, (int32_t)(((int64_t)g1.size() - off) / 3), (int32_t)P.bwd_t[l].count,
+                         rows};
+    }
+    if ((rc = upload_vec(&P.d_g1, g1))) return rc;
+    for (int l = 0; l < S.n_levels; ++l) lv[l].gemv_t = P.d_g1 + g1off[l];
+    CNB_CUDA(cudaMalloc(&P.d_lv, std::max<size_t>(1, lv.size()) * sizeof(SolveLevel)));
+    if (!lv.empty()) CNB_CUDA(cudaMemcpy(P.d_lv, lv.data(), lv.size() * sizeof(SolveLevel), cudaMemcpyHostToDevice));
   }
   P.width = width;
   return CNB_OK;
