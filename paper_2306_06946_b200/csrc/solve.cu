@@ -49,60 +49,92 @@ struct RhsView {
 // Block forward substitution L11 X = I over 32-row blocks: the diagonal block
 // of block kb is inverted already (D_kb, kept by potrf_kernel), so each block
 // step is y = D_kb v (a small product, no sequential row loop) followed by the
-// update of the rows below with the panel columns of L.
+// update of the rows below with the panel columns of L.  The task's X columns
+// live in shared memory for the whole substitution (written to M_s once at the
+// end), the next D block is staged with cp.async during the current step, and
+// each thread's L values for the update are loaded before the step waits on D:
+// a step is one shared-memory round instead of three dependent global ones.
 static_assert(32 * kInvCols == 256, "trinv_kernel: one warp per column of the block (256 threads)");
+constexpr size_t kTrinvSmem = (size_t)kInvCols * kMaxSnCols * sizeof(double);  // X columns (dynamic)
 __global__ void __launch_bounds__(256) trinv_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                     const double* __restrict__ front, const double* __restrict__ kkinv,
                                                     double* __restrict__ panel) {
-  __shared__ double sD[32][33];
-  __shared__ double v[32][kInvCols];
+  extern __shared__ double xs[];  // [kInvCols][nc]
+  __shared__ double sD[2][32][33];
   __shared__ double y[32][kInvCols];
   const int64_t s = tasks[2 * blockIdx.x], j0 = tasks[2 * blockIdx.x + 1];
-  const int64_t nc = d_nc(S, s), ldf = d_ldf(S, s);
+  const int nc = (int)d_nc(S, s);
+  const int64_t ldf = d_ldf(S, s);
   const double* F = front + S.front_off[s];
   double* X = panel + S.m_off[s];  // rows [0, nc) of M_s (stride ldf)
   const int ncols = (int)min((int64_t)kInvCols, nc - j0);
-  for (int64_t e = threadIdx.x; e < nc * ncols; e += blockDim.x) {
-    const int64_t i = e % nc, c = e / nc;
-    X[(j0 + c) * ldf + i] = (i == j0 + c) ? 1.0 : 0.0;
+  const double* Dall = kkinv + S.kk_off[s] * (32 * 32);
+  auto stage_d = [&](int kb, int buf) {  // D_kb -> sD[buf] (entries above the diagonal are never read)
+    const double* D = Dall + (kb / 32) * (32 * 32);
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) cp_async8(&sD[buf][e >> 5][e & 31], D + e, true);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  const int kb0 = (int)(j0 / 32) * 32;
+  stage_d(kb0, 0);
+  for (int e = threadIdx.x; e < kInvCols * nc; e += blockDim.x) {
+    const int c = e / nc, i = e - c * nc;
+    xs[e] = (i == j0 + c) ? 1.0 : 0.0;
   }
-  __syncthreads();
   const int r = threadIdx.x & 31, cc = threadIdx.x >> 5;  // (row, column) of the 32 x kInvCols block
-  for (int64_t kb = (j0 / 32) * 32; kb < nc; kb += 32) {
-    const int bw = (int)min((int64_t)32, nc - kb);
-    const double* D = kkinv + (S.kk_off[s] + kb / 32) * (32 * 32);
-    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
-      const int a = e >> 5, b = e & 31;
-      sD[a][b] = (a < bw && b <= a) ? D[e] : 0.0;
-    }
-    if (cc < kInvCols) v[r][cc] = (r < bw && cc < ncols) ? X[(j0 + cc) * ldf + kb + r] : 0.0;
-    __syncthreads();
-    if (cc < kInvCols) {
-      double a0 = 0.0, a1 = 0.0;
-      for (int k = 0; k + 1 <= r; k += 2) {
-        a0 = fma(sD[r][k], v[k][cc], a0);
-        a1 = fma(sD[r][k + 1], v[k + 1][cc], a1);
+  int buf = 0;
+  for (int kb = kb0; kb < nc; kb += 32, buf ^= 1) {
+    const int bw = min(32, nc - kb);
+    if (kb + 32 < nc) stage_d(kb + 32, buf ^ 1);
+    // this thread's first update row: its L values in flight before the wait
+    const int i0 = kb + bw + threadIdx.x;
+    double l0[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) l0[j] = (i0 < nc && j < bw) ? F[(int64_t)(kb + j) * ldf + i0] : 0.0;
+    if (kb + 32 < nc)
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();  // D_kb landed; the previous step's updates of xs are done
+    {
+      double yv = 0.0;
+      if (r < bw) {  // (rows past the block: y = 0; D_kb and v are only read below the diagonal)
+        const double* v = xs + cc * nc + kb;
+        double a0 = 0.0, a1 = 0.0;
+        for (int k = 0; k + 1 <= r; k += 2) {
+          a0 = fma(sD[buf][r][k], v[k], a0);
+          a1 = fma(sD[buf][r][k + 1], v[k + 1], a1);
+        }
+        if ((r & 1) == 0) a0 = fma(sD[buf][r][r], v[r], a0);
+        yv = a0 + a1;
       }
-      if ((r & 1) == 0) a0 = fma(sD[r][r], v[r][cc], a0);
-      const double yv = a0 + a1;
-      y[r][cc] = r < bw ? yv : 0.0;
-      if (r < bw && cc < ncols) X[(j0 + cc) * ldf + kb + r] = yv;
+      y[r][cc] = yv;
     }
     __syncthreads();
-    for (int64_t i = kb + bw + threadIdx.x; i < nc; i += blockDim.x) {
+    if (r < bw) xs[cc * nc + kb + r] = y[r][cc];
+    for (int i = i0; i < nc; i += blockDim.x) {
       double acc[kInvCols];
 #pragma unroll
       for (int c = 0; c < kInvCols; ++c) acc[c] = 0.0;
-      for (int j = 0; j < bw; ++j) {
-        const double l = F[(kb + j) * ldf + i];
+      if (i == i0) {
 #pragma unroll
-        for (int c = 0; c < kInvCols; ++c) acc[c] = fma(l, y[j][c], acc[c]);
+        for (int j = 0; j < 32; ++j)
+#pragma unroll
+          for (int c = 0; c < kInvCols; ++c) acc[c] = fma(l0[j], y[j][c], acc[c]);
+      } else {
+        for (int j = 0; j < bw; ++j) {
+          const double l = F[(int64_t)(kb + j) * ldf + i];
+#pragma unroll
+          for (int c = 0; c < kInvCols; ++c) acc[c] = fma(l, y[j][c], acc[c]);
+        }
       }
 #pragma unroll
-      for (int c = 0; c < kInvCols; ++c)  // compile-time index: acc stays in registers
-        if (c < ncols) X[(j0 + c) * ldf + i] -= acc[c];
+      for (int c = 0; c < kInvCols; ++c) xs[c * nc + i] -= acc[c];
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ncols * nc; e += blockDim.x) {
+    const int c = e / nc, i = e - c * nc;
+    X[(j0 + c) * ldf + i] = xs[e];
   }
 }
 
@@ -632,7 +664,12 @@ __global__ void permute_kernel(int64_t n, int64_t k, const int64_t* __restrict__
 int trinv_level(CholHandle* h, int level, cudaStream_t st) {
   const DevTasks& T = h->trinv[level];
   if (!T.count) return CNB_OK;
-  trinv_kernel<<<(unsigned)T.count, 256, 0, st>>>(h->sym(), T.ptr, h->d_front, h->d_kkinv, h->d_m);
+  static bool attr = false;
+  if (!attr) {
+    CNB_CUDA(cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrinvSmem));
+    attr = true;
+  }
+  trinv_kernel<<<(unsigned)T.count, 256, kTrinvSmem, st>>>(h->sym(), T.ptr, h->d_front, h->d_kkinv, h->d_m);
   CNB_LAUNCH_CHECK("trinv_kernel");
   const DevTasks& P = h->p21[level];
   if (P.count) {
