@@ -50,7 +50,7 @@ __global__ void scatter_kernel(int64_t nmap, const int64_t* __restrict__ src, co
 // are issued before its stores (the parent and child fronts live in one
 // buffer, so the compiler could not reorder them otherwise).
 constexpr int kEaBatch = 4;
-__global__ void __launch_bounds__(256, 6) extend_add_kernel(DevSym S, const int32_t* __restrict__ tasks,
+__global__ void __launch_bounds__(256, 4) extend_add_kernel(DevSym S, const int32_t* __restrict__ tasks,
                                                          const int32_t* __restrict__ rng, double* __restrict__ front) {
   const int32_t p = tasks[4 * blockIdx.x];
   const int32_t* kr = rng + 2 * tasks[4 * blockIdx.x + 3];
@@ -62,23 +62,59 @@ __global__ void __launch_bounds__(256, 6) extend_add_kernel(DevSym S, const int3
     const int32_t* __restrict__ rel = S.rel + S.rel_ptr[c];
     const int64_t k0 = kr[2 * (ci - S.child_ptr[p])], k1 = kr[2 * (ci - S.child_ptr[p]) + 1];
     const double* Fc = front + S.front_off[c];
-    for (int64_t k = k0; k < k1; ++k) {
-      const double* __restrict__ uc = Fc + (ncc + k) * ldc + ncc;
-      double* fcol = Fp + (int64_t)rel[k] * ldp;
-      for (int64_t i0 = k + threadIdx.x; i0 < nrc; i0 += (int64_t)kEaBatch * blockDim.x) {
-        int32_t ri[kEaBatch];
+    if (nrc - k0 >= (int64_t)kEaBatch * blockDim.x) {
+      // long columns: one column at a time, full batches
+      for (int64_t k = k0; k < k1; ++k) {
+        const double* __restrict__ uc = Fc + (ncc + k) * ldc + ncc;
+        double* fcol = Fp + (int64_t)rel[k] * ldp;
+        for (int64_t i0 = k + threadIdx.x; i0 < nrc; i0 += (int64_t)kEaBatch * blockDim.x) {
+          int32_t ri[kEaBatch];
+          double u[kEaBatch], v[kEaBatch];
+#pragma unroll
+          for (int q = 0; q < kEaBatch; ++q) {
+            const int64_t i = i0 + (int64_t)q * blockDim.x;
+            ri[q] = i < nrc ? __ldg(rel + i) : -1;
+            u[q] = i < nrc ? uc[i] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < kEaBatch; ++q) v[q] = ri[q] >= 0 ? fcol[ri[q]] : 0.0;
+#pragma unroll
+          for (int q = 0; q < kEaBatch; ++q)
+            if (ri[q] >= 0) fcol[ri[q]] = v[q] + u[q];
+        }
+      }
+    } else {
+      // short columns: the (column k, row i >= k) elements of the <= kEaCols
+      // columns flattened, so a batch of loads spans columns
+      int32_t off[kEaCols + 1];
+      off[0] = 0;
+#pragma unroll
+      for (int q = 0; q < kEaCols; ++q) off[q + 1] = off[q] + (k0 + q < k1 ? (int32_t)(nrc - (k0 + q)) : 0);
+      const int32_t tot = off[kEaCols];
+      for (int32_t e0 = threadIdx.x; e0 < tot; e0 += kEaBatch * (int32_t)blockDim.x) {
+        int32_t ri[kEaBatch], cj[kEaBatch];
         double u[kEaBatch], v[kEaBatch];
 #pragma unroll
         for (int q = 0; q < kEaBatch; ++q) {
-          const int64_t i = i0 + (int64_t)q * blockDim.x;
-          ri[q] = i < nrc ? __ldg(rel + i) : -1;
-          u[q] = i < nrc ? uc[i] : 0.0;
+          const int32_t e = e0 + q * (int32_t)blockDim.x;
+          int kk = 0;
+          int32_t base = 0;  // (compile-time indices only: off stays in registers)
+#pragma unroll
+          for (int m = 1; m < kEaCols; ++m) {
+            kk += e >= off[m] ? 1 : 0;
+            base = e >= off[m] ? off[m] : base;
+          }
+          const int64_t k = k0 + kk, i = k + (e - base);
+          const bool in = e < tot;
+          ri[q] = in ? __ldg(rel + i) : -1;
+          cj[q] = in ? __ldg(rel + k) : 0;
+          u[q] = in ? Fc[(ncc + k) * ldc + ncc + i] : 0.0;
         }
 #pragma unroll
-        for (int q = 0; q < kEaBatch; ++q) v[q] = ri[q] >= 0 ? fcol[ri[q]] : 0.0;
+        for (int q = 0; q < kEaBatch; ++q) v[q] = ri[q] >= 0 ? Fp[(int64_t)cj[q] * ldp + ri[q]] : 0.0;
 #pragma unroll
         for (int q = 0; q < kEaBatch; ++q)
-          if (ri[q] >= 0) fcol[ri[q]] = v[q] + u[q];
+          if (ri[q] >= 0) Fp[(int64_t)cj[q] * ldp + ri[q]] = v[q] + u[q];
       }
     }
     __syncthreads();
