@@ -586,6 +586,9 @@ static int chol_upload(CholHandle* h) {
   if ((rc = upload_vec(&h->d_kk_off, h->kk_off)) != CNB_OK) return rc;
   CNB_CUDA(cudaMalloc((void**)&h->d_kkinv, std::max<int64_t>(1, h->kk_off[S.ns]) * kPanel * kPanel * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_vals, std::max<int64_t>(1, S.csr_nnz) * sizeof(double)));
+  CNB_CUDA(cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));
+  CNB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CNB_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CNB_CUDA(cudaFuncSetAttribute(syrk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem));
   CNB_CUDA(cudaFuncSetAttribute(syrk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem));
   h->uploaded = true;
@@ -600,6 +603,11 @@ static void chol_free(CholHandle* h) {
   h->factor_exec = nullptr;
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   h->cap_stream = nullptr;
+  if (h->side_stream) cudaStreamDestroy(h->side_stream);
+  h->side_stream = nullptr;
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  h->ev_fork = h->ev_join = nullptr;
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->plan1.release();
@@ -674,8 +682,15 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
         CNB_LAUNCH_CHECK("syrk_kernel");
       }
     }
-    if ((rc = trinv_level(h, l, st))) return rc;
+    // L11^{-1} and P21 of this level read L11 / L21 (columns [0, nc) of its
+    // fronts) and write M_s: nothing the next levels touch, so they run on the
+    // side stream, in level order, while the factorisation goes on
+    CNB_CUDA(cudaEventRecord(h->ev_fork, st));
+    CNB_CUDA(cudaStreamWaitEvent(h->side_stream, h->ev_fork, 0));
+    if ((rc = trinv_level(h, l, h->side_stream))) return rc;
   }
+  CNB_CUDA(cudaEventRecord(h->ev_join, h->side_stream));
+  CNB_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
   return CNB_OK;
 }
 

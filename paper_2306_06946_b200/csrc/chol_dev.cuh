@@ -91,6 +91,10 @@ struct CholHandle {
   double* d_vals = nullptr;   // CSR values being factorised (fixed address for the graph)
   cudaGraphExec_t factor_exec = nullptr;
   cudaStream_t cap_stream = nullptr;
+  // L11^{-1} / P21 of a level only feed the solves: they run on a side stream
+  // beside the next levels' factorisation (fork per level, one join at the end)
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* factor_status = nullptr;
   long long factor_nodes = 0;
   std::vector<int64_t> m_off;
