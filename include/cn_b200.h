@@ -251,7 +251,8 @@ int cnb_chol_export(cnb_chol_t h, const char* name, void* dst);
 
 /* Numeric factorisation on the device from CSR values (device, same pattern
  * as analysed).  A non-positive pivot sets d_status to CNB_E_NOT_SPD, as the
- * reference's pivot check (linalg.py:77-84). */
+ * reference's pivot check (linalg.py:77-84).  Internally forks onto the
+ * handle's side stream and joins back into `stream` before returning. */
 int cnb_chol_factor(cnb_chol_t h, const double* vals, cnb_status_t* d_status, void* stream);
 
 /* X = A^{-1} B for k right-hand sides stored as k contiguous length-n
