@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(128, TRAIL ? SYRK_TRAIL_MINB : SYRK_MINB)
   }
 }
 
+constexpr double kLevelEventsMaxFlops = 5e10;  // factors whose per-level M_s events are recorded
 static int chol_upload(CholHandle* h) {
   if (h->uploaded) return CNB_OK;
   const Symbolic& S = h->S;
@@ -587,6 +588,15 @@ static int chol_upload(CholHandle* h) {
   CNB_CUDA(cudaMalloc((void**)&h->d_kkinv, std::max<int64_t>(1, h->kk_off[S.ns]) * kPanel * kPanel * sizeof(double)));
   CNB_CUDA(cudaMalloc((void**)&h->d_vals, std::max<int64_t>(1, S.csr_nnz) * sizeof(double)));
   CNB_CUDA(cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));
+  if (S.flops < kLevelEventsMaxFlops) {  // (only small factors overlap the compliance: no extra
+                                         // streams otherwise -- streams beyond the hardware queues
+                                         // alias and serialise, measured +3 ms per cfg3 step)
+    CNB_CUDA(cudaStreamCreateWithFlags(&h->comp_stream, cudaStreamNonBlocking));
+    CNB_CUDA(cudaEventCreateWithFlags(&h->ev_pre, cudaEventDisableTiming));
+    CNB_CUDA(cudaEventCreateWithFlags(&h->ev_comp, cudaEventDisableTiming));
+    h->ev_level.assign(S.n_levels, nullptr);
+    for (auto& e : h->ev_level) CNB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   CNB_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CNB_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CNB_CUDA(cudaFuncSetAttribute(syrk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem));
@@ -608,6 +618,15 @@ static void chol_free(CholHandle* h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   h->ev_fork = h->ev_join = nullptr;
+  if (h->comp_stream) cudaStreamDestroy(h->comp_stream);
+  h->comp_stream = nullptr;
+  for (cudaEvent_t e : {h->ev_pre, h->ev_comp})
+    if (e) cudaEventDestroy(e);
+  h->ev_pre = h->ev_comp = nullptr;
+  for (auto& e : h->ev_level)
+    if (e) cudaEventDestroy(e);
+  h->ev_level.clear();
+  h->level_events = false;
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->plan1.release();
@@ -688,6 +707,17 @@ static int enqueue_factor(CholHandle* h, DevStatus* d_status, cudaStream_t st) {
     CNB_CUDA(cudaEventRecord(h->ev_fork, st));
     CNB_CUDA(cudaStreamWaitEvent(h->side_stream, h->ev_fork, 0));
     if ((rc = trinv_level(h, l, h->side_stream))) return rc;
+    // level l's M_s is complete: the compliance forward solve may read it (small
+    // factors only: the external event nodes cost a large factor's graph ~4 ms
+    // per cfg3 step, and its forward solve is not overlapped anyway)
+    if (h->comp_stream) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      CNB_CUDA(cudaStreamIsCapturing(h->side_stream, &cs));
+      if (cs == cudaStreamCaptureStatusActive)
+        CNB_CUDA(cudaEventRecordWithFlags(h->ev_level[l], h->side_stream, cudaEventRecordExternal));
+      else
+        CNB_CUDA(cudaEventRecord(h->ev_level[l], h->side_stream));
+    }
   }
   CNB_CUDA(cudaEventRecord(h->ev_join, h->side_stream));
   CNB_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
@@ -787,6 +817,7 @@ int cnb_chol_factor(cnb_chol_t hh, const double* vals, cnb_status_t* d_status, v
   // values into the handle's own buffer: the captured graph reads fixed addresses
   CNB_CUDA(cudaMemcpyAsync(h->d_vals, vals, std::max<int64_t>(1, S.csr_nnz) * sizeof(double),
                            cudaMemcpyDeviceToDevice, st));
+  if (h->ev_pre) CNB_CUDA(cudaEventRecord(h->ev_pre, st));  // a following compliance forward solve starts here
   if (use_graphs()) {
     if (h->factor_exec && h->factor_status != (void*)d_status) {
       cudaGraphExecDestroy(h->factor_exec);
@@ -818,6 +849,7 @@ int cnb_chol_factor(cnb_chol_t hh, const double* vals, cnb_status_t* d_status, v
     if ((rc = enqueue_factor(h, (DevStatus*)d_status, st))) return rc;
   }
   h->factored = true;
+  h->level_events = h->comp_stream != nullptr;
   return CNB_OK;
 }
 

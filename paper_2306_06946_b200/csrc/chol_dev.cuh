@@ -95,6 +95,14 @@ struct CholHandle {
   // beside the next levels' factorisation (fork per level, one join at the end)
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // the compliance's forward solve waits only for the levels of M_s it reads:
+  // ev_level[l] is recorded (externally, from inside the factor graph) once level
+  // l's M_s is formed; it runs on comp_stream after ev_pre (the caller's stream
+  // just before the factor, or after the previous compliance's Gram)
+  std::vector<cudaEvent_t> ev_level;
+  cudaStream_t comp_stream = nullptr;
+  cudaEvent_t ev_pre = nullptr, ev_comp = nullptr;
+  bool level_events = false;
   void* factor_status = nullptr;
   long long factor_nodes = 0;
   std::vector<int64_t> m_off;

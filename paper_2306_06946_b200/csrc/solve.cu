@@ -1279,7 +1279,10 @@ static inline T* at(const GrowBuf& b, size_t off) {
 }
 
 // Forward solve of this rank's columns: Y (compact layout fyoff) = L^{-1} P E.
-static int plan_forward(CholHandle* h, const CompliancePlan& P, double* Y, cudaStream_t st) {
+constexpr double kOverlapMaxFlops = 2e10;  // forward solves overlapped with the factorisation (see compliance)
+// lev (optional): per-level events; level l waits for lev[l] (its M_s formed)
+static int plan_forward(CholHandle* h, const CompliancePlan& P, double* Y, cudaStream_t st,
+                        const cudaEvent_t* lev = nullptr) {
   const Symbolic& S = h->S;
   double* rhs = (double*)h->c_rhs.p;
   CNB_CUDA(cudaMemsetAsync(rhs, 0, std::max<int64_t>(1, P.froff[S.ns]) * sizeof(double), st));
@@ -1292,6 +1295,7 @@ static int plan_forward(CholHandle* h, const CompliancePlan& P, double* Y, cudaS
   DevSym sym = h->sym();
   RhsView R{rhs, at<int64_t>(h->c_int, P.o_froff), at<int64_t>(h->c_int, P.o_flo), at<int64_t>(h->c_int, P.o_fw)};
   for (int l = 0; l < S.n_levels; ++l) {
+    if (lev && (P.arec[l].second || P.prec[l].second)) CNB_CUDA(cudaStreamWaitEvent(st, lev[l], 0));
     if (P.arec[l].second) {
       asm_kernel<<<(unsigned)P.arec[l].second, kSolveThreads, 0, st>>>(sym, at<int32_t>(h->c_int, P.arec[l].first),
                                                                         R, 0, nullptr, S.n);
@@ -1327,14 +1331,29 @@ int compliance(CholHandle* h, int64_t ncols, const int64_t* colptr, const int64_
   CompliancePlan P;
   int rc = plan_build(h->S, ncols, colptr, rowidx, vals, 0, 1, P);
   if (rc) return rc;
-  if ((rc = plan_upload(h, P, st))) return rc;
+  // the forward solve overlaps the factorisation that produced M: on the
+  // handle's compliance stream, from the point before that factorisation (or
+  // after the previous compliance's Gram), each level after its M_s is formed;
+  // the Gram (which writes the caller's U) runs on the caller's stream after it
+  // (latency-bound forward solves only: a large one -- cfg3's 870 GFLOP per body --
+  // competes with the factor's own DMMA work and with the other bodies', measured
+  // 497 -> 502 ms per cfg3 step, while cfg1's 3.54 -> 3.20 ms)
+  const bool ov = h->level_events && h->comp_stream && P.fwd_flops < kOverlapMaxFlops;
+  cudaStream_t fs = ov ? h->comp_stream : st;
+  if (ov) CNB_CUDA(cudaStreamWaitEvent(fs, h->ev_pre, 0));
+  if ((rc = plan_upload(h, P, fs))) return rc;
   if (flops_out) {
     flops_out[0] = P.fwd_flops;
     flops_out[1] = P.gram_flops;
   }
   double* Y = (double*)h->c_y.p;
-  if ((rc = plan_forward(h, P, Y, st))) return rc;
+  if ((rc = plan_forward(h, P, Y, fs, ov ? h->ev_level.data() : nullptr))) return rc;
+  if (ov) {
+    CNB_CUDA(cudaEventRecord(h->ev_comp, fs));
+    CNB_CUDA(cudaStreamWaitEvent(st, h->ev_comp, 0));
+  }
   if ((rc = plan_gram(h, P, Y, U, ldu, nullptr, st))) return rc;
+  if (ov) CNB_CUDA(cudaEventRecord(h->ev_pre, st));  // the next forward solve reuses the buffers after this Gram
   h->last_fwd_flops = P.fwd_flops;
   h->last_gram_flops = P.gram_flops;
   return CNB_OK;
@@ -1399,6 +1418,8 @@ int compliance_split_finish(CholHandle* h, const double* tiles_all, double* U, i
                                                              P.ncols, at<int64_t>(h->c_int, P.o_sorted), U, ldu);
     CNB_LAUNCH_CHECK("scatter_tiles_kernel");
   }
+  // a later single-GPU compliance reuses the plan buffers after this point
+  if (h->ev_pre) CNB_CUDA(cudaEventRecord(h->ev_pre, st));
   return CNB_OK;
 }
 
