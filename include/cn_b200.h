@@ -269,7 +269,9 @@ int cnb_chol_solve(cnb_chol_t h, const double* B, int64_t ldb, double* X, int64_
  * CSC form (colptr, rowidx = DoF ids, vals).  Y = L^{-1} P S^T is formed only
  * on the elimination paths of the columns and U = Y^T Y by fp64 MMA tiles.
  * Replaces solve_multi(S^T) + S @ X of assemble_Wg constraints.py:175-178.
- * flops_out (host, may be NULL) = {forward-solve flops, Gram flops}. */
+ * flops_out (host, may be NULL) = {forward-solve flops, Gram flops}.
+ * For small factors the forward solve overlaps the preceding cnb_chol_factor
+ * (handle-internal stream, per-level events); U is written in `stream` order. */
 int cnb_chol_compliance(cnb_chol_t h, int64_t ncols, const int64_t* colptr, const int64_t* rowidx,
                         const double* vals, double* U, int64_t ldu, double* flops_out, void* stream);
 
