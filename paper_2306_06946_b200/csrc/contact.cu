@@ -181,6 +181,95 @@ __global__ void __launch_bounds__(256) prox_update_kernel(int64_t mo, const doub
   }
 }
 
+// Large objects: U_o is symmetric, so y = U t reads only its lower triangle.
+// One CTA per 128 x 128 tile (I, J), I >= J, all 16 rows of a warp loaded up
+// front: the row products U_IJ t_J go to part[I][J], and (I > J) the column
+// products U_IJ^T t_I to part[J][I].  Every slot is written exactly once and
+// prox_sym_sum_kernel adds each row's nt slots in J order: deterministic, and
+// 8 n^2 / 2 bytes of U per update instead of 8 n^2.
+constexpr int kPT = 128;
+constexpr int64_t kProxSymMinTiles = 8;  // below ~1 000 rows the warp-per-row GEMV is one short launch
+__global__ void __launch_bounds__(256, 2) prox_sym_tile_kernel(int64_t n, int64_t nt, const double* __restrict__ U,
+                                                            int64_t ldu, const double* __restrict__ t,
+                                                            double* __restrict__ part) {
+  const int64_t b = blockIdx.x;
+  int64_t I = (int64_t)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while (I * (I + 1) / 2 > b) --I;
+  while ((I + 1) * (I + 2) / 2 <= b) ++I;
+  const int64_t J = b - I * (I + 1) / 2;
+  __shared__ double tI[kPT], tJ[kPT];
+  __shared__ double colp[8][kPT];
+  const int64_t r0 = I * kPT, c0 = J * kPT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < kPT) {
+    const int e = threadIdx.x;
+    tI[e] = r0 + e < n ? t[r0 + e] : 0.0;
+    tJ[e] = c0 + e < n ? t[c0 + e] : 0.0;
+  }
+  __syncthreads();
+  // the warp's 16 rows in two halves of 8 (64 KB of U in flight per CTA, two CTAs per SM)
+  double rs = 0.0;
+  double ca[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    double v[8][4];
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+      const int64_t r = r0 + warp * 16 + 8 * hf + rr;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t c = c0 + lane + 32 * q;
+        v[rr][q] = (r < n && c < n) ? __ldcs(U + r * ldu + c) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+      double s = fma(v[rr][0], tJ[lane], v[rr][1] * tJ[lane + 32]) + fma(v[rr][2], tJ[lane + 64], v[rr][3] * tJ[lane + 96]);
+      s = warp_sum(s);
+      if (lane == 8 * hf + rr) rs = s;
+    }
+    if (I != J) {
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
+        const double ti = tI[warp * 16 + 8 * hf + rr];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ca[q] = fma(v[rr][q], ti, ca[q]);
+      }
+    }
+  }
+  if (lane < 16) part[(I * nt + J) * kPT + warp * 16 + lane] = rs;
+  if (I == J) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) colp[warp][lane + 32 * q] = ca[q];
+  __syncthreads();
+  if (threadIdx.x < kPT) {
+    const int e = threadIdx.x;
+    double s = colp[0][e];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) s += colp[w][e];
+    part[(J * nt + I) * kPT + e] = s;
+  }
+}
+
+__global__ void prox_sym_sum_kernel(int64_t mo, int64_t nt, const double* __restrict__ part,
+                                    const int64_t* __restrict__ idx, const int8_t* __restrict__ side, double h2,
+                                    double* __restrict__ pa, double* __restrict__ pb) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 3 * mo) return;
+  const int64_t I = r / kPT, i = r - I * kPT;
+  const double* p = part + I * nt * kPT + i;
+  double s = 0.0;
+  for (int64_t J = 0; J < nt; ++J) s += p[J * kPT];
+  const int64_t k = r / 3;
+  const int d = (int)(r - 3 * k);
+  const int64_t pair = idx ? idx[k] : k;
+  const double move = mul(h2, s);
+  if (side[k] > 0)
+    pa[3 * pair + d] = add(pa[3 * pair + d], move);
+  else
+    pb[3 * pair + d] = sub(pb[3 * pair + d], move);
+}
+
 // tg[c] = t[3 idx[c / 3] + c % 3]: the object's rows of D^T lambda, contiguous
 __global__ void prox_gather_kernel(int64_t mo, const int64_t* __restrict__ idx, const double* __restrict__ t,
                                    double* __restrict__ tg) {
@@ -483,6 +572,21 @@ int cnb_prox_update(int64_t mo, const double* U, int64_t ldu, const int64_t* idx
     prox_gather_kernel<<<grid_for(3 * mo, 256), 256, 0, st>>>(mo, idx, t, (double*)tg.p);
     CNB_LAUNCH_CHECK("prox_gather_kernel");
     tv = (const double*)tg.p;
+  }
+  const int64_t n = 3 * mo, nt = (n + kPT - 1) / kPT;
+  static const bool sym_off = [] {
+    const char* e = getenv("CNB_PROX_SYM");
+    return e && e[0] == '0';
+  }();
+  if (nt >= kProxSymMinTiles && !sym_off) {
+    static GrowBuf part;
+    int rc = part.ensure((size_t)(nt * nt * kPT) * sizeof(double));
+    if (rc) return rc;
+    prox_sym_tile_kernel<<<(unsigned)(nt * (nt + 1) / 2), 256, 0, st>>>(n, nt, U, ldu, tv, (double*)part.p);
+    CNB_LAUNCH_CHECK("prox_sym_tile_kernel");
+    prox_sym_sum_kernel<<<grid_for(n, 256), 256, 0, st>>>(mo, nt, (const double*)part.p, idx, side, h * h, p_a, p_b);
+    CNB_LAUNCH_CHECK("prox_sym_sum_kernel");
+    return CNB_OK;
   }
   const int64_t threads = 3 * mo * 32;
   prox_update_kernel<<<grid_for(threads, 256), 256, 0, st>>>(mo, U, ldu, idx, side, tv, h * h, p_a, p_b);
