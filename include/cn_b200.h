@@ -142,7 +142,10 @@ int cnb_apply_dt(int64_t groups, const double* D, const double* lam, double* t,
  * U_o is the compact (3*mo x 3*mo) restriction of the object's S A^-1 S^T to
  * the mo pairs it takes part in; idx (int64, mo) lists those pairs and
  * side (int8, mo) the side the object owns.  Replaces the per-object loop of
- * fast_update_proximity constraints.py:217-244. */
+ * fast_update_proximity constraints.py:217-244.
+ * U_o must be symmetric: from 8 row tiles of 128 up only its lower triangle is
+ * read (CNB_PROX_SYM=0 forces the full-row GEMV).  The library's workspace for
+ * this is shared: calls on different streams must not overlap. */
 int cnb_prox_update(int64_t mo, const double* U, int64_t ldu, const int64_t* idx,
                     const int8_t* side, const double* t, double h, double* p_a, double* p_b,
                     void* stream);
